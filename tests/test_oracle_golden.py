@@ -1,0 +1,249 @@
+"""Pin the CPU oracle (oracle/) against the reference's own outputs.
+
+The fixtures in tests/golden/ were produced by running the reference odegrad
+package itself (tools/make_golden.py); the known-answer values below are the
+reference test-suite's own (pkg/tests/*.py, cited per test).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import core as oc
+from oracle import revolve as orv
+from paper_2206_01298_b200 import configs
+
+TOL = 1e-12   # batching changes BLAS blocking / batch-sum order only
+
+
+def test_revolve_counts_match_reference(golden):
+    g = golden("revolve.npz")
+    for nt in range(1, 61):
+        for nc in range(1, 21):
+            assert orv.revolve_count(nt, nc) == g["counts"][nt, nc]
+            assert orv.dp_optimal_count(nt, nc) == g["counts"][nt, nc]
+
+
+def test_revolve_schedules_match_reference(golden):
+    g = golden("revolve.npz")
+    kinds = {"advance": 0, "store": 1, "restore": 2, "reverse": 3}
+    for key, arr in g.items():
+        if not key.startswith("sched_"):
+            continue
+        _, nt, nc = key.split("_")
+        acts = orv.revolve_schedule(int(nt), int(nc))
+        mine = np.array([[kinds[k], s, a, b] for k, s, a, b in acts], np.int64)
+        assert np.array_equal(mine, arr), key
+
+
+def test_revolve_spot_values_and_audit():
+    # pkg/tests/test_checkpointing.py:24-33, test_acceptance.py:110-128
+    assert orv.revolve_count(10, 3) == 6
+    assert orv.revolve_count(4, 1) == 3
+    assert orv.revolve_count(5, 4) == 0
+    for nt in range(1, 30):
+        for nc in range(1, 10):
+            extra, live = orv.audit(nt, nc)
+            assert extra == orv.revolve_count(nt, nc)
+            assert live <= nc
+
+
+def test_mlp_kernels_match_reference(golden):
+    g = golden("mlp_kernels.npz")
+    for act in ("identity", "relu", "tanh", "gelu"):
+        mlp = oc.Mlp((6, 7, 7, 5), act, g[f"{act}/theta"], time_input=True)
+        fld = oc.MlpField(mlp)
+        c = oc.Counters()
+        for b in range(4):
+            U = g[f"{act}/U"][b:b + 1]
+            t = g[f"{act}/t"][b]
+            f = fld.eval(U, t, c)
+            jtv, ptv = fld.vjp(U, t, g[f"{act}/V"][b:b + 1], c)
+            jv = fld.jvp(U, t, g[f"{act}/W"][b:b + 1], c)
+            assert np.max(np.abs(f[0] - g[f"{act}/f"][b])) <= 1e-14
+            assert np.max(np.abs(jtv[0] - g[f"{act}/jtv"][b])) <= 1e-14
+            assert np.max(np.abs(ptv - g[f"{act}/ptv"][b])) <= 1e-14
+            assert np.max(np.abs(jv[0] - g[f"{act}/jv"][b])) <= 1e-14
+
+
+def _check(res, g, prefix, tol=TOL):
+    assert oc.rel_error(res["u_final"], g[prefix + "u_final"]) <= tol
+    assert oc.rel_error(res["du0"], g[prefix + "du0"]) <= tol
+    assert oc.rel_error(res["dtheta"], g[prefix + "dtheta"]) <= tol
+    assert abs(res["loss"] - float(g[prefix + "loss"])) <= tol * max(1.0, abs(res["loss"]))
+    nf = [s.nfe_forward for s in res["sample_counters"]]
+    nb = [s.nfe_backward for s in res["sample_counters"]]
+    assert nf == list(g[prefix + "nfe_forward"])
+    assert nb == list(g[prefix + "nfe_backward"])
+    assert res["store"].stored_states == g[prefix + "stored_states"]
+    assert res["store"].stored_stage_vectors == g[prefix + "stored_stage_vectors"]
+    assert res["store"].max_live_slots == g[prefix + "max_live_slots"]
+    assert res["store"].recomputed_steps == g[prefix + "recomputed_steps"]
+
+
+SCHEMES = ("euler", "midpoint", "bosh3", "rk4", "dopri5", "beuler", "cn")
+
+
+@pytest.mark.parametrize("name", SCHEMES)
+@pytest.mark.parametrize("pol", ["store_all", "store_solutions", "revolve:3"])
+def test_small_schemes_match_reference(golden, name, pol):
+    g = golden("small_schemes.npz")
+    mlp = oc.Mlp((3, 8, 8, 3), "tanh", g[f"{name}/theta"])
+    res = oc.grad_terminal(oc.MlpField(mlp), name, g[f"{name}/u0"], 0.0, 1.0, 7, pol)
+    _check(res, g, f"{name}/{pol}/", tol=1e-11 if name in ("beuler", "cn") else TOL)
+
+
+@pytest.mark.parametrize("act", ["identity", "relu", "tanh", "gelu"])
+def test_time_input_activations_match_reference(golden, act):
+    g = golden("small_schemes.npz")
+    mlp = oc.Mlp((5, 6, 6, 4), act, g[f"act_{act}/theta"], time_input=True)
+    res = oc.grad_terminal(oc.MlpField(mlp), "dopri5", g[f"act_{act}/u0"], 0.0, 1.0, 5)
+    _check(res, g, f"act_{act}/")
+
+
+@pytest.mark.parametrize("pol", ["store_all", "store_solutions", "revolve:3"])
+def test_c1_subset_matches_reference(golden, pol):
+    g = golden("c1_sub.npz")
+    ci = configs.make_config("C1").subset(4)
+    assert np.array_equal(ci.u0, g["u0"])
+    assert float(np.sum(ci.theta * np.arange(1, ci.theta.size + 1))) == float(g["theta_checksum"])
+    fld = oc.MlpField(oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input))
+    res = oc.grad_terminal(fld, ci.scheme, ci.u0, ci.t0, ci.tF, ci.n_steps, pol)
+    _check(res, g, f"{pol}/")
+
+
+@pytest.mark.parametrize("pol", ["store_all", "revolve:8"])
+def test_c2_subset_matches_reference(golden, pol):
+    g = golden("c2_sub.npz")
+    ci = configs.make_config("C2").subset(3)
+    assert np.array_equal(ci.u0, g["u0"])
+    fld = oc.MlpField(oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input))
+    res = oc.grad_terminal(fld, ci.scheme, ci.u0, ci.t0, ci.tF, ci.n_steps, pol)
+    _check(res, g, f"{pol}/")
+
+
+def test_c5_subset_matches_reference(golden):
+    """Values match both reference kernel paths to 1e-10.  Counters match the
+    reference's numpy path exactly (same ufuncs); against its numba path they
+    may differ by a rounding-boundary GMRES stop (+-1 per solve), exactly as the
+    reference's two paths differ from each other."""
+    g = golden("c5_sub_numpy.npz")
+    gn = golden("c5_sub.npz")
+    ci = configs.make_config("C5").subset(2)
+    assert np.array_equal(ci.u0, g["u0"])
+    fld = oc.StiffField(oc.Mlp(ci.widths, ci.activation, ci.theta), ci.extras["diag"],
+                        ci.extras["scale"])
+    res = oc.grad_terminal(fld, ci.scheme, ci.u0, ci.t0, ci.tF, ci.n_steps, "store_all",
+                           cfg=oc.SolverCfg(**ci.extras["solver"]))
+    _check(res, g, "store_all/", tol=1e-10)
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(res[k], gn["store_all/" + k]) <= 1e-10
+    nf = np.array([s.nfe_forward for s in res["sample_counters"]])
+    assert np.max(np.abs(nf - gn["store_all/nfe_forward"])) <= 2
+
+
+# --- reference known-answer tests restated against the oracle -------------
+
+class _Lin:
+    """u' = k*u field with closed-form products (pkg/tests/test_integrators.py:19-21)."""
+
+    def __init__(self, k):
+        self.k = k
+        self.n_params = 0
+
+    def eval(self, U, t, c):
+        c.nfe_forward += 1
+        return self.k * U
+
+    def jvp(self, U, t, W, c):
+        c.nfe_forward += 1
+        return self.k * W
+
+    def vjp(self, U, t, V, c):
+        c.nfe_backward += 1
+        return self.k * V, np.zeros(0)
+
+    def vjp_u(self, U, t, V, c):
+        c.nfe_backward += 1
+        return self.k * V
+
+
+def test_kat_single_steps():
+    # pkg/tests/test_integrators.py:24-64
+    c = oc.Counters()
+    rec, _ = oc.rk_step(oc.explicit_tableau("euler"), _Lin(1.0), np.array([[1.0]]), 0.0, 0.1, c)
+    assert abs(rec.u_next[0, 0] - 1.1) <= 1e-15
+    rec, _ = oc.rk_step(oc.explicit_tableau("rk4"), _Lin(1.0), np.array([[1.0]]), 0.0, 0.1, c)
+    assert abs(rec.u_next[0, 0] - 1.1051708333) <= 1e-10
+    rec = oc.theta_step(1.0, _Lin(1.0), np.array([[1.0]]), 0.0, 0.5, oc.SolverCfg(), c)
+    assert abs(rec.u_next[0, 0] - 2.0) <= 1e-9
+    rec = oc.theta_step(0.5, _Lin(-1000.0), np.array([[1.0]]), 0.0, 0.1, oc.SolverCfg(), c)
+    assert abs(rec.u_next[0, 0] - (-49.0 / 51.0)) <= 1e-9
+
+
+def test_kat_fsal_counts():
+    # pkg/tests/test_integrators.py:96-108
+    for name, per, extra in (("dopri5", 6, 1), ("rk4", 4, 0), ("bosh3", 3, 1)):
+        res = oc.grad_terminal(_Lin(1.0), name, np.array([[1.0]]), 0.0, 1.0, 10)
+        assert res["counters"].nfe_forward == per * 10 + extra
+
+
+def test_kat_rk4_global_error():
+    # pkg/tests/test_integrators.py:86-93
+    res = oc.grad_terminal(_Lin(1.0), "rk4", np.array([[1.0]]), 0.0, 1.0, 20)
+    err = abs(res["u_final"][0, 0] - np.e)
+    assert abs(err - 1.358e-7) <= 0.01e-7
+
+
+def test_kat_transpose_dense_all_schemes():
+    # pkg/tests/test_acceptance.py:242-291: forward step matrix == adjoint^T
+    rng = np.random.default_rng(123)
+    A = rng.standard_normal((3, 3)) * 0.5
+
+    class LinA:
+        n_params = 0
+
+        def eval(self, U, t, c):
+            c.nfe_forward += 1
+            return U @ A.T
+
+        def jvp(self, U, t, W, c):
+            c.nfe_forward += 1
+            return W @ A.T
+
+        def vjp(self, U, t, V, c):
+            c.nfe_backward += 1
+            return V @ A, np.zeros(0)
+
+        def vjp_u(self, U, t, V, c):
+            c.nfe_backward += 1
+            return V @ A
+
+    cfg = oc.SolverCfg(newton_tol=1e-14, gmres_tol=5e-16, newton_maxit=100)
+    for name in SCHEMES:
+        sch = oc.scheme(name)
+        E = np.eye(3)
+        c = oc.Counters()
+        if sch.kind == "rk":
+            fwd = oc.rk_step(sch.tab, LinA(), E, 0.0, 0.2, c)[0].u_next.T
+            rec0 = oc.rk_step(sch.tab, LinA(), np.zeros((3, 3)), 0.0, 0.2, c)[0]
+            adj, _ = oc.rk_adjoint_step(sch.tab, LinA(), rec0, E, np.zeros(0), c)
+        else:
+            fwd = oc.theta_step(sch.theta, LinA(), E, 0.0, 0.2, cfg, c).u_next.T
+            rec0 = oc.theta_step(sch.theta, LinA(), np.zeros((3, 3)), 0.0, 0.2, cfg, c)
+            adj, _ = oc.theta_adjoint_step(sch.theta, LinA(), rec0, E, np.zeros(0), cfg, c)
+        assert np.max(np.abs(adj.T - fwd.T)) <= 1e-12, name
+
+
+def test_kat_gmres():
+    # pkg/tests/test_linalg.py:7-62
+    cfg = oc.SolverCfg()
+    x, it = oc.gmres(lambda v: v, np.array([1.0, -2.0, 3.0]), cfg)
+    assert np.allclose(x, [1.0, -2.0, 3.0], atol=1e-14) and it <= 1
+    x, it = oc.gmres(lambda v: 2 * v, np.zeros(4), cfg)
+    assert it == 0 and not np.any(x)
+    rng = np.random.default_rng(3)
+    m = rng.standard_normal((40, 40))
+    a = m @ m.T + 0.05 * np.eye(40)
+    with pytest.raises(oc.ConvergenceError):
+        oc.gmres(lambda v: a @ v, rng.standard_normal(40),
+                 oc.SolverCfg(gmres_maxit=2, gmres_restart=2))
