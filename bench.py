@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark: ODE-block forward + discrete-adjoint gradient, samples/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--policy revolve:8]
+    python bench.py --impl reference ...      # the CPU reference path (oracle port)
+
+Workload (BASELINE.json configs[1], "C2"): MLP (64+t)-256-64 tanh, fp32,
+Dopri5 x 40 on [0,1], binomial checkpointing with 8 slots, loss
+0.5*mean||u(1)||^2, batch 4096 per GPU (weak scaling: each rank owns a
+4096-sample shard of an N*4096 global batch; dtheta and the loss are reduced
+once per step with a deterministic ordered all-gather-sum over NCCL).
+
+One step = one full grad() over this rank's shard with inputs resident in HBM
+(``value``); ``e2e`` re-times the same call through the public API from pinned
+host memory with results read back.  L2 is flushed (256 MiB write) between
+timed steps.  Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ODE-block fwd+discrete-adjoint grad samples/s at 1–8 B200; % of roofline"
+WORKLOADS = {
+    "C1": "C1: MLP 64-256-64 tanh fp64, RK4 x10 on [0,1], store_all, B=512/GPU",
+    "C2": "C2: MLP (64+t)-256-64 tanh fp32, Dopri5 x40 on [0,1], revolve:8, B=4096/GPU",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--policy", default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- CPU side
+def _cpu_worker_init(cfg_name, policy):
+    global _W
+    from oracle import core as oc
+    from paper_2206_01298_b200.configs import make_config
+    ci = make_config(cfg_name, batch=64)
+    mlp = oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input)
+    if ci.kind == "stiff":
+        fld = oc.StiffField(mlp, ci.extras["diag"], ci.extras["scale"])
+        cfg = oc.SolverCfg(**ci.extras["solver"])
+    else:
+        fld = oc.MlpField(mlp)
+        cfg = oc.SolverCfg()
+    _W = (oc, ci, fld, cfg, policy)
+
+
+def _cpu_task(idx):
+    """One sample through the oracle's per-sample path (the reference's
+    forward_pass + backward_sweep restated, GEMV per sample like odegrad)."""
+    oc, ci, fld, cfg, policy = _W
+    u0 = ci.u0[idx % ci.batch: idx % ci.batch + 1]
+    oc.grad_terminal(fld, ci.scheme, u0, ci.t0, ci.tF, ci.n_steps, policy, cfg=cfg)
+    return 1
+
+
+class CpuPool:
+    def __init__(self, cfg_name, policy):
+        import multiprocessing as mp
+        self.cores = len(os.sched_getaffinity(0))
+        ctx = mp.get_context("spawn")
+        env_threads = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS")}
+        os.environ["OMP_NUM_THREADS"] = "1"
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        self.pool = ctx.Pool(self.cores, initializer=_cpu_worker_init, initargs=(cfg_name, policy))
+        for k, v in env_threads.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        self.pool.map(_cpu_task, range(self.cores))          # warm every worker
+
+    def run(self, n_samples):
+        t0 = time.perf_counter()
+        done = sum(self.pool.map(_cpu_task, range(n_samples), chunksize=1))
+        return done, time.perf_counter() - t0
+
+    def rate_for(self, seconds):
+        """samples/s from a bounded sample of about ``seconds`` of CPU work."""
+        done, el = self.run(self.cores)
+        per = el / max(1, done // self.cores)
+        n = max(self.cores, int(seconds / max(per, 1e-6)) * self.cores)
+        done, el = self.run(n)
+        return done / el, done, el
+
+    def close(self):
+        self.pool.terminate()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2206_01298_b200.configs import make_config
+    ci = make_config(args.config, batch=1)
+    policy = args.policy or ci.policy
+    pool = CpuPool(args.config, policy)
+    per_step = pool.cores * 2
+    for _ in range(args.warmup):
+        pool.run(pool.cores)
+    times = []
+    total = 0
+    for _ in range(args.steps):
+        done, el = pool.run(per_step)
+        times.append(el)
+        total += done
+    pool.close()
+    value = total / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE shapes)",
+        "config": {"workload": WORKLOADS.get(args.config, args.config), "policy": policy,
+                   "samples_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": pool.cores, "kind": "port",
+                         "sample": f"{per_step} samples/step of {args.config} through the oracle's "
+                                   "per-sample restatement of odegrad forward_pass+backward_sweep, "
+                                   "one process per core"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- GPU side
+def fp_peak(dtype):
+    """Measured FP32/FP64 FMA-pipe peak (tools/peaks_probe.cu, run on this pool)
+    or the nominal B200 figure, with the source named."""
+    path = os.path.join(ROOT, "profiles", "fp_peaks.json")
+    key = "fp32_tflops" if dtype == "f32" else "fp64_tflops"
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d[key]), "measured (profiles/fp_peaks.json)"
+    except (OSError, KeyError, ValueError):
+        nominal = 148 * (128 if dtype == "f32" else 64) * 2 * 1.965e9 / 1e12
+        return nominal, "nominal 148 SM x FMA lanes x 2 x 1.965 GHz"
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2206_01298_b200 import CheckpointPolicy, FixedController, tableau_catalog, terminal_loss
+    from paper_2206_01298_b200.configs import make_config
+    from paper_2206_01298_b200.distributed import grad_sharded, shard_bounds
+    from paper_2206_01298_b200.engine import grad
+    from paper_2206_01298_b200.workloads import field_from_config, solver_from_config
+
+    base = make_config(args.config, batch=1)
+    per_gpu = {"C1": 512, "C2": 4096, "C5": 256}[args.config]
+    ci = make_config(args.config, batch=per_gpu * world)      # weak scaling: N x per-GPU batch
+    lo, hi = shard_bounds(ci.batch, world, rank)
+    policy = CheckpointPolicy.parse(args.policy or base.policy)
+    field = field_from_config(ci)
+    scheme = tableau_catalog(ci.scheme)
+    loss = terminal_loss("half_sqnorm", ci.tF)
+    ctrl = FixedController(ci.n_steps)
+    scfg = solver_from_config(ci)
+    tdt = field.torch_dtype
+    u0_dev = torch.as_tensor(ci.u0[lo:hi], dtype=tdt, device="cuda").contiguous()
+    u0_host = torch.as_tensor(ci.u0[lo:hi], dtype=tdt).pin_memory()
+
+    def step(u0):
+        if world > 1:
+            return grad_sharded(field, scheme, loss, u0, ci.t0, ci.tF, ctrl, policy, scfg,
+                                batch_global=ci.batch)
+        return grad(field, scheme, loss, u0, ci.t0, ci.tF, ctrl, policy, scfg)
+
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        res = step(u0_dev)
+    # ---- device-resident timing (value)
+    sampler = ClockSampler(local)
+    sampler.start()
+    ms, phases = [], {"ms_pack": 0.0, "ms_forward": 0.0, "ms_reverse": 0.0, "ms_reduce": 0.0}
+    launches = 0
+    stream = torch.cuda.current_stream()
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = step(u0_dev)
+        e1.record(stream)
+        barrier()
+        ms.append(e0.elapsed_time(e1))
+        for k in phases:
+            phases[k] += res.device[k]
+        launches += res.device["kernel_launches"]
+    clocks = sampler.stop()
+    ms_step = statistics.mean(ms)
+    # ---- end-to-end through the public API from pinned host memory
+    for _ in range(2):
+        step(u0_host)
+    e2e_s = []
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        t0 = time.perf_counter()
+        r = step(u0_host)
+        _ = (np.asarray(r.dtheta) if not isinstance(r.dtheta, torch.Tensor) else r.dtheta.cpu(),
+             r.loss)
+        e2e_s.append(time.perf_counter() - t0)
+    if world > 1:
+        t = torch.tensor([ms_step, statistics.mean(e2e_s)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, e2e_mean = float(t[0]), float(t[1])
+    else:
+        e2e_mean = statistics.mean(e2e_s)
+    value = ci.batch / (ms_step / 1e3)
+    e2e_value = ci.batch / e2e_mean
+    esz = 4 if ci.dtype == "f32" else 8
+    nloc = hi - lo
+    h2d = nloc * ci.widths[-1] * esz
+    d2h = 2 * nloc * ci.widths[-1] * esz + field.n_params * esz + 8
+
+    # ---- roofline of the dominant kernel (CUDA events around each launch, in-library)
+    dev = res.device
+    Pw = sum(ci.widths[l] * ci.widths[l + 1] for l in range(len(ci.widths) - 1))
+    s = scheme.stages
+    replays = dev["steps_recomputed"]
+    fwd_evals = dev["nfe_forward"] - replays * s
+    fwd_flops = nloc * fwd_evals * 2 * Pw
+    rev_flops = nloc * (replays * s * 2 * Pw + dev["device_vjp_evals"] * 4 * Pw)
+    K = args.steps
+    kern = {"forward": (phases["ms_forward"] / K, fwd_flops),
+            "reverse": (phases["ms_reverse"] / K, rev_flops)}
+    dom = max(kern, key=lambda k: kern[k][0])
+    dms, dfl = kern[dom]
+    peak, peak_src = fp_peak(ci.dtype)
+    achieved = dfl / (dms / 1e3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(f"{args.config}:{policy}:{dom}")
+    except (OSError, ValueError):
+        pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        pool = CpuPool(args.config, str(policy))
+        rate, done, el = pool.rate_for(args.cpu_seconds)
+        pool.close()
+        cpu = {"value": rate, "unit": "samples/s", "cores": pool.cores, "kind": "port",
+               "sample": f"{done} samples of {args.config} in {el:.1f}s through the oracle's "
+                         "per-sample restatement of odegrad forward_pass+backward_sweep, "
+                         "one process per core"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": ci.dtype, "data": "synthetic (seeded, BASELINE shapes)",
+            "config": {"workload": WORKLOADS.get(args.config, args.config),
+                       "global_batch": ci.batch, "batch_per_gpu": per_gpu,
+                       "scheme": ci.scheme, "n_steps": ci.n_steps, "policy": str(policy),
+                       "parallelism": f"dp{world}",
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "tile_rows": dev["tile_rows"], "tiles": dev["tiles"]},
+            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": {"bound": "compute", "pipe": f"{ci.dtype} FMA (SIMT)", "kernel": dom,
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_flops_per_launch": dfl, "ms_per_launch": dms,
+                         "phase_ms_per_step": {k: v / K for k, v in phases.items()}},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "counters": {k: dev[k] for k in ("nfe_forward", "nfe_backward", "steps_recomputed",
+                                             "max_live_slots", "device_vjp_evals")},
+            "loss": res.loss,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,173 @@
+/*
+ * odeblock.h -- C ABI of the B200-native discrete-adjoint ODE-block engine.
+ *
+ * Every entry point replaces one reference interface of the CPU package
+ * `odegrad` (/root/reference/pkg/src/odegrad; cited file:line below).  The
+ * reference is pure Python, so there is no reference FFI; these are the calls
+ * its `Field` protocol and `grad()` would bind through ctypes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "device" pointers are CUDA global memory
+ *    (owned by the caller, e.g. torch tensors); "host" pointers are CPU memory.
+ *  - Float arrays are float32 or float64 per the descriptor's dtype.
+ *  - Every function returns an ob_status; detail text via ob_last_error()
+ *    (thread-local).  Status codes map 1:1 onto the reference exception
+ *    classes (nn.py:29-34 ValueError, integrators.py:20-25 IntegrationError,
+ *    linalg.py:14-19 ConvergenceError, adjoint.py:33-34 GradientExplosionError).
+ *  - Calls are reentrant per stream; no allocation inside the hot loop: all
+ *    scratch lives in the caller's workspace (size from *_workspace_size).
+ *  - Inputs are never mutated (reference ownership rule).
+ */
+#ifndef ODEBLOCK_H
+#define ODEBLOCK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  OB_OK = 0,
+  OB_ERR_VALUE = 1,              /* ValueError: shape / non-finite input (nn.py:26-35)       */
+  OB_ERR_INTEGRATION = 2,        /* IntegrationError: state overflow (integrators.py:219-220) */
+  OB_ERR_STIFFNESS = 3,          /* StiffnessError (adaptive only; unused by fixed stepping)  */
+  OB_ERR_CONVERGENCE = 4,        /* ConvergenceError (linalg.py:101-142)                      */
+  OB_ERR_GRADIENT_EXPLOSION = 5, /* GradientExplosionError (adjoint.py:42-44)                 */
+  OB_ERR_CUDA = 6,               /* CUDA runtime failure / no device                          */
+  OB_ERR_UNSUPPORTED = 7         /* configuration outside this build                          */
+} ob_status;
+
+enum { OB_F32 = 0, OB_F64 = 1 };
+/* activation ids: nn.py:23 (identity/relu/tanh/gelu) + softplus (C4, new) */
+enum { OB_ACT_IDENTITY = 0, OB_ACT_RELU = 1, OB_ACT_TANH = 2, OB_ACT_GELU = 3, OB_ACT_SOFTPLUS = 4 };
+/* right-hand sides: MlpField (integrators.py:76-102); a*u + s*MLP(u) as a
+   CallableField (integrators.py:105-141, config C5); CNF and conv are new */
+enum { OB_FIELD_MLP = 0, OB_FIELD_STIFF = 1, OB_FIELD_CNF = 2, OB_FIELD_CONV = 3 };
+enum { OB_SCHEME_RK = 0, OB_SCHEME_THETA = 1 };
+/* CheckpointPolicy kinds (checkpointing.py:173-190) */
+enum { OB_POLICY_STORE_ALL = 0, OB_POLICY_STORE_SOLUTIONS = 1, OB_POLICY_REVOLVE = 2 };
+/* terminal losses: 0.5*mean||u||^2 (BASELINE C1/C2/C5), per-sample MSE vs
+   targets (losses.py:78-107, K=1), CE head (C3), CNF NLL (C4) */
+enum { OB_LOSS_HALF_SQNORM = 0, OB_LOSS_MSE = 1, OB_LOSS_CE_HEAD = 2, OB_LOSS_CNF_NLL = 3 };
+/* revolve action kinds (checkpointing.py:70-80) */
+enum { OB_ACT_ADVANCE = 0, OB_ACT_STORE = 1, OB_ACT_RESTORE = 2, OB_ACT_REVERSE = 3 };
+
+#define OB_MAX_LAYERS 8
+#define OB_MAX_STAGES 8
+
+/* Vector field descriptor (MlpSpec, nn.py:38-76). widths[0..n_layers]. */
+typedef struct {
+  int32_t kind;        /* OB_FIELD_* */
+  int32_t dtype;       /* OB_F32 | OB_F64 */
+  int32_t n_layers;
+  int32_t widths[OB_MAX_LAYERS + 1];
+  int32_t activation;  /* OB_ACT_* for hidden layers; output layer is linear */
+  int32_t time_input;  /* 1: time appended as the last input (nn.py:126-129) */
+  double out_scale;    /* OB_FIELD_STIFF: s in a*u + s*MLP(u) */
+  int64_t n_params;    /* sum_l w_{l+1}*w_l + w_{l+1} (nn.py:60-63) */
+} ob_field_desc;
+
+/* Scheme (tableaux.py:14-56): explicit Butcher tableau or theta method. */
+typedef struct {
+  int32_t kind;        /* OB_SCHEME_RK | OB_SCHEME_THETA */
+  int32_t stages;
+  int32_t fsal;
+  int32_t _pad;
+  double theta;        /* theta methods: 1 = beuler, 0.5 = cn */
+  double a[OB_MAX_STAGES * OB_MAX_STAGES];  /* row-major s x s */
+  double b[OB_MAX_STAGES];
+  double c[OB_MAX_STAGES];
+} ob_scheme_desc;
+
+/* SolverConfig (linalg.py:22-34). */
+typedef struct {
+  double newton_tol;
+  double gmres_tol;
+  int32_t newton_maxit;
+  int32_t gmres_maxit;
+  int32_t gmres_restart;
+  int32_t _pad;
+} ob_solver_cfg;
+
+/* One gradient problem: grad(field, scheme, loss, u0, t0, tF, ctrl, policy,
+   solver_cfg) of adjoint.py:256-279, batched over `batch` samples. */
+typedef struct {
+  ob_field_desc field;
+  ob_scheme_desc scheme;
+  ob_solver_cfg solver;
+  int64_t batch;          /* samples handled by this call (this rank's shard)   */
+  int64_t batch_global;   /* samples across all ranks: loss = sum / batch_global */
+  int32_t n_steps;        /* FixedController / FixedGridController step count   */
+  int32_t policy;         /* OB_POLICY_*                                          */
+  int32_t nc;             /* revolve slots                                         */
+  int32_t loss;           /* OB_LOSS_*                                             */
+  const double* times;    /* HOST array, n_steps+1 boundary times (integrators.py:276) */
+} ob_problem;
+
+/* Device buffers of one gradient call. */
+typedef struct {
+  const void* theta;      /* [n_params]                                          */
+  const void* aux;        /* STIFF: diag a [N]; CNF: probes eps [B,N]; else NULL */
+  const void* u0;         /* [B, N]                                              */
+  const void* targets;    /* OB_LOSS_MSE: [B, N]; else NULL                       */
+  void* u_final;          /* out [B, N]                                          */
+  void* du0;              /* out [B, N]     (lambda_0)                           */
+  void* dtheta;           /* out [n_params] (mu_0, summed over this call's batch) */
+  double* loss;           /* out [1] float64: this call's sum of per-sample loss / batch_global */
+  void* workspace;        /* scratch, >= ob_grad_workspace_size bytes            */
+  size_t workspace_bytes;
+  int32_t* sample_stats;  /* optional out [B, OB_NSTATS] per-sample counters, or NULL */
+} ob_buffers;
+
+/* per-sample stats columns (implicit schemes; explicit: fixed by the schedule) */
+enum { OB_STAT_NFE_F = 0, OB_STAT_NFE_B = 1, OB_STAT_NEWTON = 2, OB_STAT_GMRES_F = 3,
+       OB_STAT_GMRES_B = 4, OB_NSTATS = 5 };
+
+/* NfeCounters (integrators.py:28-50) + StoreCounters (checkpointing.py:193-198),
+   reference semantics per sample trajectory, plus what the device really ran. */
+typedef struct {
+  int64_t nfe_forward, nfe_backward, steps_accepted, steps_rejected, steps_recomputed;
+  int64_t stored_states, stored_stage_vectors, max_live_slots, recomputed_steps;
+  int64_t kernel_launches;       /* kernels this call launched                          */
+  int64_t device_rhs_evals;      /* RHS evaluations the device executed (per sample)    */
+  int64_t device_vjp_evals;      /* VJP pairs the device executed (zero cotangents skipped) */
+  int64_t tile_rows;             /* samples per CTA tile                                 */
+  int64_t tiles;                 /* CTAs per persistent launch                           */
+  double ms_pack, ms_forward, ms_reverse, ms_reduce;  /* CUDA-event device times of this call */
+} ob_counters;
+
+/* ---- library ----------------------------------------------------------- */
+const char* ob_version(void);
+const char* ob_last_error(void);
+int ob_device_count(int32_t* count);
+
+/* ---- host-only schedule math (checkpointing.py:32-170) ------------------- */
+int ob_revolve_count(int32_t nt, int32_t nc, int64_t* out);
+/* actions: capacity x 4 int32 (kind, step, start, stop) as in ScheduleAction */
+int ob_revolve_schedule(int32_t nt, int32_t nc, int32_t* actions, int64_t capacity,
+                        int64_t* n_actions);
+
+/* ---- block gradient: forward integration + checkpoints + discrete adjoint --
+   replaces grad() (adjoint.py:256-279) = forward_pass (:151-210) +
+   loss_and_grad_seed (losses.py:78-107) + backward_sweep (:235-253). */
+int ob_grad_workspace_size(const ob_problem* p, size_t* bytes);
+int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream);
+
+/* ---- the Field protocol, batched (integrators.py:53-102) -----------------
+   eval: f(u,t); jvp: (df/du) w; vjp: ((df/du)^T v, sum_b (df/dtheta)^T v);
+   vjp_u: (df/du)^T v.  t is one time for the whole batch; aux as in ob_buffers. */
+int ob_field_eval(const ob_field_desc* f, int64_t batch, const void* theta, const void* aux,
+                  const void* u, double t, void* out, void* stream);
+int ob_field_jvp(const ob_field_desc* f, int64_t batch, const void* theta, const void* aux,
+                 const void* u, double t, const void* w, void* out, void* stream);
+int ob_field_vjp(const ob_field_desc* f, int64_t batch, const void* theta, const void* aux,
+                 const void* u, double t, const void* v, void* jtv, void* ptv, void* stream);
+int ob_field_vjp_u(const ob_field_desc* f, int64_t batch, const void* theta, const void* aux,
+                   const void* u, double t, const void* v, void* jtv, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ODEBLOCK_H */

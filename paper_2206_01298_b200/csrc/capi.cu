@@ -1,0 +1,613 @@
+// capi.cu -- the C ABI (include/odeblock.h) and the host engine behind it.
+//
+// The engine plans one gradient call (tile size, shared-memory layout,
+// checkpoint buffers, the reverse program compiled from the checkpoint policy,
+// reference-semantics counters), carves the caller's workspace, uploads one
+// small control blob and launches: pack_weights -> forward (persistent) ->
+// reverse (persistent) -> fixed-order tile reduction.  No allocation, no host
+// round trip inside the integration; one stream synchronisation at the end to
+// surface the reference's exceptions as status codes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/odeblock.h"
+#include "revolve.h"
+#include "rk.cuh"
+
+namespace ob {
+template <typename T> cudaError_t launch_pack(const PackParams<T>&, cudaStream_t);
+template <typename T> cudaError_t launch_rk(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
+template <typename T> cudaError_t launch_reduce(const T*, int, long long, T*, const double*, double,
+                                                double*, cudaStream_t);
+template <typename T> cudaError_t launch_field_op(const RkParams<T>&, int, int, size_t, int, double,
+                                                  const T*, const T*, T*, cudaStream_t);
+}  // namespace ob
+
+using namespace ob;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(OB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+static int pad4i(int n) { return (n + 3) & ~3; }
+
+extern "C" const char* ob_version(void) { return "odeblock-b200 0.1.0 (sm_100a)"; }
+extern "C" const char* ob_last_error(void) { return g_err.c_str(); }
+
+extern "C" int ob_device_count(int32_t* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    cudaGetLastError();
+    return fail(OB_ERR_CUDA, cudaGetErrorString(e));
+  }
+  *count = n;
+  return OB_OK;
+}
+
+extern "C" int ob_revolve_count(int32_t nt, int32_t nc, int64_t* out) {
+  if (nt < 1 || nc < 1) return fail(OB_ERR_VALUE, "need nt >= 1 and nc >= 1");
+  *out = ob::revolve_count(nt, nc);
+  return OB_OK;
+}
+
+extern "C" int ob_revolve_schedule(int32_t nt, int32_t nc, int32_t* actions, int64_t capacity,
+                                   int64_t* n_actions) {
+  if (nt < 1 || nc < 1) return fail(OB_ERR_VALUE, "need nt >= 1 and nc >= 1");
+  auto acts = ob::revolve_schedule(nt, nc);
+  *n_actions = (int64_t)acts.size();
+  if (actions == nullptr) return OB_OK;
+  if ((int64_t)acts.size() > capacity) return fail(OB_ERR_VALUE, "action buffer too small");
+  for (size_t i = 0; i < acts.size(); ++i) {
+    actions[4 * i + 0] = acts[i].kind;
+    actions[4 * i + 1] = acts[i].step;
+    actions[4 * i + 2] = acts[i].start;
+    actions[4 * i + 3] = acts[i].stop;
+  }
+  return OB_OK;
+}
+
+// ===================================================================== plan
+namespace {
+
+struct Plan {
+  int dtype = 0;
+  size_t esz = 8;
+  Dims d{};
+  int R = 1, Rp = 1, RB = 1, tiles = 1;
+  SmemLayout sm{};
+  size_t smem_bytes = 0;
+  // checkpoint program
+  int nbuf = 0, nsol = 0;
+  std::vector<int> fwd_rec, fwd_sol;
+  std::vector<int4> prog;
+  unsigned skip_vjp = 0;
+  ob_counters cnt{};
+  // workspace layout (byte offsets)
+  size_t o_ts = 0, o_fr = 0, o_fs = 0, o_pg = 0, o_stat = 0;
+  size_t off_blob = 0, blob_bytes = 0, off_w = 0, off_rec = 0, off_sol = 0, off_scr = 0,
+         off_mu = 0, off_lp = 0, total = 0;
+  long long w_elems[OB_MAX_LAYERS][2]{};
+  long long scratch_stride = 0;
+};
+
+constexpr size_t kSmemLimit = 227 * 1024;
+
+int check_field(const ob_field_desc& f) {
+  if (f.dtype != OB_F32 && f.dtype != OB_F64) return fail(OB_ERR_VALUE, "dtype must be f32 or f64");
+  if (f.n_layers < 1 || f.n_layers > OB_MAX_LAYERS)
+    return fail(OB_ERR_VALUE, "n_layers must be in [1, 8]");
+  for (int l = 0; l <= f.n_layers; ++l)
+    if (f.widths[l] <= 0) return fail(OB_ERR_VALUE, "layer widths must be positive");
+  const int N = f.widths[f.n_layers];
+  if (f.widths[0] != N + (f.time_input ? 1 : 0))  // MlpSpec.__post_init__ (nn.py:53-58)
+    return fail(OB_ERR_VALUE, "input width inconsistent with state dim and time_input");
+  if (f.activation < 0 || f.activation > OB_ACT_SOFTPLUS) return fail(OB_ERR_VALUE, "unknown activation");
+  if (f.kind != OB_FIELD_MLP && f.kind != OB_FIELD_STIFF)
+    return fail(OB_ERR_UNSUPPORTED, "field kind not built into this library version");
+  if (f.kind == OB_FIELD_STIFF && f.time_input) return fail(OB_ERR_VALUE, "stiff field is autonomous");
+  long long np = 0;
+  for (int l = 0; l < f.n_layers; ++l) np += (long long)f.widths[l + 1] * f.widths[l] + f.widths[l + 1];
+  if (np != f.n_params) return fail(OB_ERR_VALUE, "n_params does not match widths");
+  return OB_OK;
+}
+
+void make_dims(const ob_field_desc& f, Dims& d) {
+  d.L = f.n_layers;
+  d.maxwp = 0;
+  long long off = 0;
+  for (int l = 0; l <= d.L; ++l) {
+    d.w[l] = f.widths[l];
+    d.wp[l] = pad4i(f.widths[l]);
+    d.maxwp = std::max(d.maxwp, d.wp[l]);
+  }
+  for (int l = 0; l < d.L; ++l) {
+    d.woff[l] = off;
+    d.boff[l] = off + (long long)d.w[l + 1] * d.w[l];
+    off = d.boff[l] + d.w[l + 1];
+  }
+  d.N = d.w[d.L];
+  d.Np = d.wp[d.L];
+  d.act = f.activation;
+  d.time_input = f.time_input;
+}
+
+void layout_smem(Plan& P) {
+  const Dims& d = P.d;
+  SmemLayout& s = P.sm;
+  int o = 0;
+  auto take = [&](int n) { int r = o; o += (n + 7) & ~7; return r; };  // 32-byte aligned
+  s.x0 = take(P.Rp * d.wp[0]);
+  for (int l = 0; l < d.L; ++l) {
+    s.pre[l] = take(P.Rp * d.wp[l + 1]);
+    s.hid[l] = l < d.L - 1 ? take(P.Rp * d.wp[l + 1]) : 0;
+  }
+  s.dA = take(P.Rp * d.maxwp);
+  s.dB = take(P.Rp * d.maxwp);
+  s.u = take(P.Rp * d.Np);
+  s.lam = take(P.Rp * d.Np);
+  s.lamn = take(P.Rp * d.Np);
+  s.w = take(P.Rp * d.Np);
+  s.jtv = take(P.Rp * d.Np);
+  s.out = 0;
+  s.total = o;
+  P.smem_bytes = (size_t)o * P.esz;
+}
+
+int pick_rb(int R) {
+  if (R >= 16 && R % 8 == 0) return 8;
+  if (R >= 4) return 4;
+  if (R >= 2) return 2;
+  return 1;
+}
+
+void choose_tiles(Plan& P, long long B, int sm_count) {
+  int R = (int)std::max<long long>(1, (B + sm_count - 1) / sm_count);
+  for (;;) {
+    P.R = R;
+    P.RB = pick_rb(R);
+    P.Rp = (R + P.RB - 1) / P.RB * P.RB;
+    layout_smem(P);
+    if (P.smem_bytes <= kSmemLimit || R == 1) break;
+    R = std::max(1, R * 3 / 4);
+  }
+  P.tiles = (int)((B + P.R - 1) / P.R);
+}
+
+// compile the checkpoint policy into forward store directives + a reverse
+// program (checkpointing.py:242-340), with reference-semantics counters.
+int compile_policy(const ob_problem& p, Plan& P) {
+  const int nt = p.n_steps, s = p.scheme.stages;
+  P.fwd_rec.assign(nt, -1);
+  P.fwd_sol.assign(nt, -1);
+  P.prog.clear();
+  ob_counters& c = P.cnt;
+  auto replay = [&](int n, int src_kind, int src, int dst) {
+    P.prog.push_back(make_int4(kOpReplay, n, (src_kind << 24) | src, dst));
+    c.steps_recomputed += 1;
+    c.recomputed_steps += 1;
+  };
+  auto reverse = [&](int n, int buf) { P.prog.push_back(make_int4(kOpReverse, n, 0, buf)); };
+
+  if (p.policy == OB_POLICY_STORE_ALL) {
+    P.nbuf = nt;
+    for (int n = 0; n < nt; ++n) P.fwd_rec[n] = n;
+    for (int n = nt - 1; n >= 0; --n) reverse(n, n);
+    c.stored_states = nt - 1;
+    c.stored_stage_vectors = (long long)(nt - 1) * s;
+    c.max_live_slots = nt - 1;
+  } else if (p.policy == OB_POLICY_STORE_SOLUTIONS) {
+    P.nbuf = 1;
+    P.nsol = std::max(nt - 1, 0);
+    for (int n = 0; n < nt - 1; ++n) P.fwd_sol[n] = n;
+    P.fwd_rec[nt - 1] = 0;
+    reverse(nt - 1, 0);
+    for (int n = nt - 2; n >= 0; --n) {
+      replay(n, kSrcSol, n, 0);
+      reverse(n, 0);
+    }
+    c.stored_states = nt - 1;
+    c.max_live_slots = nt - 1;
+  } else if (p.policy == OB_POLICY_REVOLVE) {
+    if (p.nc < 1) return fail(OB_ERR_VALUE, "revolve requires nc >= 1");
+    auto acts = ob::revolve_schedule(nt, p.nc);
+    size_t first = 0;
+    while (acts[first].kind != kReverse) ++first;
+    // physical record buffers with reference counts (slots + the record in hand)
+    std::vector<int> refc;
+    auto alloc = [&]() {
+      for (size_t i = 0; i < refc.size(); ++i)
+        if (refc[i] == 0) { refc[i] = 1; return (int)i; }
+      refc.push_back(1);
+      return (int)refc.size() - 1;
+    };
+    std::map<int, int> slot;  // step -> buffer
+    int live_peak = 0;
+    for (size_t i = 0; i < first; ++i)
+      if (acts[i].kind == kStore) {
+        const int b = alloc();
+        slot[acts[i].step] = b;
+        P.fwd_rec[acts[i].step] = b;
+        c.stored_states += 1;
+        c.stored_stage_vectors += s;
+        live_peak = std::max(live_peak, (int)slot.size());
+      }
+    int hand = -1, hand_step = nt - 1;
+    if (P.fwd_rec[nt - 1] >= 0) { hand = P.fwd_rec[nt - 1]; refc[hand] += 1; }
+    else { hand = alloc(); P.fwd_rec[nt - 1] = hand; }
+    int src_kind = kSrcRecNext, src = hand;  // executor position after the forward sweep
+    auto drop_hand = [&]() { if (hand >= 0) { refc[hand] -= 1; hand = -1; hand_step = -2; } };
+    for (size_t i = first; i < acts.size(); ++i) {
+      const Action& a = acts[i];
+      if (a.kind == kRestore) {
+        if (a.step == -1) { src_kind = kSrcU0; src = 0; }
+        else { src_kind = kSrcRecNext; src = slot.at(a.step); }
+        drop_hand();
+      } else if (a.kind == kAdvance) {
+        for (int n = a.start; n < a.stop; ++n) {
+          int dst;
+          if (hand >= 0 && refc[hand] == 1) dst = hand;  // only the hand holds it: reuse
+          else { drop_hand(); dst = alloc(); }
+          hand = dst;
+          replay(n, src_kind, src, dst);
+          hand_step = n;
+          src_kind = kSrcRecNext;
+          src = dst;
+        }
+      } else if (a.kind == kStore) {
+        if (hand < 0 || hand_step != a.step) return fail(OB_ERR_VALUE, "schedule bug: no record in hand");
+        slot[a.step] = hand;
+        refc[hand] += 1;
+        live_peak = std::max(live_peak, (int)slot.size());
+      } else {  // reverse
+        int buf;
+        if (hand >= 0 && hand_step == a.step) buf = hand;
+        else {
+          auto it = slot.find(a.step);
+          if (it == slot.end()) return fail(OB_ERR_VALUE, "schedule bug: record unavailable");
+          buf = it->second;
+          refc[buf] -= 1;
+          slot.erase(it);
+          // the buffer stays readable for this op; it can only be reused by a later replay
+        }
+        reverse(a.step, buf);
+      }
+    }
+    P.nbuf = (int)refc.size();
+    c.max_live_slots = live_peak;
+  } else {
+    return fail(OB_ERR_VALUE, "unknown checkpoint policy");
+  }
+  return OB_OK;
+}
+
+int plan_problem(const ob_problem& p, Plan& P) {
+  int st = check_field(p.field);
+  if (st) return st;
+  if (p.scheme.kind != OB_SCHEME_RK)
+    return fail(OB_ERR_UNSUPPORTED, "theta schemes are not built into this library version");
+  if (p.scheme.stages < 1 || p.scheme.stages > OB_MAX_STAGES) return fail(OB_ERR_VALUE, "bad stage count");
+  if (p.n_steps < 1) return fail(OB_ERR_VALUE, "fixed mode requires at least one step");
+  if (p.batch < 1) return fail(OB_ERR_VALUE, "batch must be >= 1");
+  if (!p.times) return fail(OB_ERR_VALUE, "times array is required");
+  for (int i = 0; i < p.n_steps; ++i)
+    if (!(p.times[i + 1] > p.times[i])) return fail(OB_ERR_VALUE, "step size must be positive");
+  if (p.loss != OB_LOSS_HALF_SQNORM && p.loss != OB_LOSS_MSE)
+    return fail(OB_ERR_UNSUPPORTED, "loss kind not supported for this field");
+  P.dtype = p.field.dtype;
+  P.esz = P.dtype == OB_F32 ? 4 : 8;
+  make_dims(p.field, P.d);
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  } else {
+    cudaGetLastError();
+  }
+  choose_tiles(P, p.batch, sms);
+  if (P.smem_bytes > kSmemLimit) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
+  st = compile_policy(p, P);
+  if (st) return st;
+  // zero-cotangent stages: b_i == 0 and a_ji == 0 for all j > i  (dopri5 stage 7)
+  const int s = p.scheme.stages;
+  P.skip_vjp = 0;
+  for (int i = 0; i < s; ++i) {
+    bool zero = p.scheme.b[i] == 0.0;
+    for (int j = i + 1; j < s && zero; ++j) zero = p.scheme.a[j * OB_MAX_STAGES + i] == 0.0;
+    if (zero) P.skip_vjp |= 1u << i;
+  }
+  // reference-semantics NFE counters, per trajectory (integrators.py:83-102)
+  ob_counters& c = P.cnt;
+  const long long nt = p.n_steps;
+  c.nfe_forward = s * nt - (p.scheme.fsal ? nt - 1 : 0) + c.steps_recomputed * s;
+  c.nfe_backward = s * nt;
+  c.steps_accepted = nt;
+  c.device_rhs_evals = c.nfe_forward;
+  c.device_vjp_evals = (s - __builtin_popcount(P.skip_vjp)) * nt;
+  c.tile_rows = P.R;
+  c.tiles = P.tiles;
+  c.kernel_launches = 4;
+  // workspace
+  const long long B = p.batch, N = P.d.N;
+  size_t o = 0;
+  P.off_blob = o;
+  P.o_ts = 0;
+  P.o_fr = P.o_ts + sizeof(double) * (nt + 1);
+  P.o_fs = P.o_fr + sizeof(int) * nt;
+  P.o_pg = align_up(P.o_fs + sizeof(int) * nt, 16);
+  P.o_stat = P.o_pg + sizeof(int4) * P.prog.size();
+  P.blob_bytes = P.o_stat + sizeof(int) * 4;
+  o = align_up(o + P.blob_bytes, 256);
+  P.off_w = o;
+  for (int l = 0; l < P.d.L; ++l) {
+    P.w_elems[l][0] = (long long)P.d.wp[l] * P.d.w[l + 1];
+    P.w_elems[l][1] = (long long)P.d.wp[l + 1] * P.d.w[l];
+    o = align_up(o + P.esz * P.w_elems[l][0], 256);
+    o = align_up(o + P.esz * P.w_elems[l][1], 256);
+  }
+  P.off_rec = o;
+  o = align_up(o + P.esz * (size_t)P.nbuf * (s + 1) * B * N, 256);
+  P.off_sol = o;
+  o = align_up(o + P.esz * (size_t)P.nsol * B * N, 256);
+  P.off_scr = o;
+  P.scratch_stride = 2LL * s * P.Rp * P.d.Np;
+  o = align_up(o + P.esz * (size_t)P.tiles * P.scratch_stride, 256);
+  P.off_mu = o;
+  o = align_up(o + P.esz * (size_t)P.tiles * p.field.n_params, 256);
+  P.off_lp = o;
+  o = align_up(o + sizeof(double) * P.tiles, 256);
+  P.total = o;
+  return OB_OK;
+}
+
+template <typename T>
+int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st) {
+  char* ws = static_cast<char*>(b.workspace);
+  const int nt = p.n_steps, s = p.scheme.stages;
+  // ---- control blob: ts | fwd_rec | fwd_sol | prog | status
+  std::vector<char> blob(P.blob_bytes, 0);
+  std::memcpy(blob.data() + P.o_ts, p.times, sizeof(double) * (nt + 1));
+  std::memcpy(blob.data() + P.o_fr, P.fwd_rec.data(), sizeof(int) * nt);
+  std::memcpy(blob.data() + P.o_fs, P.fwd_sol.data(), sizeof(int) * nt);
+  if (!P.prog.empty()) std::memcpy(blob.data() + P.o_pg, P.prog.data(), sizeof(int4) * P.prog.size());
+  const size_t o_ts = P.o_ts, o_fr = P.o_fr, o_fs = P.o_fs, o_pg = P.o_pg, o_stat = P.o_stat;
+  CU(cudaMemcpyAsync(ws + P.off_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
+
+  RkParams<T> rp{};
+  rp.d = P.d;
+  rp.sm = P.sm;
+  PackParams<T> pp{};
+  pp.d = P.d;
+  pp.theta = static_cast<const T*>(b.theta);
+  size_t wo = P.off_w;
+  for (int l = 0; l < P.d.L; ++l) {
+    pp.wt[l] = reinterpret_cast<T*>(ws + wo);
+    wo = align_up(wo + P.esz * P.w_elems[l][0], 256);
+    pp.wn[l] = reinterpret_cast<T*>(ws + wo);
+    wo = align_up(wo + P.esz * P.w_elems[l][1], 256);
+    rp.W.wt[l] = pp.wt[l];
+    rp.W.wn[l] = pp.wn[l];
+    rp.W.bias[l] = pp.theta + P.d.boff[l];
+  }
+  rp.s = s;
+  rp.fsal = p.scheme.fsal;
+  std::memcpy(rp.a, p.scheme.a, sizeof(rp.a));
+  std::memcpy(rp.b, p.scheme.b, sizeof(rp.b));
+  std::memcpy(rp.c, p.scheme.c, sizeof(rp.c));
+  rp.skip_vjp = P.skip_vjp;
+  rp.field_kind = p.field.kind;
+  rp.diag = static_cast<const T*>(b.aux);
+  rp.out_scale = T(p.field.out_scale);
+  rp.B = (int)p.batch;
+  rp.R = P.R;
+  rp.Rp = P.Rp;
+  rp.n_steps = nt;
+  rp.ts = reinterpret_cast<const double*>(ws + P.off_blob + o_ts);
+  rp.loss_kind = p.loss;
+  rp.targets = static_cast<const T*>(b.targets);
+  rp.batch_global = double(p.batch_global > 0 ? p.batch_global : p.batch);
+  rp.inv_batch_global = 1.0 / rp.batch_global;
+  rp.u0 = static_cast<const T*>(b.u0);
+  rp.u_final = static_cast<T*>(b.u_final);
+  rp.du0 = static_cast<T*>(b.du0);
+  rp.rec = reinterpret_cast<T*>(ws + P.off_rec);
+  rp.sol = reinterpret_cast<T*>(ws + P.off_sol);
+  rp.fwd_rec = reinterpret_cast<const int*>(ws + P.off_blob + o_fr);
+  rp.fwd_sol = reinterpret_cast<const int*>(ws + P.off_blob + o_fs);
+  rp.prog = reinterpret_cast<const int4*>(ws + P.off_blob + o_pg);
+  rp.prog_len = (int)P.prog.size();
+  rp.scratch = reinterpret_cast<T*>(ws + P.off_scr);
+  rp.scratch_stride = P.scratch_stride;
+  rp.mu = reinterpret_cast<T*>(ws + P.off_mu);
+  rp.n_params = p.field.n_params;
+  rp.loss_part = reinterpret_cast<double*>(ws + P.off_lp);
+  int* status = reinterpret_cast<int*>(ws + P.off_blob + o_stat);
+  rp.status = status;
+
+  // per-phase CUDA events on the launch stream (bench roofline timing)
+  static thread_local cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (!ev[0])
+    for (auto& e : ev) CU(cudaEventCreate(&e));
+  CU(cudaMemsetAsync(rp.mu, 0, P.esz * (size_t)P.tiles * p.field.n_params, st));
+  CU(cudaEventRecord(ev[0], st));
+  CU(launch_pack<T>(pp, st));
+  CU(cudaEventRecord(ev[1], st));
+  CU(launch_rk<T>(rp, P.RB, P.tiles, P.smem_bytes, st, true));
+  CU(cudaEventRecord(ev[2], st));
+  CU(launch_rk<T>(rp, P.RB, P.tiles, P.smem_bytes, st, false));
+  CU(cudaEventRecord(ev[3], st));
+  CU(launch_reduce<T>(rp.mu, P.tiles, p.field.n_params, static_cast<T*>(b.dtheta), rp.loss_part,
+                      rp.inv_batch_global, b.loss, st));
+  CU(cudaEventRecord(ev[4], st));
+  int hs[2] = {0, 0};
+  CU(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  float ms[4] = {0, 0, 0, 0};
+  for (int i = 0; i < 4; ++i) CU(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+  P.cnt.ms_pack = ms[0];
+  P.cnt.ms_forward = ms[1];
+  P.cnt.ms_reverse = ms[2];
+  P.cnt.ms_reduce = ms[3];
+  if (hs[0] != 0) {
+    char msg[256];
+    if (hs[0] == OB_ERR_INTEGRATION) {
+      const double t = p.times[hs[1]], h = p.times[hs[1] + 1] - p.times[hs[1]];
+      snprintf(msg, sizeof msg, "state overflowed at t=%.17g (h=%.17g)", t, h);
+    } else if (hs[0] == OB_ERR_GRADIENT_EXPLOSION) {
+      snprintf(msg, sizeof msg, "non-finite adjoint state in reverse sweep (step %d)", hs[1]);
+    } else if (hs[0] == OB_ERR_VALUE) {
+      snprintf(msg, sizeof msg, "vector contains non-finite entries");
+    } else {
+      snprintf(msg, sizeof msg, "device status %d (%d)", hs[0], hs[1]);
+    }
+    return fail(hs[0], msg);
+  }
+  return OB_OK;
+}
+
+}  // namespace
+
+extern "C" int ob_grad_workspace_size(const ob_problem* p, size_t* bytes) {
+  if (!p || !bytes) return fail(OB_ERR_VALUE, "null argument");
+  Plan P;
+  int st = plan_problem(*p, P);
+  if (st) return st;
+  *bytes = P.total;
+  return OB_OK;
+}
+
+extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream) {
+  if (!p || !b) return fail(OB_ERR_VALUE, "null argument");
+  Plan P;
+  int st = plan_problem(*p, P);
+  if (st) return st;
+  if (!b->workspace || b->workspace_bytes < P.total)
+    return fail(OB_ERR_VALUE, "workspace too small (need " + std::to_string(P.total) + " bytes)");
+  if (!b->theta || !b->u0 || !b->u_final || !b->du0 || !b->dtheta || !b->loss)
+    return fail(OB_ERR_VALUE, "null device buffer");
+  if (p->field.kind == OB_FIELD_STIFF && !b->aux) return fail(OB_ERR_VALUE, "stiff field needs diag");
+  if (p->loss == OB_LOSS_MSE && !b->targets) return fail(OB_ERR_VALUE, "mse loss needs targets");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = P.dtype == OB_F32 ? run_grad<float>(*p, *b, P, s) : run_grad<double>(*p, *b, P, s);
+  if (out) *out = P.cnt;
+  return st;
+}
+
+// ============================================================ field ops
+namespace {
+
+enum { kEval = 0, kJvp = 1, kVjp = 2, kVjpU = 3 };
+
+template <typename T>
+int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const void* aux,
+                 const void* u, double t, const void* w, void* out, void* ptv, int mode,
+                 cudaStream_t st) {
+  Plan P;
+  P.dtype = f.dtype;
+  P.esz = sizeof(T);
+  make_dims(f, P.d);
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  choose_tiles(P, batch, sms);
+  if (P.smem_bytes > kSmemLimit) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
+  size_t wbytes = 0;
+  for (int l = 0; l < P.d.L; ++l) {
+    P.w_elems[l][0] = (long long)P.d.wp[l] * P.d.w[l + 1];
+    P.w_elems[l][1] = (long long)P.d.wp[l + 1] * P.d.w[l];
+    wbytes = align_up(wbytes + P.esz * P.w_elems[l][0], 256);
+    wbytes = align_up(wbytes + P.esz * P.w_elems[l][1], 256);
+  }
+  const size_t mu_bytes = mode == kVjp ? P.esz * (size_t)P.tiles * f.n_params : 0;
+  char* ws = nullptr;
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes + mu_bytes + 256, st));
+  RkParams<T> rp{};
+  rp.d = P.d;
+  rp.sm = P.sm;
+  PackParams<T> pp{};
+  pp.d = P.d;
+  pp.theta = static_cast<const T*>(theta);
+  size_t wo = 0;
+  for (int l = 0; l < P.d.L; ++l) {
+    pp.wt[l] = reinterpret_cast<T*>(ws + wo);
+    wo = align_up(wo + P.esz * P.w_elems[l][0], 256);
+    pp.wn[l] = reinterpret_cast<T*>(ws + wo);
+    wo = align_up(wo + P.esz * P.w_elems[l][1], 256);
+    rp.W.wt[l] = pp.wt[l];
+    rp.W.wn[l] = pp.wn[l];
+    rp.W.bias[l] = pp.theta + P.d.boff[l];
+  }
+  rp.field_kind = f.kind;
+  rp.diag = static_cast<const T*>(aux);
+  rp.out_scale = T(f.out_scale);
+  rp.B = (int)batch;
+  rp.R = P.R;
+  rp.Rp = P.Rp;
+  rp.n_params = f.n_params;
+  rp.mu = mode == kVjp ? reinterpret_cast<T*>(ws + wbytes) : nullptr;
+  int rc = OB_OK;
+  cudaError_t e = cudaSuccess;
+  if (mu_bytes) e = cudaMemsetAsync(rp.mu, 0, mu_bytes, st);
+  if (e == cudaSuccess) e = launch_pack<T>(pp, st);
+  if (e == cudaSuccess)
+    e = launch_field_op<T>(rp, P.RB, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
+                           static_cast<const T*>(w), static_cast<T*>(out), st);
+  if (e == cudaSuccess && mode == kVjp)
+    e = launch_reduce<T>(rp.mu, P.tiles, f.n_params, static_cast<T*>(ptv), nullptr, 0.0, nullptr, st);
+  cudaFreeAsync(ws, st);
+  if (e != cudaSuccess) rc = fail(OB_ERR_CUDA, cudaGetErrorString(e));
+  return rc;
+}
+
+int field_op(const ob_field_desc* f, int64_t batch, const void* theta, const void* aux,
+             const void* u, double t, const void* w, void* out, void* ptv, int mode, void* stream) {
+  if (!f || !theta || !u || !out) return fail(OB_ERR_VALUE, "null argument");
+  int st = check_field(*f);
+  if (st) return st;
+  if (batch < 1) return fail(OB_ERR_VALUE, "batch must be >= 1");
+  if ((mode != kEval) && !w) return fail(OB_ERR_VALUE, "null tangent/cotangent");
+  if (mode == kVjp && !ptv) return fail(OB_ERR_VALUE, "null ptv");
+  if (f->kind == OB_FIELD_STIFF && !aux) return fail(OB_ERR_VALUE, "stiff field needs diag");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return f->dtype == OB_F32 ? run_field_op<float>(*f, batch, theta, aux, u, t, w, out, ptv, mode, s)
+                            : run_field_op<double>(*f, batch, theta, aux, u, t, w, out, ptv, mode, s);
+}
+
+}  // namespace
+
+extern "C" int ob_field_eval(const ob_field_desc* f, int64_t batch, const void* theta,
+                             const void* aux, const void* u, double t, void* out, void* stream) {
+  return field_op(f, batch, theta, aux, u, t, nullptr, out, nullptr, kEval, stream);
+}
+extern "C" int ob_field_jvp(const ob_field_desc* f, int64_t batch, const void* theta,
+                            const void* aux, const void* u, double t, const void* w, void* out,
+                            void* stream) {
+  return field_op(f, batch, theta, aux, u, t, w, out, nullptr, kJvp, stream);
+}
+extern "C" int ob_field_vjp(const ob_field_desc* f, int64_t batch, const void* theta,
+                            const void* aux, const void* u, double t, const void* v, void* jtv,
+                            void* ptv, void* stream) {
+  return field_op(f, batch, theta, aux, u, t, v, jtv, ptv, kVjp, stream);
+}
+extern "C" int ob_field_vjp_u(const ob_field_desc* f, int64_t batch, const void* theta,
+                              const void* aux, const void* u, double t, const void* v, void* jtv,
+                              void* stream) {
+  return field_op(f, batch, theta, aux, u, t, v, jtv, nullptr, kVjpU, stream);
+}

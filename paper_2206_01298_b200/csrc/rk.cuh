@@ -1,0 +1,66 @@
+// rk.cuh -- parameters shared by the persistent explicit-RK kernels and the
+// host engine.
+#pragma once
+
+#include "tile.cuh"
+
+namespace ob {
+
+// reverse-program opcodes (host-compiled from the checkpoint policy)
+enum { kOpReplay = 0, kOpReverse = 1 };
+// replay start-state sources
+enum { kSrcU0 = 0, kSrcRecNext = 1, kSrcSol = 2 };
+
+struct SmemLayout {      // offsets in elements of T
+  int x0, pre[OB_MAX_LAYERS], hid[OB_MAX_LAYERS], dA, dB;
+  int u, lam, lamn, w, jtv, out;
+  int total;
+};
+
+template <typename T>
+struct RkParams {
+  Dims d;
+  Weights<T> W;
+  SmemLayout sm;
+  // scheme (tableaux.py:14-56)
+  int s, fsal;
+  double a[OB_MAX_STAGES * OB_MAX_STAGES], b[OB_MAX_STAGES], c[OB_MAX_STAGES];
+  unsigned skip_vjp;      // bit i: stage i cotangent is identically zero
+  // field
+  int field_kind;
+  const T* diag;          // stiff: a
+  T out_scale;            // stiff: s
+  // problem
+  int B, R, Rp, n_steps;
+  const double* ts;       // [n_steps+1]
+  int loss_kind;
+  const T* targets;
+  double inv_batch_global;
+  double batch_global;
+  // buffers
+  const T* u0;
+  T* u_final;
+  T* du0;
+  T* rec;                 // [nbuf][s+1][B][N]: stage states then u_next
+  T* sol;                 // [nsol][B][N]
+  const int* fwd_rec;     // [n_steps] record buffer written in the forward, or -1
+  const int* fwd_sol;     // [n_steps] solution slot written in the forward, or -1
+  const int4* prog;       // reverse program
+  int prog_len;
+  T* scratch;             // per tile [2][s][Rp][Np]: ks (forward), Lam (reverse)
+  long long scratch_stride;
+  T* mu;                  // [tiles][n_params] per-CTA parameter cotangent slots
+  long long n_params;
+  double* loss_part;      // [tiles]
+  int* status;            // [2] first error code, step
+};
+
+template <typename T>
+struct PackParams {
+  Dims d;
+  const T* theta;
+  T* wt[OB_MAX_LAYERS];
+  T* wn[OB_MAX_LAYERS];
+};
+
+}  // namespace ob

@@ -1,0 +1,452 @@
+// rk_kernels.cu -- persistent explicit Runge-Kutta forward / discrete-adjoint
+// reverse kernels (one CTA = one fixed tile of samples for the whole sweep).
+//
+// Forward: integrate (integrators.py:252-292) -> explicit_rk_step
+// (:196-222) with FSAL carry, writing the checkpoint records the policy asks
+// for (checkpointing.py:242-269).  Reverse: executes a host-compiled program
+// of REPLAY / REVERSE ops (checkpointing.py:286-340 + replay_step,
+// integrators.py:352-368) and the stage-wise transpose rk_adjoint_step
+// (adjoint.py:67-94).  Stage sums ascend in j with the scalar (h*a_ij) formed
+// first and exact zeros skipped, with round-to-nearest mul/add (no FMA
+// contraction), reproducing the reference combination bit-for-bit in fp64.
+#include <algorithm>
+
+#include "rk.cuh"
+
+namespace ob {
+
+template <typename T>
+OB_DEV void set_status(int* status, int code, int info) {
+  if (atomicCAS(status, 0, code) == 0) status[1] = info;
+}
+
+template <typename T>
+OB_DEV MlpSmem<T> carve(T* sm, const SmemLayout& L, int nl) {
+  MlpSmem<T> s;
+  s.x0 = sm + L.x0;
+  for (int l = 0; l < nl; ++l) {
+    s.pre[l] = sm + L.pre[l];
+    s.hid[l] = sm + L.hid[l];
+  }
+  s.dA = sm + L.dA;
+  s.dB = sm + L.dB;
+  return s;
+}
+
+// f(x0) -> out ([Rp][Np], N valid columns, pad columns written 0)
+template <typename T, int RB>
+OB_DEV void field_eval(const RkParams<T>& p, MlpTile<T, RB>& mt, T* out) {
+  mt.forward();
+  const int N = p.d.N, Np = p.d.Np, L = p.d.L;
+  const T* y = mt.s.pre[L - 1];
+  for (int i = threadIdx.x; i < p.Rp * Np; i += blockDim.x) {
+    const int r = i / Np, j = i % Np;
+    T v = T(0);
+    if (j < N) {
+      v = y[r * Np + j];
+      if (p.field_kind == OB_FIELD_STIFF)  // a*u + s*mlp(u)
+        v = Num<T>::add(Num<T>::mul(p.diag[j], mt.s.x0[r * p.d.wp[0] + j]),
+                        Num<T>::mul(p.out_scale, v));
+    }
+    out[i] = v;
+  }
+  __syncthreads();
+}
+
+// ((df/du)^T w, mu += h * (df/dtheta)^T w) at the state in x0
+template <typename T, int RB>
+OB_DEV void field_vjp(const RkParams<T>& p, MlpTile<T, RB>& mt, const T* w, T* jtv, T* mu,
+                      double h, int Rv) {
+  mt.forward();
+  const int Np = p.d.Np;
+  if (p.field_kind == OB_FIELD_STIFF) {
+    mt.vjp(w, Np, Rv, jtv, Np, mu, T(h * double(p.out_scale)));
+    for (int i = threadIdx.x; i < p.Rp * Np; i += blockDim.x) {
+      const int j = i % Np;
+      if (j < p.d.N)
+        jtv[i] = Num<T>::add(Num<T>::mul(p.diag[j], w[i]), Num<T>::mul(p.out_scale, jtv[i]));
+    }
+    __syncthreads();
+  } else {
+    mt.vjp(w, Np, Rv, jtv, Np, mu, T(h));
+  }
+}
+
+// One explicit RK step of the tile from the state in `u` (smem [Rp][Np]).
+// ks: this tile's stage-derivative scratch [s][Rp][Np].  rec (may be null):
+// record base for this step ([s+1][B][N]).  On return `u` holds u_next.
+// Returns false (block-uniform) if u_next has a non-finite entry.
+template <typename T, int RB>
+OB_DEV bool rk_step_tile(const RkParams<T>& p, MlpTile<T, RB>& mt, T* u, T* ks, double t,
+                         double h, bool carry, T* rec, int row0, int Rv) {
+  const int N = p.d.N, Np = p.d.Np, Rp = p.Rp, s = p.s, wp0 = p.d.wp[0];
+  const long long kst = (long long)Rp * Np;
+  const long long vec = (long long)p.B * N;
+  T* x0 = mt.s.x0;
+  for (int i = 0; i < s; ++i) {
+    for (int idx = threadIdx.x; idx < Rp * N; idx += blockDim.x) {
+      const int r = idx / N, j = idx % N;
+      T v = u[r * Np + j];
+      for (int q = 0; q < i; ++q) {
+        const double aiq = p.a[i * OB_MAX_STAGES + q];
+        if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), ks[q * kst + r * Np + j]));
+      }
+      x0[r * wp0 + j] = v;
+      if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * N + j] = v;
+    }
+    if (p.d.time_input)
+      for (int r = threadIdx.x; r < Rp; r += blockDim.x) x0[r * wp0 + N] = T(t + p.c[i] * h);
+    __syncthreads();
+    if (i == 0 && carry) {  // FSAL: k_0 of this step is k_{s-1} of the previous one
+      for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) ks[idx] = ks[(s - 1) * kst + idx];
+      __syncthreads();
+    } else {
+      field_eval<T, RB>(p, mt, ks + i * kst);
+    }
+  }
+  int bad = 0;
+  for (int idx = threadIdx.x; idx < Rp * N; idx += blockDim.x) {
+    const int r = idx / N, j = idx % N;
+    T v = u[r * Np + j];
+    for (int i = 0; i < s; ++i)
+      if (p.b[i] != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * p.b[i]), ks[i * kst + r * Np + j]));
+    u[r * Np + j] = v;
+    if (r < Rv) {
+      if (!Num<T>::finite(v)) bad = 1;
+      if (rec) rec[s * vec + (long long)(row0 + r) * N + j] = v;
+    }
+  }
+  return __syncthreads_or(bad) == 0;
+}
+
+template <typename T>
+OB_DEV void zero_smem(T* sm, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = T(0);
+  __syncthreads();
+}
+
+template <typename T>
+OB_DEV void load_rows(T* dst, int Np, const T* src, int N, int row0, int Rv) {
+  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+    const int r = idx / N, j = idx % N;
+    dst[r * Np + j] = src[(long long)(row0 + r) * N + j];
+  }
+}
+
+template <typename T>
+OB_DEV void store_rows(T* dst, int N, const T* src, int Np, int row0, int Rv) {
+  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+    const int r = idx / N, j = idx % N;
+    dst[(long long)(row0 + r) * N + j] = src[r * Np + j];
+  }
+}
+
+// --------------------------------------------------------------- forward
+template <typename T, int RB>
+__global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_constant__ RkParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  zero_smem(sm, p.sm.total);
+  const int tile = blockIdx.x;
+  const int row0 = tile * p.R;
+  const int Rv = min(p.R, p.B - row0);
+  MlpSmem<T> ms = carve(sm, p.sm, p.d.L);
+  MlpTile<T, RB> mt(p.d, p.W, ms, p.Rp);
+  T* u = sm + p.sm.u;
+  T* ks = p.scratch + tile * p.scratch_stride;
+  const int N = p.d.N, Np = p.d.Np;
+  const long long vec = (long long)p.B * N;
+
+  load_rows(u, Np, p.u0, N, row0, Rv);
+  __syncthreads();
+  int bad = 0;  // as_state rejects non-finite inputs (nn.py:31-32)
+  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x)
+    if (!Num<T>::finite(u[(idx / N) * Np + idx % N])) bad = 1;
+  if (__syncthreads_or(bad)) {
+    if (threadIdx.x == 0) set_status<T>(p.status, OB_ERR_VALUE, -1);
+    return;
+  }
+  for (int n = 0; n < p.n_steps; ++n) {
+    const double t = p.ts[n], h = p.ts[n + 1] - p.ts[n];
+    if (p.fwd_sol[n] >= 0) {
+      store_rows(p.sol + p.fwd_sol[n] * vec, N, u, Np, row0, Rv);
+      __syncthreads();
+    }
+    T* rec = p.fwd_rec[n] >= 0 ? p.rec + (long long)p.fwd_rec[n] * (p.s + 1) * vec : nullptr;
+    const bool ok = rk_step_tile<T, RB>(p, mt, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv);
+    if (!ok) {  // integrators.py:219-220
+      if (threadIdx.x == 0) set_status<T>(p.status, OB_ERR_INTEGRATION, n);
+      return;
+    }
+  }
+  store_rows(p.u_final, N, u, Np, row0, Rv);
+  // terminal loss partial (fp64, fixed order per tile; losses.py:78-107 / BASELINE)
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int r = 0; r < Rv; ++r) {
+      double sr = 0.0;
+      for (int j = 0; j < N; ++j) {
+        double v = double(u[r * Np + j]);
+        if (p.loss_kind == OB_LOSS_MSE) {
+          v -= double(p.targets[(long long)(row0 + r) * N + j]);
+          sr += v * v;
+        } else {
+          sr += v * v;
+        }
+      }
+      acc += (p.loss_kind == OB_LOSS_MSE) ? sr / N : 0.5 * sr;
+    }
+    p.loss_part[tile] = acc;
+  }
+}
+
+// --------------------------------------------------------------- reverse
+template <typename T, int RB>
+__global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_constant__ RkParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  zero_smem(sm, p.sm.total);
+  const int tile = blockIdx.x;
+  const int row0 = tile * p.R;
+  const int Rv = min(p.R, p.B - row0);
+  MlpSmem<T> ms = carve(sm, p.sm, p.d.L);
+  MlpTile<T, RB> mt(p.d, p.W, ms, p.Rp);
+  const int N = p.d.N, Np = p.d.Np, Rp = p.Rp, s = p.s, wp0 = p.d.wp[0];
+  const long long vec = (long long)p.B * N;
+  const long long kst = (long long)Rp * Np;
+  T* u = sm + p.sm.u;
+  T* lam = sm + p.sm.lam;
+  T* lamn = sm + p.sm.lamn;
+  T* w = sm + p.sm.w;
+  T* jtv = sm + p.sm.jtv;
+  T* ks = p.scratch + tile * p.scratch_stride;
+  T* Lam = ks + s * kst;
+  T* mu = p.mu + tile * p.n_params;
+  if (*(volatile int*)p.status != 0) return;  // forward failed
+
+  // terminal seed lambda_N = dL/du(T) (losses.py:78-107 with the batch mean)
+  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+    const int r = idx / N, j = idx % N;
+    const long long g = (long long)(row0 + r) * N + j;
+    T v = p.u_final[g];
+    if (p.loss_kind == OB_LOSS_MSE) v = T(2) * (v - p.targets[g]) / T(N);
+    lam[r * Np + j] = v / T(p.batch_global);
+  }
+  __syncthreads();
+
+  for (int pc = 0; pc < p.prog_len; ++pc) {
+    const int4 op = p.prog[pc];
+    const int n = op.y;
+    const double t = p.ts[n], h = p.ts[n + 1] - p.ts[n];
+    if (op.x == kOpReplay) {
+      // start state: u0 | record u_next | stored solution  (restore semantics,
+      // checkpointing.py:312-325); replay never reuses FSAL (integrators.py:363)
+      const int src_kind = op.z >> 24, src = op.z & 0xffffff;
+      const T* srcp = src_kind == kSrcU0 ? p.u0
+                    : src_kind == kSrcSol ? p.sol + src * vec
+                    : p.rec + ((long long)src * (s + 1) + s) * vec;
+      load_rows(u, Np, srcp, N, row0, Rv);
+      __syncthreads();
+      T* rec = p.rec + (long long)op.w * (s + 1) * vec;
+      rk_step_tile<T, RB>(p, mt, u, ks, t, h, false, rec, row0, Rv);
+      continue;
+    }
+    // REVERSE(n) from record buffer op.w: rk_adjoint_step (adjoint.py:67-94)
+    const T* rec = p.rec + (long long)op.w * (s + 1) * vec;
+    for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) lamn[idx] = lam[idx];
+    __syncthreads();
+    for (int i = s - 1; i >= 0; --i) {
+      if (p.skip_vjp & (1u << i)) {  // w_i == 0 exactly: Lam_i = 0 (still counted, B8)
+        for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) Lam[i * kst + idx] = T(0);
+        continue;
+      }
+      // w_i = b_i lam_{n+1} + sum_{j>i, a_ji != 0} a_ji Lam_j
+      for (int idx = threadIdx.x; idx < Rp * Np; idx += blockDim.x) {
+        T v = Num<T>::mul(T(p.b[i]), lam[idx]);
+        for (int j = i + 1; j < s; ++j) {
+          const double aji = p.a[j * OB_MAX_STAGES + i];
+          if (aji != 0.0) v = Num<T>::add(v, Num<T>::mul(T(aji), Lam[j * kst + idx]));
+        }
+        w[idx] = v;
+      }
+      // stage state U_i into x0 (+ stage time)
+      for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+        const int r = idx / N, j = idx % N;
+        ms.x0[r * wp0 + j] = rec[i * vec + (long long)(row0 + r) * N + j];
+      }
+      if (p.d.time_input)
+        for (int r = threadIdx.x; r < Rp; r += blockDim.x) ms.x0[r * wp0 + N] = T(t + p.c[i] * h);
+      __syncthreads();
+      field_vjp<T, RB>(p, mt, w, jtv, mu, h, Rv);
+      // Lam_i = h * jtv; lam += Lam_i
+      for (int idx = threadIdx.x; idx < Rp * Np; idx += blockDim.x) {
+        const T li = Num<T>::mul(T(h), jtv[idx]);
+        Lam[i * kst + idx] = li;
+        lamn[idx] = Num<T>::add(lamn[idx], li);
+      }
+      __syncthreads();
+    }
+    int bad = 0;
+    for (int idx = threadIdx.x; idx < Rp * Np; idx += blockDim.x) {
+      lam[idx] = lamn[idx];
+      if (!Num<T>::finite(lamn[idx])) bad = 1;
+    }
+    if (__syncthreads_or(bad)) {  // AdjointState.check_finite (adjoint.py:42-44)
+      if (threadIdx.x == 0) set_status<T>(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
+      return;
+    }
+  }
+  store_rows(p.du0, N, lam, Np, row0, Rv);
+}
+
+// --------------------------------------------------------------- helpers
+template <typename T>
+__global__ void pack_weights_kernel(const __grid_constant__ PackParams<T> p) {
+  // W^T [wp_l][w_{l+1}] and W [wp_{l+1}][w_l] per layer, zero padded
+  for (int l = 0; l < p.d.L; ++l) {
+    const int nin = p.d.w[l], nout = p.d.w[l + 1];
+    const T* Wl = p.theta + p.d.woff[l];
+    const int nt = p.d.wp[l] * nout;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += gridDim.x * blockDim.x) {
+      const int k = i / nout, n = i % nout;
+      p.wt[l][i] = k < nin ? Wl[(long long)n * nin + k] : T(0);
+    }
+    const int nn = p.d.wp[l + 1] * nin;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
+      const int n = i / nin, k = i % nin;
+      p.wn[l][i] = n < nout ? Wl[(long long)n * nin + k] : T(0);
+    }
+  }
+}
+
+// dtheta[j] = sum_tiles mu[tile][j] in tile order (deterministic); loss likewise.
+template <typename T>
+__global__ void reduce_tiles_kernel(const T* mu, int tiles, long long np, T* dtheta,
+                                    const double* loss_part, double inv_b, double* loss) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < np;
+       j += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < tiles; ++t) acc += double(mu[t * np + j]);
+    dtheta[j] = T(acc);
+  }
+  if (loss && blockIdx.x == 0 && threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int t = 0; t < tiles; ++t) acc += loss_part[t];
+    *loss = acc * inv_b;
+  }
+}
+
+// Field protocol ops on a batch (integrators.py:53-102): eval / jvp / vjp / vjp_u.
+template <typename T, int RB>
+__global__ void __launch_bounds__(kThreads, 1)
+field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const T* u,
+                const T* w, T* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  zero_smem(sm, p.sm.total);
+  const int tile = blockIdx.x;
+  const int row0 = tile * p.R;
+  const int Rv = min(p.R, p.B - row0);
+  MlpSmem<T> ms = carve(sm, p.sm, p.d.L);
+  MlpTile<T, RB> mt(p.d, p.W, ms, p.Rp);
+  const int N = p.d.N, Np = p.d.Np, wp0 = p.d.wp[0];
+  T* wb = sm + p.sm.w;
+  T* res = sm + p.sm.jtv;
+  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+    const int r = idx / N, j = idx % N;
+    ms.x0[r * wp0 + j] = u[(long long)(row0 + r) * N + j];
+  }
+  if (p.d.time_input)
+    for (int r = threadIdx.x; r < p.Rp; r += blockDim.x) ms.x0[r * wp0 + N] = T(t);
+  if (mode != 0) load_rows(wb, Np, w, N, row0, Rv);
+  __syncthreads();
+  if (mode == 0) {
+    field_eval<T, RB>(p, mt, res);
+  } else if (mode == 1) {
+    mt.forward();
+    mt.jvp(wb, Np, res, Np);
+    if (p.field_kind == OB_FIELD_STIFF) {
+      for (int i = threadIdx.x; i < p.Rp * Np; i += blockDim.x) {
+        const int j = i % Np;
+        if (j < N) res[i] = Num<T>::add(Num<T>::mul(p.diag[j], wb[i]), Num<T>::mul(p.out_scale, res[i]));
+      }
+      __syncthreads();
+    }
+  } else {
+    field_vjp<T, RB>(p, mt, wb, res, mode == 2 ? p.mu + tile * p.n_params : nullptr, 1.0, Rv);
+  }
+  store_rows(out, N, res, Np, row0, Rv);
+}
+
+// ------------------------------------------------------------ launchers
+template <typename T>
+cudaError_t launch_pack(const PackParams<T>& pp, cudaStream_t st) {
+  pack_weights_kernel<T><<<148, 256, 0, st>>>(pp);
+  return cudaGetLastError();
+}
+
+template <typename T, int RB>
+static cudaError_t launch_rk_rb(const RkParams<T>& p, int tiles, size_t smem, cudaStream_t st,
+                                bool forward) {
+  auto kf = forward ? rk_forward_kernel<T, RB> : rk_reverse_kernel<T, RB>;
+  cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kf<<<tiles, kThreads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_rk(const RkParams<T>& p, int rb, int tiles, size_t smem, cudaStream_t st,
+                      bool forward) {
+  switch (rb) {
+    case 1: return launch_rk_rb<T, 1>(p, tiles, smem, st, forward);
+    case 2: return launch_rk_rb<T, 2>(p, tiles, smem, st, forward);
+    case 4: return launch_rk_rb<T, 4>(p, tiles, smem, st, forward);
+    default: return launch_rk_rb<T, 8>(p, tiles, smem, st, forward);
+  }
+}
+
+template <typename T, int RB>
+static cudaError_t launch_field_rb(const RkParams<T>& p, int tiles, size_t smem, int mode, double t,
+                                   const T* u, const T* w, T* out, cudaStream_t st) {
+  auto kf = field_op_kernel<T, RB>;
+  cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kf<<<tiles, kThreads, smem, st>>>(p, mode, t, u, w, out);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_field_op(const RkParams<T>& p, int rb, int tiles, size_t smem, int mode,
+                            double t, const T* u, const T* w, T* out, cudaStream_t st) {
+  switch (rb) {
+    case 1: return launch_field_rb<T, 1>(p, tiles, smem, mode, t, u, w, out, st);
+    case 2: return launch_field_rb<T, 2>(p, tiles, smem, mode, t, u, w, out, st);
+    case 4: return launch_field_rb<T, 4>(p, tiles, smem, mode, t, u, w, out, st);
+    default: return launch_field_rb<T, 8>(p, tiles, smem, mode, t, u, w, out, st);
+  }
+}
+
+template <typename T>
+cudaError_t launch_reduce(const T* mu, int tiles, long long np, T* dtheta, const double* lp,
+                          double inv_b, double* loss, cudaStream_t st) {
+  const int blocks = (int)std::min<long long>((np + 255) / 256, 148 * 4);
+  reduce_tiles_kernel<T><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(mu, tiles, np, dtheta, lp,
+                                                                    inv_b, loss);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_pack<float>(const PackParams<float>&, cudaStream_t);
+template cudaError_t launch_pack<double>(const PackParams<double>&, cudaStream_t);
+template cudaError_t launch_rk<float>(const RkParams<float>&, int, int, size_t, cudaStream_t, bool);
+template cudaError_t launch_rk<double>(const RkParams<double>&, int, int, size_t, cudaStream_t, bool);
+template cudaError_t launch_field_op<float>(const RkParams<float>&, int, int, size_t, int, double,
+                                            const float*, const float*, float*, cudaStream_t);
+template cudaError_t launch_field_op<double>(const RkParams<double>&, int, int, size_t, int, double,
+                                             const double*, const double*, double*, cudaStream_t);
+template cudaError_t launch_reduce<float>(const float*, int, long long, float*, const double*,
+                                          double, double*, cudaStream_t);
+template cudaError_t launch_reduce<double>(const double*, int, long long, double*, const double*,
+                                           double, double*, cudaStream_t);
+
+}  // namespace ob

@@ -1,0 +1,138 @@
+"""grad(): forward integration + checkpoints + discrete adjoint on the device
+(reference adjoint.py:224-279: forward_pass :151-210, loss_and_grad_seed
+losses.py:78-107, backward_sweep :235-253), batched over samples.
+
+One call = one ``ob_grad`` into the native engine: two persistent kernels
+(forward sweep, reverse program) plus weight packing and a fixed-order
+reduction.  Host inputs (numpy arrays / CPU tensors) are copied to the device
+and results copied back; device inputs stay on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .controls import (NfeCounters, SolverConfig, StoreCounters, boundary_times, raise_status)
+from .fields import Field, stream_ptr, to_device
+from .losses import LossSpec
+from .policies import CheckpointPolicy
+from .schemes import Scheme, to_desc
+
+
+@dataclass
+class GradResult:
+    dtheta: object
+    du0: object
+    loss: float
+    counters: NfeCounters
+    predictions: list
+    u_final: object
+    store_counters: StoreCounters = None
+    device: dict = dc_field(default_factory=dict)
+
+
+_WS_CACHE = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    key = (device.index,)
+    buf = _WS_CACHE.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = buf
+    return buf
+
+
+def build_problem(field: Field, scheme: Scheme, loss: LossSpec, batch: int, ts: np.ndarray,
+                  policy: CheckpointPolicy, solver_cfg: SolverConfig, batch_global: int):
+    prob = _lib.Problem()
+    prob.field = field.desc()
+    prob.scheme = to_desc(scheme)
+    prob.solver = solver_cfg.to_desc()
+    prob.batch = batch
+    prob.batch_global = batch_global
+    prob.n_steps = len(ts) - 1
+    prob.policy = _lib.OB_POLICY[policy.kind]
+    prob.nc = policy.nc
+    prob.loss = _lib.OB_LOSS[loss.kind]
+    times = np.ascontiguousarray(ts, dtype=np.float64)
+    prob.times = times.ctypes.data_as(C.POINTER(C.c_double))
+    return prob, times
+
+
+def workspace_size(prob) -> int:
+    n = C.c_size_t()
+    raise_status(_lib.load().ob_grad_workspace_size(C.byref(prob), C.byref(n)), _lib.last_error())
+    return int(n.value)
+
+
+def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
+         policy=CheckpointPolicy("store_all"), solver_cfg=None, counters=None, *,
+         batch_global=None) -> GradResult:
+    """Loss, dL/dtheta and dL/du0 by forward solve + discrete adjoint sweep."""
+    solver_cfg = solver_cfg or SolverConfig()
+    counters = counters if counters is not None else NfeCounters()
+    if loss.times[-1] > tF + 1e-9 * max(1.0, abs(tF)):
+        raise ValueError("observations extend past the final time")
+    if abs(loss.times[-1] - tF) > 1e-9 * max(1.0, abs(tF)):
+        raise NotImplementedError("observations before tF are not built (SURVEY 8f row 3)")
+    ts = boundary_times(ctrl, t0, tF)
+    host_io = not (isinstance(u0, torch.Tensor) and u0.is_cuda)
+    dt = field.torch_dtype
+    if isinstance(u0, torch.Tensor) and not u0.is_cuda:
+        u0d = u0.to(device=torch.device("cuda", torch.cuda.current_device()), dtype=dt,
+                    non_blocking=True).contiguous()
+    else:
+        u0d = to_device(u0, dt)
+    if u0d.dim() == 1:
+        u0d = u0d.unsqueeze(0)
+    B, N = u0d.shape
+    if N != field.n:
+        raise ValueError(f"expected length {field.n}, got {N}")
+    bg = int(batch_global) if batch_global is not None else B
+    prob, _times = build_problem(field, scheme, loss, B, ts, policy, solver_cfg, bg)
+    nbytes = workspace_size(prob)
+    dev = u0d.device
+    ws = _workspace(nbytes, dev)
+    u_final = torch.empty_like(u0d)
+    du0 = torch.empty_like(u0d)
+    dtheta = torch.empty(field.n_params, dtype=dt, device=dev)
+    loss_t = torch.zeros(1, dtype=torch.float64, device=dev)
+    targets = to_device(loss.values, dt) if loss.kind == "mse" else None
+    if targets is not None and tuple(targets.shape) != (B, N):
+        raise ValueError("targets must be [B, N]")
+    aux = field.aux()
+    bufs = _lib.Buffers()
+    bufs.theta = field.theta_tensor().data_ptr()
+    bufs.aux = aux.data_ptr() if aux is not None else None
+    bufs.u0 = u0d.data_ptr()
+    bufs.targets = targets.data_ptr() if targets is not None else None
+    bufs.u_final = u_final.data_ptr()
+    bufs.du0 = du0.data_ptr()
+    bufs.dtheta = dtheta.data_ptr()
+    bufs.loss = loss_t.data_ptr()
+    bufs.workspace = ws.data_ptr()
+    bufs.workspace_bytes = ws.numel()
+    bufs.sample_stats = None
+    cnt = _lib.Counters()
+    rc = _lib.load().ob_grad(C.byref(prob), C.byref(bufs), C.byref(cnt), stream_ptr())
+    raise_status(rc, _lib.last_error())
+    c = cnt.as_dict()
+    counters.nfe_forward += c["nfe_forward"]
+    counters.nfe_backward += c["nfe_backward"]
+    counters.steps_accepted += c["steps_accepted"]
+    counters.steps_recomputed += c["steps_recomputed"]
+    sc = StoreCounters(c["stored_states"], c["stored_stage_vectors"], c["max_live_slots"],
+                       c["recomputed_steps"])
+    loss_v = float(loss_t.item())
+    if host_io:
+        dtheta_o, du0_o, uf_o = dtheta.cpu().numpy(), du0.cpu().numpy(), u_final.cpu().numpy()
+    else:
+        dtheta_o, du0_o, uf_o = dtheta, du0, u_final
+    return GradResult(dtheta=dtheta_o, du0=du0_o, loss=loss_v, counters=counters,
+                      predictions=[uf_o], u_final=uf_o, store_counters=sc, device=c)
