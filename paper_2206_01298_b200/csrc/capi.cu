@@ -23,8 +23,8 @@
 namespace ob {
 template <typename T> cudaError_t launch_pack(const PackParams<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_rk(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
-template <typename T> cudaError_t launch_reduce(const T*, int, long long, T*, const double*, double,
-                                                double*, cudaStream_t);
+template <typename T> cudaError_t launch_reduce(const Dims&, const T*, int, long long, T*,
+                                                const double*, double, double*, cudaStream_t);
 template <typename T> cudaError_t launch_field_op(const RkParams<T>&, int, int, size_t, int, double,
                                                   const T*, const T*, T*, cudaStream_t);
 }  // namespace ob
@@ -92,7 +92,8 @@ struct Plan {
   int dtype = 0;
   size_t esz = 8;
   Dims d{};
-  int R = 1, Rp = 1, RB = 1, tiles = 1;
+  int R = 1, Rt = 4, LR = 1, tiles = 1;
+  bool need_jvp = false;
   SmemLayout sm{};
   size_t smem_bytes = 0;
   // checkpoint program
@@ -105,7 +106,7 @@ struct Plan {
   size_t o_ts = 0, o_fr = 0, o_fs = 0, o_pg = 0, o_stat = 0;
   size_t off_blob = 0, blob_bytes = 0, off_w = 0, off_rec = 0, off_sol = 0, off_scr = 0,
          off_mu = 0, off_lp = 0, total = 0;
-  long long w_elems[OB_MAX_LAYERS][2]{};
+  size_t off_pk = 0;
   long long scratch_stride = 0;
 };
 
@@ -130,61 +131,86 @@ int check_field(const ob_field_desc& f) {
   return OB_OK;
 }
 
-void make_dims(const ob_field_desc& f, Dims& d) {
+int ld_quad_odd(int x) {  // >= x, multiple of 4, (ld/4) odd: conflict-free strided rows
+  int l = (x + 3) & ~3;
+  if (((l / 4) & 1) == 0) l += 4;
+  return l;
+}
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+void make_dims(const ob_field_desc& f, int LR, Dims& d) {
+  const int CT = 4 * (32 / LR);
+  d = Dims{};
   d.L = f.n_layers;
-  d.maxwp = 0;
-  long long off = 0;
+  d.N = f.widths[f.n_layers];
+  d.maxw = 0;
   for (int l = 0; l <= d.L; ++l) {
     d.w[l] = f.widths[l];
-    d.wp[l] = pad4i(f.widths[l]);
-    d.maxwp = std::max(d.maxwp, d.wp[l]);
+    d.lda[l] = ld_quad_odd(f.widths[l]);
+    d.maxw = std::max(d.maxw, d.w[l]);
   }
+  long long off = 0, po = 0, mo = 0;
   for (int l = 0; l < d.L; ++l) {
+    const int K = d.w[l], Nn = d.w[l + 1], Kout = l == 0 ? d.N : K;
     d.woff[l] = off;
-    d.boff[l] = off + (long long)d.w[l + 1] * d.w[l];
-    off = d.boff[l] + d.w[l + 1];
+    d.boff[l] = off + (long long)Nn * K;
+    off = d.boff[l] + Nn;
+    d.nrow[l] = round_up(Nn, CT);
+    d.ldw[l] = ld_quad_odd(std::max(round_up(K, 4), round_up(Kout, CT)));
+    d.pwoff[l] = po;
+    po += (long long)d.nrow[l] * d.ldw[l];
+    d.ldm[l] = round_up(K, 4);
+    d.mwoff[l] = mo;
+    mo += (long long)Nn * d.ldm[l];
+    d.mboff[l] = mo;
+    mo += round_up(Nn, 4);
   }
-  d.N = d.w[d.L];
-  d.Np = d.wp[d.L];
+  d.n_packed = po;
+  d.n_mu = mo;
+  d.ldn = ld_quad_odd(d.N);
   d.act = f.activation;
   d.time_input = f.time_input;
+  d.need_pre = (f.activation == OB_ACT_GELU || f.activation == OB_ACT_SOFTPLUS);
+  d.ldt = ld_quad_odd(d.maxw);
 }
 
+// shared-memory layout for Rt rows; weights staged in smem when they fit
 void layout_smem(Plan& P) {
   const Dims& d = P.d;
   SmemLayout& s = P.sm;
   int o = 0;
-  auto take = [&](int n) { int r = o; o += (n + 7) & ~7; return r; };  // 32-byte aligned
-  s.x0 = take(P.Rp * d.wp[0]);
-  for (int l = 0; l < d.L; ++l) {
-    s.pre[l] = take(P.Rp * d.wp[l + 1]);
-    s.hid[l] = l < d.L - 1 ? take(P.Rp * d.wp[l + 1]) : 0;
+  auto take = [&](long long n) { int r = o; o += (int)((n + 7) & ~7LL); return r; };  // 32 B aligned
+  s.x0 = take((long long)P.Rt * d.lda[0]);
+  for (int l = 0; l < OB_MAX_LAYERS; ++l) {
+    s.hid[l] = (l < d.L - 1) ? take((long long)P.Rt * d.lda[l + 1]) : -1;
+    s.pre[l] = (l < d.L - 1 && d.need_pre) ? take((long long)P.Rt * d.lda[l + 1]) : -1;
   }
-  s.dA = take(P.Rp * d.maxwp);
-  s.dB = take(P.Rp * d.maxwp);
-  s.u = take(P.Rp * d.Np);
-  s.lam = take(P.Rp * d.Np);
-  s.lamn = take(P.Rp * d.Np);
-  s.w = take(P.Rp * d.Np);
-  s.jtv = take(P.Rp * d.Np);
-  s.out = 0;
+  s.tA = P.need_jvp ? take((long long)P.Rt * d.ldt) : -1;
+  s.tB = P.need_jvp ? take((long long)P.Rt * d.ldt) : -1;
+  s.u = take((long long)P.Rt * d.ldn);
+  s.lam = take((long long)P.Rt * d.ldn);
+  s.lamn = take((long long)P.Rt * d.ldn);
+  s.w = take((long long)P.Rt * d.ldn);
+  s.jtv = take((long long)P.Rt * d.ldn);
   s.total = o;
-  P.smem_bytes = (size_t)o * P.esz;
+  s.wts = -1;
+  if ((size_t)(o + d.n_packed) * P.esz <= kSmemLimit) {
+    s.wts = take(d.n_packed);
+    s.total = o;
+  }
+  P.smem_bytes = (size_t)s.total * P.esz;
 }
 
-int pick_rb(int R) {
-  if (R >= 16 && R % 8 == 0) return 8;
-  if (R >= 4) return 4;
-  if (R >= 2) return 2;
-  return 1;
-}
+int pick_lr(int R) { return R <= 4 ? 1 : R <= 8 ? 2 : R <= 16 ? 4 : 8; }
 
-void choose_tiles(Plan& P, long long B, int sm_count) {
+void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   int R = (int)std::max<long long>(1, (B + sm_count - 1) / sm_count);
+  R = std::min(R, 32);
   for (;;) {
     P.R = R;
-    P.RB = pick_rb(R);
-    P.Rp = (R + P.RB - 1) / P.RB * P.RB;
+    P.LR = pick_lr(R);
+    P.Rt = round_up(R, 4 * P.LR);
+    make_dims(f, P.LR, P.d);
     layout_smem(P);
     if (P.smem_bytes <= kSmemLimit || R == 1) break;
     R = std::max(1, R * 3 / 4);
@@ -314,14 +340,13 @@ int plan_problem(const ob_problem& p, Plan& P) {
     return fail(OB_ERR_UNSUPPORTED, "loss kind not supported for this field");
   P.dtype = p.field.dtype;
   P.esz = P.dtype == OB_F32 ? 4 : 8;
-  make_dims(p.field, P.d);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
   } else {
     cudaGetLastError();
   }
-  choose_tiles(P, p.batch, sms);
+  choose_tiles(P, p.field, p.batch, sms);
   if (P.smem_bytes > kSmemLimit) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   st = compile_policy(p, P);
   if (st) return st;
@@ -355,22 +380,17 @@ int plan_problem(const ob_problem& p, Plan& P) {
   P.o_stat = P.o_pg + sizeof(int4) * P.prog.size();
   P.blob_bytes = P.o_stat + sizeof(int) * 4;
   o = align_up(o + P.blob_bytes, 256);
-  P.off_w = o;
-  for (int l = 0; l < P.d.L; ++l) {
-    P.w_elems[l][0] = (long long)P.d.wp[l] * P.d.w[l + 1];
-    P.w_elems[l][1] = (long long)P.d.wp[l + 1] * P.d.w[l];
-    o = align_up(o + P.esz * P.w_elems[l][0], 256);
-    o = align_up(o + P.esz * P.w_elems[l][1], 256);
-  }
+  P.off_pk = o;
+  o = align_up(o + P.esz * (size_t)P.d.n_packed, 256);
   P.off_rec = o;
   o = align_up(o + P.esz * (size_t)P.nbuf * (s + 1) * B * N, 256);
   P.off_sol = o;
   o = align_up(o + P.esz * (size_t)P.nsol * B * N, 256);
   P.off_scr = o;
-  P.scratch_stride = 2LL * s * P.Rp * P.d.Np;
+  P.scratch_stride = 2LL * s * P.Rt * P.d.ldn;
   o = align_up(o + P.esz * (size_t)P.tiles * P.scratch_stride, 256);
   P.off_mu = o;
-  o = align_up(o + P.esz * (size_t)P.tiles * p.field.n_params, 256);
+  o = align_up(o + P.esz * (size_t)P.tiles * P.d.n_mu, 256);
   P.off_lp = o;
   o = align_up(o + sizeof(double) * P.tiles, 256);
   P.total = o;
@@ -396,16 +416,9 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   PackParams<T> pp{};
   pp.d = P.d;
   pp.theta = static_cast<const T*>(b.theta);
-  size_t wo = P.off_w;
-  for (int l = 0; l < P.d.L; ++l) {
-    pp.wt[l] = reinterpret_cast<T*>(ws + wo);
-    wo = align_up(wo + P.esz * P.w_elems[l][0], 256);
-    pp.wn[l] = reinterpret_cast<T*>(ws + wo);
-    wo = align_up(wo + P.esz * P.w_elems[l][1], 256);
-    rp.W.wt[l] = pp.wt[l];
-    rp.W.wn[l] = pp.wn[l];
-    rp.W.bias[l] = pp.theta + P.d.boff[l];
-  }
+  pp.packed = reinterpret_cast<T*>(ws + P.off_pk);
+  rp.packed = pp.packed;
+  for (int l = 0; l < P.d.L; ++l) rp.W.bias[l] = pp.theta + P.d.boff[l];
   rp.s = s;
   rp.fsal = p.scheme.fsal;
   std::memcpy(rp.a, p.scheme.a, sizeof(rp.a));
@@ -417,7 +430,7 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   rp.out_scale = T(p.field.out_scale);
   rp.B = (int)p.batch;
   rp.R = P.R;
-  rp.Rp = P.Rp;
+  rp.Rt = P.Rt;
   rp.n_steps = nt;
   rp.ts = reinterpret_cast<const double*>(ws + P.off_blob + o_ts);
   rp.loss_kind = p.loss;
@@ -445,16 +458,16 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   static thread_local cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   if (!ev[0])
     for (auto& e : ev) CU(cudaEventCreate(&e));
-  CU(cudaMemsetAsync(rp.mu, 0, P.esz * (size_t)P.tiles * p.field.n_params, st));
+  CU(cudaMemsetAsync(rp.mu, 0, P.esz * (size_t)P.tiles * P.d.n_mu, st));
   CU(cudaEventRecord(ev[0], st));
   CU(launch_pack<T>(pp, st));
   CU(cudaEventRecord(ev[1], st));
-  CU(launch_rk<T>(rp, P.RB, P.tiles, P.smem_bytes, st, true));
+  CU(launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, true));
   CU(cudaEventRecord(ev[2], st));
-  CU(launch_rk<T>(rp, P.RB, P.tiles, P.smem_bytes, st, false));
+  CU(launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, false));
   CU(cudaEventRecord(ev[3], st));
-  CU(launch_reduce<T>(rp.mu, P.tiles, p.field.n_params, static_cast<T*>(b.dtheta), rp.loss_part,
-                      rp.inv_batch_global, b.loss, st));
+  CU(launch_reduce<T>(P.d, rp.mu, P.tiles, p.field.n_params, static_cast<T*>(b.dtheta),
+                      rp.loss_part, rp.inv_batch_global, b.loss, st));
   CU(cudaEventRecord(ev[4], st));
   int hs[2] = {0, 0};
   CU(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -522,55 +535,43 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
   Plan P;
   P.dtype = f.dtype;
   P.esz = sizeof(T);
-  make_dims(f, P.d);
+  P.need_jvp = (mode == kJvp);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  choose_tiles(P, batch, sms);
+  choose_tiles(P, f, batch, sms);
   if (P.smem_bytes > kSmemLimit) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
-  size_t wbytes = 0;
-  for (int l = 0; l < P.d.L; ++l) {
-    P.w_elems[l][0] = (long long)P.d.wp[l] * P.d.w[l + 1];
-    P.w_elems[l][1] = (long long)P.d.wp[l + 1] * P.d.w[l];
-    wbytes = align_up(wbytes + P.esz * P.w_elems[l][0], 256);
-    wbytes = align_up(wbytes + P.esz * P.w_elems[l][1], 256);
-  }
-  const size_t mu_bytes = mode == kVjp ? P.esz * (size_t)P.tiles * f.n_params : 0;
+  const size_t pk_bytes = align_up(P.esz * (size_t)P.d.n_packed, 256);
+  const size_t mu_bytes = mode == kVjp ? P.esz * (size_t)P.tiles * P.d.n_mu : 0;
   char* ws = nullptr;
-  CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes + mu_bytes + 256, st));
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), pk_bytes + mu_bytes + 256, st));
   RkParams<T> rp{};
   rp.d = P.d;
   rp.sm = P.sm;
   PackParams<T> pp{};
   pp.d = P.d;
   pp.theta = static_cast<const T*>(theta);
-  size_t wo = 0;
-  for (int l = 0; l < P.d.L; ++l) {
-    pp.wt[l] = reinterpret_cast<T*>(ws + wo);
-    wo = align_up(wo + P.esz * P.w_elems[l][0], 256);
-    pp.wn[l] = reinterpret_cast<T*>(ws + wo);
-    wo = align_up(wo + P.esz * P.w_elems[l][1], 256);
-    rp.W.wt[l] = pp.wt[l];
-    rp.W.wn[l] = pp.wn[l];
-    rp.W.bias[l] = pp.theta + P.d.boff[l];
-  }
+  pp.packed = reinterpret_cast<T*>(ws);
+  rp.packed = pp.packed;
+  for (int l = 0; l < P.d.L; ++l) rp.W.bias[l] = pp.theta + P.d.boff[l];
   rp.field_kind = f.kind;
   rp.diag = static_cast<const T*>(aux);
   rp.out_scale = T(f.out_scale);
   rp.B = (int)batch;
   rp.R = P.R;
-  rp.Rp = P.Rp;
+  rp.Rt = P.Rt;
   rp.n_params = f.n_params;
-  rp.mu = mode == kVjp ? reinterpret_cast<T*>(ws + wbytes) : nullptr;
+  rp.mu = mode == kVjp ? reinterpret_cast<T*>(ws + pk_bytes) : nullptr;
   int rc = OB_OK;
   cudaError_t e = cudaSuccess;
   if (mu_bytes) e = cudaMemsetAsync(rp.mu, 0, mu_bytes, st);
   if (e == cudaSuccess) e = launch_pack<T>(pp, st);
   if (e == cudaSuccess)
-    e = launch_field_op<T>(rp, P.RB, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
+    e = launch_field_op<T>(rp, P.LR, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
                            static_cast<const T*>(w), static_cast<T*>(out), st);
   if (e == cudaSuccess && mode == kVjp)
-    e = launch_reduce<T>(rp.mu, P.tiles, f.n_params, static_cast<T*>(ptv), nullptr, 0.0, nullptr, st);
+    e = launch_reduce<T>(P.d, rp.mu, P.tiles, f.n_params, static_cast<T*>(ptv), nullptr, 0.0,
+                         nullptr, st);
   cudaFreeAsync(ws, st);
   if (e != cudaSuccess) rc = fail(OB_ERR_CUDA, cudaGetErrorString(e));
   return rc;

@@ -11,9 +11,10 @@ enum { kOpReplay = 0, kOpReverse = 1 };
 // replay start-state sources
 enum { kSrcU0 = 0, kSrcRecNext = 1, kSrcSol = 2 };
 
-struct SmemLayout {      // offsets in elements of T
-  int x0, pre[OB_MAX_LAYERS], hid[OB_MAX_LAYERS], dA, dB;
-  int u, lam, lamn, w, jtv, out;
+struct SmemLayout {      // offsets in elements of T (-1: not allocated)
+  int x0, hid[OB_MAX_LAYERS], pre[OB_MAX_LAYERS], tA, tB;
+  int u, lam, lamn, w, jtv;
+  int wts;                // packed weights staged in shared memory, or -1
   int total;
 };
 
@@ -31,7 +32,7 @@ struct RkParams {
   const T* diag;          // stiff: a
   T out_scale;            // stiff: s
   // problem
-  int B, R, Rp, n_steps;
+  int B, R, Rt, n_steps;
   const double* ts;       // [n_steps+1]
   int loss_kind;
   const T* targets;
@@ -47,9 +48,10 @@ struct RkParams {
   const int* fwd_sol;     // [n_steps] solution slot written in the forward, or -1
   const int4* prog;       // reverse program
   int prog_len;
-  T* scratch;             // per tile [2][s][Rp][Np]: ks (forward), Lam (reverse)
+  const T* packed;        // packed weights in global memory (n_packed elements)
+  T* scratch;             // per tile [2][s][Rt][ldn]: ks (forward), Lam (reverse)
   long long scratch_stride;
-  T* mu;                  // [tiles][n_params] per-CTA parameter cotangent slots
+  T* mu;                  // [tiles][n_mu] per-CTA padded parameter cotangent slots
   long long n_params;
   double* loss_part;      // [tiles]
   int* status;            // [2] first error code, step
@@ -59,8 +61,7 @@ template <typename T>
 struct PackParams {
   Dims d;
   const T* theta;
-  T* wt[OB_MAX_LAYERS];
-  T* wn[OB_MAX_LAYERS];
+  T* packed;
 };
 
 }  // namespace ob

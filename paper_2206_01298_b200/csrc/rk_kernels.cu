@@ -15,102 +15,119 @@
 
 namespace ob {
 
-template <typename T>
 OB_DEV void set_status(int* status, int code, int info) {
   if (atomicCAS(status, 0, code) == 0) status[1] = info;
 }
 
 template <typename T>
-OB_DEV MlpSmem<T> carve(T* sm, const SmemLayout& L, int nl) {
-  MlpSmem<T> s;
-  s.x0 = sm + L.x0;
-  for (int l = 0; l < nl; ++l) {
-    s.pre[l] = sm + L.pre[l];
-    s.hid[l] = sm + L.hid[l];
-  }
-  s.dA = sm + L.dA;
-  s.dB = sm + L.dB;
-  return s;
+OB_DEV void zero_smem(T* sm, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = T(0);
+  __syncthreads();
 }
 
-// f(x0) -> out ([Rp][Np], N valid columns, pad columns written 0)
-template <typename T, int RB>
-OB_DEV void field_eval(const RkParams<T>& p, MlpTile<T, RB>& mt, T* out) {
-  mt.forward();
-  const int N = p.d.N, Np = p.d.Np, L = p.d.L;
-  const T* y = mt.s.pre[L - 1];
-  for (int i = threadIdx.x; i < p.Rp * Np; i += blockDim.x) {
-    const int r = i / Np, j = i % Np;
-    T v = T(0);
-    if (j < N) {
-      v = y[r * Np + j];
-      if (p.field_kind == OB_FIELD_STIFF)  // a*u + s*mlp(u)
-        v = Num<T>::add(Num<T>::mul(p.diag[j], mt.s.x0[r * p.d.wp[0] + j]),
-                        Num<T>::mul(p.out_scale, v));
-    }
-    out[i] = v;
+// carve the MLP tile out of shared memory; stage packed weights into smem when
+// the layout reserved room for them (one L2 read per CTA per launch)
+template <typename T>
+OB_DEV void setup_tile(const RkParams<T>& p, T* sm, MlpSmem<T>& ms, Weights<T>& W) {
+  const SmemLayout& L = p.sm;
+  ms.x0 = sm + L.x0;
+  for (int l = 0; l < OB_MAX_LAYERS; ++l) {
+    ms.hid[l] = L.hid[l] >= 0 ? sm + L.hid[l] : nullptr;
+    ms.pre[l] = L.pre[l] >= 0 ? sm + L.pre[l] : nullptr;
+  }
+  ms.tA = L.tA >= 0 ? sm + L.tA : nullptr;
+  ms.tB = L.tB >= 0 ? sm + L.tB : nullptr;
+  const T* base = p.packed;
+  if (L.wts >= 0) {
+    T* dst = sm + L.wts;
+    const long long n16 = p.d.n_packed * (long long)sizeof(T) / 16;  // packed length is a multiple of 4
+    const float4* src4 = reinterpret_cast<const float4*>(p.packed);
+    float4* dst4 = reinterpret_cast<float4*>(dst);
+    for (long long i = threadIdx.x; i < n16; i += blockDim.x) dst4[i] = src4[i];
+    base = dst;
+  }
+  for (int l = 0; l < p.d.L; ++l) {
+    W.W[l] = base + p.d.pwoff[l];
+    W.bias[l] = p.W.bias[l];
   }
   __syncthreads();
 }
 
-// ((df/du)^T w, mu += h * (df/dtheta)^T w) at the state in x0
-template <typename T, int RB>
-OB_DEV void field_vjp(const RkParams<T>& p, MlpTile<T, RB>& mt, const T* w, T* jtv, T* mu,
-                      double h, int Rv) {
-  mt.forward();
-  const int Np = p.d.Np;
-  if (p.field_kind == OB_FIELD_STIFF) {
-    mt.vjp(w, Np, Rv, jtv, Np, mu, T(h * double(p.out_scale)));
-    for (int i = threadIdx.x; i < p.Rp * Np; i += blockDim.x) {
-      const int j = i % Np;
-      if (j < p.d.N)
-        jtv[i] = Num<T>::add(Num<T>::mul(p.diag[j], w[i]), Num<T>::mul(p.out_scale, jtv[i]));
+// f(x0) -> out ([Rt][ldn]; columns >= N untouched)
+template <typename T, int LR>
+OB_DEV void field_eval(const RkParams<T>& p, MlpTile<T, LR>& mt, T* out) {
+  const int N = p.d.N, ldn = p.d.ldn;
+  mt.forward(out, ldn, p.d.L);
+  if (p.field_kind == OB_FIELD_STIFF) {  // a*u + s*mlp(u)
+    const int ld0 = p.d.lda[0];
+    for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
+      const int r = i / N, j = i % N;
+      out[r * ldn + j] = Num<T>::add(Num<T>::mul(p.diag[j], mt.s.x0[r * ld0 + j]),
+                                     Num<T>::mul(p.out_scale, out[r * ldn + j]));
     }
     __syncthreads();
-  } else {
-    mt.vjp(w, Np, Rv, jtv, Np, mu, T(h));
   }
 }
 
-// One explicit RK step of the tile from the state in `u` (smem [Rp][Np]).
-// ks: this tile's stage-derivative scratch [s][Rp][Np].  rec (may be null):
+// ((df/du)^T w, mu += h * (df/dtheta)^T w) at the state in x0
+template <typename T, int LR>
+OB_DEV void field_vjp(const RkParams<T>& p, MlpTile<T, LR>& mt, const T* w, T* jtv, T* mu,
+                      double h, int Rv) {
+  mt.forward(nullptr, 0, p.d.L - 1);  // hidden layers only: the output value is not needed
+  const int ldn = p.d.ldn;
+  if (p.field_kind == OB_FIELD_STIFF) {
+    mt.vjp(w, ldn, Rv, jtv, ldn, mu, T(h * double(p.out_scale)));
+    const int N = p.d.N;
+    for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
+      const int r = i / N, j = i % N;
+      jtv[r * ldn + j] = Num<T>::add(Num<T>::mul(p.diag[j], w[r * ldn + j]),
+                                     Num<T>::mul(p.out_scale, jtv[r * ldn + j]));
+    }
+    __syncthreads();
+  } else {
+    mt.vjp(w, ldn, Rv, jtv, ldn, mu, T(h));
+  }
+}
+
+// One explicit RK step of the tile from the state in `u` (smem [Rt][ldn]).
+// ks: this tile's stage-derivative scratch [s][Rt][ldn].  rec (nullable):
 // record base for this step ([s+1][B][N]).  On return `u` holds u_next.
 // Returns false (block-uniform) if u_next has a non-finite entry.
-template <typename T, int RB>
-OB_DEV bool rk_step_tile(const RkParams<T>& p, MlpTile<T, RB>& mt, T* u, T* ks, double t,
+template <typename T, int LR>
+OB_DEV bool rk_step_tile(const RkParams<T>& p, MlpTile<T, LR>& mt, T* u, T* ks, double t,
                          double h, bool carry, T* rec, int row0, int Rv) {
-  const int N = p.d.N, Np = p.d.Np, Rp = p.Rp, s = p.s, wp0 = p.d.wp[0];
-  const long long kst = (long long)Rp * Np;
+  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0];
+  const long long kst = (long long)Rt * ldn;
   const long long vec = (long long)p.B * N;
   T* x0 = mt.s.x0;
   for (int i = 0; i < s; ++i) {
-    for (int idx = threadIdx.x; idx < Rp * N; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
       const int r = idx / N, j = idx % N;
-      T v = u[r * Np + j];
+      T v = u[r * ldn + j];
       for (int q = 0; q < i; ++q) {
         const double aiq = p.a[i * OB_MAX_STAGES + q];
-        if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), ks[q * kst + r * Np + j]));
+        if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), ks[q * kst + r * ldn + j]));
       }
-      x0[r * wp0 + j] = v;
+      x0[r * ld0 + j] = v;
       if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * N + j] = v;
     }
     if (p.d.time_input)
-      for (int r = threadIdx.x; r < Rp; r += blockDim.x) x0[r * wp0 + N] = T(t + p.c[i] * h);
+      for (int r = threadIdx.x; r < Rt; r += blockDim.x) x0[r * ld0 + N] = T(t + p.c[i] * h);
     __syncthreads();
     if (i == 0 && carry) {  // FSAL: k_0 of this step is k_{s-1} of the previous one
       for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) ks[idx] = ks[(s - 1) * kst + idx];
       __syncthreads();
     } else {
-      field_eval<T, RB>(p, mt, ks + i * kst);
+      field_eval<T, LR>(p, mt, ks + i * kst);
     }
   }
   int bad = 0;
-  for (int idx = threadIdx.x; idx < Rp * N; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
-    T v = u[r * Np + j];
+    T v = u[r * ldn + j];
     for (int i = 0; i < s; ++i)
-      if (p.b[i] != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * p.b[i]), ks[i * kst + r * Np + j]));
-    u[r * Np + j] = v;
+      if (p.b[i] != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * p.b[i]), ks[i * kst + r * ldn + j]));
+    u[r * ldn + j] = v;
     if (r < Rv) {
       if (!Num<T>::finite(v)) bad = 1;
       if (rec) rec[s * vec + (long long)(row0 + r) * N + j] = v;
@@ -120,79 +137,71 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, MlpTile<T, RB>& mt, T* u, T* ks, 
 }
 
 template <typename T>
-OB_DEV void zero_smem(T* sm, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = T(0);
-  __syncthreads();
-}
-
-template <typename T>
-OB_DEV void load_rows(T* dst, int Np, const T* src, int N, int row0, int Rv) {
+OB_DEV void load_rows(T* dst, int ldd, const T* src, int N, int row0, int Rv) {
   for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
-    dst[r * Np + j] = src[(long long)(row0 + r) * N + j];
+    dst[r * ldd + j] = src[(long long)(row0 + r) * N + j];
   }
 }
 
 template <typename T>
-OB_DEV void store_rows(T* dst, int N, const T* src, int Np, int row0, int Rv) {
+OB_DEV void store_rows(T* dst, int N, const T* src, int lds, int row0, int Rv) {
   for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
-    dst[(long long)(row0 + r) * N + j] = src[r * Np + j];
+    dst[(long long)(row0 + r) * N + j] = src[r * lds + j];
   }
 }
 
 // --------------------------------------------------------------- forward
-template <typename T, int RB>
+template <typename T, int LR>
 __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_constant__ RkParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  zero_smem(sm, p.sm.total);
+  zero_smem(sm, p.sm.wts >= 0 ? p.sm.wts : p.sm.total);
   const int tile = blockIdx.x;
   const int row0 = tile * p.R;
   const int Rv = min(p.R, p.B - row0);
-  MlpSmem<T> ms = carve(sm, p.sm, p.d.L);
-  MlpTile<T, RB> mt(p.d, p.W, ms, p.Rp);
+  MlpSmem<T> ms;
+  Weights<T> W;
+  setup_tile(p, sm, ms, W);
+  MlpTile<T, LR> mt(p.d, W, ms, p.Rt);
   T* u = sm + p.sm.u;
   T* ks = p.scratch + tile * p.scratch_stride;
-  const int N = p.d.N, Np = p.d.Np;
+  const int N = p.d.N, ldn = p.d.ldn;
   const long long vec = (long long)p.B * N;
 
-  load_rows(u, Np, p.u0, N, row0, Rv);
+  load_rows(u, ldn, p.u0, N, row0, Rv);
   __syncthreads();
   int bad = 0;  // as_state rejects non-finite inputs (nn.py:31-32)
   for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x)
-    if (!Num<T>::finite(u[(idx / N) * Np + idx % N])) bad = 1;
+    if (!Num<T>::finite(u[(idx / N) * ldn + idx % N])) bad = 1;
   if (__syncthreads_or(bad)) {
-    if (threadIdx.x == 0) set_status<T>(p.status, OB_ERR_VALUE, -1);
+    if (threadIdx.x == 0) set_status(p.status, OB_ERR_VALUE, -1);
     return;
   }
   for (int n = 0; n < p.n_steps; ++n) {
     const double t = p.ts[n], h = p.ts[n + 1] - p.ts[n];
     if (p.fwd_sol[n] >= 0) {
-      store_rows(p.sol + p.fwd_sol[n] * vec, N, u, Np, row0, Rv);
+      store_rows(p.sol + p.fwd_sol[n] * vec, N, u, ldn, row0, Rv);
       __syncthreads();
     }
     T* rec = p.fwd_rec[n] >= 0 ? p.rec + (long long)p.fwd_rec[n] * (p.s + 1) * vec : nullptr;
-    const bool ok = rk_step_tile<T, RB>(p, mt, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv);
+    const bool ok = rk_step_tile<T, LR>(p, mt, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv);
     if (!ok) {  // integrators.py:219-220
-      if (threadIdx.x == 0) set_status<T>(p.status, OB_ERR_INTEGRATION, n);
+      if (threadIdx.x == 0) set_status(p.status, OB_ERR_INTEGRATION, n);
       return;
     }
   }
-  store_rows(p.u_final, N, u, Np, row0, Rv);
+  store_rows(p.u_final, N, u, ldn, row0, Rv);
   // terminal loss partial (fp64, fixed order per tile; losses.py:78-107 / BASELINE)
   if (threadIdx.x == 0) {
     double acc = 0.0;
     for (int r = 0; r < Rv; ++r) {
       double sr = 0.0;
       for (int j = 0; j < N; ++j) {
-        double v = double(u[r * Np + j]);
-        if (p.loss_kind == OB_LOSS_MSE) {
-          v -= double(p.targets[(long long)(row0 + r) * N + j]);
-          sr += v * v;
-        } else {
-          sr += v * v;
-        }
+        double v = double(u[r * ldn + j]);
+        if (p.loss_kind == OB_LOSS_MSE) v -= double(p.targets[(long long)(row0 + r) * N + j]);
+        sr += v * v;
       }
       acc += (p.loss_kind == OB_LOSS_MSE) ? sr / N : 0.5 * sr;
     }
@@ -201,19 +210,22 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
 }
 
 // --------------------------------------------------------------- reverse
-template <typename T, int RB>
+template <typename T, int LR>
 __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_constant__ RkParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  zero_smem(sm, p.sm.total);
+  if (*(volatile int*)p.status != 0) return;  // forward failed
+  zero_smem(sm, p.sm.wts >= 0 ? p.sm.wts : p.sm.total);
   const int tile = blockIdx.x;
   const int row0 = tile * p.R;
   const int Rv = min(p.R, p.B - row0);
-  MlpSmem<T> ms = carve(sm, p.sm, p.d.L);
-  MlpTile<T, RB> mt(p.d, p.W, ms, p.Rp);
-  const int N = p.d.N, Np = p.d.Np, Rp = p.Rp, s = p.s, wp0 = p.d.wp[0];
+  MlpSmem<T> ms;
+  Weights<T> W;
+  setup_tile(p, sm, ms, W);
+  MlpTile<T, LR> mt(p.d, W, ms, p.Rt);
+  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0];
   const long long vec = (long long)p.B * N;
-  const long long kst = (long long)Rp * Np;
+  const long long kst = (long long)Rt * ldn;
   T* u = sm + p.sm.u;
   T* lam = sm + p.sm.lam;
   T* lamn = sm + p.sm.lamn;
@@ -221,8 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
   T* jtv = sm + p.sm.jtv;
   T* ks = p.scratch + tile * p.scratch_stride;
   T* Lam = ks + s * kst;
-  T* mu = p.mu + tile * p.n_params;
-  if (*(volatile int*)p.status != 0) return;  // forward failed
+  T* mu = p.mu + tile * p.d.n_mu;
 
   // terminal seed lambda_N = dL/du(T) (losses.py:78-107 with the batch mean)
   for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
@@ -230,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
     const long long g = (long long)(row0 + r) * N + j;
     T v = p.u_final[g];
     if (p.loss_kind == OB_LOSS_MSE) v = T(2) * (v - p.targets[g]) / T(N);
-    lam[r * Np + j] = v / T(p.batch_global);
+    lam[r * ldn + j] = v / T(p.batch_global);
   }
   __syncthreads();
 
@@ -245,10 +256,10 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       const T* srcp = src_kind == kSrcU0 ? p.u0
                     : src_kind == kSrcSol ? p.sol + src * vec
                     : p.rec + ((long long)src * (s + 1) + s) * vec;
-      load_rows(u, Np, srcp, N, row0, Rv);
+      load_rows(u, ldn, srcp, N, row0, Rv);
       __syncthreads();
       T* rec = p.rec + (long long)op.w * (s + 1) * vec;
-      rk_step_tile<T, RB>(p, mt, u, ks, t, h, false, rec, row0, Rv);
+      rk_step_tile<T, LR>(p, mt, u, ks, t, h, false, rec, row0, Rv);
       continue;
     }
     // REVERSE(n) from record buffer op.w: rk_adjoint_step (adjoint.py:67-94)
@@ -260,73 +271,127 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
         for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) Lam[i * kst + idx] = T(0);
         continue;
       }
-      // w_i = b_i lam_{n+1} + sum_{j>i, a_ji != 0} a_ji Lam_j
-      for (int idx = threadIdx.x; idx < Rp * Np; idx += blockDim.x) {
-        T v = Num<T>::mul(T(p.b[i]), lam[idx]);
+      // w_i = b_i lam_{n+1} + sum_{j>i, a_ji != 0} a_ji Lam_j   (pad rows stay 0)
+      for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
+        const int o = (idx / N) * ldn + idx % N;
+        T v = Num<T>::mul(T(p.b[i]), lam[o]);
         for (int j = i + 1; j < s; ++j) {
           const double aji = p.a[j * OB_MAX_STAGES + i];
-          if (aji != 0.0) v = Num<T>::add(v, Num<T>::mul(T(aji), Lam[j * kst + idx]));
+          if (aji != 0.0) v = Num<T>::add(v, Num<T>::mul(T(aji), Lam[j * kst + o]));
         }
-        w[idx] = v;
+        w[o] = v;
       }
       // stage state U_i into x0 (+ stage time)
       for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
         const int r = idx / N, j = idx % N;
-        ms.x0[r * wp0 + j] = rec[i * vec + (long long)(row0 + r) * N + j];
+        ms.x0[r * ld0 + j] = rec[i * vec + (long long)(row0 + r) * N + j];
       }
       if (p.d.time_input)
-        for (int r = threadIdx.x; r < Rp; r += blockDim.x) ms.x0[r * wp0 + N] = T(t + p.c[i] * h);
+        for (int r = threadIdx.x; r < Rt; r += blockDim.x) ms.x0[r * ld0 + N] = T(t + p.c[i] * h);
       __syncthreads();
-      field_vjp<T, RB>(p, mt, w, jtv, mu, h, Rv);
-      // Lam_i = h * jtv; lam += Lam_i
-      for (int idx = threadIdx.x; idx < Rp * Np; idx += blockDim.x) {
-        const T li = Num<T>::mul(T(h), jtv[idx]);
-        Lam[i * kst + idx] = li;
-        lamn[idx] = Num<T>::add(lamn[idx], li);
+      field_vjp<T, LR>(p, mt, w, jtv, mu, h, Rv);
+      // Lam_i = h * jtv; lam_n += Lam_i
+      for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
+        const int o = (idx / N) * ldn + idx % N;
+        const T li = Num<T>::mul(T(h), jtv[o]);
+        Lam[i * kst + o] = li;
+        lamn[o] = Num<T>::add(lamn[o], li);
       }
       __syncthreads();
     }
     int bad = 0;
-    for (int idx = threadIdx.x; idx < Rp * Np; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) {
       lam[idx] = lamn[idx];
       if (!Num<T>::finite(lamn[idx])) bad = 1;
     }
     if (__syncthreads_or(bad)) {  // AdjointState.check_finite (adjoint.py:42-44)
-      if (threadIdx.x == 0) set_status<T>(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
+      if (threadIdx.x == 0) set_status(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
       return;
     }
   }
-  store_rows(p.du0, N, lam, Np, row0, Rv);
+  store_rows(p.du0, N, lam, ldn, row0, Rv);
+}
+
+// Field protocol ops on a batch (integrators.py:53-102): eval / jvp / vjp / vjp_u.
+template <typename T, int LR>
+__global__ void __launch_bounds__(kThreads, 1)
+field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const T* u,
+                const T* w, T* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  zero_smem(sm, p.sm.wts >= 0 ? p.sm.wts : p.sm.total);
+  const int tile = blockIdx.x;
+  const int row0 = tile * p.R;
+  const int Rv = min(p.R, p.B - row0);
+  MlpSmem<T> ms;
+  Weights<T> W;
+  setup_tile(p, sm, ms, W);
+  MlpTile<T, LR> mt(p.d, W, ms, p.Rt);
+  const int N = p.d.N, ldn = p.d.ldn, ld0 = p.d.lda[0];
+  T* wb = sm + p.sm.w;
+  T* res = sm + p.sm.jtv;
+  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+    const int r = idx / N, j = idx % N;
+    ms.x0[r * ld0 + j] = u[(long long)(row0 + r) * N + j];
+  }
+  if (p.d.time_input)
+    for (int r = threadIdx.x; r < p.Rt; r += blockDim.x) ms.x0[r * ld0 + N] = T(t);
+  if (mode != 0) load_rows(wb, ldn, w, N, row0, Rv);
+  __syncthreads();
+  if (mode == 0) {
+    field_eval<T, LR>(p, mt, res);
+  } else if (mode == 1) {
+    mt.forward(nullptr, 0, p.d.L - 1);
+    mt.jvp(wb, ldn, res, ldn);
+    if (p.field_kind == OB_FIELD_STIFF) {
+      for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
+        const int o = (i / N) * ldn + i % N, j = i % N;
+        res[o] = Num<T>::add(Num<T>::mul(p.diag[j], wb[o]), Num<T>::mul(p.out_scale, res[o]));
+      }
+      __syncthreads();
+    }
+  } else {
+    field_vjp<T, LR>(p, mt, wb, res, mode == 2 ? p.mu + tile * p.d.n_mu : nullptr, 1.0, Rv);
+  }
+  store_rows(out, N, res, ldn, row0, Rv);
 }
 
 // --------------------------------------------------------------- helpers
+// packed W_l: [nrow_l][ldw_l] row-major copy of theta's W_l, zero padded
 template <typename T>
 __global__ void pack_weights_kernel(const __grid_constant__ PackParams<T> p) {
-  // W^T [wp_l][w_{l+1}] and W [wp_{l+1}][w_l] per layer, zero padded
   for (int l = 0; l < p.d.L; ++l) {
-    const int nin = p.d.w[l], nout = p.d.w[l + 1];
+    const int nin = p.d.w[l], nout = p.d.w[l + 1], ldw = p.d.ldw[l];
     const T* Wl = p.theta + p.d.woff[l];
-    const int nt = p.d.wp[l] * nout;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += gridDim.x * blockDim.x) {
-      const int k = i / nout, n = i % nout;
-      p.wt[l][i] = k < nin ? Wl[(long long)n * nin + k] : T(0);
-    }
-    const int nn = p.d.wp[l + 1] * nin;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
-      const int n = i / nin, k = i % nin;
-      p.wn[l][i] = n < nout ? Wl[(long long)n * nin + k] : T(0);
+    T* dst = p.packed + p.d.pwoff[l];
+    const long long n = (long long)p.d.nrow[l] * ldw;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+      const int r = (int)(i / ldw), k = (int)(i % ldw);
+      dst[i] = (r < nout && k < nin) ? Wl[(long long)r * nin + k] : T(0);
     }
   }
 }
 
-// dtheta[j] = sum_tiles mu[tile][j] in tile order (deterministic); loss likewise.
+// dtheta = sum over tiles of the padded mu slots, in tile order (deterministic),
+// scattered back to the reference flat layout; loss likewise.
 template <typename T>
-__global__ void reduce_tiles_kernel(const T* mu, int tiles, long long np, T* dtheta,
-                                    const double* loss_part, double inv_b, double* loss) {
+__global__ void reduce_tiles_kernel(const __grid_constant__ Dims d, const T* mu, int tiles,
+                                    long long np, T* dtheta, const double* loss_part,
+                                    double inv_b, double* loss) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < np;
        j += (long long)gridDim.x * blockDim.x) {
+    int l = 0;
+    while (l + 1 < d.L && j >= d.woff[l + 1]) ++l;
+    long long src;
+    if (j < d.boff[l]) {
+      const long long q = j - d.woff[l];
+      src = d.mwoff[l] + (q / d.w[l]) * d.ldm[l] + q % d.w[l];
+    } else {
+      src = d.mboff[l] + (j - d.boff[l]);
+    }
     double acc = 0.0;
-    for (int t = 0; t < tiles; ++t) acc += double(mu[t * np + j]);
+    for (int t = 0; t < tiles; ++t) acc += double(mu[t * d.n_mu + src]);
     dtheta[j] = T(acc);
   }
   if (loss && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -336,48 +401,6 @@ __global__ void reduce_tiles_kernel(const T* mu, int tiles, long long np, T* dth
   }
 }
 
-// Field protocol ops on a batch (integrators.py:53-102): eval / jvp / vjp / vjp_u.
-template <typename T, int RB>
-__global__ void __launch_bounds__(kThreads, 1)
-field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const T* u,
-                const T* w, T* out) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>(smem_raw);
-  zero_smem(sm, p.sm.total);
-  const int tile = blockIdx.x;
-  const int row0 = tile * p.R;
-  const int Rv = min(p.R, p.B - row0);
-  MlpSmem<T> ms = carve(sm, p.sm, p.d.L);
-  MlpTile<T, RB> mt(p.d, p.W, ms, p.Rp);
-  const int N = p.d.N, Np = p.d.Np, wp0 = p.d.wp[0];
-  T* wb = sm + p.sm.w;
-  T* res = sm + p.sm.jtv;
-  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
-    const int r = idx / N, j = idx % N;
-    ms.x0[r * wp0 + j] = u[(long long)(row0 + r) * N + j];
-  }
-  if (p.d.time_input)
-    for (int r = threadIdx.x; r < p.Rp; r += blockDim.x) ms.x0[r * wp0 + N] = T(t);
-  if (mode != 0) load_rows(wb, Np, w, N, row0, Rv);
-  __syncthreads();
-  if (mode == 0) {
-    field_eval<T, RB>(p, mt, res);
-  } else if (mode == 1) {
-    mt.forward();
-    mt.jvp(wb, Np, res, Np);
-    if (p.field_kind == OB_FIELD_STIFF) {
-      for (int i = threadIdx.x; i < p.Rp * Np; i += blockDim.x) {
-        const int j = i % Np;
-        if (j < N) res[i] = Num<T>::add(Num<T>::mul(p.diag[j], wb[i]), Num<T>::mul(p.out_scale, res[i]));
-      }
-      __syncthreads();
-    }
-  } else {
-    field_vjp<T, RB>(p, mt, wb, res, mode == 2 ? p.mu + tile * p.n_params : nullptr, 1.0, Rv);
-  }
-  store_rows(out, N, res, Np, row0, Rv);
-}
-
 // ------------------------------------------------------------ launchers
 template <typename T>
 cudaError_t launch_pack(const PackParams<T>& pp, cudaStream_t st) {
@@ -385,53 +408,48 @@ cudaError_t launch_pack(const PackParams<T>& pp, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <typename T, int RB>
-static cudaError_t launch_rk_rb(const RkParams<T>& p, int tiles, size_t smem, cudaStream_t st,
+template <typename K, typename... A>
+static cudaError_t launch_smem(K kf, int grid, size_t smem, cudaStream_t st, A... args) {
+  cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kf<<<grid, kThreads, smem, st>>>(args...);
+  return cudaGetLastError();
+}
+
+template <typename T, int LR>
+static cudaError_t launch_rk_lr(const RkParams<T>& p, int tiles, size_t smem, cudaStream_t st,
                                 bool forward) {
-  auto kf = forward ? rk_forward_kernel<T, RB> : rk_reverse_kernel<T, RB>;
-  cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kf<<<tiles, kThreads, smem, st>>>(p);
-  return cudaGetLastError();
+  return forward ? launch_smem(rk_forward_kernel<T, LR>, tiles, smem, st, p)
+                 : launch_smem(rk_reverse_kernel<T, LR>, tiles, smem, st, p);
 }
 
 template <typename T>
-cudaError_t launch_rk(const RkParams<T>& p, int rb, int tiles, size_t smem, cudaStream_t st,
+cudaError_t launch_rk(const RkParams<T>& p, int lr, int tiles, size_t smem, cudaStream_t st,
                       bool forward) {
-  switch (rb) {
-    case 1: return launch_rk_rb<T, 1>(p, tiles, smem, st, forward);
-    case 2: return launch_rk_rb<T, 2>(p, tiles, smem, st, forward);
-    case 4: return launch_rk_rb<T, 4>(p, tiles, smem, st, forward);
-    default: return launch_rk_rb<T, 8>(p, tiles, smem, st, forward);
+  switch (lr) {
+    case 1: return launch_rk_lr<T, 1>(p, tiles, smem, st, forward);
+    case 2: return launch_rk_lr<T, 2>(p, tiles, smem, st, forward);
+    case 4: return launch_rk_lr<T, 4>(p, tiles, smem, st, forward);
+    default: return launch_rk_lr<T, 8>(p, tiles, smem, st, forward);
   }
 }
 
-template <typename T, int RB>
-static cudaError_t launch_field_rb(const RkParams<T>& p, int tiles, size_t smem, int mode, double t,
-                                   const T* u, const T* w, T* out, cudaStream_t st) {
-  auto kf = field_op_kernel<T, RB>;
-  cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kf<<<tiles, kThreads, smem, st>>>(p, mode, t, u, w, out);
-  return cudaGetLastError();
-}
-
 template <typename T>
-cudaError_t launch_field_op(const RkParams<T>& p, int rb, int tiles, size_t smem, int mode,
+cudaError_t launch_field_op(const RkParams<T>& p, int lr, int tiles, size_t smem, int mode,
                             double t, const T* u, const T* w, T* out, cudaStream_t st) {
-  switch (rb) {
-    case 1: return launch_field_rb<T, 1>(p, tiles, smem, mode, t, u, w, out, st);
-    case 2: return launch_field_rb<T, 2>(p, tiles, smem, mode, t, u, w, out, st);
-    case 4: return launch_field_rb<T, 4>(p, tiles, smem, mode, t, u, w, out, st);
-    default: return launch_field_rb<T, 8>(p, tiles, smem, mode, t, u, w, out, st);
+  switch (lr) {
+    case 1: return launch_smem(field_op_kernel<T, 1>, tiles, smem, st, p, mode, t, u, w, out);
+    case 2: return launch_smem(field_op_kernel<T, 2>, tiles, smem, st, p, mode, t, u, w, out);
+    case 4: return launch_smem(field_op_kernel<T, 4>, tiles, smem, st, p, mode, t, u, w, out);
+    default: return launch_smem(field_op_kernel<T, 8>, tiles, smem, st, p, mode, t, u, w, out);
   }
 }
 
 template <typename T>
-cudaError_t launch_reduce(const T* mu, int tiles, long long np, T* dtheta, const double* lp,
-                          double inv_b, double* loss, cudaStream_t st) {
+cudaError_t launch_reduce(const Dims& d, const T* mu, int tiles, long long np, T* dtheta,
+                          const double* lp, double inv_b, double* loss, cudaStream_t st) {
   const int blocks = (int)std::min<long long>((np + 255) / 256, 148 * 4);
-  reduce_tiles_kernel<T><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(mu, tiles, np, dtheta, lp,
+  reduce_tiles_kernel<T><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(d, mu, tiles, np, dtheta, lp,
                                                                     inv_b, loss);
   return cudaGetLastError();
 }
@@ -444,9 +462,9 @@ template cudaError_t launch_field_op<float>(const RkParams<float>&, int, int, si
                                             const float*, const float*, float*, cudaStream_t);
 template cudaError_t launch_field_op<double>(const RkParams<double>&, int, int, size_t, int, double,
                                              const double*, const double*, double*, cudaStream_t);
-template cudaError_t launch_reduce<float>(const float*, int, long long, float*, const double*,
-                                          double, double*, cudaStream_t);
-template cudaError_t launch_reduce<double>(const double*, int, long long, double*, const double*,
-                                           double, double*, cudaStream_t);
+template cudaError_t launch_reduce<float>(const Dims&, const float*, int, long long, float*,
+                                          const double*, double, double*, cudaStream_t);
+template cudaError_t launch_reduce<double>(const Dims&, const double*, int, long long, double*,
+                                           const double*, double, double*, cudaStream_t);
 
 }  // namespace ob

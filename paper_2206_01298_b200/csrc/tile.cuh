@@ -88,224 +88,157 @@ template <typename T> OB_DEV T act_second(T x, int id) {
 OB_DEV int pad4(int n) { return (n + 3) & ~3; }
 
 // ---------------------------------------------------------------- params
+// Host-computed geometry of one MLP (see capi.cu: make_dims / layout).
 struct Dims {
-  int L;                        // affine layers
-  int w[OB_MAX_LAYERS + 1];     // widths
-  int wp[OB_MAX_LAYERS + 1];    // widths padded to 4
-  int N, Np;                    // state dim, padded
+  int L;                          // affine layers
+  int w[OB_MAX_LAYERS + 1];       // widths
+  int lda[OB_MAX_LAYERS + 1];     // leading dim of the activation buffer of width w[l]
+  int ldw[OB_MAX_LAYERS];         // leading dim of packed W_l ([nrow_l][ldw_l])
+  int nrow[OB_MAX_LAYERS];        // rows of packed W_l (w[l+1] rounded up to the col tile)
+  long long woff[OB_MAX_LAYERS], boff[OB_MAX_LAYERS];    // W / b offsets in theta
+  long long pwoff[OB_MAX_LAYERS];                        // packed W_l offsets (elements)
+  long long mwoff[OB_MAX_LAYERS], mboff[OB_MAX_LAYERS];  // padded mu offsets
+  int ldm[OB_MAX_LAYERS];         // padded mu row stride (w[l] rounded to 4)
+  long long n_mu;                 // padded mu length
+  long long n_packed;             // packed weights length
+  int N, ldn;                     // state dim, its buffer leading dim
   int act, time_input;
-  long long woff[OB_MAX_LAYERS], boff[OB_MAX_LAYERS];  // W / b offsets in theta
-  int maxwp;
+  int need_pre;                   // act' needs the pre-activation (gelu / softplus)
+  int maxw, ldt;                  // widest layer, tangent buffer leading dim
 };
 
 template <typename T>
 struct Weights {
-  const T* wt[OB_MAX_LAYERS];    // [wp_l][w_{l+1}]  W^T, zero rows for k >= w_l
-  const T* wn[OB_MAX_LAYERS];    // [wp_{l+1}][w_l]  W,   zero rows for n >= w_{l+1}
-  const T* bias[OB_MAX_LAYERS];  // [w_{l+1}] (into theta)
+  const T* W[OB_MAX_LAYERS];      // packed W_l (shared memory or global)
+  const T* bias[OB_MAX_LAYERS];   // [w_{l+1}] (into theta)
 };
 
 // shared-memory tile of one MLP evaluation
 template <typename T>
 struct MlpSmem {
-  T* x0;                        // [Rp][wp0] layer-0 input (state | time)
-  T* pre[OB_MAX_LAYERS];        // [Rp][wp_{l+1}] pre-activations (last = output)
-  T* hid[OB_MAX_LAYERS];        // [Rp][wp_{l+1}] act(pre) for hidden layers
-  T* dA;                        // [Rp][maxwp] cotangent / tangent ping-pong
-  T* dB;
+  T* x0;                          // [Rt][lda0] layer-0 input (state | time)
+  T* hid[OB_MAX_LAYERS];          // [Rt][lda_{l+1}] act(pre) of hidden layers, reused
+                                  //   in place as the layer cotangent during a VJP
+  T* pre[OB_MAX_LAYERS];          // pre-activations (only when need_pre)
+  T* tA;                          // tangent ping-pong (JVP only) [Rt][ldt]
+  T* tB;
 };
 
-// ------------------------------------------------------------ affine ops
-// Z[r][n] = sum_k X[r][k] * WT[k][n] (+ bias[n]);  rows r < Rp, n < N.
-// Each thread owns RB rows x 1 column; k advances 4 at a time (X vector loads
-// from smem, W^T coalesced across the warp from L1/L2).
-template <typename T, int RB>
-OB_DEV void affine_fwd(const T* __restrict__ X, int ldx, int Rp, int Kp,
-                       const T* __restrict__ WT, const T* __restrict__ bias, int N,
-                       T* __restrict__ Z, int ldz, T* __restrict__ A, int act) {
-  const int nrb = Rp / RB;
-  for (int item = threadIdx.x; item < nrb * N; item += blockDim.x) {
-    const int n = item % N;
-    const int r0 = (item / N) * RB;
-    T acc[RB];
-#pragma unroll
-    for (int j = 0; j < RB; ++j) acc[j] = T(0);
-    const T* xr = X + r0 * ldx;
-    for (int k = 0; k < Kp; k += 4) {
-      const T w0 = __ldg(WT + (k + 0) * N + n);
-      const T w1 = __ldg(WT + (k + 1) * N + n);
-      const T w2 = __ldg(WT + (k + 2) * N + n);
-      const T w3 = __ldg(WT + (k + 3) * N + n);
-#pragma unroll
-      for (int j = 0; j < RB; ++j) {
-        T x[4];
-        load4(xr + j * ldx + k, x);
-        acc[j] = Num<T>::fma(x[0], w0, acc[j]);
-        acc[j] = Num<T>::fma(x[1], w1, acc[j]);
-        acc[j] = Num<T>::fma(x[2], w2, acc[j]);
-        acc[j] = Num<T>::fma(x[3], w3, acc[j]);
-      }
-    }
-    const T b = bias ? __ldg(bias + n) : T(0);
-#pragma unroll
-    for (int j = 0; j < RB; ++j) {
-      const T z = bias ? Num<T>::add(acc[j], b) : acc[j];
-      Z[(r0 + j) * ldz + n] = z;
-      if (A) A[(r0 + j) * ldz + n] = act_fn(z, act);
-    }
+template <typename T> OB_DEV T act_prime_from(T a, T z, int id) {
+  // derivative from the activation value when possible (tanh: 1 - a^2;
+  // relu: a > 0 <=> z > 0), else from the pre-activation
+  switch (id) {
+    case OB_ACT_IDENTITY: return T(1);
+    case OB_ACT_RELU: return a > T(0) ? T(1) : T(0);
+    case OB_ACT_TANH: return T(1) - a * a;
+    default: return act_prime(z, id);
   }
 }
 
-// Out[r][k] = sum_n D[r][n] * WN[n][k] for k < K  (input-side VJP product, d <- W^T d
-// written as the row-vector product np.dot(d, w) of kernels.py:182).
-template <typename T, int RB>
-OB_DEV void affine_bwd(const T* __restrict__ D, int ldd, int Rp, int Np,
-                       const T* __restrict__ WN, int Kfull, int K,
-                       T* __restrict__ Out, int ldo) {
-  const int nrb = Rp / RB;
-  for (int item = threadIdx.x; item < nrb * K; item += blockDim.x) {
-    const int k = item % K;
-    const int r0 = (item / K) * RB;
-    T acc[RB];
-#pragma unroll
-    for (int j = 0; j < RB; ++j) acc[j] = T(0);
-    const T* dr = D + r0 * ldd;
-    for (int n = 0; n < Np; n += 4) {
-      const T w0 = __ldg(WN + (n + 0) * Kfull + k);
-      const T w1 = __ldg(WN + (n + 1) * Kfull + k);
-      const T w2 = __ldg(WN + (n + 2) * Kfull + k);
-      const T w3 = __ldg(WN + (n + 3) * Kfull + k);
-#pragma unroll
-      for (int j = 0; j < RB; ++j) {
-        T d[4];
-        load4(dr + j * ldd + n, d);
-        acc[j] = Num<T>::fma(d[0], w0, acc[j]);
-        acc[j] = Num<T>::fma(d[1], w1, acc[j]);
-        acc[j] = Num<T>::fma(d[2], w2, acc[j]);
-        acc[j] = Num<T>::fma(d[3], w3, acc[j]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < RB; ++j) Out[(r0 + j) * ldo + k] = acc[j];
-  }
-}
+}  // namespace ob
 
-// Parameter cotangent of one layer, summed over the tile's rows and scaled:
-//   muW[n][k] += scale * sum_r D[r][n] X[r][k];   mub[n] += scale * sum_r D[r][n]
-// (dW = outer(d, x), db = d per sample, kernels.py:177-179; mu += h*ptv,
-// adjoint.py:91).  muW is this CTA's private slot -> plain read-modify-write.
-template <typename T>
-OB_DEV void accum_dparam(const T* __restrict__ D, int ldd, const T* __restrict__ X, int ldx,
-                         int R, int N, int K, T scale, T* __restrict__ muW,
-                         T* __restrict__ mub) {
-  const int kq = (K + 3) / 4;
-  const int items = N * kq;
-  for (int item = threadIdx.x; item < items + N; item += blockDim.x) {
-    if (item < items) {
-      const int n = item / kq;
-      const int k0 = (item % kq) * 4;
-      T s[4] = {T(0), T(0), T(0), T(0)};
-      for (int r = 0; r < R; ++r) {
-        const T d = D[r * ldd + n];
-        T x[4];
-        load4(X + r * ldx + k0, x);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) s[q] = Num<T>::fma(d, x[q], s[q]);
-      }
-      T* dst = muW + (long long)n * K + k0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (k0 + q < K) dst[q] = Num<T>::add(dst[q], Num<T>::mul(scale, s[q]));
-    } else {
-      const int n = item - items;
-      T s = T(0);
-      for (int r = 0; r < R; ++r) s = Num<T>::add(s, D[r * ldd + n]);
-      mub[n] = Num<T>::add(mub[n], Num<T>::mul(scale, s));
-    }
-  }
-}
+#include "gemm.cuh"
+
+namespace ob {
 
 // ------------------------------------------------------------- MLP tile
-template <typename T, int RB>
+template <typename T, int LR>
 struct MlpTile {
   const Dims& d;
   const Weights<T>& W;
   MlpSmem<T>& s;
-  int Rp;
+  int Rt;
 
-  OB_DEV MlpTile(const Dims& d_, const Weights<T>& W_, MlpSmem<T>& s_, int Rp_)
-      : d(d_), W(W_), s(s_), Rp(Rp_) {}
+  OB_DEV MlpTile(const Dims& d_, const Weights<T>& W_, MlpSmem<T>& s_, int Rt_)
+      : d(d_), W(W_), s(s_), Rt(Rt_) {}
 
   OB_DEV const T* in(int l) const { return l == 0 ? s.x0 : s.hid[l - 1]; }
 
-  // x0 must be filled; output lands in s.pre[L-1] ([Rp][wp_L]).
-  OB_DEV void forward() {
-    for (int l = 0; l < d.L; ++l) {
-      affine_fwd<T, RB>(in(l), d.wp[l], Rp, d.wp[l], W.wt[l], W.bias[l], d.w[l + 1],
-                        s.pre[l], d.wp[l + 1], l < d.L - 1 ? s.hid[l] : nullptr, d.act);
+  // Layers [0, nl) from x0; the last of them writes z = W a + b to out[r*ldo+n]
+  // when nl == L (hidden layers store act(z) into hid, and z into pre if needed).
+  OB_DEV void forward(T* out, int ldo, int nl) {
+    for (int l = 0; l < nl; ++l) {
+      const T* b = W.bias[l];
+      const bool last = (l == d.L - 1);
+      const int ldh = d.lda[l + 1];
+      T* hid = last ? nullptr : s.hid[l];
+      T* pre = (last || !d.need_pre) ? nullptr : s.pre[l];
+      const int act = d.act;
+      gemm_nt<T, LR>(in(l), d.lda[l], Rt, W.W[l], d.ldw[l], d.w[l + 1], (d.w[l] + 3) & ~3,
+                     [&](int r, int n, T acc) {
+                       const T z = Num<T>::add(acc, b[n]);
+                       if (last) {
+                         out[r * ldo + n] = z;
+                       } else {
+                         hid[r * ldh + n] = act_fn(z, act);
+                         if (pre) pre[r * ldh + n] = z;
+                       }
+                     });
       __syncthreads();
     }
   }
 
-  // Reverse pass through the cached forward.  v: [Rp][ld_v] cotangent on the
-  // output (not modified).  jtv (may be null): [Rp][ld_o] receives the state
-  // part (k < N) of the input cotangent.  mu (may be null): this CTA's
-  // parameter-cotangent slot; receives scale * sum_rows (df/dtheta)^T v.
-  OB_DEV void vjp(const T* v, int ld_v, int R, T* jtv, int ld_o, T* mu, T scale) {
-    T* cur = s.dA;
-    T* nxt = s.dB;
-    const int L = d.L;
-    // copy the output cotangent into the ping-pong buffer
-    for (int i = threadIdx.x; i < Rp * d.wp[L]; i += blockDim.x) {
-      const int r = i / d.wp[L], n = i % d.wp[L];
-      cur[r * d.maxwp + n] = v[r * ld_v + n];
-    }
-    __syncthreads();
-    for (int l = L - 1; l >= 0; --l) {
-      const int nout = d.w[l + 1];
-      if (l < L - 1) {
-        for (int i = threadIdx.x; i < Rp * nout; i += blockDim.x) {
-          const int r = i / nout, n = i % nout;
-          cur[r * d.maxwp + n] *= act_prime(s.pre[l][r * d.wp[l + 1] + n], d.act);
-        }
+  // Reverse pass through the cached forward (forward(.., L-1) must have run).
+  // v: [Rt][ldv] output cotangent (rows >= Rv zero).  jtv (nullable): state part
+  // of the input cotangent.  mu (nullable): padded parameter-cotangent slot,
+  // receives scale * sum_{r<Rv} (df/dtheta)^T v.  Hidden activations are
+  // overwritten by the layer cotangents.
+  OB_DEV void vjp(const T* v, int ldv, int Rv, T* jtv, int ldo, T* mu, T scale) {
+    for (int l = d.L - 1; l >= 0; --l) {
+      const T* D = (l == d.L - 1) ? v : s.hid[l];
+      const int ldD = (l == d.L - 1) ? ldv : d.lda[l + 1];
+      if (mu) {
+        gemm_tn_accum<T>(D, ldD, in(l), d.lda[l], Rv, d.w[l + 1], d.w[l], scale, mu + d.mwoff[l],
+                         d.ldm[l], mu + d.mboff[l]);
         __syncthreads();
       }
-      if (mu) accum_dparam<T>(cur, d.maxwp, in(l), d.wp[l], R, nout, d.w[l], scale,
-                              mu + d.woff[l], mu + d.boff[l]);
+      const int Np = (d.w[l + 1] + 3) & ~3;
       if (l > 0) {
-        affine_bwd<T, RB>(cur, d.maxwp, Rp, d.wp[l + 1], W.wn[l], d.w[l], d.w[l], nxt, d.maxwp);
+        T* h = s.hid[l - 1];
+        const T* z = d.need_pre ? s.pre[l - 1] : nullptr;
+        const int ldh = d.lda[l];
+        const int act = d.act;
+        gemm_nn<T, LR>(D, ldD, Rt, W.W[l], d.ldw[l], Np, d.w[l], [&](int r, int k, T acc) {
+          const T a = h[r * ldh + k];
+          h[r * ldh + k] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + k] : a, act));
+        });
       } else if (jtv) {
-        affine_bwd<T, RB>(cur, d.maxwp, Rp, d.wp[1], W.wn[0], d.w[0], d.N, jtv, ld_o);
+        gemm_nn<T, LR>(D, ldD, Rt, W.W[0], d.ldw[0], Np, d.N,
+                       [&](int r, int k, T acc) { jtv[r * ldo + k] = acc; });
       }
+      __syncthreads();
+    }
+  }
+
+  // Tangent pass through the cached linearisation (forward(.., L-1) must have
+  // run; time tangent held at 0, nn.py:177-180).  w: [Rt][ldw_] (rows/cols
+  // beyond the state zero); out: [Rt][ldo].
+  OB_DEV void jvp(const T* w, int ldw_, T* out, int ldo) {
+    T* cur = s.tA;
+    T* nxt = s.tB;
+    for (int i = threadIdx.x; i < Rt * d.ldt; i += blockDim.x) {
+      const int r = i / d.ldt, k = i % d.ldt;
+      cur[i] = k < d.N ? w[r * ldw_ + k] : T(0);
+    }
+    __syncthreads();
+    for (int l = 0; l < d.L; ++l) {
+      const bool last = (l == d.L - 1);
+      const T* h = last ? nullptr : s.hid[l];
+      const T* z = (last || !d.need_pre) ? nullptr : s.pre[l];
+      const int ldh = d.lda[l + 1], ldt = d.ldt, act = d.act;
+      T* dst = last ? out : nxt;
+      gemm_nt<T, LR>(cur, ldt, Rt, W.W[l], d.ldw[l], d.w[l + 1], (d.w[l] + 3) & ~3,
+                     [&](int r, int n, T acc) {
+                       if (last) {
+                         dst[r * ldo + n] = acc;
+                       } else {
+                         const T a = h[r * ldh + n];
+                         dst[r * ldt + n] =
+                             Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + n] : a, act));
+                       }
+                     });
       __syncthreads();
       T* tmp = cur; cur = nxt; nxt = tmp;
-    }
-  }
-
-  // Tangent pass through the cached linearisation (time tangent held at 0,
-  // nn.py:177-180).  w: [Rp][ld_w] state tangent; out: [Rp][ld_o].
-  OB_DEV void jvp(const T* w, int ld_w, T* out, int ld_o) {
-    T* cur = s.dA;
-    T* nxt = s.dB;
-    for (int i = threadIdx.x; i < Rp * d.wp[0]; i += blockDim.x) {
-      const int r = i / d.wp[0], k = i % d.wp[0];
-      cur[r * d.maxwp + k] = k < d.N ? w[r * ld_w + k] : T(0);
-    }
-    __syncthreads();
-    for (int l = 0; l < d.L; ++l) {
-      const int nout = d.w[l + 1];
-      T* dst = (l == d.L - 1) ? out : nxt;
-      const int ldd = (l == d.L - 1) ? ld_o : d.maxwp;
-      affine_fwd<T, RB>(cur, d.maxwp, Rp, d.wp[l], W.wt[l], nullptr, nout, dst, ldd, nullptr, 0);
-      __syncthreads();
-      if (l < d.L - 1) {
-        for (int i = threadIdx.x; i < Rp * nout; i += blockDim.x) {
-          const int r = i / nout, n = i % nout;
-          nxt[r * d.maxwp + n] *= act_prime(s.pre[l][r * d.wp[l + 1] + n], d.act);
-        }
-        __syncthreads();
-        T* tmp = cur; cur = nxt; nxt = tmp;
-      }
     }
   }
 };
