@@ -22,11 +22,29 @@
 
 namespace ob {
 template <typename T> cudaError_t launch_pack(const PackParams<T>&, cudaStream_t);
-template <typename T> cudaError_t launch_rk(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
+template <typename T, bool WS>
+cudaError_t launch_rk_ws(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
+template <typename T, bool WS>
+cudaError_t launch_field_ws(const RkParams<T>&, int, int, size_t, int, double, const T*, const T*,
+                            T*, cudaStream_t);
 template <typename T> cudaError_t launch_reduce(const Dims&, const T*, int, long long, T*,
                                                 const double*, double, double*, cudaStream_t);
-template <typename T> cudaError_t launch_field_op(const RkParams<T>&, int, int, size_t, int, double,
-                                                  const T*, const T*, T*, cudaStream_t);
+
+// dispatch on where the weights live (fp32 only stages them in shared memory)
+template <typename T>
+cudaError_t launch_rk(const RkParams<T>& p, int lr, int tiles, size_t smem, cudaStream_t st,
+                      bool forward) {
+  if constexpr (sizeof(T) == 4)
+    if (p.sm.wts >= 0) return launch_rk_ws<T, true>(p, lr, tiles, smem, st, forward);
+  return launch_rk_ws<T, false>(p, lr, tiles, smem, st, forward);
+}
+template <typename T>
+cudaError_t launch_field_op(const RkParams<T>& p, int lr, int tiles, size_t smem, int mode,
+                            double t, const T* u, const T* w, T* out, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4)
+    if (p.sm.wts >= 0) return launch_field_ws<T, true>(p, lr, tiles, smem, mode, t, u, w, out, st);
+  return launch_field_ws<T, false>(p, lr, tiles, smem, mode, t, u, w, out, st);
+}
 }  // namespace ob
 
 using namespace ob;
@@ -194,18 +212,20 @@ void layout_smem(Plan& P) {
   s.jtv = take((long long)P.Rt * d.ldn);
   s.total = o;
   s.wts = -1;
-  if ((size_t)(o + d.n_packed) * P.esz <= kSmemLimit) {
+  // fp32 weights are staged in shared memory when they fit (fp64 kernels
+  // always read L1/L2-resident weights: halves the kernel instantiations)
+  if (P.esz == 4 && (size_t)(o + d.n_packed) * P.esz <= kSmemLimit) {
     s.wts = take(d.n_packed);
     s.total = o;
   }
   P.smem_bytes = (size_t)s.total * P.esz;
 }
 
-int pick_lr(int R) { return R <= 4 ? 1 : R <= 8 ? 2 : R <= 16 ? 4 : 8; }
+int pick_lr(int R) { return R <= 4 ? 1 : R <= 8 ? 2 : 8; }
 
 void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   int R = (int)std::max<long long>(1, (B + sm_count - 1) / sm_count);
-  R = std::min(R, 32);
+  R = std::min(R, P.esz == 8 ? 8 : 32);   // fp64 kernels are built for tiles of <= 8 rows
   for (;;) {
     P.R = R;
     P.LR = pick_lr(R);

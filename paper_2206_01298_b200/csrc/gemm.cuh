@@ -1,26 +1,64 @@
 // gemm.cuh -- register-tiled CTA GEMMs for the persistent sample-tile kernels.
 //
-// A CTA holds R (<= a few dozen) samples; its contractions are small GEMMs with
-// the sample rows on one side and a weight matrix (shared memory when it fits,
-// else L1/L2-resident global) on the other.  Every thread owns a 4 x 4 output
-// block (16 FMAs per 8 vector loads); a warp's 32 lanes are arranged LR x LC
-// (LR*LC = 32) so one warp covers a (4*LR) x (4*LC) tile.  Row r of a thread
-// block is r0 + lr + LR*i and column n is c0 + lc + LC*j (strided), which makes
-// every 16-byte shared-memory access conflict-free when leading dimensions are
-// "odd quads" (ld/4 odd, see ld_quad_odd).
+// A CTA holds R (<= 32) samples; its contractions are small GEMMs with the
+// sample rows on one side and a weight matrix (shared memory when it fits,
+// else L1/L2-resident global) on the other.  A thread owns a TR x TC output
+// block; a warp's 32 lanes are arranged LR x LC (LR*LC = 32) so one warp covers
+// a (TR*LR) x (TC*LC) tile.  Rows of a thread block are r0 + lr + LR*i and
+// columns c0 + lc + LC*j (strided), which makes every 16-byte shared-memory
+// access conflict-free when leading dimensions are "odd quads" (ld/4 odd).
+// Activation operands are always shared memory and are read with explicit
+// ld.shared vector loads; weights use ld.shared (WS) or ld.global.nc.
 //
-// Operands are row-major with the contraction dimension contiguous:
 //   gemm_nt : Z[r][n] = sum_k X[r][k] W[n][k]        (forward / JVP, z = W x)
 //   gemm_nn : O[r][k] = sum_n D[r][n] W[n][k]        (VJP input product d W)
 //   gemm_tn : M[n][k] += s * sum_r D[r][n] X[r][k]   (parameter cotangent)
-// Padding contract: X/D rows up to the row tile, columns up to the next 4 (and
-// W rows / columns up to the tile the op reads) exist and are finite; weight
-// padding is zero, so padded lanes contribute exact zeros.
+// Padding contract: operand rows up to the row tile and columns up to the next
+// multiple of 4 (weights: up to the column tile the op reads) exist and are
+// finite; weight padding is zero, so padded lanes contribute exact zeros.
 #pragma once
 
 #include "tile.cuh"
 
 namespace ob {
+
+OB_DEV uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <typename T> struct Ld;
+template <> struct Ld<float> {
+  static OB_DEV void s4(uint32_t a, float v[4]) {
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(a));
+  }
+  static OB_DEV void g4(const float* p, float v[4]) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  }
+};
+template <> struct Ld<double> {
+  static OB_DEV void s4(uint32_t a, double v[4]) {
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + 16));
+  }
+  static OB_DEV void g4(const double* p, double v[4]) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+};
+
+// weight operand: shared (byte address) or global pointer
+template <typename T, bool WS> struct WOp;
+template <typename T> struct WOp<T, true> {
+  uint32_t base;
+  OB_DEV WOp(const T* p) : base(smem_addr(p)) {}
+  OB_DEV void ld4(long long off, T v[4]) const { Ld<T>::s4(base + (uint32_t)(off * sizeof(T)), v); }
+};
+template <typename T> struct WOp<T, false> {
+  const T* base;
+  OB_DEV WOp(const T* p) : base(p) {}
+  OB_DEV void ld4(long long off, T v[4]) const { Ld<T>::g4(base + off, v); }
+};
 
 template <typename T> struct Vec4;
 template <> struct Vec4<float> {
@@ -48,80 +86,96 @@ OB_DEV int warp_id() { return threadIdx.x >> 5; }
 OB_DEV int lane_id() { return threadIdx.x & 31; }
 OB_DEV int n_warps() { return blockDim.x >> 5; }
 
-// Z[r][n] = sum_{k<Kp} X[r][k] * W[n][k];  epi(r, n, acc) for r < Rv... (caller
-// guards), n < N.  Rt = rows to compute (multiple of 4*LR).
-template <typename T, int LR, class Epi>
-OB_DEV void gemm_nt(const T* __restrict__ X, int ldx, int Rt, const T* __restrict__ W, int ldw,
-                    int N, int Kp, Epi epi) {
-  constexpr int LC = 32 / LR, RT = 4 * LR, CT = 4 * LC;
+// Warp range executing an op: warps [w0, w0 + nw) of the CTA.
+struct Warps {
+  int w0, nw;
+  OB_DEV static Warps all() { return {0, n_warps()}; }
+  OB_DEV bool mine() const { return warp_id() >= w0 && warp_id() < w0 + nw; }
+  OB_DEV int me() const { return warp_id() - w0; }
+};
+
+// Z[r][n] = sum_{k in [kb, ke)} X[r][k] * W[n][k];  epi(r, n, acc) for n < N.
+// Rt: rows to compute (multiple of TR*LR).  split > 1 partitions k into
+// `split` slices (multiples of 4) and calls epi(r, n, acc, slice).
+template <typename T, int TR, int TC, int LR, bool WS, class Epi>
+OB_DEV void gemm_nt(const T* X, int ldx, int Rt, const T* W, int ldw, int N, int Kp, Warps ws,
+                    int split, Epi epi) {
+  constexpr int LC = 32 / LR, RT = TR * LR, CT = TC * LC;
+  if (!ws.mine()) return;
   const int lr = lane_id() % LR, lc = lane_id() / LR;
   const int rtiles = Rt / RT, ctiles = (N + CT - 1) / CT;
-  for (int task = warp_id(); task < rtiles * ctiles; task += n_warps()) {
-    const int r0 = (task % rtiles) * RT + lr, c0 = (task / rtiles) * CT + lc;
-    T acc[4][4];
+  const int kq = Kp / 4, per = (kq + split - 1) / split;
+  const uint32_t xs = smem_addr(X);
+  const WOp<T, WS> wo(W);
+  for (int task = ws.me(); task < rtiles * ctiles * split; task += ws.nw) {
+    const int sl = task / (rtiles * ctiles), rc = task % (rtiles * ctiles);
+    const int r0 = (rc % rtiles) * RT + lr, c0 = (rc / rtiles) * CT + lc;
+    const int kb = sl * per * 4, ke = min(Kp, (sl + 1) * per * 4);
+    T acc[TR][TC];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TR; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
-    const T* xp = X + r0 * ldx;
-    const T* wp = W + c0 * ldw;
-    for (int k = 0; k < Kp; k += 4) {
-      T x[4][4], w[4][4];
+      for (int j = 0; j < TC; ++j) acc[i][j] = T(0);
+    for (int k = kb; k < ke; k += 4) {
+      T x[TR][4], w[TC][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) Vec4<T>::ld(xp + i * LR * ldx + k, x[i]);
+      for (int i = 0; i < TR; ++i)
+        Ld<T>::s4(xs + (uint32_t)(((r0 + i * LR) * ldx + k) * sizeof(T)), x[i]);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) Vec4<T>::ld(wp + j * LC * ldw + k, w[j]);
+      for (int j = 0; j < TC; ++j) wo.ld4((long long)(c0 + j * LC) * ldw + k, w[j]);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < TR; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = Num<T>::fma(x[i][q], w[j][q], acc[i][j]);
+          for (int j = 0; j < TC; ++j) acc[i][j] = Num<T>::fma(x[i][q], w[j][q], acc[i][j]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TR; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < TC; ++j) {
         const int n = c0 + j * LC;
-        if (n < N) epi(r0 + i * LR, n, acc[i][j]);
+        if (n < N) epi(r0 + i * LR, n, acc[i][j], sl);
       }
   }
 }
 
 // O[r][k] = sum_{n<Np} D[r][n] * W[n][k]; epi(r, k, acc) for k < K.  Thread
-// columns here are contiguous (k = c0 + 4*lc + j) so W rows load as one vector.
-template <typename T, int LR, class Epi>
-OB_DEV void gemm_nn(const T* __restrict__ D, int ldd, int Rt, const T* __restrict__ W, int ldw,
-                    int Np, int K, Epi epi) {
-  constexpr int LC = 32 / LR, RT = 4 * LR, CT = 4 * LC;
+// columns here are contiguous (k = c0 + TC*lc + j) so W rows load as vectors.
+template <typename T, int TR, int LR, bool WS, class Epi>
+OB_DEV void gemm_nn(const T* D, int ldd, int Rt, const T* W, int ldw, int Np, int K, Warps ws,
+                    Epi epi) {
+  constexpr int TC = 4, LC = 32 / LR, RT = TR * LR, CT = TC * LC;
+  if (!ws.mine()) return;
   const int lr = lane_id() % LR, lc = lane_id() / LR;
   const int rtiles = Rt / RT, ctiles = (K + CT - 1) / CT;
-  for (int task = warp_id(); task < rtiles * ctiles; task += n_warps()) {
-    const int r0 = (task % rtiles) * RT + lr, k0 = (task / rtiles) * CT + 4 * lc;
-    T acc[4][4];
+  const uint32_t ds = smem_addr(D);
+  const WOp<T, WS> wo(W);
+  for (int task = ws.me(); task < rtiles * ctiles; task += ws.nw) {
+    const int r0 = (task % rtiles) * RT + lr, k0 = (task / rtiles) * CT + TC * lc;
+    T acc[TR][TC];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TR; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
-    const T* dp = D + r0 * ldd;
-    const T* wp = W + k0;
+      for (int j = 0; j < TC; ++j) acc[i][j] = T(0);
     for (int n = 0; n < Np; n += 4) {
-      T d[4][4], w[4][4];
+      T d[TR][4], w[4][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) Vec4<T>::ld(dp + i * LR * ldd + n, d[i]);
+      for (int i = 0; i < TR; ++i)
+        Ld<T>::s4(ds + (uint32_t)(((r0 + i * LR) * ldd + n) * sizeof(T)), d[i]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) Vec4<T>::ld(wp + (n + q) * ldw, w[q]);
+      for (int q = 0; q < 4; ++q) wo.ld4((long long)(n + q) * ldw + k0, w[q]);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < TR; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = Num<T>::fma(d[i][q], w[q][j], acc[i][j]);
+          for (int j = 0; j < TC; ++j) acc[i][j] = Num<T>::fma(d[i][q], w[q][j], acc[i][j]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TR; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < TC; ++j)
         if (k0 + j < K) epi(r0 + i * LR, k0 + j, acc[i][j]);
   }
 }
@@ -131,12 +185,14 @@ OB_DEV void gemm_nn(const T* __restrict__ D, int ldd, int Rt, const T* __restric
 // block of M held in registers for the R-loop, then one vector read-modify-write.
 // The slot is private to the CTA, so plain RMW is race-free and deterministic.
 template <typename T>
-OB_DEV void gemm_tn_accum(const T* __restrict__ D, int ldd, const T* __restrict__ X, int ldx,
-                          int R, int N, int K, T scale, T* __restrict__ M, int ldm,
-                          T* __restrict__ mb) {
+OB_DEV void gemm_tn_accum(const T* D, int ldd, const T* X, int ldx, int R, int N, int K, T scale,
+                          T* __restrict__ M, int ldm, T* __restrict__ mb, Warps ws) {
+  if (!ws.mine()) return;
+  const int tid = ws.me() * 32 + lane_id(), nth = ws.nw * 32;
   const int nq = (N + 3) / 4, kq = (K + 3) / 4;
   const int items = nq * kq;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+  const uint32_t ds = smem_addr(D), xs = smem_addr(X);
+  for (int it = tid; it < items; it += nth) {
     const int n0 = (it / kq) * 4, k0 = (it % kq) * 4;
     T acc[4][4];
 #pragma unroll
@@ -145,8 +201,8 @@ OB_DEV void gemm_tn_accum(const T* __restrict__ D, int ldd, const T* __restrict_
       for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
     for (int r = 0; r < R; ++r) {
       T d[4], x[4];
-      Vec4<T>::ld(D + r * ldd + n0, d);
-      Vec4<T>::ld(X + r * ldx + k0, x);
+      Ld<T>::s4(ds + (uint32_t)((r * ldd + n0) * sizeof(T)), d);
+      Ld<T>::s4(xs + (uint32_t)((r * ldx + k0) * sizeof(T)), x);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -164,7 +220,7 @@ OB_DEV void gemm_tn_accum(const T* __restrict__ D, int ldd, const T* __restrict_
       }
     }
   }
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+  for (int n = tid; n < N; n += nth) {
     T s = T(0);
     for (int r = 0; r < R; ++r) s = Num<T>::add(s, D[r * ldd + n]);
     mb[n] = Num<T>::add(mb[n], Num<T>::mul(scale, s));

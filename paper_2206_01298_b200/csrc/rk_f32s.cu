@@ -1,0 +1,11 @@
+// rk_f32s.cu -- explicit instantiations of the persistent RK kernels (fp32, weights in shared memory); the
+// kernel families are split across translation units so they compile in parallel.
+#include "rk_impl.cuh"
+
+namespace ob {
+template cudaError_t launch_rk_ws<float, true>(const RkParams<float>&, int, int, size_t, cudaStream_t,
+                                               bool);
+template cudaError_t launch_field_ws<float, true>(const RkParams<float>&, int, int, size_t, int,
+                                                  double, const float*, const float*, float*,
+                                                  cudaStream_t);
+}  // namespace ob

@@ -1,4 +1,4 @@
-// rk_kernels.cu -- persistent explicit Runge-Kutta forward / discrete-adjoint
+// rk_impl.cuh -- persistent explicit Runge-Kutta forward / discrete-adjoint
 // reverse kernels (one CTA = one fixed tile of samples for the whole sweep).
 //
 // Forward: integrate (integrators.py:252-292) -> explicit_rk_step
@@ -9,6 +9,7 @@
 // (adjoint.py:67-94).  Stage sums ascend in j with the scalar (h*a_ij) formed
 // first and exact zeros skipped, with round-to-nearest mul/add (no FMA
 // contraction), reproducing the reference combination bit-for-bit in fp64.
+#pragma once
 #include <algorithm>
 
 #include "rk.cuh"
@@ -54,8 +55,8 @@ OB_DEV void setup_tile(const RkParams<T>& p, T* sm, MlpSmem<T>& ms, Weights<T>& 
 }
 
 // f(x0) -> out ([Rt][ldn]; columns >= N untouched)
-template <typename T, int LR>
-OB_DEV void field_eval(const RkParams<T>& p, MlpTile<T, LR>& mt, T* out) {
+template <typename T, int LR, bool WS>
+OB_DEV void field_eval(const RkParams<T>& p, MlpTile<T, LR, WS>& mt, T* out) {
   const int N = p.d.N, ldn = p.d.ldn;
   mt.forward(out, ldn, p.d.L);
   if (p.field_kind == OB_FIELD_STIFF) {  // a*u + s*mlp(u)
@@ -70,8 +71,8 @@ OB_DEV void field_eval(const RkParams<T>& p, MlpTile<T, LR>& mt, T* out) {
 }
 
 // ((df/du)^T w, mu += h * (df/dtheta)^T w) at the state in x0
-template <typename T, int LR>
-OB_DEV void field_vjp(const RkParams<T>& p, MlpTile<T, LR>& mt, const T* w, T* jtv, T* mu,
+template <typename T, int LR, bool WS>
+OB_DEV void field_vjp(const RkParams<T>& p, MlpTile<T, LR, WS>& mt, const T* w, T* jtv, T* mu,
                       double h, int Rv) {
   mt.forward(nullptr, 0, p.d.L - 1);  // hidden layers only: the output value is not needed
   const int ldn = p.d.ldn;
@@ -93,8 +94,8 @@ OB_DEV void field_vjp(const RkParams<T>& p, MlpTile<T, LR>& mt, const T* w, T* j
 // ks: this tile's stage-derivative scratch [s][Rt][ldn].  rec (nullable):
 // record base for this step ([s+1][B][N]).  On return `u` holds u_next.
 // Returns false (block-uniform) if u_next has a non-finite entry.
-template <typename T, int LR>
-OB_DEV bool rk_step_tile(const RkParams<T>& p, MlpTile<T, LR>& mt, T* u, T* ks, double t,
+template <typename T, int LR, bool WS>
+OB_DEV bool rk_step_tile(const RkParams<T>& p, MlpTile<T, LR, WS>& mt, T* u, T* ks, double t,
                          double h, bool carry, T* rec, int row0, int Rv) {
   const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0];
   const long long kst = (long long)Rt * ldn;
@@ -118,7 +119,7 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, MlpTile<T, LR>& mt, T* u, T* ks, 
       for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) ks[idx] = ks[(s - 1) * kst + idx];
       __syncthreads();
     } else {
-      field_eval<T, LR>(p, mt, ks + i * kst);
+      field_eval<T, LR, WS>(p, mt, ks + i * kst);
     }
   }
   int bad = 0;
@@ -153,7 +154,7 @@ OB_DEV void store_rows(T* dst, int N, const T* src, int lds, int row0, int Rv) {
 }
 
 // --------------------------------------------------------------- forward
-template <typename T, int LR>
+template <typename T, int LR, bool WS>
 __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_constant__ RkParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -164,7 +165,11 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
-  MlpTile<T, LR> mt(p.d, W, ms, p.Rt);
+  MlpTile<T, LR, WS> mt(p.d, W, ms, p.Rt);
+  // split-K scratch: the same lamn | w | jtv region as the reverse kernel's
+  // replays, so forward and replayed steps sum identically (bit-identical records)
+  mt.scratch = sm + p.sm.lamn;
+  mt.scratch_elems = p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn;
   T* u = sm + p.sm.u;
   T* ks = p.scratch + tile * p.scratch_stride;
   const int N = p.d.N, ldn = p.d.ldn;
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
       __syncthreads();
     }
     T* rec = p.fwd_rec[n] >= 0 ? p.rec + (long long)p.fwd_rec[n] * (p.s + 1) * vec : nullptr;
-    const bool ok = rk_step_tile<T, LR>(p, mt, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv);
+    const bool ok = rk_step_tile<T, LR, WS>(p, mt, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv);
     if (!ok) {  // integrators.py:219-220
       if (threadIdx.x == 0) set_status(p.status, OB_ERR_INTEGRATION, n);
       return;
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
 }
 
 // --------------------------------------------------------------- reverse
-template <typename T, int LR>
+template <typename T, int LR, bool WS>
 __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_constant__ RkParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -222,7 +227,9 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
-  MlpTile<T, LR> mt(p.d, W, ms, p.Rt);
+  MlpTile<T, LR, WS> mt(p.d, W, ms, p.Rt);
+  mt.scratch = sm + p.sm.lamn;                 // lamn | w | jtv are free during replays
+  mt.scratch_elems = p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn;
   const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0];
   const long long vec = (long long)p.B * N;
   const long long kst = (long long)Rt * ldn;
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       load_rows(u, ldn, srcp, N, row0, Rv);
       __syncthreads();
       T* rec = p.rec + (long long)op.w * (s + 1) * vec;
-      rk_step_tile<T, LR>(p, mt, u, ks, t, h, false, rec, row0, Rv);
+      rk_step_tile<T, LR, WS>(p, mt, u, ks, t, h, false, rec, row0, Rv);
       continue;
     }
     // REVERSE(n) from record buffer op.w: rk_adjoint_step (adjoint.py:67-94)
@@ -289,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       if (p.d.time_input)
         for (int r = threadIdx.x; r < Rt; r += blockDim.x) ms.x0[r * ld0 + N] = T(t + p.c[i] * h);
       __syncthreads();
-      field_vjp<T, LR>(p, mt, w, jtv, mu, h, Rv);
+      field_vjp<T, LR, WS>(p, mt, w, jtv, mu, h, Rv);
       // Lam_i = h * jtv; lam_n += Lam_i
       for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
         const int o = (idx / N) * ldn + idx % N;
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
 }
 
 // Field protocol ops on a batch (integrators.py:53-102): eval / jvp / vjp / vjp_u.
-template <typename T, int LR>
+template <typename T, int LR, bool WS>
 __global__ void __launch_bounds__(kThreads, 1)
 field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const T* u,
                 const T* w, T* out) {
@@ -326,7 +333,7 @@ field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
-  MlpTile<T, LR> mt(p.d, W, ms, p.Rt);
+  MlpTile<T, LR, WS> mt(p.d, W, ms, p.Rt);
   const int N = p.d.N, ldn = p.d.ldn, ld0 = p.d.lda[0];
   T* wb = sm + p.sm.w;
   T* res = sm + p.sm.jtv;
@@ -339,7 +346,7 @@ field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const
   if (mode != 0) load_rows(wb, ldn, w, N, row0, Rv);
   __syncthreads();
   if (mode == 0) {
-    field_eval<T, LR>(p, mt, res);
+    field_eval<T, LR, WS>(p, mt, res);
   } else if (mode == 1) {
     mt.forward(nullptr, 0, p.d.L - 1);
     mt.jvp(wb, ldn, res, ldn);
@@ -351,7 +358,7 @@ field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const
       __syncthreads();
     }
   } else {
-    field_vjp<T, LR>(p, mt, wb, res, mode == 2 ? p.mu + tile * p.d.n_mu : nullptr, 1.0, Rv);
+    field_vjp<T, LR, WS>(p, mt, wb, res, mode == 2 ? p.mu + tile * p.d.n_mu : nullptr, 1.0, Rv);
   }
   store_rows(out, N, res, ldn, row0, Rv);
 }
@@ -416,32 +423,37 @@ static cudaError_t launch_smem(K kf, int grid, size_t smem, cudaStream_t st, A..
   return cudaGetLastError();
 }
 
-template <typename T, int LR>
+template <typename T, int LR, bool WS>
 static cudaError_t launch_rk_lr(const RkParams<T>& p, int tiles, size_t smem, cudaStream_t st,
                                 bool forward) {
-  return forward ? launch_smem(rk_forward_kernel<T, LR>, tiles, smem, st, p)
-                 : launch_smem(rk_reverse_kernel<T, LR>, tiles, smem, st, p);
+  return forward ? launch_smem(rk_forward_kernel<T, LR, WS>, tiles, smem, st, p)
+                 : launch_smem(rk_reverse_kernel<T, LR, WS>, tiles, smem, st, p);
 }
 
-template <typename T>
-cudaError_t launch_rk(const RkParams<T>& p, int lr, int tiles, size_t smem, cudaStream_t st,
-                      bool forward) {
+// lane-row variants: LR 1 / 2 / 8 (tiles of <= 4, <= 8, <= 32 samples; fp64 tiles
+// are capped at 8 rows by the planner)
+template <typename T, bool WS>
+cudaError_t launch_rk_ws(const RkParams<T>& p, int lr, int tiles, size_t smem, cudaStream_t st,
+                         bool forward) {
   switch (lr) {
-    case 1: return launch_rk_lr<T, 1>(p, tiles, smem, st, forward);
-    case 2: return launch_rk_lr<T, 2>(p, tiles, smem, st, forward);
-    case 4: return launch_rk_lr<T, 4>(p, tiles, smem, st, forward);
-    default: return launch_rk_lr<T, 8>(p, tiles, smem, st, forward);
+    case 1: return launch_rk_lr<T, 1, WS>(p, tiles, smem, st, forward);
+    case 2: return launch_rk_lr<T, 2, WS>(p, tiles, smem, st, forward);
+    default:
+      if constexpr (sizeof(T) == 4) return launch_rk_lr<T, 8, WS>(p, tiles, smem, st, forward);
+      return cudaErrorInvalidConfiguration;
   }
 }
 
-template <typename T>
-cudaError_t launch_field_op(const RkParams<T>& p, int lr, int tiles, size_t smem, int mode,
+template <typename T, bool WS>
+cudaError_t launch_field_ws(const RkParams<T>& p, int lr, int tiles, size_t smem, int mode,
                             double t, const T* u, const T* w, T* out, cudaStream_t st) {
   switch (lr) {
-    case 1: return launch_smem(field_op_kernel<T, 1>, tiles, smem, st, p, mode, t, u, w, out);
-    case 2: return launch_smem(field_op_kernel<T, 2>, tiles, smem, st, p, mode, t, u, w, out);
-    case 4: return launch_smem(field_op_kernel<T, 4>, tiles, smem, st, p, mode, t, u, w, out);
-    default: return launch_smem(field_op_kernel<T, 8>, tiles, smem, st, p, mode, t, u, w, out);
+    case 1: return launch_smem(field_op_kernel<T, 1, WS>, tiles, smem, st, p, mode, t, u, w, out);
+    case 2: return launch_smem(field_op_kernel<T, 2, WS>, tiles, smem, st, p, mode, t, u, w, out);
+    default:
+      if constexpr (sizeof(T) == 4)
+        return launch_smem(field_op_kernel<T, 8, WS>, tiles, smem, st, p, mode, t, u, w, out);
+      return cudaErrorInvalidConfiguration;
   }
 }
 
@@ -453,18 +465,5 @@ cudaError_t launch_reduce(const Dims& d, const T* mu, int tiles, long long np, T
                                                                     inv_b, loss);
   return cudaGetLastError();
 }
-
-template cudaError_t launch_pack<float>(const PackParams<float>&, cudaStream_t);
-template cudaError_t launch_pack<double>(const PackParams<double>&, cudaStream_t);
-template cudaError_t launch_rk<float>(const RkParams<float>&, int, int, size_t, cudaStream_t, bool);
-template cudaError_t launch_rk<double>(const RkParams<double>&, int, int, size_t, cudaStream_t, bool);
-template cudaError_t launch_field_op<float>(const RkParams<float>&, int, int, size_t, int, double,
-                                            const float*, const float*, float*, cudaStream_t);
-template cudaError_t launch_field_op<double>(const RkParams<double>&, int, int, size_t, int, double,
-                                             const double*, const double*, double*, cudaStream_t);
-template cudaError_t launch_reduce<float>(const Dims&, const float*, int, long long, float*,
-                                          const double*, double, double*, cudaStream_t);
-template cudaError_t launch_reduce<double>(const Dims&, const double*, int, long long, double*,
-                                           const double*, double, double*, cudaStream_t);
 
 }  // namespace ob

@@ -142,39 +142,89 @@ template <typename T> OB_DEV T act_prime_from(T a, T z, int id) {
 namespace ob {
 
 // ------------------------------------------------------------- MLP tile
-template <typename T, int LR>
+// LR: lane rows of the wide 4x4 GEMM variant (row tile 4*LR); the narrow 2x4
+// variant uses 2*LR lane rows (same row tile, half the column tile) so layers
+// of width ~64 still occupy every warp.  WS: weights in shared memory.
+template <typename T, int LR, bool WS>
 struct MlpTile {
   const Dims& d;
   const Weights<T>& W;
   MlpSmem<T>& s;
   int Rt;
+  T* scratch;          // split-K partials for narrow output layers (nullable)
+  int scratch_elems;
 
   OB_DEV MlpTile(const Dims& d_, const Weights<T>& W_, MlpSmem<T>& s_, int Rt_)
-      : d(d_), W(W_), s(s_), Rt(Rt_) {}
+      : d(d_), W(W_), s(s_), Rt(Rt_), scratch(nullptr), scratch_elems(0) {}
 
   OB_DEV const T* in(int l) const { return l == 0 ? s.x0 : s.hid[l - 1]; }
 
-  // Layers [0, nl) from x0; the last of them writes z = W a + b to out[r*ldo+n]
-  // when nl == L (hidden layers store act(z) into hid, and z into pre if needed).
+  static constexpr int kWideCT = 4 * (32 / LR);
+  static constexpr int kNarrowCT = 4 * (32 / (2 * LR));
+  OB_DEV int tasks_wide(int n) const { return (Rt / (4 * LR)) * ((n + kWideCT - 1) / kWideCT); }
+  OB_DEV int tasks_narrow(int n) const { return (Rt / (4 * LR)) * ((n + kNarrowCT - 1) / kNarrowCT); }
+
+  template <class Epi>
+  OB_DEV void nt(const T* X, int ldx, int l, int split, Warps ws, Epi epi) {
+    const int N = d.w[l + 1], Kp = (d.w[l] + 3) & ~3;
+    if (tasks_wide(N) * split >= ws.nw || 2 * LR > 32)
+      gemm_nt<T, 4, 4, LR, WS>(X, ldx, Rt, W.W[l], d.ldw[l], N, Kp, ws, split, epi);
+    else
+      gemm_nt<T, 2, 4, (2 * LR > 32 ? 32 : 2 * LR), WS>(X, ldx, Rt, W.W[l], d.ldw[l], N, Kp, ws,
+                                                         split, epi);
+  }
+  template <class Epi>
+  OB_DEV void nn(const T* D, int ldD, int l, int K, Warps ws, Epi epi) {
+    const int Np = (d.w[l + 1] + 3) & ~3;
+    if (tasks_wide(K) >= ws.nw || 2 * LR > 32)
+      gemm_nn<T, 4, LR, WS>(D, ldD, Rt, W.W[l], d.ldw[l], Np, K, ws, epi);
+    else
+      gemm_nn<T, 2, (2 * LR > 32 ? 32 : 2 * LR), WS>(D, ldD, Rt, W.W[l], d.ldw[l], Np, K, ws, epi);
+  }
+
+  // Layers [0, nl) from x0; when nl == L the last writes z = W a + b to
+  // out[r*ldo+n] (hidden layers store act(z) into hid, and z into pre if needed).
   OB_DEV void forward(T* out, int ldo, int nl) {
     for (int l = 0; l < nl; ++l) {
       const T* b = W.bias[l];
       const bool last = (l == d.L - 1);
-      const int ldh = d.lda[l + 1];
-      T* hid = last ? nullptr : s.hid[l];
-      T* pre = (last || !d.need_pre) ? nullptr : s.pre[l];
-      const int act = d.act;
-      gemm_nt<T, LR>(in(l), d.lda[l], Rt, W.W[l], d.ldw[l], d.w[l + 1], (d.w[l] + 3) & ~3,
-                     [&](int r, int n, T acc) {
-                       const T z = Num<T>::add(acc, b[n]);
-                       if (last) {
-                         out[r * ldo + n] = z;
-                       } else {
-                         hid[r * ldh + n] = act_fn(z, act);
-                         if (pre) pre[r * ldh + n] = z;
-                       }
-                     });
-      __syncthreads();
+      const int ldh = d.lda[l + 1], N = d.w[l + 1];
+      if (last) {
+        // narrow output layer: deterministic split-K through the scratch partials
+        int split = 1;
+        const int tn = tasks_narrow(N);
+        if (scratch && tn < n_warps()) {
+          split = min(n_warps() / max(tn, 1), scratch_elems / (Rt * N));
+          split = max(1, min(split, (d.w[l] + 3) / 4));
+        }
+        if (split == 1) {
+          nt(in(l), d.lda[l], l, 1, Warps::all(),
+             [&](int r, int n, T acc, int) { out[r * ldo + n] = Num<T>::add(acc, b[n]); });
+          __syncthreads();
+        } else {
+          T* part = scratch;
+          const int pst = Rt * N;
+          nt(in(l), d.lda[l], l, split, Warps::all(),
+             [&](int r, int n, T acc, int sl) { part[sl * pst + r * N + n] = acc; });
+          __syncthreads();
+          for (int i = threadIdx.x; i < Rt * N; i += blockDim.x) {
+            T acc = part[i];
+            for (int sl = 1; sl < split; ++sl) acc = Num<T>::add(acc, part[sl * pst + i]);
+            out[(i / N) * ldo + i % N] = Num<T>::add(acc, b[i % N]);
+          }
+          __syncthreads();
+        }
+      } else {
+        T* hid = s.hid[l];
+        T* pre = d.need_pre ? s.pre[l] : nullptr;
+        const int act = d.act;
+        nt(in(l), d.lda[l], l, 1, Warps::all(), [&](int r, int n, T acc, int) {
+          const T z = Num<T>::add(acc, b[n]);
+          hid[r * ldh + n] = act_fn(z, act);
+          if (pre) pre[r * ldh + n] = z;
+        });
+        __syncthreads();
+      }
     }
   }
 
@@ -187,26 +237,33 @@ struct MlpTile {
     for (int l = d.L - 1; l >= 0; --l) {
       const T* D = (l == d.L - 1) ? v : s.hid[l];
       const int ldD = (l == d.L - 1) ? ldv : d.lda[l + 1];
-      if (mu) {
-        gemm_tn_accum<T>(D, ldD, in(l), d.lda[l], Rv, d.w[l + 1], d.w[l], scale, mu + d.mwoff[l],
-                         d.ldm[l], mu + d.mboff[l]);
-        __syncthreads();
-      }
-      const int Np = (d.w[l + 1] + 3) & ~3;
       if (l > 0) {
+        if (mu) {
+          gemm_tn_accum<T>(D, ldD, in(l), d.lda[l], Rv, d.w[l + 1], d.w[l], scale,
+                           mu + d.mwoff[l], d.ldm[l], mu + d.mboff[l], Warps::all());
+          __syncthreads();
+        }
         T* h = s.hid[l - 1];
         const T* z = d.need_pre ? s.pre[l - 1] : nullptr;
-        const int ldh = d.lda[l];
-        const int act = d.act;
-        gemm_nn<T, LR>(D, ldD, Rt, W.W[l], d.ldw[l], Np, d.w[l], [&](int r, int k, T acc) {
+        const int ldh = d.lda[l], act = d.act;
+        nn(D, ldD, l, d.w[l], Warps::all(), [&](int r, int k, T acc) {
           const T a = h[r * ldh + k];
           h[r * ldh + k] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + k] : a, act));
         });
-      } else if (jtv) {
-        gemm_nn<T, LR>(D, ldD, Rt, W.W[0], d.ldw[0], Np, d.N,
-                       [&](int r, int k, T acc) { jtv[r * ldo + k] = acc; });
+        __syncthreads();
+      } else {
+        // first layer: the input product (narrow, N columns) and the dW0
+        // accumulation read the same operands -> one phase on split warps
+        const int nw = n_warps();
+        const bool both = mu && jtv;
+        const Warps wn = both ? Warps{0, nw / 2} : Warps::all();
+        const Warps wa = both ? Warps{nw / 2, nw - nw / 2} : Warps::all();
+        if (jtv) nn(D, ldD, 0, d.N, wn, [&](int r, int k, T acc) { jtv[r * ldo + k] = acc; });
+        if (mu)
+          gemm_tn_accum<T>(D, ldD, s.x0, d.lda[0], Rv, d.w[1], d.w[0], scale, mu + d.mwoff[0],
+                           d.ldm[0], mu + d.mboff[0], wa);
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
 
@@ -227,16 +284,14 @@ struct MlpTile {
       const T* z = (last || !d.need_pre) ? nullptr : s.pre[l];
       const int ldh = d.lda[l + 1], ldt = d.ldt, act = d.act;
       T* dst = last ? out : nxt;
-      gemm_nt<T, LR>(cur, ldt, Rt, W.W[l], d.ldw[l], d.w[l + 1], (d.w[l] + 3) & ~3,
-                     [&](int r, int n, T acc) {
-                       if (last) {
-                         dst[r * ldo + n] = acc;
-                       } else {
-                         const T a = h[r * ldh + n];
-                         dst[r * ldt + n] =
-                             Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + n] : a, act));
-                       }
-                     });
+      nt(cur, ldt, l, 1, Warps::all(), [&](int r, int n, T acc, int) {
+        if (last) {
+          dst[r * ldo + n] = acc;
+        } else {
+          const T a = h[r * ldh + n];
+          dst[r * ldt + n] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + n] : a, act));
+        }
+      });
       __syncthreads();
       T* tmp = cur; cur = nxt; nxt = tmp;
     }

@@ -30,9 +30,7 @@ def _lib():
     if not torch.cuda.is_available():
         pytest.fail("GPU tests need a CUDA device")
     from paper_2206_01298_b200 import _lib as L
-    from paper_2206_01298_b200 import build
-    build.build()
-    L.load()
+    L.load()      # the prebuilt in-tree library; a missing one fails loudly
 
 
 def oracle_run(ci, policy=None):

@@ -19,8 +19,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2206_01298_b200 import build
-    build.build()
+    import os
+    if not os.path.exists(_lib.LIB_PATH):      # CPU container: build once if absent
+        from paper_2206_01298_b200 import build
+        build.build()
     return _lib.load()
 
 
