@@ -29,6 +29,8 @@ cudaError_t launch_field_ws(const RkParams<T>&, int, int, size_t, int, double, c
                             T*, cudaStream_t);
 template <typename T> cudaError_t launch_reduce(const Dims&, const T*, int, long long, T*,
                                                 const double*, double, double*, cudaStream_t);
+template <typename T>
+cudaError_t launch_theta(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
 
 // dispatch on where the weights live (fp32 only stages them in shared memory)
 template <typename T>
@@ -112,6 +114,9 @@ struct Plan {
   Dims d{};
   int R = 1, Rt = 4, LR = 1, tiles = 1;
   bool need_jvp = false;
+  bool theta = false;
+  size_t off_kry = 0, off_stats = 0;
+  long long krylov_stride = 0;
   SmemLayout sm{};
   size_t smem_bytes = 0;
   // checkpoint program
@@ -210,6 +215,7 @@ void layout_smem(Plan& P) {
   s.lamn = take((long long)P.Rt * d.ldn);
   s.w = take((long long)P.Rt * d.ldn);
   s.jtv = take((long long)P.Rt * d.ldn);
+  for (int i = 0; i < 8; ++i) s.vec[i] = P.theta ? take((long long)P.Rt * d.ldn) : -1;
   s.total = o;
   s.wts = -1;
   // fp32 weights are staged in shared memory when they fit (fp64 kernels
@@ -348,8 +354,19 @@ int compile_policy(const ob_problem& p, Plan& P) {
 int plan_problem(const ob_problem& p, Plan& P) {
   int st = check_field(p.field);
   if (st) return st;
-  if (p.scheme.kind != OB_SCHEME_RK)
-    return fail(OB_ERR_UNSUPPORTED, "theta schemes are not built into this library version");
+  P.theta = (p.scheme.kind == OB_SCHEME_THETA);
+  if (P.theta) {
+    if (!(p.scheme.theta > 0.0 && p.scheme.theta <= 1.0)) return fail(OB_ERR_VALUE, "theta must lie in (0, 1]");
+    if (p.scheme.stages != 2) return fail(OB_ERR_VALUE, "theta schemes carry 2 stage states");
+    const ob_solver_cfg& sc = p.solver;
+    if (!(sc.newton_tol > 0 && sc.newton_tol < 1 && sc.gmres_tol > 0 && sc.gmres_tol < 1))
+      return fail(OB_ERR_VALUE, "tolerances must lie in (0, 1)");
+    if (sc.newton_maxit < 1 || sc.gmres_maxit < 1 || sc.gmres_restart < 1)
+      return fail(OB_ERR_VALUE, "iteration caps must be >= 1");
+    P.need_jvp = true;
+  } else if (p.scheme.kind != OB_SCHEME_RK) {
+    return fail(OB_ERR_VALUE, "unknown scheme kind");
+  }
   if (p.scheme.stages < 1 || p.scheme.stages > OB_MAX_STAGES) return fail(OB_ERR_VALUE, "bad stage count");
   if (p.n_steps < 1) return fail(OB_ERR_VALUE, "fixed mode requires at least one step");
   if (p.batch < 1) return fail(OB_ERR_VALUE, "batch must be >= 1");
@@ -373,7 +390,7 @@ int plan_problem(const ob_problem& p, Plan& P) {
   // zero-cotangent stages: b_i == 0 and a_ji == 0 for all j > i  (dopri5 stage 7)
   const int s = p.scheme.stages;
   P.skip_vjp = 0;
-  for (int i = 0; i < s; ++i) {
+  for (int i = 0; i < s && !P.theta; ++i) {
     bool zero = p.scheme.b[i] == 0.0;
     for (int j = i + 1; j < s && zero; ++j) zero = p.scheme.a[j * OB_MAX_STAGES + i] == 0.0;
     if (zero) P.skip_vjp |= 1u << i;
@@ -386,6 +403,9 @@ int plan_problem(const ob_problem& p, Plan& P) {
   c.steps_accepted = nt;
   c.device_rhs_evals = c.nfe_forward;
   c.device_vjp_evals = (s - __builtin_popcount(P.skip_vjp)) * nt;
+  if (P.theta) {  // data dependent: filled from the per-sample device counters after the run
+    c.nfe_forward = c.nfe_backward = c.device_rhs_evals = c.device_vjp_evals = 0;
+  }
   c.tile_rows = P.R;
   c.tiles = P.tiles;
   c.kernel_launches = 4;
@@ -411,6 +431,14 @@ int plan_problem(const ob_problem& p, Plan& P) {
   o = align_up(o + P.esz * (size_t)P.tiles * P.scratch_stride, 256);
   P.off_mu = o;
   o = align_up(o + P.esz * (size_t)P.tiles * P.d.n_mu, 256);
+  P.off_kry = o;
+  if (P.theta) {
+    const long long m = std::min(p.solver.gmres_restart, P.d.N);
+    P.krylov_stride = (long long)P.Rt * ((m + 1) * P.d.ldn + (m + 1) * m + 2 * m + (m + 1) + m);
+    o = align_up(o + P.esz * (size_t)P.tiles * P.krylov_stride, 256);
+  }
+  P.off_stats = o;
+  o = align_up(o + sizeof(int) * (size_t)p.batch * OB_NSTATS, 256);
   P.off_lp = o;
   o = align_up(o + sizeof(double) * P.tiles, 256);
   P.total = o;
@@ -473,6 +501,17 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   rp.loss_part = reinterpret_cast<double*>(ws + P.off_lp);
   int* status = reinterpret_cast<int*>(ws + P.off_blob + o_stat);
   rp.status = status;
+  rp.theta = p.scheme.theta;
+  rp.newton_tol = p.solver.newton_tol;
+  rp.gmres_tol = p.solver.gmres_tol;
+  rp.newton_maxit = p.solver.newton_maxit;
+  rp.gmres_maxit = p.solver.gmres_maxit;
+  rp.gmres_restart = p.solver.gmres_restart;
+  rp.krylov = reinterpret_cast<T*>(ws + P.off_kry);
+  rp.krylov_stride = P.krylov_stride;
+  int* stats = reinterpret_cast<int*>(ws + P.off_stats);
+  rp.sample_stats = stats;
+  CU(cudaMemsetAsync(stats, 0, sizeof(int) * (size_t)p.batch * OB_NSTATS, st));
 
   // per-phase CUDA events on the launch stream (bench roofline timing)
   static thread_local cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -482,16 +521,35 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   CU(cudaEventRecord(ev[0], st));
   CU(launch_pack<T>(pp, st));
   CU(cudaEventRecord(ev[1], st));
-  CU(launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, true));
+  if (P.theta) CU(launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, true));
+  else CU(launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, true));
   CU(cudaEventRecord(ev[2], st));
-  CU(launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, false));
+  if (P.theta) CU(launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, false));
+  else CU(launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, false));
   CU(cudaEventRecord(ev[3], st));
   CU(launch_reduce<T>(P.d, rp.mu, P.tiles, p.field.n_params, static_cast<T*>(b.dtheta),
                       rp.loss_part, rp.inv_batch_global, b.loss, st));
   CU(cudaEventRecord(ev[4], st));
   int hs[2] = {0, 0};
   CU(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  std::vector<int> hstats;
+  if (P.theta) {
+    hstats.resize((size_t)p.batch * OB_NSTATS);
+    CU(cudaMemcpyAsync(hstats.data(), stats, sizeof(int) * hstats.size(), cudaMemcpyDeviceToHost, st));
+  }
+  if (b.sample_stats)
+    CU(cudaMemcpyAsync(b.sample_stats, stats, sizeof(int) * (size_t)p.batch * OB_NSTATS,
+                       cudaMemcpyDeviceToDevice, st));
   CU(cudaStreamSynchronize(st));
+  if (P.theta) {  // reference-semantics NFE of the critical-path trajectory (max over samples)
+    long long mf = 0, mb = 0;
+    for (long long i = 0; i < p.batch; ++i) {
+      mf = std::max<long long>(mf, hstats[i * OB_NSTATS + OB_STAT_NFE_F]);
+      mb = std::max<long long>(mb, hstats[i * OB_NSTATS + OB_STAT_NFE_B]);
+    }
+    P.cnt.nfe_forward = P.cnt.device_rhs_evals = mf;
+    P.cnt.nfe_backward = P.cnt.device_vjp_evals = mb;
+  }
   float ms[4] = {0, 0, 0, 0};
   for (int i = 0; i < 4; ++i) CU(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
   P.cnt.ms_pack = ms[0];
@@ -505,6 +563,9 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
       snprintf(msg, sizeof msg, "state overflowed at t=%.17g (h=%.17g)", t, h);
     } else if (hs[0] == OB_ERR_GRADIENT_EXPLOSION) {
       snprintf(msg, sizeof msg, "non-finite adjoint state in reverse sweep (step %d)", hs[1]);
+    } else if (hs[0] == OB_ERR_CONVERGENCE) {
+      const double t = p.times[hs[1]];
+      snprintf(msg, sizeof msg, "implicit step at t=%.17g failed: Newton/GMRES did not converge", t);
     } else if (hs[0] == OB_ERR_VALUE) {
       snprintf(msg, sizeof msg, "vector contains non-finite entries");
     } else {

@@ -14,6 +14,7 @@ enum { kSrcU0 = 0, kSrcRecNext = 1, kSrcSol = 2 };
 struct SmemLayout {      // offsets in elements of T (-1: not allocated)
   int x0, hid[OB_MAX_LAYERS], pre[OB_MAX_LAYERS], tA, tB;
   int u, lam, lamn, w, jtv;
+  int vec[8];             // theta-method work vectors [Rt][ldn] (-1 when unused)
   int wts;                // packed weights staged in shared memory, or -1
   int total;
 };
@@ -55,6 +56,13 @@ struct RkParams {
   long long n_params;
   double* loss_part;      // [tiles]
   int* status;            // [2] first error code, step
+  // theta methods (integrators.py:225-244, linalg.py:37-142)
+  double theta;
+  double newton_tol, gmres_tol;
+  int newton_maxit, gmres_maxit, gmres_restart;
+  T* krylov;              // per tile: Q [R][m+1][ldn] | H [R][m+1][m] | cs, sn [R][m] | g [R][m+1] | y [R][m]
+  long long krylov_stride;
+  int* sample_stats;      // [B][OB_NSTATS] per-sample counters (nullable)
 };
 
 template <typename T>

@@ -267,6 +267,42 @@ struct MlpTile {
     }
   }
 
+  // Reverse pass that keeps the cached forward intact (repeated transposed
+  // products at one linearisation point, e.g. the adjoint GMRES): layer
+  // cotangents ping-pong through tA/tB, and each layer's parameter
+  // accumulation runs on half the warps beside its input product.
+  OB_DEV void vjp_keep(const T* v, int ldv, int Rv, T* jtv, int ldo, T* mu, T scale) {
+    const T* cur = v;
+    int ldc = ldv;
+    T* bufs[2] = {s.tA, s.tB};
+    int nb = 0;
+    const int nw = n_warps();
+    for (int l = d.L - 1; l >= 0; --l) {
+      const bool both = mu && (l > 0 || jtv);
+      const Warps wn = both ? Warps{0, nw / 2} : Warps::all();
+      const Warps wa = both ? Warps{nw / 2, nw - nw / 2} : Warps::all();
+      T* dst = bufs[nb];
+      if (l > 0) {
+        const T* h = s.hid[l - 1];
+        const T* z = d.need_pre ? s.pre[l - 1] : nullptr;
+        const int ldh = d.lda[l], ldt = d.ldt, act = d.act;
+        nn(cur, ldc, l, d.w[l], wn, [&](int r, int k, T acc) {
+          const T a = h[r * ldh + k];
+          dst[r * ldt + k] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + k] : a, act));
+        });
+      } else if (jtv) {
+        nn(cur, ldc, 0, d.N, wn, [&](int r, int k, T acc) { jtv[r * ldo + k] = acc; });
+      }
+      if (mu)
+        gemm_tn_accum<T>(cur, ldc, in(l), d.lda[l], Rv, d.w[l + 1], d.w[l], scale,
+                         mu + d.mwoff[l], d.ldm[l], mu + d.mboff[l], wa);
+      __syncthreads();
+      cur = dst;
+      ldc = d.ldt;
+      nb ^= 1;
+    }
+  }
+
   // Tangent pass through the cached linearisation (forward(.., L-1) must have
   // run; time tangent held at 0, nn.py:177-180).  w: [Rt][ldw_] (rows/cols
   // beyond the state zero); out: [Rt][ldo].

@@ -34,6 +34,10 @@ class GradResult:
     u_final: object
     store_counters: StoreCounters = None
     device: dict = dc_field(default_factory=dict)
+    # per-sample reference counters (numpy int arrays over the batch): nfe_forward,
+    # nfe_backward, newton_iters, gmres_iters_forward, gmres_iters_adjoint
+    # (implicit schemes; explicit ones repeat the schedule-fixed counts)
+    sample_counters: dict = None
 
 
 _WS_CACHE = {}
@@ -118,7 +122,8 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     bufs.loss = loss_t.data_ptr()
     bufs.workspace = ws.data_ptr()
     bufs.workspace_bytes = ws.numel()
-    bufs.sample_stats = None
+    stats = torch.zeros((B, _lib.OB_NSTATS), dtype=torch.int32, device=dev)
+    bufs.sample_stats = stats.data_ptr()
     cnt = _lib.Counters()
     rc = _lib.load().ob_grad(C.byref(prob), C.byref(bufs), C.byref(cnt), stream_ptr())
     raise_status(rc, _lib.last_error())
@@ -129,10 +134,18 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     counters.steps_recomputed += c["steps_recomputed"]
     sc = StoreCounters(c["stored_states"], c["stored_stage_vectors"], c["max_live_slots"],
                        c["recomputed_steps"])
+    if scheme.kind == "theta":
+        st = stats.cpu().numpy().astype(np.int64)
+        samp = {"nfe_forward": st[:, 0], "nfe_backward": st[:, 1], "newton_iters": st[:, 2],
+                "gmres_iters_forward": st[:, 3], "gmres_iters_adjoint": st[:, 4]}
+    else:
+        samp = {"nfe_forward": np.full(B, c["nfe_forward"]),
+                "nfe_backward": np.full(B, c["nfe_backward"])}
     loss_v = float(loss_t.item())
     if host_io:
         dtheta_o, du0_o, uf_o = dtheta.cpu().numpy(), du0.cpu().numpy(), u_final.cpu().numpy()
     else:
         dtheta_o, du0_o, uf_o = dtheta, du0, u_final
     return GradResult(dtheta=dtheta_o, du0=du0_o, loss=loss_v, counters=counters,
-                      predictions=[uf_o], u_final=uf_o, store_counters=sc, device=c)
+                      predictions=[uf_o], u_final=uf_o, store_counters=sc, device=c,
+                      sample_counters=samp)

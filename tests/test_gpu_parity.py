@@ -148,11 +148,47 @@ def test_batch_shards_sum_to_full_batch():
     assert np.array_equal(np.concatenate([a.du0, b.du0]), full.du0)
 
 
+# ------------------------------------------------------------------ C5 fp64
+def test_c5_subset_matches_reference_golden(golden):
+    """Stiff Crank-Nicolson, Newton 1e-10 + GMRES(30): values to 1e-10 against
+    both reference kernel paths; per-sample NFE within rounding-boundary GMRES
+    stops of the reference (whose own numba and numpy paths differ by 1)."""
+    g, gn = golden("c5_sub.npz"), golden("c5_sub_numpy.npz")
+    ci = make_config("C5").subset(2)
+    res = run_config(ci)
+    for ref in (g, gn):
+        for k in ("u_final", "du0", "dtheta"):
+            assert oc.rel_error(np_(getattr(res, k)), ref["store_all/" + k]) <= TOL64, k
+        sc = res.sample_counters
+        assert np.max(np.abs(sc["nfe_forward"] - ref["store_all/nfe_forward"])) <= 6
+        assert np.max(np.abs(sc["nfe_backward"] - ref["store_all/nfe_backward"])) <= 6
+
+
+def test_c5_batch_matches_oracle_and_policies_agree():
+    ci = make_config("C5").subset(8)
+    fld = field_from_config(ci)
+    u0 = torch.as_tensor(ci.u0, device="cuda")
+    base = run_config(ci, "store_all", field=fld, u0=u0)
+    for pol in ("revolve:4", "store_solutions"):
+        other = run_config(ci, pol, field=fld, u0=u0)
+        assert torch.equal(base.dtheta, other.dtheta)
+        assert torch.equal(base.du0, other.du0)
+        assert base.loss == other.loss
+    ref = oracle_run(ci, "store_all")
+    assert_close(base, ref, TOL64)
+    nf = np.array([s.nfe_forward for s in ref["sample_counters"]])
+    nb = np.array([s.nfe_backward for s in ref["sample_counters"]])
+    assert np.max(np.abs(base.sample_counters["nfe_forward"] - nf)) <= 6
+    assert np.max(np.abs(base.sample_counters["nfe_backward"] - nb)) <= 6
+    assert np.all(base.sample_counters["newton_iters"] >= 20)
+
+
 # ------------------------------------------------- all schemes, policies
 EXPLICIT = ("euler", "midpoint", "bosh3", "rk4", "dopri5")
+THETA = ("beuler", "cn")
 
 
-@pytest.mark.parametrize("name", EXPLICIT)
+@pytest.mark.parametrize("name", EXPLICIT + THETA)
 @pytest.mark.parametrize("pol", ["store_all", "store_solutions", "revolve:3"])
 def test_small_schemes_match_reference_golden(golden, name, pol):
     g = golden("small_schemes.npz")
@@ -160,11 +196,19 @@ def test_small_schemes_match_reference_golden(golden, name, pol):
     res = grad(MlpField(model), tableau_catalog(name), terminal_loss("half_sqnorm", 1.0),
                g[f"{name}/u0"], 0.0, 1.0, FixedController(7), CheckpointPolicy.parse(pol))
     pre = f"{name}/{pol}/"
+    # implicit steps: Newton stops at |F| <= 1e-10, so the solution itself is
+    # only defined to that level; the GPU must still agree to 1e-9
+    tol = TOL64 if name in EXPLICIT else 1e-9
     for k in ("u_final", "du0", "dtheta"):
-        assert oc.rel_error(res.__dict__[k], g[pre + k]) <= TOL64, k
-    assert abs(res.loss - float(g[pre + "loss"])) <= 1e-13
-    assert res.counters.nfe_forward == g[pre + "nfe_forward"][0]
-    assert res.counters.nfe_backward == g[pre + "nfe_backward"][0]
+        assert oc.rel_error(res.__dict__[k], g[pre + k]) <= tol, k
+    assert abs(res.loss - float(g[pre + "loss"])) <= 1e-9
+    if name in EXPLICIT:
+        assert res.counters.nfe_forward == g[pre + "nfe_forward"][0]
+        assert res.counters.nfe_backward == g[pre + "nfe_backward"][0]
+    else:   # data-dependent: per-sample counts within a rounding-boundary GMRES stop
+        sc = res.sample_counters
+        assert np.max(np.abs(sc["nfe_forward"] - g[pre + "nfe_forward"])) <= 4
+        assert np.max(np.abs(sc["nfe_backward"] - g[pre + "nfe_backward"])) <= 4
     assert res.store_counters.stored_states == g[pre + "stored_states"]
     assert res.store_counters.stored_stage_vectors == g[pre + "stored_stage_vectors"]
     assert res.store_counters.max_live_slots == g[pre + "max_live_slots"]
