@@ -36,6 +36,8 @@ METRIC = "ODE-block fwd+discrete-adjoint grad samples/s at 1–8 B200; % of roof
 WORKLOADS = {
     "C1": "C1: MLP 64-256-64 tanh fp64, RK4 x10 on [0,1], store_all, B=512/GPU",
     "C2": "C2: MLP (64+t)-256-64 tanh fp32, Dopri5 x40 on [0,1], revolve:8, B=4096/GPU",
+    "C5": "C5: stiff a*u + 0.1*MLP 128-512-128 tanh fp64, Crank-Nicolson x20, Newton 1e-10 + "
+          "GMRES(30) (maxit 1000), store_all, B=256/GPU",
 }
 
 

@@ -1,0 +1,120 @@
+"""TEST INFRASTRUCTURE ONLY -- restated right-hand sides with no reference
+counterpart (C3 conv block, C4 CNF), in float64, with the batched Field
+protocol of oracle/core.py so the restated reference integrator / adjoint
+(core.grad_terminal) drives them unchanged (the reference's
+CallableField plugin, integrators.py:105-141).
+
+Parity for these is "restated RHS": nothing in the reference pins them; they
+are pinned here by central finite differences and the adjoint identity
+(tests/test_oracle_ext.py), in the style of pkg/tests/test_nn.py:112-201.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .core import Mlp, act, act_prime, act_second
+
+LOG2PI = float(np.log(2.0 * np.pi))
+
+
+class CnfField:
+    """Continuous normalizing flow with a Hutchinson trace estimator.
+
+    State y = [z (D), Delta]; f_aug(y, t) = [f(z, t), -eps^T (df/dz) eps] with a
+    fixed Rademacher probe eps per sample and f an MLP with time appended to
+    its input.  The VJP needs the second-order terms of eps^T J eps
+    (forward-over-reverse through the tangent chain).
+    """
+
+    def __init__(self, mlp: Mlp, eps):
+        assert mlp.time_input
+        self.mlp = mlp
+        self.eps = np.asarray(eps, dtype=np.float64)   # [B, D]
+        self.D = mlp.widths[-1]
+        self.n = self.D + 1
+        self.n_params = mlp.n_params
+
+    def _chains(self, Z, t, eps):
+        """Forward (z_l, a_l) and tangent (s_l raw, u_l) chains of every layer."""
+        m = self.mlp
+        B = Z.shape[0]
+        a = np.concatenate([Z, np.full((B, 1), float(t))], axis=1)
+        u = np.concatenate([eps, np.zeros((B, 1))], axis=1)
+        A, U, Zs, S = [a], [u], [], []
+        L = len(m.layers)
+        for l in range(L):
+            W, b = m.W(l), m.b(l)
+            z = a @ W.T + b
+            s = u @ W.T
+            Zs.append(z)
+            S.append(s)
+            if l < L - 1:
+                a = act(z, m.activation)
+                u = act_prime(z, m.activation) * s
+                A.append(a)
+                U.append(u)
+        return A, U, Zs, S
+
+    def _eps(self, B):
+        return self.eps[:B] if self.eps.shape[0] != B else self.eps
+
+    def eval(self, Y, t, c):
+        c.nfe_forward += 1
+        Z = Y[:, :self.D]
+        eps = self._eps(Y.shape[0])
+        _, _, Zs, S = self._chains(Z, t, eps)
+        f = Zs[-1]
+        g = -np.sum(eps * S[-1], axis=1, keepdims=True)
+        return np.concatenate([f, g], axis=1)
+
+    def vjp(self, Y, t, V, c, want_theta=True):
+        c.nfe_backward += 1
+        m = self.mlp
+        Z = Y[:, :self.D]
+        eps = self._eps(Y.shape[0])
+        A, U, Zs, S = self._chains(Z, t, eps)
+        vz = V[:, :self.D]
+        vd = V[:, self.D:self.D + 1]
+        L = len(m.layers)
+        dth = np.zeros(m.n_params)
+        zbar = vz                      # cotangent of the last layer's output z_L
+        sbar = -vd * eps               # cotangent of its tangent output s_L
+        for l in range(L - 1, -1, -1):
+            o, ob, nin, nout = m.layers[l]
+            W = m.W(l)
+            if want_theta:
+                dth[o:ob] = (zbar.T @ A[l] + sbar.T @ U[l]).ravel()
+                dth[ob:ob + nout] = zbar.sum(axis=0)
+            abar = zbar @ W
+            ubar = sbar @ W
+            if l > 0:
+                z, s = Zs[l - 1], S[l - 1]
+                sp = act_prime(z, m.activation)
+                spp = act_second(z, m.activation)
+                sbar = sp * ubar
+                zbar = spp * s * ubar + sp * abar
+            else:
+                jz = abar[:, :self.D]
+        jtv = np.concatenate([jz, np.zeros((Y.shape[0], 1))], axis=1)
+        return jtv, dth
+
+    def vjp_u(self, Y, t, V, c):
+        return self.vjp(Y, t, V, c, want_theta=False)[0]
+
+
+def cnf_seed(D, B):
+    """NLL = 0.5||z(1)||^2 + D/2 log(2 pi) + Delta(1) per sample, batch mean:
+    (loss, lambda_N) with lambda_N = [z/B, 1/B]."""
+    def seed(Y):
+        z = Y[:, :D]
+        nll = 0.5 * np.sum(z * z, axis=1) + 0.5 * D * LOG2PI + Y[:, D]
+        lam = np.concatenate([z / B, np.full((Y.shape[0], 1), 1.0 / B)], axis=1)
+        return float(np.mean(nll)) if Y.shape[0] == B else float(np.sum(nll) / B), lam
+    return seed
+
+
+def cnf_initial_state(z0):
+    """[z0, Delta=0]."""
+    z0 = np.asarray(z0, dtype=np.float64)
+    return np.concatenate([z0, np.zeros((z0.shape[0], 1))], axis=1)

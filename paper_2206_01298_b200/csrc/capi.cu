@@ -31,6 +31,11 @@ template <typename T> cudaError_t launch_reduce(const Dims&, const T*, int, long
                                                 const double*, double, double*, cudaStream_t);
 template <typename T>
 cudaError_t launch_theta(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
+template <typename T>
+cudaError_t launch_cnf(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
+template <typename T>
+cudaError_t launch_cnf_field(const RkParams<T>&, int, int, size_t, int, double, const T*, const T*,
+                             T*, cudaStream_t);
 
 // dispatch on where the weights live (fp32 only stages them in shared memory)
 template <typename T>
@@ -115,7 +120,8 @@ struct Plan {
   int R = 1, Rt = 4, LR = 1, tiles = 1;
   bool need_jvp = false;
   bool theta = false;
-  size_t off_kry = 0, off_stats = 0;
+  size_t off_kry = 0, off_stats = 0, off_cnf = 0;
+  long long cnf_stride = 0;
   long long krylov_stride = 0;
   SmemLayout sm{};
   size_t smem_bytes = 0;
@@ -145,8 +151,13 @@ int check_field(const ob_field_desc& f) {
   if (f.widths[0] != N + (f.time_input ? 1 : 0))  // MlpSpec.__post_init__ (nn.py:53-58)
     return fail(OB_ERR_VALUE, "input width inconsistent with state dim and time_input");
   if (f.activation < 0 || f.activation > OB_ACT_SOFTPLUS) return fail(OB_ERR_VALUE, "unknown activation");
-  if (f.kind != OB_FIELD_MLP && f.kind != OB_FIELD_STIFF)
+  if (f.kind != OB_FIELD_MLP && f.kind != OB_FIELD_STIFF && f.kind != OB_FIELD_CNF)
     return fail(OB_ERR_UNSUPPORTED, "field kind not built into this library version");
+  if (f.kind == OB_FIELD_CNF) {
+    if (!f.time_input) return fail(OB_ERR_VALUE, "CNF field takes time as an input");
+    if (f.dtype != OB_F32) return fail(OB_ERR_UNSUPPORTED, "CNF kernels are built for fp32");
+    if (f.n_layers < 2) return fail(OB_ERR_VALUE, "CNF field needs a hidden layer");
+  }
   if (f.kind == OB_FIELD_STIFF && f.time_input) return fail(OB_ERR_VALUE, "stiff field is autonomous");
   long long np = 0;
   for (int l = 0; l < f.n_layers; ++l) np += (long long)f.widths[l + 1] * f.widths[l] + f.widths[l + 1];
@@ -165,7 +176,9 @@ void make_dims(const ob_field_desc& f, int LR, Dims& d) {
   const int CT = 4 * (32 / LR);
   d = Dims{};
   d.L = f.n_layers;
-  d.N = f.widths[f.n_layers];
+  d.cnf = f.kind == OB_FIELD_CNF;
+  d.nin = f.widths[f.n_layers];
+  d.N = d.nin + (d.cnf ? 1 : 0);           // CNF state carries the log-density Delta
   d.maxw = 0;
   for (int l = 0; l <= d.L; ++l) {
     d.w[l] = f.widths[l];
@@ -174,7 +187,7 @@ void make_dims(const ob_field_desc& f, int LR, Dims& d) {
   }
   long long off = 0, po = 0, mo = 0;
   for (int l = 0; l < d.L; ++l) {
-    const int K = d.w[l], Nn = d.w[l + 1], Kout = l == 0 ? d.N : K;
+    const int K = d.w[l], Nn = d.w[l + 1], Kout = l == 0 ? d.nin : K;
     d.woff[l] = off;
     d.boff[l] = off + (long long)Nn * K;
     off = d.boff[l] + Nn;
@@ -193,7 +206,7 @@ void make_dims(const ob_field_desc& f, int LR, Dims& d) {
   d.ldn = ld_quad_odd(d.N);
   d.act = f.activation;
   d.time_input = f.time_input;
-  d.need_pre = (f.activation == OB_ACT_GELU || f.activation == OB_ACT_SOFTPLUS);
+  d.need_pre = !d.cnf && (f.activation == OB_ACT_GELU || f.activation == OB_ACT_SOFTPLUS);
   d.ldt = ld_quad_odd(d.maxw);
 }
 
@@ -203,11 +216,13 @@ void layout_smem(Plan& P) {
   SmemLayout& s = P.sm;
   int o = 0;
   auto take = [&](long long n) { int r = o; o += (int)((n + 7) & ~7LL); return r; };  // 32 B aligned
-  s.x0 = take((long long)P.Rt * d.lda[0]);
+  const int Rm = d.cnf ? 2 * P.Rt : P.Rt;   // MLP rows (CNF: forward + tangent rows)
+  s.x0 = take((long long)Rm * d.lda[0]);
   for (int l = 0; l < OB_MAX_LAYERS; ++l) {
-    s.hid[l] = (l < d.L - 1) ? take((long long)P.Rt * d.lda[l + 1]) : -1;
-    s.pre[l] = (l < d.L - 1 && d.need_pre) ? take((long long)P.Rt * d.lda[l + 1]) : -1;
+    s.hid[l] = (l < d.L - 1) ? take((long long)Rm * d.lda[l + 1]) : -1;
+    s.pre[l] = (l < d.L - 1 && d.need_pre) ? take((long long)Rm * d.lda[l + 1]) : -1;
   }
+  s.aux = d.cnf ? take((long long)Rm * d.lda[d.L]) : -1;
   s.tA = P.need_jvp ? take((long long)P.Rt * d.ldt) : -1;
   s.tB = P.need_jvp ? take((long long)P.Rt * d.ldt) : -1;
   s.u = take((long long)P.Rt * d.ldn);
@@ -231,6 +246,18 @@ int pick_lr(int R) { return R <= 4 ? 1 : R <= 8 ? 2 : 8; }
 
 void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   int R = (int)std::max<long long>(1, (B + sm_count - 1) / sm_count);
+  if (f.kind == OB_FIELD_CNF) {  // stacked forward|tangent rows: 2*Rt = 4*LR
+    for (R = std::min(R, 16);; R = std::max(1, R / 2)) {
+      P.LR = R <= 4 ? 2 : R <= 8 ? 4 : 8;
+      P.Rt = 2 * P.LR;
+      P.R = std::min(R, P.Rt);
+      make_dims(f, P.LR, P.d);
+      layout_smem(P);
+      if (P.smem_bytes <= kSmemLimit || R == 1) break;
+    }
+    P.tiles = (int)((B + P.R - 1) / P.R);
+    return;
+  }
   R = std::min(R, P.esz == 8 ? 8 : 32);   // fp64 kernels are built for tiles of <= 8 rows
   for (;;) {
     P.R = R;
@@ -373,8 +400,11 @@ int plan_problem(const ob_problem& p, Plan& P) {
   if (!p.times) return fail(OB_ERR_VALUE, "times array is required");
   for (int i = 0; i < p.n_steps; ++i)
     if (!(p.times[i + 1] > p.times[i])) return fail(OB_ERR_VALUE, "step size must be positive");
-  if (p.loss != OB_LOSS_HALF_SQNORM && p.loss != OB_LOSS_MSE)
+  if (p.loss != OB_LOSS_HALF_SQNORM && p.loss != OB_LOSS_MSE &&
+      !(p.loss == OB_LOSS_CNF_NLL && p.field.kind == OB_FIELD_CNF))
     return fail(OB_ERR_UNSUPPORTED, "loss kind not supported for this field");
+  if (p.field.kind == OB_FIELD_CNF && p.scheme.kind != OB_SCHEME_RK)
+    return fail(OB_ERR_UNSUPPORTED, "CNF field is built for explicit schemes");
   P.dtype = p.field.dtype;
   P.esz = P.dtype == OB_F32 ? 4 : 8;
   int dev = 0, sms = 148;
@@ -439,6 +469,12 @@ int plan_problem(const ob_problem& p, Plan& P) {
   }
   P.off_stats = o;
   o = align_up(o + sizeof(int) * (size_t)p.batch * OB_NSTATS, 256);
+  P.off_cnf = o;
+  P.cnf_stride = 0;
+  if (P.d.cnf) {
+    for (int l = 0; l < P.d.L - 1; ++l) P.cnf_stride += 2LL * P.Rt * P.d.lda[l + 1];
+    o = align_up(o + P.esz * (size_t)P.tiles * P.cnf_stride, 256);
+  }
   P.off_lp = o;
   o = align_up(o + sizeof(double) * P.tiles, 256);
   P.total = o;
@@ -511,6 +547,9 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   rp.krylov_stride = P.krylov_stride;
   int* stats = reinterpret_cast<int*>(ws + P.off_stats);
   rp.sample_stats = stats;
+  rp.eps = static_cast<const T*>(b.aux);
+  rp.cnf_pre = reinterpret_cast<T*>(ws + P.off_cnf);
+  rp.cnf_pre_stride = P.cnf_stride;
   CU(cudaMemsetAsync(stats, 0, sizeof(int) * (size_t)p.batch * OB_NSTATS, st));
 
   // per-phase CUDA events on the launch stream (bench roofline timing)
@@ -521,11 +560,17 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   CU(cudaEventRecord(ev[0], st));
   CU(launch_pack<T>(pp, st));
   CU(cudaEventRecord(ev[1], st));
-  if (P.theta) CU(launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, true));
-  else CU(launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, true));
+  auto sweep = [&](bool fwd) -> cudaError_t {
+    if (P.theta) return launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
+    if (P.d.cnf) {
+      if constexpr (sizeof(T) == 4) return launch_cnf<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
+      return cudaErrorNotSupported;
+    }
+    return launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
+  };
+  CU(sweep(true));
   CU(cudaEventRecord(ev[2], st));
-  if (P.theta) CU(launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, false));
-  else CU(launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, false));
+  CU(sweep(false));
   CU(cudaEventRecord(ev[3], st));
   CU(launch_reduce<T>(P.d, rp.mu, P.tiles, p.field.n_params, static_cast<T*>(b.dtheta),
                       rp.loss_part, rp.inv_batch_global, b.loss, st));
@@ -597,6 +642,7 @@ extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* ou
   if (!b->theta || !b->u0 || !b->u_final || !b->du0 || !b->dtheta || !b->loss)
     return fail(OB_ERR_VALUE, "null device buffer");
   if (p->field.kind == OB_FIELD_STIFF && !b->aux) return fail(OB_ERR_VALUE, "stiff field needs diag");
+  if (p->field.kind == OB_FIELD_CNF && !b->aux) return fail(OB_ERR_VALUE, "CNF field needs probes");
   if (p->loss == OB_LOSS_MSE && !b->targets) return fail(OB_ERR_VALUE, "mse loss needs targets");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   st = P.dtype == OB_F32 ? run_grad<float>(*p, *b, P, s) : run_grad<double>(*p, *b, P, s);
@@ -624,8 +670,11 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
   if (P.smem_bytes > kSmemLimit) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   const size_t pk_bytes = align_up(P.esz * (size_t)P.d.n_packed, 256);
   const size_t mu_bytes = mode == kVjp ? P.esz * (size_t)P.tiles * P.d.n_mu : 0;
+  long long cnf_stride = 0;
+  for (int l = 0; P.d.cnf && l < P.d.L - 1; ++l) cnf_stride += 2LL * P.Rt * P.d.lda[l + 1];
+  const size_t cnf_bytes = align_up(P.esz * (size_t)P.tiles * cnf_stride, 256);
   char* ws = nullptr;
-  CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), pk_bytes + mu_bytes + 256, st));
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), pk_bytes + mu_bytes + cnf_bytes + 256, st));
   RkParams<T> rp{};
   rp.d = P.d;
   rp.sm = P.sm;
@@ -643,13 +692,23 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
   rp.Rt = P.Rt;
   rp.n_params = f.n_params;
   rp.mu = mode == kVjp ? reinterpret_cast<T*>(ws + pk_bytes) : nullptr;
+  rp.eps = static_cast<const T*>(aux);
+  rp.cnf_pre = reinterpret_cast<T*>(ws + pk_bytes + align_up(mu_bytes, 256));
+  rp.cnf_pre_stride = cnf_stride;
   int rc = OB_OK;
   cudaError_t e = cudaSuccess;
   if (mu_bytes) e = cudaMemsetAsync(rp.mu, 0, mu_bytes, st);
   if (e == cudaSuccess) e = launch_pack<T>(pp, st);
-  if (e == cudaSuccess)
-    e = launch_field_op<T>(rp, P.LR, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
-                           static_cast<const T*>(w), static_cast<T*>(out), st);
+  if (e == cudaSuccess) {
+    if (P.d.cnf) {
+      if constexpr (sizeof(T) == 4)
+        e = launch_cnf_field<T>(rp, P.LR, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
+                                static_cast<const T*>(w), static_cast<T*>(out), st);
+    } else {
+      e = launch_field_op<T>(rp, P.LR, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
+                             static_cast<const T*>(w), static_cast<T*>(out), st);
+    }
+  }
   if (e == cudaSuccess && mode == kVjp)
     e = launch_reduce<T>(P.d, rp.mu, P.tiles, f.n_params, static_cast<T*>(ptv), nullptr, 0.0,
                          nullptr, st);
@@ -666,7 +725,10 @@ int field_op(const ob_field_desc* f, int64_t batch, const void* theta, const voi
   if (batch < 1) return fail(OB_ERR_VALUE, "batch must be >= 1");
   if ((mode != kEval) && !w) return fail(OB_ERR_VALUE, "null tangent/cotangent");
   if (mode == kVjp && !ptv) return fail(OB_ERR_VALUE, "null ptv");
-  if (f->kind == OB_FIELD_STIFF && !aux) return fail(OB_ERR_VALUE, "stiff field needs diag");
+  if ((f->kind == OB_FIELD_STIFF || f->kind == OB_FIELD_CNF) && !aux)
+    return fail(OB_ERR_VALUE, "field needs its auxiliary array");
+  if (f->kind == OB_FIELD_CNF && mode == kJvp)
+    return fail(OB_ERR_UNSUPPORTED, "CNF field has no JVP (explicit schemes only)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return f->dtype == OB_F32 ? run_field_op<float>(*f, batch, theta, aux, u, t, w, out, ptv, mode, s)
                             : run_field_op<double>(*f, batch, theta, aux, u, t, w, out, ptv, mode, s);

@@ -86,6 +86,20 @@ OB_DEV int warp_id() { return threadIdx.x >> 5; }
 OB_DEV int lane_id() { return threadIdx.x & 31; }
 OB_DEV int n_warps() { return blockDim.x >> 5; }
 
+template <typename T>
+OB_DEV T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+OB_DEV T warp_dot(const T* a, const T* b, int n) {
+  T s = T(0);
+  for (int j = lane_id(); j < n; j += 32) s = Num<T>::fma(a[j], b[j], s);
+  return warp_sum(s);
+}
+
 // Warp range executing an op: warps [w0, w0 + nw) of the CTA.
 struct Warps {
   int w0, nw;
@@ -186,7 +200,9 @@ OB_DEV void gemm_nn(const T* D, int ldd, int Rt, const T* W, int ldw, int Np, in
 // The slot is private to the CTA, so plain RMW is race-free and deterministic.
 template <typename T>
 OB_DEV void gemm_tn_accum(const T* D, int ldd, const T* X, int ldx, int R, int N, int K, T scale,
-                          T* __restrict__ M, int ldm, T* __restrict__ mb, Warps ws) {
+                          T* __restrict__ M, int ldm, T* __restrict__ mb, Warps ws,
+                          int bias_rows = -1) {
+  if (bias_rows < 0) bias_rows = R;   // rows contributing to the bias (CNF: forward rows only)
   if (!ws.mine()) return;
   const int tid = ws.me() * 32 + lane_id(), nth = ws.nw * 32;
   const int nq = (N + 3) / 4, kq = (K + 3) / 4;
@@ -222,7 +238,7 @@ OB_DEV void gemm_tn_accum(const T* D, int ldd, const T* X, int ldx, int R, int N
   }
   for (int n = tid; n < N; n += nth) {
     T s = T(0);
-    for (int r = 0; r < R; ++r) s = Num<T>::add(s, D[r * ldd + n]);
+    for (int r = 0; r < bias_rows; ++r) s = Num<T>::add(s, D[r * ldd + n]);
     mb[n] = Num<T>::add(mb[n], Num<T>::mul(scale, s));
   }
 }

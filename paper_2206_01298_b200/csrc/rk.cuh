@@ -15,6 +15,7 @@ struct SmemLayout {      // offsets in elements of T (-1: not allocated)
   int x0, hid[OB_MAX_LAYERS], pre[OB_MAX_LAYERS], tA, tB;
   int u, lam, lamn, w, jtv;
   int vec[8];             // theta-method work vectors [Rt][ldn] (-1 when unused)
+  int aux;                // CNF: output-layer buffer [2Rt][lda_L]
   int wts;                // packed weights staged in shared memory, or -1
   int total;
 };
@@ -63,6 +64,10 @@ struct RkParams {
   T* krylov;              // per tile: Q [R][m+1][ldn] | H [R][m+1][m] | cs, sn [R][m] | g [R][m+1] | y [R][m]
   long long krylov_stride;
   int* sample_stats;      // [B][OB_NSTATS] per-sample counters (nullable)
+  // CNF (config C4)
+  const T* eps;           // Hutchinson probes [B][D]
+  T* cnf_pre;             // per tile [L-1][2Rt][lda] pre-activations (forward | raw tangent)
+  long long cnf_pre_stride;
 };
 
 template <typename T>

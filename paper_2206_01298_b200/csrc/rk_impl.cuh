@@ -54,53 +54,83 @@ OB_DEV void setup_tile(const RkParams<T>& p, T* sm, MlpSmem<T>& ms, Weights<T>& 
   __syncthreads();
 }
 
-// f(x0) -> out ([Rt][ldn]; columns >= N untouched)
-template <typename T, int LR, bool WS>
-OB_DEV void field_eval(const RkParams<T>& p, MlpTile<T, LR, WS>& mt, T* out) {
-  const int N = p.d.N, ldn = p.d.ldn;
-  mt.forward(out, ldn, p.d.L);
-  if (p.field_kind == OB_FIELD_STIFF) {  // a*u + s*mlp(u)
-    const int ld0 = p.d.lda[0];
-    for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
-      const int r = i / N, j = i % N;
-      out[r * ldn + j] = Num<T>::add(Num<T>::mul(p.diag[j], mt.s.x0[r * ld0 + j]),
-                                     Num<T>::mul(p.out_scale, out[r * ldn + j]));
-    }
-    __syncthreads();
-  }
-}
+// ------------------------------------------------------------ field adapters
+// The RK kernels are generic over the right-hand side: an adapter exposes the
+// tile's input buffer (x0, rows [0, Rt), state columns [0, nin) then time),
+// eval (f(x0) -> out [Rt][ldn]) and vjp (cotangent w -> jtv, mu).
 
-// ((df/du)^T w, mu += h * (df/dtheta)^T w) at the state in x0
+// MlpField / the stiff a*u + s*MLP(u) field (integrators.py:76-141)
 template <typename T, int LR, bool WS>
-OB_DEV void field_vjp(const RkParams<T>& p, MlpTile<T, LR, WS>& mt, const T* w, T* jtv, T* mu,
-                      double h, int Rv) {
-  mt.forward(nullptr, 0, p.d.L - 1);  // hidden layers only: the output value is not needed
-  const int ldn = p.d.ldn;
-  if (p.field_kind == OB_FIELD_STIFF) {
-    mt.vjp(w, ldn, Rv, jtv, ldn, mu, T(h * double(p.out_scale)));
-    const int N = p.d.N;
-    for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
-      const int r = i / N, j = i % N;
-      jtv[r * ldn + j] = Num<T>::add(Num<T>::mul(p.diag[j], w[r * ldn + j]),
-                                     Num<T>::mul(p.out_scale, jtv[r * ldn + j]));
+struct MlpAdapter {
+  const RkParams<T>& p;
+  MlpTile<T, LR, WS> mt;
+  OB_DEV MlpAdapter(const RkParams<T>& p_, const Weights<T>& W, MlpSmem<T>& ms, T*, int, int)
+      : p(p_), mt(p_.d, W, ms, p_.Rt) {}
+  OB_DEV MlpAdapter(const RkParams<T>& p_, const MlpTile<T, LR, WS>& m) : p(p_), mt(m) {}
+  OB_DEV T* x0() { return mt.s.x0; }
+  OB_DEV int nin() const { return p.d.N; }
+  OB_DEV void set_scratch(T* s, int n) { mt.scratch = s; mt.scratch_elems = n; }
+  static constexpr bool kHasJvp = true;
+
+  // (df/du) w at x0 (integrators.py:88-92)
+  OB_DEV void jvp(const T* w, T* out) {
+    const int N = p.d.N, ldn = p.d.ldn;
+    mt.forward(nullptr, 0, p.d.L - 1);
+    mt.jvp(w, ldn, out, ldn);
+    if (p.field_kind == OB_FIELD_STIFF) {
+      for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
+        const int o = (i / N) * ldn + i % N, j = i % N;
+        out[o] = Num<T>::add(Num<T>::mul(p.diag[j], w[o]), Num<T>::mul(p.out_scale, out[o]));
+      }
+      __syncthreads();
     }
-    __syncthreads();
-  } else {
-    mt.vjp(w, ldn, Rv, jtv, ldn, mu, T(h));
   }
-}
+
+  // f(x0) -> out ([Rt][ldn]; columns >= N untouched)
+  OB_DEV void eval(T* out) {
+    const int N = p.d.N, ldn = p.d.ldn;
+    mt.forward(out, ldn, p.d.L);
+    if (p.field_kind == OB_FIELD_STIFF) {  // a*u + s*mlp(u)
+      const int ld0 = p.d.lda[0];
+      for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
+        const int r = i / N, j = i % N;
+        out[r * ldn + j] = Num<T>::add(Num<T>::mul(p.diag[j], mt.s.x0[r * ld0 + j]),
+                                       Num<T>::mul(p.out_scale, out[r * ldn + j]));
+      }
+      __syncthreads();
+    }
+  }
+
+  // ((df/du)^T w, mu += h * (df/dtheta)^T w) at the state in x0
+  OB_DEV void vjp(const T* w, T* jtv, T* mu, double h, int Rv) {
+    mt.forward(nullptr, 0, p.d.L - 1);  // hidden layers only: the output value is not needed
+    const int ldn = p.d.ldn;
+    if (p.field_kind == OB_FIELD_STIFF) {
+      mt.vjp(w, ldn, Rv, jtv, ldn, mu, T(h * double(p.out_scale)));
+      const int N = p.d.N;
+      for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
+        const int r = i / N, j = i % N;
+        jtv[r * ldn + j] = Num<T>::add(Num<T>::mul(p.diag[j], w[r * ldn + j]),
+                                       Num<T>::mul(p.out_scale, jtv[r * ldn + j]));
+      }
+      __syncthreads();
+    } else {
+      mt.vjp(w, ldn, Rv, jtv, ldn, mu, T(h));
+    }
+  }
+};
 
 // One explicit RK step of the tile from the state in `u` (smem [Rt][ldn]).
 // ks: this tile's stage-derivative scratch [s][Rt][ldn].  rec (nullable):
 // record base for this step ([s+1][B][N]).  On return `u` holds u_next.
 // Returns false (block-uniform) if u_next has a non-finite entry.
-template <typename T, int LR, bool WS>
-OB_DEV bool rk_step_tile(const RkParams<T>& p, MlpTile<T, LR, WS>& mt, T* u, T* ks, double t,
-                         double h, bool carry, T* rec, int row0, int Rv) {
-  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0];
+template <typename T, class F>
+OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, double h, bool carry,
+                         T* rec, int row0, int Rv) {
+  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0], nin = f.nin();
   const long long kst = (long long)Rt * ldn;
   const long long vec = (long long)p.B * N;
-  T* x0 = mt.s.x0;
+  T* x0 = f.x0();
   for (int i = 0; i < s; ++i) {
     for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
       const int r = idx / N, j = idx % N;
@@ -109,17 +139,17 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, MlpTile<T, LR, WS>& mt, T* u, T* 
         const double aiq = p.a[i * OB_MAX_STAGES + q];
         if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), ks[q * kst + r * ldn + j]));
       }
-      x0[r * ld0 + j] = v;
+      if (j < nin) x0[r * ld0 + j] = v;
       if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * N + j] = v;
     }
     if (p.d.time_input)
-      for (int r = threadIdx.x; r < Rt; r += blockDim.x) x0[r * ld0 + N] = T(t + p.c[i] * h);
+      for (int r = threadIdx.x; r < Rt; r += blockDim.x) x0[r * ld0 + nin] = T(t + p.c[i] * h);
     __syncthreads();
     if (i == 0 && carry) {  // FSAL: k_0 of this step is k_{s-1} of the previous one
       for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) ks[idx] = ks[(s - 1) * kst + idx];
       __syncthreads();
     } else {
-      field_eval<T, LR, WS>(p, mt, ks + i * kst);
+      f.eval(ks + i * kst);
     }
   }
   int bad = 0;
@@ -153,8 +183,52 @@ OB_DEV void store_rows(T* dst, int N, const T* src, int lds, int row0, int Rv) {
   }
 }
 
+// --------------------------------------------------------------- losses
+// Terminal losses (losses.py:78-107 with the batch mean; BASELINE configs):
+// per-tile fp64 partial sums in fixed order, and the seed lambda_N = dL/du(T).
+constexpr double kLog2Pi = 1.8378770664093454836;
+
+template <typename T>
+OB_DEV void loss_partial(const RkParams<T>& p, const T* u, int row0, int Rv, int tile) {
+  if (threadIdx.x != 0) return;
+  const int N = p.d.N, ldn = p.d.ldn;
+  double acc = 0.0;
+  for (int r = 0; r < Rv; ++r) {
+    double sr = 0.0;
+    if (p.loss_kind == OB_LOSS_CNF_NLL) {  // NLL = 0.5|z|^2 + D/2 log 2pi + Delta
+      const int D = N - 1;
+      for (int j = 0; j < D; ++j) {
+        const double v = double(u[r * ldn + j]);
+        sr += v * v;
+      }
+      acc += 0.5 * sr + 0.5 * D * kLog2Pi + double(u[r * ldn + D]);
+      continue;
+    }
+    for (int j = 0; j < N; ++j) {
+      double v = double(u[r * ldn + j]);
+      if (p.loss_kind == OB_LOSS_MSE) v -= double(p.targets[(long long)(row0 + r) * N + j]);
+      sr += v * v;
+    }
+    acc += (p.loss_kind == OB_LOSS_MSE) ? sr / N : 0.5 * sr;
+  }
+  p.loss_part[tile] = acc;
+}
+
+template <typename T>
+OB_DEV void loss_seed(const RkParams<T>& p, T* lam, int row0, int Rv) {
+  const int N = p.d.N, ldn = p.d.ldn;
+  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+    const int r = idx / N, j = idx % N;
+    const long long g = (long long)(row0 + r) * N + j;
+    T v = p.u_final[g];
+    if (p.loss_kind == OB_LOSS_MSE) v = T(2) * (v - p.targets[g]) / T(N);
+    if (p.loss_kind == OB_LOSS_CNF_NLL && j == N - 1) v = T(1);
+    lam[r * ldn + j] = v / T(p.batch_global);
+  }
+}
+
 // --------------------------------------------------------------- forward
-template <typename T, int LR, bool WS>
+template <typename T, class F>
 __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_constant__ RkParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -165,11 +239,10 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
-  MlpTile<T, LR, WS> mt(p.d, W, ms, p.Rt);
+  F f(p, W, ms, sm, row0, Rv);
   // split-K scratch: the same lamn | w | jtv region as the reverse kernel's
   // replays, so forward and replayed steps sum identically (bit-identical records)
-  mt.scratch = sm + p.sm.lamn;
-  mt.scratch_elems = p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn;
+  f.set_scratch(sm + p.sm.lamn, p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn);
   T* u = sm + p.sm.u;
   T* ks = p.scratch + tile * p.scratch_stride;
   const int N = p.d.N, ldn = p.d.ldn;
@@ -191,31 +264,18 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
       __syncthreads();
     }
     T* rec = p.fwd_rec[n] >= 0 ? p.rec + (long long)p.fwd_rec[n] * (p.s + 1) * vec : nullptr;
-    const bool ok = rk_step_tile<T, LR, WS>(p, mt, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv);
+    const bool ok = rk_step_tile<T, F>(p, f, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv);
     if (!ok) {  // integrators.py:219-220
       if (threadIdx.x == 0) set_status(p.status, OB_ERR_INTEGRATION, n);
       return;
     }
   }
   store_rows(p.u_final, N, u, ldn, row0, Rv);
-  // terminal loss partial (fp64, fixed order per tile; losses.py:78-107 / BASELINE)
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int r = 0; r < Rv; ++r) {
-      double sr = 0.0;
-      for (int j = 0; j < N; ++j) {
-        double v = double(u[r * ldn + j]);
-        if (p.loss_kind == OB_LOSS_MSE) v -= double(p.targets[(long long)(row0 + r) * N + j]);
-        sr += v * v;
-      }
-      acc += (p.loss_kind == OB_LOSS_MSE) ? sr / N : 0.5 * sr;
-    }
-    p.loss_part[tile] = acc;
-  }
+  loss_partial(p, u, row0, Rv, tile);
 }
 
 // --------------------------------------------------------------- reverse
-template <typename T, int LR, bool WS>
+template <typename T, class F>
 __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_constant__ RkParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -227,10 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
-  MlpTile<T, LR, WS> mt(p.d, W, ms, p.Rt);
-  mt.scratch = sm + p.sm.lamn;                 // lamn | w | jtv are free during replays
-  mt.scratch_elems = p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn;
-  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0];
+  F f(p, W, ms, sm, row0, Rv);
+  f.set_scratch(sm + p.sm.lamn, p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn);  // free during replays
+  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0], nin = f.nin();
   const long long vec = (long long)p.B * N;
   const long long kst = (long long)Rt * ldn;
   T* u = sm + p.sm.u;
@@ -241,15 +300,9 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
   T* ks = p.scratch + tile * p.scratch_stride;
   T* Lam = ks + s * kst;
   T* mu = p.mu + tile * p.d.n_mu;
+  T* x0 = f.x0();
 
-  // terminal seed lambda_N = dL/du(T) (losses.py:78-107 with the batch mean)
-  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
-    const int r = idx / N, j = idx % N;
-    const long long g = (long long)(row0 + r) * N + j;
-    T v = p.u_final[g];
-    if (p.loss_kind == OB_LOSS_MSE) v = T(2) * (v - p.targets[g]) / T(N);
-    lam[r * ldn + j] = v / T(p.batch_global);
-  }
+  loss_seed(p, lam, row0, Rv);
   __syncthreads();
 
   for (int pc = 0; pc < p.prog_len; ++pc) {
@@ -266,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       load_rows(u, ldn, srcp, N, row0, Rv);
       __syncthreads();
       T* rec = p.rec + (long long)op.w * (s + 1) * vec;
-      rk_step_tile<T, LR, WS>(p, mt, u, ks, t, h, false, rec, row0, Rv);
+      rk_step_tile<T, F>(p, f, u, ks, t, h, false, rec, row0, Rv);
       continue;
     }
     // REVERSE(n) from record buffer op.w: rk_adjoint_step (adjoint.py:67-94)
@@ -289,14 +342,14 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
         w[o] = v;
       }
       // stage state U_i into x0 (+ stage time)
-      for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
-        const int r = idx / N, j = idx % N;
-        ms.x0[r * ld0 + j] = rec[i * vec + (long long)(row0 + r) * N + j];
+      for (int idx = threadIdx.x; idx < Rv * nin; idx += blockDim.x) {
+        const int r = idx / nin, j = idx % nin;
+        x0[r * ld0 + j] = rec[i * vec + (long long)(row0 + r) * N + j];
       }
       if (p.d.time_input)
-        for (int r = threadIdx.x; r < Rt; r += blockDim.x) ms.x0[r * ld0 + N] = T(t + p.c[i] * h);
+        for (int r = threadIdx.x; r < Rt; r += blockDim.x) x0[r * ld0 + nin] = T(t + p.c[i] * h);
       __syncthreads();
-      field_vjp<T, LR, WS>(p, mt, w, jtv, mu, h, Rv);
+      f.vjp(w, jtv, mu, h, Rv);
       // Lam_i = h * jtv; lam_n += Lam_i
       for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
         const int o = (idx / N) * ldn + idx % N;
@@ -320,7 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
 }
 
 // Field protocol ops on a batch (integrators.py:53-102): eval / jvp / vjp / vjp_u.
-template <typename T, int LR, bool WS>
+// jvp needs the MLP tangent pass (MlpAdapter); other adapters reject mode 1 on the host.
+template <typename T, class F>
 __global__ void __launch_bounds__(kThreads, 1)
 field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const T* u,
                 const T* w, T* out) {
@@ -333,32 +387,25 @@ field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
-  MlpTile<T, LR, WS> mt(p.d, W, ms, p.Rt);
-  const int N = p.d.N, ldn = p.d.ldn, ld0 = p.d.lda[0];
+  F f(p, W, ms, sm, row0, Rv);
+  const int N = p.d.N, ldn = p.d.ldn, ld0 = p.d.lda[0], nin = f.nin();
   T* wb = sm + p.sm.w;
   T* res = sm + p.sm.jtv;
-  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
-    const int r = idx / N, j = idx % N;
-    ms.x0[r * ld0 + j] = u[(long long)(row0 + r) * N + j];
+  T* x0 = f.x0();
+  for (int idx = threadIdx.x; idx < Rv * nin; idx += blockDim.x) {
+    const int r = idx / nin, j = idx % nin;
+    x0[r * ld0 + j] = u[(long long)(row0 + r) * N + j];
   }
   if (p.d.time_input)
-    for (int r = threadIdx.x; r < p.Rt; r += blockDim.x) ms.x0[r * ld0 + N] = T(t);
+    for (int r = threadIdx.x; r < p.Rt; r += blockDim.x) x0[r * ld0 + nin] = T(t);
   if (mode != 0) load_rows(wb, ldn, w, N, row0, Rv);
   __syncthreads();
   if (mode == 0) {
-    field_eval<T, LR, WS>(p, mt, res);
+    f.eval(res);
   } else if (mode == 1) {
-    mt.forward(nullptr, 0, p.d.L - 1);
-    mt.jvp(wb, ldn, res, ldn);
-    if (p.field_kind == OB_FIELD_STIFF) {
-      for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
-        const int o = (i / N) * ldn + i % N, j = i % N;
-        res[o] = Num<T>::add(Num<T>::mul(p.diag[j], wb[o]), Num<T>::mul(p.out_scale, res[o]));
-      }
-      __syncthreads();
-    }
+    if constexpr (F::kHasJvp) f.jvp(wb, res);
   } else {
-    field_vjp<T, LR, WS>(p, mt, wb, res, mode == 2 ? p.mu + tile * p.d.n_mu : nullptr, 1.0, Rv);
+    f.vjp(wb, res, mode == 2 ? p.mu + tile * p.d.n_mu : nullptr, 1.0, Rv);
   }
   store_rows(out, N, res, ldn, row0, Rv);
 }
@@ -426,8 +473,9 @@ static cudaError_t launch_smem(K kf, int grid, size_t smem, cudaStream_t st, A..
 template <typename T, int LR, bool WS>
 static cudaError_t launch_rk_lr(const RkParams<T>& p, int tiles, size_t smem, cudaStream_t st,
                                 bool forward) {
-  return forward ? launch_smem(rk_forward_kernel<T, LR, WS>, tiles, smem, st, p)
-                 : launch_smem(rk_reverse_kernel<T, LR, WS>, tiles, smem, st, p);
+  using F = MlpAdapter<T, LR, WS>;
+  return forward ? launch_smem(rk_forward_kernel<T, F>, tiles, smem, st, p)
+                 : launch_smem(rk_reverse_kernel<T, F>, tiles, smem, st, p);
 }
 
 // lane-row variants: LR 1 / 2 / 8 (tiles of <= 4, <= 8, <= 32 samples; fp64 tiles
@@ -448,11 +496,14 @@ template <typename T, bool WS>
 cudaError_t launch_field_ws(const RkParams<T>& p, int lr, int tiles, size_t smem, int mode,
                             double t, const T* u, const T* w, T* out, cudaStream_t st) {
   switch (lr) {
-    case 1: return launch_smem(field_op_kernel<T, 1, WS>, tiles, smem, st, p, mode, t, u, w, out);
-    case 2: return launch_smem(field_op_kernel<T, 2, WS>, tiles, smem, st, p, mode, t, u, w, out);
+    case 1:
+      return launch_smem(field_op_kernel<T, MlpAdapter<T, 1, WS>>, tiles, smem, st, p, mode, t, u, w, out);
+    case 2:
+      return launch_smem(field_op_kernel<T, MlpAdapter<T, 2, WS>>, tiles, smem, st, p, mode, t, u, w, out);
     default:
       if constexpr (sizeof(T) == 4)
-        return launch_smem(field_op_kernel<T, 8, WS>, tiles, smem, st, p, mode, t, u, w, out);
+        return launch_smem(field_op_kernel<T, MlpAdapter<T, 8, WS>>, tiles, smem, st, p, mode, t, u,
+                           w, out);
       return cudaErrorInvalidConfiguration;
   }
 }

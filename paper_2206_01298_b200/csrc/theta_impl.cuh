@@ -27,20 +27,6 @@ struct SampleState {
   double tol;
 };
 
-template <typename T>
-OB_DEV T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-template <typename T>
-OB_DEV T warp_dot(const T* a, const T* b, int n) {
-  T s = T(0);
-  for (int j = lane_id(); j < n; j += 32) s = Num<T>::fma(a[j], b[j], s);
-  return warp_sum(s);
-}
-
 // per-tile theta-method context (shared memory vectors + per-sample state)
 template <typename T>
 struct ThetaCtx {
@@ -251,7 +237,8 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
 template <typename T, int LR, bool WS>
 OB_DEV void theta_eval(const RkParams<T>& p, MlpTile<T, LR, WS>& mt, ThetaCtx<T>& c, int Rv,
                        bool count_all) {
-  field_eval<T, LR, WS>(p, mt, c.fb);
+  MlpAdapter<T, LR, WS> f{p, mt};
+  f.eval(c.fb);
   if (threadIdx.x < Rv && (count_all || c.active[threadIdx.x]))
     c.cnt[threadIdx.x * OB_NSTATS + OB_STAT_NFE_F] += 1;
 }
@@ -435,19 +422,7 @@ theta_forward_kernel(const __grid_constant__ RkParams<T> p) {
   }
   store_rows(p.u_final, N, u, ldn, row0, Rv);
   flush_stats(p, c, row0, Rv);
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int r = 0; r < Rv; ++r) {
-      double sr = 0.0;
-      for (int j = 0; j < N; ++j) {
-        double v = double(u[r * ldn + j]);
-        if (p.loss_kind == OB_LOSS_MSE) v -= double(p.targets[(long long)(row0 + r) * N + j]);
-        sr += v * v;
-      }
-      acc += (p.loss_kind == OB_LOSS_MSE) ? sr / N : 0.5 * sr;
-    }
-    p.loss_part[tile] = acc;
-  }
+  loss_partial(p, u, row0, Rv, tile);
 }
 
 // --------------------------------------------------------------- reverse
@@ -474,13 +449,7 @@ theta_reverse_kernel(const __grid_constant__ RkParams<T> p) {
   T* kry = p.krylov + tile * p.krylov_stride;
   T* mu = p.mu + tile * p.d.n_mu;
   const double th = p.theta;
-  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
-    const int r = idx / N, j = idx % N;
-    const long long g = (long long)(row0 + r) * N + j;
-    T v = p.u_final[g];
-    if (p.loss_kind == OB_LOSS_MSE) v = T(2) * (v - p.targets[g]) / T(N);
-    lam[r * ldn + j] = v / T(p.batch_global);
-  }
+  loss_seed(p, lam, row0, Rv);
   __syncthreads();
   for (int pc = 0; pc < p.prog_len; ++pc) {
     const int4 op = p.prog[pc];

@@ -102,6 +102,8 @@ struct Dims {
   long long n_mu;                 // padded mu length
   long long n_packed;             // packed weights length
   int N, ldn;                     // state dim, its buffer leading dim
+  int nin;                        // state components fed to the MLP (CNF: N - 1)
+  int cnf;                        // 1: continuous normalizing flow field (C4)
   int act, time_input;
   int need_pre;                   // act' needs the pre-activation (gelu / softplus)
   int maxw, ldt;                  // widest layer, tangent buffer leading dim

@@ -259,3 +259,33 @@ class StiffMlpField(MlpField):
         d = super().desc()
         d.out_scale = self.scale
         return d
+
+
+class CnfField(MlpField):
+    """Continuous normalizing flow with a Hutchinson trace estimator (config C4).
+
+    State [z (D), Delta]; f_aug = [f(z, t), -eps^T (df/dz) eps] with f an MLP
+    taking time as its last input and one fixed probe eps per sample
+    ([B, D], e.g. Rademacher).  The probes bind the field to a batch.  No
+    reference counterpart; restated oracle in
+    oracle/fields_ext.py.
+    """
+
+    kind = _lib.OB_FIELD_CNF
+
+    def __init__(self, model: MlpModel, eps):
+        if not model.spec.time_input:
+            raise ValueError("CNF field takes time as an input")
+        if model.spec.dtype != "f32":
+            raise NotImplementedError("CNF kernels are built for fp32")
+        super().__init__(model)
+        self.eps = to_device(eps, model.spec.torch_dtype)
+        if self.eps.dim() != 2 or self.eps.shape[1] != model.n:
+            raise ValueError("eps must be [B, D]")
+
+    @property
+    def n(self):
+        return self.model.n + 1
+
+    def aux(self):
+        return self.eps

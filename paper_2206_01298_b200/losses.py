@@ -5,6 +5,8 @@ loss, so the seed is lambda_N,b = grad ell(u_b(T)) / B.
   * ``half_sqnorm``: ell(u) = 0.5 ||u||^2 (the BASELINE configs' loss).
   * ``mse``: ell(u) = sum((u - y)^2) / N with per-sample targets y, i.e. the
     reference's K=1 MSE (seed 2 r / N, losses.py:100-107), averaged over B.
+  * ``cnf_nll``: for CnfField states [z, Delta]: -log p(x) = 0.5||z||^2 +
+    D/2 log(2 pi) + Delta (standard-normal base, log p(x) = log N(z(1)) - Delta(1)).
 Multi-observation losses, MAE and min-max scaling are the next component
  and raise NotImplementedError.
 """
@@ -13,7 +15,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-KINDS = ("half_sqnorm", "mse")
+KINDS = ("half_sqnorm", "mse", "cnf_nll")
 
 
 @dataclass(frozen=True)

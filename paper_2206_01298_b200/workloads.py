@@ -6,10 +6,12 @@
 
 from __future__ import annotations
 
+import numpy as np
+
 from .configs import ConfigInputs
 from .controls import FixedController, SolverConfig
 from .engine import grad
-from .fields import MlpField, MlpModel, MlpSpec, StiffMlpField
+from .fields import CnfField, MlpField, MlpModel, MlpSpec, StiffMlpField
 from .losses import terminal_loss
 from .policies import CheckpointPolicy
 from .schemes import tableau_catalog
@@ -22,6 +24,8 @@ def field_from_config(ci: ConfigInputs):
         return MlpField(model)
     if ci.kind == "stiff":
         return StiffMlpField(model, ci.extras["diag"], ci.extras["scale"])
+    if ci.kind == "cnf":
+        return CnfField(model, ci.extras["eps"])
     raise NotImplementedError(f"config kind {ci.kind!r} is not built yet")
 
 
@@ -30,9 +34,20 @@ def solver_from_config(ci: ConfigInputs):
     return SolverConfig(**s) if s else SolverConfig()
 
 
+def initial_state(ci: ConfigInputs):
+    """Integration state at t0 (CNF: [z0, Delta = 0])."""
+    if ci.kind == "cnf":
+        return np.concatenate([ci.u0, np.zeros((ci.batch, 1))], axis=1)
+    return ci.u0
+
+
+def loss_kind(ci: ConfigInputs) -> str:
+    return "cnf_nll" if ci.kind == "cnf" else "half_sqnorm"
+
+
 def run_config(ci: ConfigInputs, policy: str = None, field=None, u0=None, **kw):
     field = field if field is not None else field_from_config(ci)
     pol = CheckpointPolicy.parse(policy or ci.policy)
-    return grad(field, tableau_catalog(ci.scheme), terminal_loss("half_sqnorm", ci.tF),
-                ci.u0 if u0 is None else u0, ci.t0, ci.tF, FixedController(ci.n_steps), pol,
-                solver_from_config(ci), **kw)
+    return grad(field, tableau_catalog(ci.scheme), terminal_loss(loss_kind(ci), ci.tF),
+                initial_state(ci) if u0 is None else u0, ci.t0, ci.tF,
+                FixedController(ci.n_steps), pol, solver_from_config(ci), **kw)

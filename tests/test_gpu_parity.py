@@ -183,6 +183,48 @@ def test_c5_batch_matches_oracle_and_policies_agree():
     assert np.all(base.sample_counters["newton_iters"] >= 20)
 
 
+# ------------------------------------------------------------------ C4 fp32 CNF
+def _cnf_oracle(ci, policy="store_all"):
+    from oracle import fields_ext as ox
+    mlp = oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input)
+    fld = ox.CnfField(mlp, ci.extras["eps"])
+    Y0 = ox.cnf_initial_state(ci.u0)
+    return oc.grad_terminal(fld, ci.scheme, Y0, ci.t0, ci.tF, ci.n_steps, policy,
+                            seed_fn=ox.cnf_seed(fld.D, ci.batch))
+
+
+def test_c4_field_protocol_matches_restated_oracle():
+    from oracle import fields_ext as ox
+    from paper_2206_01298_b200.workloads import initial_state
+    ci = make_config("C4").subset(12)
+    fld = field_from_config(ci)
+    ofl = ox.CnfField(oc.Mlp(ci.widths, ci.activation, ci.theta, True), ci.extras["eps"])
+    rng = np.random.default_rng(3)
+    Y = initial_state(ci).astype(np.float32).astype(np.float64)
+    Y[:, -1] = rng.standard_normal(ci.batch)
+    V = rng.standard_normal(Y.shape).astype(np.float32).astype(np.float64)
+    f_ref = ofl.eval(Y, 0.4, oc.Counters())
+    j_ref, p_ref = ofl.vjp(Y, 0.4, V, oc.Counters())
+    f = np_(fld.eval(Y, 0.4))
+    j, p = fld.vjp(Y, 0.4, V)
+    assert oc.rel_error(f, f_ref) <= TOL32
+    assert oc.rel_error(np_(j), j_ref) <= TOL32
+    assert oc.rel_error(np_(p), p_ref) <= TOL32
+
+
+def test_c4_subset_matches_restated_oracle_and_policies_agree():
+    ci = make_config("C4").subset(24)
+    fld = field_from_config(ci)
+    base = run_config(ci, "store_all", field=fld)
+    rev = run_config(ci, "revolve:5", field=fld)
+    assert np.array_equal(base.dtheta, rev.dtheta) and base.loss == rev.loss
+    ref = _cnf_oracle(ci)
+    errs = {k: oc.rel_error(np_(getattr(base, k)), ref[k]) for k in ("u_final", "du0", "dtheta")}
+    assert max(errs.values()) <= TOL32, errs
+    assert abs(base.loss - ref["loss"]) <= TOL32 * abs(ref["loss"])
+    assert base.counters.nfe_forward == 121 and base.counters.nfe_backward == 140
+
+
 # ------------------------------------------------- all schemes, policies
 EXPLICIT = ("euler", "midpoint", "bosh3", "rk4", "dopri5")
 THETA = ("beuler", "cn")
