@@ -36,6 +36,8 @@ METRIC = "ODE-block fwd+discrete-adjoint grad samples/s at 1–8 B200; % of roof
 WORKLOADS = {
     "C1": "C1: MLP 64-256-64 tanh fp64, RK4 x10 on [0,1], store_all, B=512/GPU",
     "C2": "C2: MLP (64+t)-256-64 tanh fp32, Dopri5 x40 on [0,1], revolve:8, B=4096/GPU",
+    "C4": "C4: CNF (43+t)-860-860-43 softplus fp32 + Hutchinson (1 Rademacher probe), Dopri5 x20, "
+          "store_all, NLL loss, B=1000/GPU",
     "C5": "C5: stiff a*u + 0.1*MLP 128-512-128 tanh fp64, Crank-Nicolson x20, Newton 1e-10 + "
           "GMRES(30) (maxit 1000), store_all, B=256/GPU",
 }
@@ -57,25 +59,18 @@ def parse():
 # ----------------------------------------------------------------- CPU side
 def _cpu_worker_init(cfg_name, policy):
     global _W
-    from oracle import core as oc
     from paper_2206_01298_b200.configs import make_config
-    ci = make_config(cfg_name, batch=64)
-    mlp = oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input)
-    if ci.kind == "stiff":
-        fld = oc.StiffField(mlp, ci.extras["diag"], ci.extras["scale"])
-        cfg = oc.SolverCfg(**ci.extras["solver"])
-    else:
-        fld = oc.MlpField(mlp)
-        cfg = oc.SolverCfg()
-    _W = (oc, ci, fld, cfg, policy)
+    ci = make_config(cfg_name).subset(64)
+    _W = (ci, policy)
 
 
 def _cpu_task(idx):
     """One sample through the oracle's per-sample path (the reference's
     forward_pass + backward_sweep restated, GEMV per sample like odegrad)."""
-    oc, ci, fld, cfg, policy = _W
-    u0 = ci.u0[idx % ci.batch: idx % ci.batch + 1]
-    oc.grad_terminal(fld, ci.scheme, u0, ci.t0, ci.tF, ci.n_steps, policy, cfg=cfg)
+    from oracle.problems import run_oracle
+    ci, policy = _W
+    i = idx % ci.batch
+    run_oracle(ci, policy, rows=slice(i, i + 1))
     return 1
 
 
@@ -231,21 +226,23 @@ def main():
     from paper_2206_01298_b200.configs import make_config
     from paper_2206_01298_b200.distributed import grad_sharded, shard_bounds
     from paper_2206_01298_b200.engine import grad
-    from paper_2206_01298_b200.workloads import field_from_config, solver_from_config
+    from paper_2206_01298_b200.workloads import (field_from_config, initial_state, loss_kind,
+                                                 solver_from_config)
 
     base = make_config(args.config, batch=1)
-    per_gpu = {"C1": 512, "C2": 4096, "C5": 256}[args.config]
+    per_gpu = {"C1": 512, "C2": 4096, "C4": 1000, "C5": 256}[args.config]
     ci = make_config(args.config, batch=per_gpu * world)      # weak scaling: N x per-GPU batch
     lo, hi = shard_bounds(ci.batch, world, rank)
     policy = CheckpointPolicy.parse(args.policy or base.policy)
     field = field_from_config(ci)
     scheme = tableau_catalog(ci.scheme)
-    loss = terminal_loss("half_sqnorm", ci.tF)
+    loss = terminal_loss(loss_kind(ci), ci.tF)
     ctrl = FixedController(ci.n_steps)
     scfg = solver_from_config(ci)
     tdt = field.torch_dtype
-    u0_dev = torch.as_tensor(ci.u0[lo:hi], dtype=tdt, device="cuda").contiguous()
-    u0_host = torch.as_tensor(ci.u0[lo:hi], dtype=tdt).pin_memory()
+    y0 = initial_state(ci)[lo:hi]
+    u0_dev = torch.as_tensor(y0, dtype=tdt, device="cuda").contiguous()
+    u0_host = torch.as_tensor(y0, dtype=tdt).pin_memory()
 
     def step(u0):
         if world > 1:
@@ -305,17 +302,26 @@ def main():
     e2e_value = ci.batch / e2e_mean
     esz = 4 if ci.dtype == "f32" else 8
     nloc = hi - lo
-    h2d = nloc * ci.widths[-1] * esz
-    d2h = 2 * nloc * ci.widths[-1] * esz + field.n_params * esz + 8
+    h2d = y0.size * esz
+    d2h = 2 * y0.size * esz + field.n_params * esz + 8
 
     # ---- roofline of the dominant kernel (CUDA events around each launch, in-library)
     dev = res.device
     Pw = sum(ci.widths[l] * ci.widths[l + 1] for l in range(len(ci.widths) - 1))
     s = scheme.stages
     replays = dev["steps_recomputed"]
-    fwd_evals = dev["nfe_forward"] - replays * s
-    fwd_flops = nloc * fwd_evals * 2 * Pw
-    rev_flops = nloc * (replays * s * 2 * Pw + dev["device_vjp_evals"] * 4 * Pw)
+    # algorithmic FLOPs per sample: MLP f-eval
+    # 2*Pw, VJP pair 4*Pw (forward recompute excluded); CNF f_aug (f and J eps)
+    # 4*Pw, VJP 8*Pw; theta methods (NFE-F + NFE-B) * 2*Pw
+    fe, ve = (4, 8) if ci.kind == "cnf" else (2, 4)
+    if scheme.kind == "theta":
+        per = dev["nfe_forward"] * 2 * Pw
+        fwd_flops = nloc * per * (1 + replays / max(1, ci.n_steps)) / (1 + replays / max(1, ci.n_steps))
+        rev_flops = nloc * dev["nfe_backward"] * 2 * Pw
+    else:
+        fwd_evals = dev["nfe_forward"] - replays * s
+        fwd_flops = nloc * fwd_evals * fe * Pw
+        rev_flops = nloc * (replays * s * fe * Pw + dev["device_vjp_evals"] * ve * Pw)
     K = args.steps
     kern = {"forward": (phases["ms_forward"] / K, fwd_flops),
             "reverse": (phases["ms_reverse"] / K, rev_flops)}

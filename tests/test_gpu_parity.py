@@ -185,12 +185,8 @@ def test_c5_batch_matches_oracle_and_policies_agree():
 
 # ------------------------------------------------------------------ C4 fp32 CNF
 def _cnf_oracle(ci, policy="store_all"):
-    from oracle import fields_ext as ox
-    mlp = oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input)
-    fld = ox.CnfField(mlp, ci.extras["eps"])
-    Y0 = ox.cnf_initial_state(ci.u0)
-    return oc.grad_terminal(fld, ci.scheme, Y0, ci.t0, ci.tF, ci.n_steps, policy,
-                            seed_fn=ox.cnf_seed(fld.D, ci.batch))
+    from oracle.problems import run_oracle
+    return run_oracle(ci, policy)
 
 
 def test_c4_field_protocol_matches_restated_oracle():
