@@ -45,6 +45,10 @@ enum { OB_ACT_IDENTITY = 0, OB_ACT_RELU = 1, OB_ACT_TANH = 2, OB_ACT_GELU = 3, O
 /* right-hand sides: MlpField (integrators.py:76-102); a*u + s*MLP(u) as a
    CallableField (integrators.py:105-141, config C5); CNF and conv are new */
 enum { OB_FIELD_MLP = 0, OB_FIELD_STIFF = 1, OB_FIELD_CNF = 2, OB_FIELD_CONV = 3 };
+/* OB_FIELD_CONV (config C3): state = 16x16 NHWC image with C = widths[2] channels;
+   f = conv3x3(C+1 -> C)(cat(u, t)) -> relu -> conv3x3(C -> C), padding 1, i.e.
+   n_layers = 2, widths = {C+1, C, C}, time_input = 1, activation = relu;
+   theta = [W1 (C x 3 x 3 x (C+1)), b1, W2 (C x 3 x 3 x C), b2]. */
 enum { OB_SCHEME_RK = 0, OB_SCHEME_THETA = 1 };
 /* CheckpointPolicy kinds (checkpointing.py:173-190) */
 enum { OB_POLICY_STORE_ALL = 0, OB_POLICY_STORE_SOLUTIONS = 1, OB_POLICY_REVOLVE = 2 };
@@ -119,6 +123,12 @@ typedef struct {
   void* workspace;        /* scratch, >= ob_grad_workspace_size bytes            */
   size_t workspace_bytes;
   int32_t* sample_stats;  /* optional out [B, OB_NSTATS] per-sample counters, or NULL */
+  /* OB_LOSS_CE_HEAD (config C3): global-average-pool + linear + cross-entropy head */
+  const void* head;       /* [n_classes*C + n_classes] head parameters (W row-major, b) */
+  const int32_t* labels;  /* [B] class labels                                      */
+  void* dhead;            /* out [n_classes*C + n_classes] head gradient (this batch) */
+  int32_t n_classes;
+  int32_t _pad;
 } ob_buffers;
 
 /* per-sample stats columns (implicit schemes; explicit: fixed by the schedule) */

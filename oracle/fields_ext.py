@@ -118,3 +118,101 @@ def cnf_initial_state(z0):
     """[z0, Delta=0]."""
     z0 = np.asarray(z0, dtype=np.float64)
     return np.concatenate([z0, np.zeros((z0.shape[0], 1))], axis=1)
+
+
+# --------------------------------------------------------------------- C3 conv
+def _im2col(X):
+    """[B, H, W, C] -> [B, H*W, 9*C] patches of a 3x3 stencil with zero padding 1,
+    patch order (kh, kw, c) matching weights stored [Cout][kh][kw][Cin]."""
+    B, H, W, C = X.shape
+    Xp = np.zeros((B, H + 2, W + 2, C))
+    Xp[:, 1:-1, 1:-1] = X
+    cols = [Xp[:, kh:kh + H, kw:kw + W, :] for kh in range(3) for kw in range(3)]
+    return np.concatenate(cols, axis=3).reshape(B, H * W, 9 * C)
+
+
+def _col2im(G, H, W, C):
+    """Adjoint of _im2col: [B, H*W, 9*C] -> [B, H, W, C]."""
+    B = G.shape[0]
+    G = G.reshape(B, H, W, 9, C)
+    Xp = np.zeros((B, H + 2, W + 2, C))
+    s = 0
+    for kh in range(3):
+        for kw in range(3):
+            Xp[:, kh:kh + H, kw:kw + W, :] += G[:, :, :, s, :]
+            s += 1
+    return Xp[:, 1:-1, 1:-1]
+
+
+class ConvField:
+    """C3 ODE block: f(u, t) = conv3x3(C+1 -> C)(cat(u, t)) -> relu -> conv3x3(C -> C),
+    padding 1, NHWC state flattened to [B, H*W*C].  theta = [W1 (C x 3 x 3 x (C+1)),
+    b1, W2 (C x 3 x 3 x C), b2] (paper_2206_01298_b200/configs.py make_c3)."""
+
+    def __init__(self, theta, C=64, H=16, W=16):
+        self.C, self.H, self.W = C, H, W
+        th = np.asarray(theta, dtype=np.float64)
+        n1 = C * 9 * (C + 1)
+        n2 = C * 9 * C
+        self.W1 = th[:n1].reshape(C, 9 * (C + 1))
+        self.b1 = th[n1:n1 + C]
+        self.W2 = th[n1 + C:n1 + C + n2].reshape(C, 9 * C)
+        self.b2 = th[n1 + C + n2:n1 + 2 * C + n2]
+        self.n_params = th.size
+        self.n = H * W * C
+
+    def _fwd(self, U, t):
+        B = U.shape[0]
+        X = np.concatenate([U.reshape(B, self.H, self.W, self.C),
+                            np.full((B, self.H, self.W, 1), float(t))], axis=3)
+        P1 = _im2col(X)
+        Z1 = P1 @ self.W1.T + self.b1
+        Hh = np.maximum(Z1, 0.0)
+        P2 = _im2col(Hh.reshape(B, self.H, self.W, self.C))
+        F = P2 @ self.W2.T + self.b2
+        return P1, Z1, P2, F
+
+    def eval(self, U, t, c):
+        c.nfe_forward += 1
+        return self._fwd(U, t)[3].reshape(U.shape[0], -1)
+
+    def vjp(self, U, t, V, c, want_theta=True):
+        c.nfe_backward += 1
+        B, C = U.shape[0], self.C
+        P1, Z1, P2, _ = self._fwd(U, t)
+        Vr = V.reshape(B, self.H * self.W, C)
+        dH = _col2im(Vr @ self.W2, self.H, self.W, C).reshape(B, self.H * self.W, C)
+        dZ1 = dH * (Z1 > 0.0)
+        dX = _col2im(dZ1 @ self.W1, self.H, self.W, C + 1)[..., :C]
+        dth = None
+        if want_theta:
+            dW1 = np.einsum("bpo,bpk->ok", dZ1, P1)
+            dW2 = np.einsum("bpo,bpk->ok", Vr, P2)
+            dth = np.concatenate([dW1.ravel(), dZ1.sum(axis=(0, 1)), dW2.ravel(),
+                                  Vr.sum(axis=(0, 1))])
+        return dX.reshape(B, -1), dth
+
+    def vjp_u(self, U, t, V, c):
+        return self.vjp(U, t, V, c, want_theta=False)[0]
+
+
+def head_loss(Uf, head, labels, C=64, H=16, W=16, n_classes=10, batch_global=None):
+    """Global-average-pool + linear C -> n_classes + cross-entropy, batch mean.
+    Returns (loss, lambda_N [B, H*W*C], dhead [n_classes*C + n_classes])."""
+    B = Uf.shape[0]
+    Bg = batch_global or B
+    Wh = head[:n_classes * C].reshape(n_classes, C)
+    bh = head[n_classes * C:]
+    gap = Uf.reshape(B, H * W, C).mean(axis=1)
+    logits = gap @ Wh.T + bh
+    m = logits.max(axis=1, keepdims=True)
+    ex = np.exp(logits - m)
+    lse = m[:, 0] + np.log(ex.sum(axis=1))
+    loss = float(np.sum(lse - logits[np.arange(B), labels]) / Bg)
+    dlog = ex / ex.sum(axis=1, keepdims=True)
+    dlog[np.arange(B), labels] -= 1.0
+    dlog /= Bg
+    dgap = dlog @ Wh
+    lam = np.repeat(dgap[:, None, :] / (H * W), H * W, axis=1).reshape(B, -1)
+    dhead = np.concatenate([(dlog.T @ gap).ravel(), dlog.sum(axis=0)])
+    return loss, lam, dhead

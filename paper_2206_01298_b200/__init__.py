@@ -12,7 +12,7 @@ from .controls import (ConvergenceError, DeviceError, FixedController, FixedGrid
                        GradientExplosionError, IntegrationError, NfeCounters, SolverConfig,
                        StiffnessError, StoreCounters)
 from .engine import GradResult, grad
-from .fields import (ACTIVATION_IDS, CnfField, Field, MlpField, MlpModel, MlpSpec, StiffMlpField, init_model,
+from .fields import (ACTIVATION_IDS, CnfField, ConvField, Field, MlpField, MlpModel, MlpSpec, StiffMlpField, init_model,
                      mlp_spec)
 from .losses import LossSpec, terminal_loss
 from .policies import CheckpointPolicy, ScheduleAction, revolve_count, revolve_schedule
@@ -21,7 +21,7 @@ from .schemes import SCHEME_NAMES, ButcherTableau, Scheme, tableau_catalog
 __version__ = "0.1.0"
 
 __all__ = [
-    "ACTIVATION_IDS", "ButcherTableau", "CnfField", "CheckpointPolicy", "ConfigInputs", "ConvergenceError",
+    "ACTIVATION_IDS", "ButcherTableau", "CnfField", "CheckpointPolicy", "ConvField", "ConfigInputs", "ConvergenceError",
     "DeviceError", "Field", "FixedController", "FixedGridController", "GradResult",
     "GradientExplosionError", "IntegrationError", "LossSpec", "MlpField", "MlpModel", "MlpSpec",
     "NfeCounters", "SCHEME_NAMES", "ScheduleAction", "Scheme", "SolverConfig", "StiffMlpField",

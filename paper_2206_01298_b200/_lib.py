@@ -66,7 +66,9 @@ class Buffers(C.Structure):
     _fields_ = [("theta", C.c_void_p), ("aux", C.c_void_p), ("u0", C.c_void_p),
                 ("targets", C.c_void_p), ("u_final", C.c_void_p), ("du0", C.c_void_p),
                 ("dtheta", C.c_void_p), ("loss", C.c_void_p), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t), ("sample_stats", C.c_void_p)]
+                ("workspace_bytes", C.c_size_t), ("sample_stats", C.c_void_p),
+                ("head", C.c_void_p), ("labels", C.c_void_p), ("dhead", C.c_void_p),
+                ("n_classes", C.c_int32), ("_pad", C.c_int32)]
 
 
 class Counters(C.Structure):

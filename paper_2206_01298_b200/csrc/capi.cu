@@ -36,6 +36,14 @@ cudaError_t launch_cnf(const RkParams<T>&, int, int, size_t, cudaStream_t, bool)
 template <typename T>
 cudaError_t launch_cnf_field(const RkParams<T>&, int, int, size_t, int, double, const T*, const T*,
                              T*, cudaStream_t);
+template <typename T>
+cudaError_t launch_conv(const RkParams<T>&, int, size_t, cudaStream_t, bool);
+template <typename T>
+cudaError_t launch_conv_field(const RkParams<T>&, int, size_t, int, double, const T*, const T*, T*,
+                              cudaStream_t);
+template <typename T> cudaError_t launch_pack_conv(const PackParams<T>&, cudaStream_t);
+template <typename T>
+cudaError_t launch_reduce_plain(const T*, int, long long, long long, T*, cudaStream_t);
 
 // dispatch on where the weights live (fp32 only stages them in shared memory)
 template <typename T>
@@ -120,7 +128,7 @@ struct Plan {
   int R = 1, Rt = 4, LR = 1, tiles = 1;
   bool need_jvp = false;
   bool theta = false;
-  size_t off_kry = 0, off_stats = 0, off_cnf = 0;
+  size_t off_kry = 0, off_stats = 0, off_cnf = 0, off_state = 0, off_head = 0;
   long long cnf_stride = 0;
   long long krylov_stride = 0;
   SmemLayout sm{};
@@ -151,8 +159,18 @@ int check_field(const ob_field_desc& f) {
   if (f.widths[0] != N + (f.time_input ? 1 : 0))  // MlpSpec.__post_init__ (nn.py:53-58)
     return fail(OB_ERR_VALUE, "input width inconsistent with state dim and time_input");
   if (f.activation < 0 || f.activation > OB_ACT_SOFTPLUS) return fail(OB_ERR_VALUE, "unknown activation");
-  if (f.kind != OB_FIELD_MLP && f.kind != OB_FIELD_STIFF && f.kind != OB_FIELD_CNF)
+  if (f.kind != OB_FIELD_MLP && f.kind != OB_FIELD_STIFF && f.kind != OB_FIELD_CNF &&
+      f.kind != OB_FIELD_CONV)
     return fail(OB_ERR_UNSUPPORTED, "field kind not built into this library version");
+  if (f.kind == OB_FIELD_CONV) {
+    if (f.n_layers != 2 || f.widths[0] != 65 || f.widths[1] != 64 || f.widths[2] != 64 ||
+        !f.time_input || f.activation != OB_ACT_RELU)
+      return fail(OB_ERR_UNSUPPORTED, "conv kernels are built for the 16x16x64 C3 block");
+    if (f.dtype != OB_F32) return fail(OB_ERR_UNSUPPORTED, "conv kernels are built for fp32");
+    if (f.n_params != 64LL * 9 * 65 + 64 + 64LL * 9 * 64 + 64)
+      return fail(OB_ERR_VALUE, "n_params does not match the conv block");
+    return OB_OK;
+  }
   if (f.kind == OB_FIELD_CNF) {
     if (!f.time_input) return fail(OB_ERR_VALUE, "CNF field takes time as an input");
     if (f.dtype != OB_F32) return fail(OB_ERR_UNSUPPORTED, "CNF kernels are built for fp32");
@@ -172,7 +190,40 @@ int ld_quad_odd(int x) {  // >= x, multiple of 4, (ld/4) odd: conflict-free stri
 }
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+void make_conv_dims(const ob_field_desc& f, Dims& d) {
+  d = Dims{};
+  d.L = 2;
+  d.conv = 1;
+  for (int l = 0; l <= 2; ++l) d.w[l] = f.widths[l];
+  d.N = d.nin = d.ldn = 256 * 64;
+  d.conv_cin[0] = 65;
+  d.conv_cin[1] = 64;
+  long long off = 0, mo = 0;
+  for (int l = 0; l < 2; ++l) {
+    d.woff[l] = off;
+    d.boff[l] = off + 64LL * 9 * d.conv_cin[l];
+    off = d.boff[l] + 64;
+    d.ldm[l] = 9 * 68;
+    d.mwoff[l] = mo;
+    mo += 64LL * d.ldm[l];
+    d.mboff[l] = mo;
+    mo += 64;
+  }
+  d.n_mu = mo;
+  d.pwoff[0] = 0;
+  d.pwoff[1] = 64LL * 9 * 68;
+  d.pwoff[2] = 2 * 64LL * 9 * 68;
+  d.pwoff[3] = d.pwoff[2] + 9LL * 64 * 68;
+  d.n_packed = d.pwoff[3] + 9LL * 64 * 68;
+  d.act = f.activation;
+  d.time_input = 1;
+}
+
 void make_dims(const ob_field_desc& f, int LR, Dims& d) {
+  if (f.kind == OB_FIELD_CONV) {
+    make_conv_dims(f, d);
+    return;
+  }
   const int CT = 4 * (32 / LR);
   d = Dims{};
   d.L = f.n_layers;
@@ -216,6 +267,17 @@ void layout_smem(Plan& P) {
   SmemLayout& s = P.sm;
   int o = 0;
   auto take = [&](long long n) { int r = o; o += (int)((n + 7) & ~7LL); return r; };  // 32 B aligned
+  if (d.conv) {   // two zero-halo image tiles; state buffers live in global memory
+    s = SmemLayout{};
+    s.x0 = take(18 * 18 * 68);
+    for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
+    s.hid[0] = take(18 * 18 * 68);
+    s.tA = s.tB = s.u = s.lam = s.lamn = s.w = s.jtv = s.aux = s.wts = -1;
+    for (int i = 0; i < 8; ++i) s.vec[i] = -1;
+    s.total = o;
+    P.smem_bytes = (size_t)o * P.esz;
+    return;
+  }
   const int Rm = d.cnf ? 2 * P.Rt : P.Rt;   // MLP rows (CNF: forward + tangent rows)
   s.x0 = take((long long)Rm * d.lda[0]);
   for (int l = 0; l < OB_MAX_LAYERS; ++l) {
@@ -246,6 +308,13 @@ int pick_lr(int R) { return R <= 4 ? 1 : R <= 8 ? 2 : 8; }
 
 void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   int R = (int)std::max<long long>(1, (B + sm_count - 1) / sm_count);
+  if (f.kind == OB_FIELD_CONV) {   // one sample (a 64 KB image) per CTA
+    P.R = P.Rt = P.LR = 1;
+    make_dims(f, 1, P.d);
+    layout_smem(P);
+    P.tiles = (int)B;
+    return;
+  }
   if (f.kind == OB_FIELD_CNF) {  // stacked forward|tangent rows: 2*Rt = 4*LR
     for (R = std::min(R, 16);; R = std::max(1, R / 2)) {
       P.LR = R <= 4 ? 2 : R <= 8 ? 4 : 8;
@@ -401,10 +470,12 @@ int plan_problem(const ob_problem& p, Plan& P) {
   for (int i = 0; i < p.n_steps; ++i)
     if (!(p.times[i + 1] > p.times[i])) return fail(OB_ERR_VALUE, "step size must be positive");
   if (p.loss != OB_LOSS_HALF_SQNORM && p.loss != OB_LOSS_MSE &&
-      !(p.loss == OB_LOSS_CNF_NLL && p.field.kind == OB_FIELD_CNF))
+      !(p.loss == OB_LOSS_CNF_NLL && p.field.kind == OB_FIELD_CNF) &&
+      !(p.loss == OB_LOSS_CE_HEAD && p.field.kind == OB_FIELD_CONV))
     return fail(OB_ERR_UNSUPPORTED, "loss kind not supported for this field");
-  if (p.field.kind == OB_FIELD_CNF && p.scheme.kind != OB_SCHEME_RK)
-    return fail(OB_ERR_UNSUPPORTED, "CNF field is built for explicit schemes");
+  if ((p.field.kind == OB_FIELD_CNF || p.field.kind == OB_FIELD_CONV) &&
+      p.scheme.kind != OB_SCHEME_RK)
+    return fail(OB_ERR_UNSUPPORTED, "CNF / conv fields are built for explicit schemes");
   P.dtype = p.field.dtype;
   P.esz = P.dtype == OB_F32 ? 4 : 8;
   int dev = 0, sms = 148;
@@ -473,8 +544,14 @@ int plan_problem(const ob_problem& p, Plan& P) {
   P.cnf_stride = 0;
   if (P.d.cnf) {
     for (int l = 0; l < P.d.L - 1; ++l) P.cnf_stride += 2LL * P.Rt * P.d.lda[l + 1];
-    o = align_up(o + P.esz * (size_t)P.tiles * P.cnf_stride, 256);
+  } else if (P.d.conv) {
+    P.cnf_stride = 18LL * 18 * 68;   // parked input tile
   }
+  o = align_up(o + P.esz * (size_t)P.tiles * P.cnf_stride, 256);
+  P.off_state = o;
+  if (P.sm.u < 0) o = align_up(o + P.esz * (size_t)P.tiles * 5 * P.Rt * P.d.ldn, 256);
+  P.off_head = o;
+  if (p.loss == OB_LOSS_CE_HEAD) o = align_up(o + P.esz * (size_t)P.tiles * (10 * 64 + 10), 256);
   P.off_lp = o;
   o = align_up(o + sizeof(double) * P.tiles, 256);
   P.total = o;
@@ -550,6 +627,12 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   rp.eps = static_cast<const T*>(b.aux);
   rp.cnf_pre = reinterpret_cast<T*>(ws + P.off_cnf);
   rp.cnf_pre_stride = P.cnf_stride;
+  rp.state_glob = reinterpret_cast<T*>(ws + P.off_state);
+  rp.state_stride = 5LL * P.Rt * P.d.ldn;
+  rp.head = static_cast<const T*>(b.head);
+  rp.labels = b.labels;
+  rp.n_classes = b.n_classes;
+  rp.head_part = reinterpret_cast<T*>(ws + P.off_head);
   CU(cudaMemsetAsync(stats, 0, sizeof(int) * (size_t)p.batch * OB_NSTATS, st));
 
   // per-phase CUDA events on the launch stream (bench roofline timing)
@@ -558,12 +641,19 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
     for (auto& e : ev) CU(cudaEventCreate(&e));
   CU(cudaMemsetAsync(rp.mu, 0, P.esz * (size_t)P.tiles * P.d.n_mu, st));
   CU(cudaEventRecord(ev[0], st));
-  CU(launch_pack<T>(pp, st));
+  if (P.d.conv) {
+    if constexpr (sizeof(T) == 4) CU(launch_pack_conv<T>(pp, st));
+  } else {
+    CU(launch_pack<T>(pp, st));
+  }
   CU(cudaEventRecord(ev[1], st));
   auto sweep = [&](bool fwd) -> cudaError_t {
     if (P.theta) return launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
-    if (P.d.cnf) {
-      if constexpr (sizeof(T) == 4) return launch_cnf<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
+    if (P.d.cnf || P.d.conv) {
+      if constexpr (sizeof(T) == 4) {
+        if (P.d.conv) return launch_conv<T>(rp, P.tiles, P.smem_bytes, st, fwd);
+        return launch_cnf<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
+      }
       return cudaErrorNotSupported;
     }
     return launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
@@ -574,6 +664,11 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   CU(cudaEventRecord(ev[3], st));
   CU(launch_reduce<T>(P.d, rp.mu, P.tiles, p.field.n_params, static_cast<T*>(b.dtheta),
                       rp.loss_part, rp.inv_batch_global, b.loss, st));
+  if (p.loss == OB_LOSS_CE_HEAD && b.dhead) {
+    if constexpr (sizeof(T) == 4)
+      CU(launch_reduce_plain<T>(rp.head_part, P.tiles, 10 * 64 + 10, 10 * 64 + 10,
+                                static_cast<T*>(b.dhead), st));
+  }
   CU(cudaEventRecord(ev[4], st));
   int hs[2] = {0, 0};
   CU(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -643,6 +738,8 @@ extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* ou
     return fail(OB_ERR_VALUE, "null device buffer");
   if (p->field.kind == OB_FIELD_STIFF && !b->aux) return fail(OB_ERR_VALUE, "stiff field needs diag");
   if (p->field.kind == OB_FIELD_CNF && !b->aux) return fail(OB_ERR_VALUE, "CNF field needs probes");
+  if (p->loss == OB_LOSS_CE_HEAD && (!b->head || !b->labels || b->n_classes != 10))
+    return fail(OB_ERR_VALUE, "cross-entropy head needs head parameters, labels and 10 classes");
   if (p->loss == OB_LOSS_MSE && !b->targets) return fail(OB_ERR_VALUE, "mse loss needs targets");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   st = P.dtype == OB_F32 ? run_grad<float>(*p, *b, P, s) : run_grad<double>(*p, *b, P, s);
@@ -672,9 +769,12 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
   const size_t mu_bytes = mode == kVjp ? P.esz * (size_t)P.tiles * P.d.n_mu : 0;
   long long cnf_stride = 0;
   for (int l = 0; P.d.cnf && l < P.d.L - 1; ++l) cnf_stride += 2LL * P.Rt * P.d.lda[l + 1];
+  if (P.d.conv) cnf_stride = 18LL * 18 * 68;
   const size_t cnf_bytes = align_up(P.esz * (size_t)P.tiles * cnf_stride, 256);
+  const size_t st_bytes = P.sm.u < 0 ? align_up(P.esz * (size_t)P.tiles * 5 * P.Rt * P.d.ldn, 256) : 0;
   char* ws = nullptr;
-  CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), pk_bytes + mu_bytes + cnf_bytes + 256, st));
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), pk_bytes + mu_bytes + cnf_bytes + st_bytes + 256,
+                     st));
   RkParams<T> rp{};
   rp.d = P.d;
   rp.sm = P.sm;
@@ -695,12 +795,24 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
   rp.eps = static_cast<const T*>(aux);
   rp.cnf_pre = reinterpret_cast<T*>(ws + pk_bytes + align_up(mu_bytes, 256));
   rp.cnf_pre_stride = cnf_stride;
+  rp.state_glob = reinterpret_cast<T*>(ws + pk_bytes + align_up(mu_bytes, 256) + cnf_bytes);
+  rp.state_stride = 5LL * P.Rt * P.d.ldn;
   int rc = OB_OK;
   cudaError_t e = cudaSuccess;
   if (mu_bytes) e = cudaMemsetAsync(rp.mu, 0, mu_bytes, st);
-  if (e == cudaSuccess) e = launch_pack<T>(pp, st);
   if (e == cudaSuccess) {
-    if (P.d.cnf) {
+    if (P.d.conv) {
+      if constexpr (sizeof(T) == 4) e = launch_pack_conv<T>(pp, st);
+    } else {
+      e = launch_pack<T>(pp, st);
+    }
+  }
+  if (e == cudaSuccess) {
+    if (P.d.conv) {
+      if constexpr (sizeof(T) == 4)
+        e = launch_conv_field<T>(rp, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
+                                 static_cast<const T*>(w), static_cast<T*>(out), st);
+    } else if (P.d.cnf) {
       if constexpr (sizeof(T) == 4)
         e = launch_cnf_field<T>(rp, P.LR, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
                                 static_cast<const T*>(w), static_cast<T*>(out), st);
@@ -727,7 +839,7 @@ int field_op(const ob_field_desc* f, int64_t batch, const void* theta, const voi
   if (mode == kVjp && !ptv) return fail(OB_ERR_VALUE, "null ptv");
   if ((f->kind == OB_FIELD_STIFF || f->kind == OB_FIELD_CNF) && !aux)
     return fail(OB_ERR_VALUE, "field needs its auxiliary array");
-  if (f->kind == OB_FIELD_CNF && mode == kJvp)
+  if ((f->kind == OB_FIELD_CNF || f->kind == OB_FIELD_CONV) && mode == kJvp)
     return fail(OB_ERR_UNSUPPORTED, "CNF field has no JVP (explicit schemes only)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return f->dtype == OB_F32 ? run_field_op<float>(*f, batch, theta, aux, u, t, w, out, ptv, mode, s)

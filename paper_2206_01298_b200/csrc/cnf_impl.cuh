@@ -46,6 +46,10 @@ struct CnfAdapter {
   }
   OB_DEV T* x0() { return mt.s.x0; }
   OB_DEV int nin() const { return p.d.N - 1; }
+  OB_DEV void put(int r, int j, T v) { mt.s.x0[r * p.d.lda[0] + j] = v; }
+  OB_DEV void put_time(double t) {
+    for (int r = threadIdx.x; r < Rt; r += blockDim.x) mt.s.x0[r * p.d.lda[0] + D] = T(t);
+  }
   OB_DEV void set_scratch(T*, int) {}
   OB_DEV void jvp(const T*, T*) {}
 

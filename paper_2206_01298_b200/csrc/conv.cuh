@@ -1,0 +1,156 @@
+// conv.cuh -- 3x3 (padding 1) convolution GEMMs on one sample's 16x16 NHWC
+// image held in shared memory with a one-pixel zero halo (18x18 pixels x CP
+// channels, CP = 68 = an "odd quad" so 16-byte accesses of 8 consecutive pixels
+// hit distinct banks).  Implicit GEMM: rows are the 256 pixels, the reduction
+// runs over the 9 stencil taps x channels.  Thread tiles are 4 pixels x 4
+// channels (pixels x + 8i, channels strided/contiguous as in gemm.cuh), so a
+// warp covers 32 pixels x 16 channels.
+//   conv_fwd  : out[p][co] = sum_{s,ci} X[p + off(s)][ci] Wf[co][s][ci]
+//   conv_bwd  : out[p][ci] = sum_{s,co} D[p - off(s)][co] Wb[s][co][ci]   (transposed)
+//   conv_wgrad: M[co][s][ci] += scale * sum_p D[p][co] X[p + off(s)][ci]; mb[co] += ...
+// Weights stay in global memory (L1/L2 resident, 0.3 MB per conv pair).
+#pragma once
+
+#include "tile.cuh"   // (tile.cuh pulls gemm.cuh in at the right point)
+
+namespace ob {
+
+constexpr int kImg = 16;          // image side
+constexpr int kHalo = 18;         // with the zero border
+constexpr int kCP = 68;           // padded channel stride in shared memory
+constexpr int kPix = kImg * kImg;
+
+OB_DEV int halo_idx(int p, int dy, int dx) {   // pixel p shifted by (dy, dx) in [0, 2]
+  return ((p / kImg) + dy) * kHalo + (p % kImg) + dx;
+}
+
+// out[p][co] (co < Cout) = sum over taps and ci < Kc of X[...] * Wf[co][s*kCP + ci]
+template <typename T, class Epi>
+OB_DEV void conv_fwd(const T* Xh, const T* Wf, int Cout, int Kc, Warps ws, Epi epi) {
+  constexpr int LR = 8, LC = 4;
+  if (!ws.mine()) return;
+  const int lr = lane_id() % LR, lc = lane_id() / LR;
+  const int ctiles = (Cout + 15) / 16;
+  const uint32_t xs = smem_addr(Xh);
+  const int ldw = 9 * kCP;
+  for (int task = ws.me(); task < (kPix / 32) * ctiles; task += ws.nw) {
+    const int p0 = (task % (kPix / 32)) * 32 + lr, c0 = (task / (kPix / 32)) * 16 + lc;
+    T acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+    for (int s = 0; s < 9; ++s) {
+      const int dy = s / 3, dx = s % 3;
+      int hx[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hx[i] = halo_idx(p0 + i * LR, dy, dx) * kCP;
+      const T* wrow = Wf + s * kCP;
+      for (int ci = 0; ci < Kc; ci += 4) {
+        T x[4][4], w[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Ld<T>::s4(xs + (uint32_t)((hx[i] + ci) * sizeof(T)), x[i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) Ld<T>::g4(wrow + (long long)(c0 + j * LC) * ldw + ci, w[j]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = Num<T>::fma(x[i][q], w[j][q], acc[i][j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (c0 + j * LC < Cout) epi(p0 + i * LR, c0 + j * LC, acc[i][j]);
+  }
+}
+
+// transposed conv: out[p][ci] (ci < Cout) = sum_{s, co < 64} D[p - off(s)][co] * Wb[(s*64+co)][ci]
+template <typename T, class Epi>
+OB_DEV void conv_bwd(const T* Dh, const T* Wb, int ldw, int Cout, Warps ws, Epi epi) {
+  constexpr int LR = 8, LC = 4;
+  if (!ws.mine()) return;
+  const int lr = lane_id() % LR, lc = lane_id() / LR;
+  const int ctiles = (Cout + 15) / 16;
+  const uint32_t ds = smem_addr(Dh);
+  for (int task = ws.me(); task < (kPix / 32) * ctiles; task += ws.nw) {
+    const int p0 = (task % (kPix / 32)) * 32 + lr, k0 = (task / (kPix / 32)) * 16 + 4 * lc;
+    T acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+    for (int s = 0; s < 9; ++s) {
+      const int dy = 2 - s / 3, dx = 2 - s % 3;
+      int hx[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hx[i] = halo_idx(p0 + i * LR, dy, dx) * kCP;
+      const T* wb = Wb + (long long)s * 64 * ldw + k0;
+      for (int co = 0; co < 64; co += 4) {
+        T d[4][4], w[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Ld<T>::s4(ds + (uint32_t)((hx[i] + co) * sizeof(T)), d[i]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Ld<T>::g4(wb + (long long)(co + q) * ldw, w[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = Num<T>::fma(d[i][q], w[q][j], acc[i][j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (k0 + j < Cout) epi(p0 + i * LR, k0 + j, acc[i][j]);
+  }
+}
+
+// M[co][s*kCP + ci] += scale * sum_p D[p][co] X[p + off(s)][ci]  (ci < Kc, Kc % 4 == 0)
+// mb[co] += scale * sum_p D[p][co].  D and X are halo buffers (D read at the centre).
+template <typename T>
+OB_DEV void conv_wgrad(const T* Dh, const T* Xh, int Kc, T scale, T* M, T* mb, Warps ws) {
+  if (!ws.mine()) return;
+  const int tid = ws.me() * 32 + lane_id(), nth = ws.nw * 32;
+  const int kq = Kc / 4, items = 16 * 9 * kq;
+  const uint32_t ds = smem_addr(Dh), xs = smem_addr(Xh);
+  for (int it = tid; it < items; it += nth) {
+    const int co0 = (it % 16) * 4, rest = it / 16, s = rest / kq, ci0 = (rest % kq) * 4;
+    const int dy = s / 3, dx = s % 3;
+    T acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+    for (int p = 0; p < kPix; ++p) {
+      T d[4], x[4];
+      Ld<T>::s4(ds + (uint32_t)((halo_idx(p, 1, 1) * kCP + co0) * sizeof(T)), d);
+      Ld<T>::s4(xs + (uint32_t)((halo_idx(p, dy, dx) * kCP + ci0) * sizeof(T)), x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = Num<T>::fma(d[i], x[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      T* m = M + (long long)(co0 + i) * (9 * kCP) + s * kCP + ci0;
+      T cur[4];
+      Vec4<T>::ld(m, cur);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cur[j] = Num<T>::add(cur[j], Num<T>::mul(scale, acc[i][j]));
+      Vec4<T>::st(m, cur);
+    }
+  }
+  for (int co = tid; co < 64; co += nth) {
+    T sacc = T(0);
+    for (int p = 0; p < kPix; ++p) sacc = Num<T>::add(sacc, Dh[halo_idx(p, 1, 1) * kCP + co]);
+    mb[co] = Num<T>::add(mb[co], Num<T>::mul(scale, sacc));
+  }
+}
+
+}  // namespace ob

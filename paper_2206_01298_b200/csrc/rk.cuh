@@ -64,6 +64,14 @@ struct RkParams {
   T* krylov;              // per tile: Q [R][m+1][ldn] | H [R][m+1][m] | cs, sn [R][m] | g [R][m+1] | y [R][m]
   long long krylov_stride;
   int* sample_stats;      // [B][OB_NSTATS] per-sample counters (nullable)
+  // state buffers (u, lam, lamn, w, jtv) in global memory when sm.u < 0 (C3)
+  T* state_glob;
+  long long state_stride;
+  // classification head (OB_LOSS_CE_HEAD, config C3)
+  const T* head;
+  const int* labels;
+  int n_classes;
+  T* head_part;           // [tiles][n_head] per-tile head-gradient partials
   // CNF (config C4)
   const T* eps;           // Hutchinson probes [B][D]
   T* cnf_pre;             // per tile [L-1][2Rt][lda] pre-activations (forward | raw tangent)

@@ -69,6 +69,12 @@ struct MlpAdapter {
   OB_DEV MlpAdapter(const RkParams<T>& p_, const MlpTile<T, LR, WS>& m) : p(p_), mt(m) {}
   OB_DEV T* x0() { return mt.s.x0; }
   OB_DEV int nin() const { return p.d.N; }
+  // field input: state element j of row r, and the time column (CTA-wide)
+  OB_DEV void put(int r, int j, T v) { mt.s.x0[r * p.d.lda[0] + j] = v; }
+  OB_DEV void put_time(double t) {
+    if (p.d.time_input)
+      for (int r = threadIdx.x; r < p.Rt; r += blockDim.x) mt.s.x0[r * p.d.lda[0] + p.d.N] = T(t);
+  }
   OB_DEV void set_scratch(T* s, int n) { mt.scratch = s; mt.scratch_elems = n; }
   static constexpr bool kHasJvp = true;
 
@@ -127,10 +133,9 @@ struct MlpAdapter {
 template <typename T, class F>
 OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, double h, bool carry,
                          T* rec, int row0, int Rv) {
-  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0], nin = f.nin();
+  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, nin = f.nin();
   const long long kst = (long long)Rt * ldn;
   const long long vec = (long long)p.B * N;
-  T* x0 = f.x0();
   for (int i = 0; i < s; ++i) {
     for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
       const int r = idx / N, j = idx % N;
@@ -139,11 +144,10 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
         const double aiq = p.a[i * OB_MAX_STAGES + q];
         if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), ks[q * kst + r * ldn + j]));
       }
-      if (j < nin) x0[r * ld0 + j] = v;
+      if (j < nin) f.put(r, j, v);
       if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * N + j] = v;
     }
-    if (p.d.time_input)
-      for (int r = threadIdx.x; r < Rt; r += blockDim.x) x0[r * ld0 + nin] = T(t + p.c[i] * h);
+    f.put_time(t + p.c[i] * h);
     __syncthreads();
     if (i == 0 && carry) {  // FSAL: k_0 of this step is k_{s-1} of the previous one
       for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) ks[idx] = ks[(s - 1) * kst + idx];
@@ -183,13 +187,75 @@ OB_DEV void store_rows(T* dst, int N, const T* src, int lds, int row0, int Rv) {
   }
 }
 
+// state-shaped buffers (0 u, 1 lam, 2 lamn, 3 w, 4 jtv): shared memory, or a
+// per-tile global scratch for states too large for it (C3: 16384 per sample)
+template <typename T>
+OB_DEV T* state_buf(const RkParams<T>& p, T* sm, int k) {
+  if (p.sm.u >= 0) {
+    const int off[5] = {p.sm.u, p.sm.lam, p.sm.lamn, p.sm.w, p.sm.jtv};
+    return sm + off[k];
+  }
+  return p.state_glob + blockIdx.x * p.state_stride + (long long)k * p.Rt * p.d.ldn;
+}
+
 // --------------------------------------------------------------- losses
 // Terminal losses (losses.py:78-107 with the batch mean; BASELINE configs):
 // per-tile fp64 partial sums in fixed order, and the seed lambda_N = dL/du(T).
 constexpr double kLog2Pi = 1.8378770664093454836;
 
+// Classification head (config C3): global average pool over the 16x16 pixels,
+// logits = Wh gap + bh, softmax cross-entropy.  Row r's gap/logits/dlogits are
+// computed by warp r; returns nothing, fills g[C], dl[n_classes] (smem).
+template <typename T>
+OB_DEV void ce_head_row(const RkParams<T>& p, const T* urow, int label, double* gap, double* dl,
+                        double* loss) {
+  const int C = p.d.w[2], K = p.n_classes, P = p.d.N / C;
+  for (int c = lane_id(); c < C; c += 32) {
+    double s = 0.0;
+    for (int q = 0; q < P; ++q) s += double(urow[q * C + c]);
+    gap[c] = s / P;
+  }
+  __syncwarp();
+  if (lane_id() == 0) {
+    double mx = -1e300;
+    for (int k = 0; k < K; ++k) {
+      double z = double(p.head[K * C + k]);
+      for (int c = 0; c < C; ++c) z += double(p.head[k * C + c]) * gap[c];
+      dl[k] = z;
+      mx = z > mx ? z : mx;
+    }
+    double se = 0.0;
+    for (int k = 0; k < K; ++k) se += exp(dl[k] - mx);
+    *loss = mx + log(se) - dl[label];
+    for (int k = 0; k < K; ++k) dl[k] = exp(dl[k] - mx) / se - (k == label ? 1.0 : 0.0);
+  }
+  __syncwarp();
+}
+
 template <typename T>
 OB_DEV void loss_partial(const RkParams<T>& p, const T* u, int row0, int Rv, int tile) {
+  if (p.loss_kind == OB_LOSS_CE_HEAD) {
+    // per-tile loss sum and head-gradient partial (dWh = dl gap^T / B, dbh = dl / B)
+    __shared__ double gap[8][64], dl[8][16], lrow[8];
+    const int C = p.d.w[2], K = p.n_classes;
+    const int ldn = p.d.ldn;
+    for (int r = warp_id(); r < Rv && r < 8; r += n_warps())
+      ce_head_row(p, u + r * ldn, p.labels[row0 + r], gap[r], dl[r], &lrow[r]);
+    __syncthreads();
+    T* hp = p.head_part + (long long)tile * (K * C + K);
+    const double ib = 1.0 / p.batch_global;
+    for (int i = threadIdx.x; i < K * C + K; i += blockDim.x) {
+      double acc = 0.0;
+      for (int r = 0; r < Rv; ++r) acc += (i < K * C ? dl[r][i / C] * gap[r][i % C] : dl[r][i - K * C]);
+      hp[i] = T(acc * ib);
+    }
+    if (threadIdx.x == 0) {
+      double acc = 0.0;
+      for (int r = 0; r < Rv; ++r) acc += lrow[r];
+      p.loss_part[tile] = acc;
+    }
+    return;
+  }
   if (threadIdx.x != 0) return;
   const int N = p.d.N, ldn = p.d.ldn;
   double acc = 0.0;
@@ -217,6 +283,27 @@ OB_DEV void loss_partial(const RkParams<T>& p, const T* u, int row0, int Rv, int
 template <typename T>
 OB_DEV void loss_seed(const RkParams<T>& p, T* lam, int row0, int Rv) {
   const int N = p.d.N, ldn = p.d.ldn;
+  if (p.loss_kind == OB_LOSS_CE_HEAD) {
+    // lambda = d CE / du(T) = (dl Wh) / (P * B) broadcast over the pixels
+    __shared__ double gap[8][64], dl[8][16], lrow[8], dg[8][64];
+    const int C = p.d.w[2], K = p.n_classes, P = N / C;
+    for (int r = warp_id(); r < Rv && r < 8; r += n_warps())
+      ce_head_row(p, p.u_final + (long long)(row0 + r) * N, p.labels[row0 + r], gap[r], dl[r],
+                  &lrow[r]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < Rv * C; i += blockDim.x) {
+      const int r = i / C, c = i % C;
+      double s = 0.0;
+      for (int k = 0; k < K; ++k) s += dl[r][k] * double(p.head[k * C + c]);
+      dg[r][c] = s / (double(P) * p.batch_global);
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+      const int r = idx / N, j = idx % N;
+      lam[(long long)r * ldn + j] = T(dg[r][j % C]);
+    }
+    return;
+  }
   for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
     const long long g = (long long)(row0 + r) * N + j;
@@ -242,8 +329,8 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
   F f(p, W, ms, sm, row0, Rv);
   // split-K scratch: the same lamn | w | jtv region as the reverse kernel's
   // replays, so forward and replayed steps sum identically (bit-identical records)
-  f.set_scratch(sm + p.sm.lamn, p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn);
-  T* u = sm + p.sm.u;
+  if (p.sm.u >= 0) f.set_scratch(sm + p.sm.lamn, p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn);
+  T* u = state_buf(p, sm, 0);
   T* ks = p.scratch + tile * p.scratch_stride;
   const int N = p.d.N, ldn = p.d.ldn;
   const long long vec = (long long)p.B * N;
@@ -288,19 +375,19 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
   Weights<T> W;
   setup_tile(p, sm, ms, W);
   F f(p, W, ms, sm, row0, Rv);
-  f.set_scratch(sm + p.sm.lamn, p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn);  // free during replays
-  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, ld0 = p.d.lda[0], nin = f.nin();
+  if (p.sm.u >= 0)  // lamn | w | jtv are free during replays
+    f.set_scratch(sm + p.sm.lamn, p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn);
+  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, nin = f.nin();
   const long long vec = (long long)p.B * N;
   const long long kst = (long long)Rt * ldn;
-  T* u = sm + p.sm.u;
-  T* lam = sm + p.sm.lam;
-  T* lamn = sm + p.sm.lamn;
-  T* w = sm + p.sm.w;
-  T* jtv = sm + p.sm.jtv;
+  T* u = state_buf(p, sm, 0);
+  T* lam = state_buf(p, sm, 1);
+  T* lamn = state_buf(p, sm, 2);
+  T* w = state_buf(p, sm, 3);
+  T* jtv = state_buf(p, sm, 4);
   T* ks = p.scratch + tile * p.scratch_stride;
   T* Lam = ks + s * kst;
   T* mu = p.mu + tile * p.d.n_mu;
-  T* x0 = f.x0();
 
   loss_seed(p, lam, row0, Rv);
   __syncthreads();
@@ -341,13 +428,12 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
         }
         w[o] = v;
       }
-      // stage state U_i into x0 (+ stage time)
+      // stage state U_i into the field input (+ stage time)
       for (int idx = threadIdx.x; idx < Rv * nin; idx += blockDim.x) {
         const int r = idx / nin, j = idx % nin;
-        x0[r * ld0 + j] = rec[i * vec + (long long)(row0 + r) * N + j];
+        f.put(r, j, rec[i * vec + (long long)(row0 + r) * N + j]);
       }
-      if (p.d.time_input)
-        for (int r = threadIdx.x; r < Rt; r += blockDim.x) x0[r * ld0 + nin] = T(t + p.c[i] * h);
+      f.put_time(t + p.c[i] * h);
       __syncthreads();
       f.vjp(w, jtv, mu, h, Rv);
       // Lam_i = h * jtv; lam_n += Lam_i
@@ -388,16 +474,14 @@ field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const
   Weights<T> W;
   setup_tile(p, sm, ms, W);
   F f(p, W, ms, sm, row0, Rv);
-  const int N = p.d.N, ldn = p.d.ldn, ld0 = p.d.lda[0], nin = f.nin();
-  T* wb = sm + p.sm.w;
-  T* res = sm + p.sm.jtv;
-  T* x0 = f.x0();
+  const int N = p.d.N, ldn = p.d.ldn, nin = f.nin();
+  T* wb = state_buf(p, sm, 3);
+  T* res = state_buf(p, sm, 4);
   for (int idx = threadIdx.x; idx < Rv * nin; idx += blockDim.x) {
     const int r = idx / nin, j = idx % nin;
-    x0[r * ld0 + j] = u[(long long)(row0 + r) * N + j];
+    f.put(r, j, u[(long long)(row0 + r) * N + j]);
   }
-  if (p.d.time_input)
-    for (int r = threadIdx.x; r < p.Rt; r += blockDim.x) x0[r * ld0 + nin] = T(t);
+  f.put_time(t);
   if (mode != 0) load_rows(wb, ldn, w, N, row0, Rv);
   __syncthreads();
   if (mode == 0) {
@@ -438,7 +522,12 @@ __global__ void reduce_tiles_kernel(const __grid_constant__ Dims d, const T* mu,
     int l = 0;
     while (l + 1 < d.L && j >= d.woff[l + 1]) ++l;
     long long src;
-    if (j < d.boff[l]) {
+    if (j < d.boff[l] && d.conv) {   // theta [co][tap][cin] -> mu [co][tap][68]
+      const long long q = j - d.woff[l];
+      const int cin = d.conv_cin[l];
+      const long long co = q / (9 * cin), r = q % (9 * cin);
+      src = d.mwoff[l] + co * d.ldm[l] + (r / cin) * 68 + r % cin;
+    } else if (j < d.boff[l]) {
       const long long q = j - d.woff[l];
       src = d.mwoff[l] + (q / d.w[l]) * d.ldm[l] + q % d.w[l];
     } else {

@@ -104,6 +104,8 @@ struct Dims {
   int N, ldn;                     // state dim, its buffer leading dim
   int nin;                        // state components fed to the MLP (CNF: N - 1)
   int cnf;                        // 1: continuous normalizing flow field (C4)
+  int conv;                       // 1: 3x3 conv block on a 16x16 NHWC image (C3)
+  int conv_cin[OB_MAX_LAYERS];    // conv: input channels per stencil tap in theta
   int act, time_input;
   int need_pre;                   // act' needs the pre-activation (gelu / softplus)
   int maxw, ldt;                  // widest layer, tangent buffer leading dim

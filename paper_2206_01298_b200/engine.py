@@ -38,6 +38,7 @@ class GradResult:
     # nfe_backward, newton_iters, gmres_iters_forward, gmres_iters_adjoint
     # (implicit schemes; explicit ones repeat the schedule-fixed counts)
     sample_counters: dict = None
+    dtheta_head: object = None      # ce_head loss: gradient of the classification head
 
 
 _WS_CACHE = {}
@@ -124,6 +125,15 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     bufs.workspace_bytes = ws.numel()
     stats = torch.zeros((B, _lib.OB_NSTATS), dtype=torch.int32, device=dev)
     bufs.sample_stats = stats.data_ptr()
+    dhead = None
+    if loss.kind == "ce_head":
+        head = to_device(loss.values[0], dt).reshape(-1)
+        labels = to_device(loss.values[1], torch.int32).reshape(-1)
+        if head.numel() != 10 * 64 + 10 or labels.numel() != B:
+            raise ValueError("ce_head needs 650 head parameters and one label per sample")
+        dhead = torch.empty_like(head)
+        bufs.head, bufs.labels, bufs.dhead = head.data_ptr(), labels.data_ptr(), dhead.data_ptr()
+        bufs.n_classes = 10
     cnt = _lib.Counters()
     rc = _lib.load().ob_grad(C.byref(prob), C.byref(bufs), C.byref(cnt), stream_ptr())
     raise_status(rc, _lib.last_error())
@@ -146,6 +156,8 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
         dtheta_o, du0_o, uf_o = dtheta.cpu().numpy(), du0.cpu().numpy(), u_final.cpu().numpy()
     else:
         dtheta_o, du0_o, uf_o = dtheta, du0, u_final
+    if dhead is not None and host_io:
+        dhead = dhead.cpu().numpy()
     return GradResult(dtheta=dtheta_o, du0=du0_o, loss=loss_v, counters=counters,
                       predictions=[uf_o], u_final=uf_o, store_counters=sc, device=c,
-                      sample_counters=samp)
+                      sample_counters=samp, dtheta_head=dhead)

@@ -289,3 +289,47 @@ class CnfField(MlpField):
 
     def aux(self):
         return self.eps
+
+
+class ConvField(Field):
+    """Image-classifier ODE block (config C3): state = 16x16x64 NHWC image
+    flattened to [B, 16384]; f(u, t) = conv3x3(65 -> 64)(cat(u, t)) -> relu ->
+    conv3x3(64 -> 64), padding 1.  theta = [W1 (64 x 3 x 3 x 65), b1,
+    W2 (64 x 3 x 3 x 64), b2].  No reference counterpart (SURVEY 8a row a20);
+    restated oracle in oracle/fields_ext.py."""
+
+    kind = _lib.OB_FIELD_CONV
+    C = 64
+    widths = (65, 64, 64)
+
+    def __init__(self, theta, dtype="f32"):
+        if dtype != "f32":
+            raise NotImplementedError("conv kernels are built for fp32")
+        self.n_params = 64 * 9 * 65 + 64 + 64 * 9 * 64 + 64
+        self.theta = to_device(theta, torch.float32).reshape(-1)
+        if self.theta.numel() != self.n_params:
+            raise ValueError(f"expected length {self.n_params}, got {self.theta.numel()}")
+
+    @property
+    def torch_dtype(self):
+        return torch.float32
+
+    @property
+    def n(self):
+        return 16 * 16 * self.C
+
+    def theta_tensor(self):
+        return self.theta
+
+    def desc(self) -> _lib.FieldDesc:
+        d = _lib.FieldDesc()
+        d.kind = self.kind
+        d.dtype = _lib.OB_F32
+        d.n_layers = 2
+        for i, w in enumerate(self.widths):
+            d.widths[i] = w
+        d.activation = ACTIVATION_IDS["relu"]
+        d.time_input = 1
+        d.out_scale = 1.0
+        d.n_params = self.n_params
+        return d

@@ -11,13 +11,15 @@ import numpy as np
 from .configs import ConfigInputs
 from .controls import FixedController, SolverConfig
 from .engine import grad
-from .fields import CnfField, MlpField, MlpModel, MlpSpec, StiffMlpField
+from .fields import CnfField, ConvField, MlpField, MlpModel, MlpSpec, StiffMlpField
 from .losses import terminal_loss
 from .policies import CheckpointPolicy
 from .schemes import tableau_catalog
 
 
 def field_from_config(ci: ConfigInputs):
+    if ci.kind == "conv":
+        return ConvField(ci.theta)
     spec = MlpSpec(tuple(ci.widths), ci.activation, ci.time_input, ci.dtype)
     model = MlpModel(spec, ci.theta)
     if ci.kind == "mlp":
@@ -38,16 +40,25 @@ def initial_state(ci: ConfigInputs):
     """Integration state at t0 (CNF: [z0, Delta = 0])."""
     if ci.kind == "cnf":
         return np.concatenate([ci.u0, np.zeros((ci.batch, 1))], axis=1)
+    if ci.kind == "conv":
+        return ci.u0.reshape(ci.batch, -1)
     return ci.u0
 
 
 def loss_kind(ci: ConfigInputs) -> str:
-    return "cnf_nll" if ci.kind == "cnf" else "half_sqnorm"
+    return {"cnf": "cnf_nll", "conv": "ce_head"}.get(ci.kind, "half_sqnorm")
+
+
+def loss_for(ci: ConfigInputs, rows=slice(None)):
+    kind = loss_kind(ci)
+    if kind == "ce_head":
+        return terminal_loss(kind, ci.tF, (ci.extras["head"], ci.extras["labels"][rows]))
+    return terminal_loss(kind, ci.tF)
 
 
 def run_config(ci: ConfigInputs, policy: str = None, field=None, u0=None, **kw):
     field = field if field is not None else field_from_config(ci)
     pol = CheckpointPolicy.parse(policy or ci.policy)
-    return grad(field, tableau_catalog(ci.scheme), terminal_loss(loss_kind(ci), ci.tF),
+    return grad(field, tableau_catalog(ci.scheme), loss_for(ci),
                 initial_state(ci) if u0 is None else u0, ci.t0, ci.tF,
                 FixedController(ci.n_steps), pol, solver_from_config(ci), **kw)

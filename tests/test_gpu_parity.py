@@ -221,6 +221,40 @@ def test_c4_subset_matches_restated_oracle_and_policies_agree():
     assert base.counters.nfe_forward == 121 and base.counters.nfe_backward == 140
 
 
+# ------------------------------------------------------------------ C3 fp32 conv
+def test_c3_field_protocol_matches_restated_oracle():
+    from oracle import fields_ext as ox
+    ci = make_config("C3").subset(3)
+    fld = field_from_config(ci)
+    ofl = ox.ConvField(ci.theta)
+    rng = np.random.default_rng(9)
+    U = ci.u0.reshape(3, -1)
+    V = rng.standard_normal(U.shape).astype(np.float32).astype(np.float64)
+    f_ref = ofl.eval(U, 0.35, oc.Counters())
+    j_ref, p_ref = ofl.vjp(U, 0.35, V, oc.Counters())
+    assert oc.rel_error(np_(fld.eval(U, 0.35)), f_ref) <= TOL32
+    j, p = fld.vjp(U, 0.35, V)
+    assert oc.rel_error(np_(j), j_ref) <= TOL32
+    assert oc.rel_error(np_(p), p_ref) <= TOL32
+
+
+def test_c3_subset_matches_restated_oracle_and_policies_agree():
+    from oracle import fields_ext as ox
+    from oracle.problems import run_oracle
+    ci = make_config("C3").subset(6)
+    fld = field_from_config(ci)
+    base = run_config(ci, "store_all", field=fld)
+    rev = run_config(ci, "revolve:3", field=fld)
+    assert np.array_equal(base.dtheta, rev.dtheta) and base.loss == rev.loss
+    ref = run_oracle(ci, "store_all")
+    errs = {k: oc.rel_error(np_(getattr(base, k)), ref[k]) for k in ("u_final", "du0", "dtheta")}
+    assert max(errs.values()) <= TOL32, errs
+    assert abs(base.loss - ref["loss"]) <= TOL32 * abs(ref["loss"])
+    dhead = ox.head_loss(ref["u_final"], ci.extras["head"], ci.extras["labels"])[2]
+    assert oc.rel_error(np_(base.dtheta_head), dhead) <= TOL32
+    assert base.counters.nfe_forward == 40 and base.counters.nfe_backward == 40
+
+
 # ------------------------------------------------- all schemes, policies
 EXPLICIT = ("euler", "midpoint", "bosh3", "rk4", "dopri5")
 THETA = ("beuler", "cn")

@@ -88,3 +88,39 @@ def test_cnf_full_gradient_matches_finite_differences():
         e[idx] = 1e-6
         gy[idx] = (loss_of(y0=Y + e) - loss_of(y0=Y - e)) / 2e-6
     assert oc.rel_error(res["du0"], gy) <= 1e-6
+
+
+def test_conv_vjp_matches_finite_differences():
+    rng = np.random.default_rng(5)
+    C, H = 3, 4
+    n1, n2 = C * 9 * (C + 1), C * 9 * C
+    theta = rng.standard_normal(n1 + n2 + 2 * C) * 0.3
+    fld = ox.ConvField(theta, C=C, H=H, W=H)
+    U = rng.standard_normal((2, H * H * C))
+    V = rng.standard_normal(U.shape)
+    jtv, ptv = fld.vjp(U, 0.6, V, oc.Counters())
+
+    def phi(u=U, th=theta):
+        f2 = ox.ConvField(th, C=C, H=H, W=H)
+        return float(np.sum(V * f2.eval(u, 0.6, oc.Counters())))
+
+    g = np.array([(phi(u=U + e.reshape(U.shape)) - phi(u=U - e.reshape(U.shape))) / 2e-6
+                  for e in np.eye(U.size) * 1e-6]).reshape(U.shape)
+    assert oc.rel_error(jtv, g) <= 1e-7
+    gt = np.array([(phi(th=theta + e) - phi(th=theta - e)) / 2e-6 for e in np.eye(theta.size) * 1e-6])
+    assert oc.rel_error(ptv, gt) <= 1e-7
+
+
+def test_conv_head_loss_gradients_match_finite_differences():
+    rng = np.random.default_rng(6)
+    C, H, K = 3, 4, 5
+    Uf = rng.standard_normal((3, H * H * C))
+    head = rng.standard_normal(K * C + K)
+    labels = rng.integers(0, K, 3)
+    loss, lam, dhead = ox.head_loss(Uf, head, labels, C=C, H=H, W=H, n_classes=K)
+    f = lambda u, h: ox.head_loss(u, h, labels, C=C, H=H, W=H, n_classes=K)[0]   # noqa: E731
+    g = np.array([(f(Uf + e.reshape(Uf.shape), head) - f(Uf - e.reshape(Uf.shape), head)) / 2e-6
+                  for e in np.eye(Uf.size) * 1e-6]).reshape(Uf.shape)
+    assert oc.rel_error(lam, g) <= 1e-7
+    gh = np.array([(f(Uf, head + e) - f(Uf, head - e)) / 2e-6 for e in np.eye(head.size) * 1e-6])
+    assert oc.rel_error(dhead, gh) <= 1e-7
