@@ -36,6 +36,8 @@ METRIC = "ODE-block fwd+discrete-adjoint grad samples/s at 1–8 B200; % of roof
 WORKLOADS = {
     "C1": "C1: MLP 64-256-64 tanh fp64, RK4 x10 on [0,1], store_all, B=512/GPU",
     "C2": "C2: MLP (64+t)-256-64 tanh fp32, Dopri5 x40 on [0,1], revolve:8, B=4096/GPU",
+    "C3": "C3: conv ODE block 16x16x64 fp32, conv3x3(65->64)+relu+conv3x3(64->64), RK4 x10, "
+          "store_all, GAP+linear+CE head, B=256/GPU",
     "C4": "C4: CNF (43+t)-860-860-43 softplus fp32 + Hutchinson (1 Rademacher probe), Dopri5 x20, "
           "store_all, NLL loss, B=1000/GPU",
     "C5": "C5: stiff a*u + 0.1*MLP 128-512-128 tanh fp64, Crank-Nicolson x20, Newton 1e-10 + "
@@ -226,17 +228,17 @@ def main():
     from paper_2206_01298_b200.configs import make_config
     from paper_2206_01298_b200.distributed import grad_sharded, shard_bounds
     from paper_2206_01298_b200.engine import grad
-    from paper_2206_01298_b200.workloads import (field_from_config, initial_state, loss_kind,
+    from paper_2206_01298_b200.workloads import (field_from_config, initial_state, loss_for,
                                                  solver_from_config)
 
     base = make_config(args.config, batch=1)
-    per_gpu = {"C1": 512, "C2": 4096, "C4": 1000, "C5": 256}[args.config]
+    per_gpu = {"C1": 512, "C2": 4096, "C3": 256, "C4": 1000, "C5": 256}[args.config]
     ci = make_config(args.config, batch=per_gpu * world)      # weak scaling: N x per-GPU batch
     lo, hi = shard_bounds(ci.batch, world, rank)
     policy = CheckpointPolicy.parse(args.policy or base.policy)
     field = field_from_config(ci)
     scheme = tableau_catalog(ci.scheme)
-    loss = terminal_loss(loss_kind(ci), ci.tF)
+    loss = loss_for(ci, slice(lo, hi))
     ctrl = FixedController(ci.n_steps)
     scfg = solver_from_config(ci)
     tdt = field.torch_dtype
@@ -308,6 +310,8 @@ def main():
     # ---- roofline of the dominant kernel (CUDA events around each launch, in-library)
     dev = res.device
     Pw = sum(ci.widths[l] * ci.widths[l + 1] for l in range(len(ci.widths) - 1))
+    if ci.kind == "conv":   # MACs per sample of one f-eval: 256 px x 9 taps x (65*64 + 64*64)
+        Pw = 256 * 9 * (65 * 64 + 64 * 64)
     s = scheme.stages
     replays = dev["steps_recomputed"]
     # algorithmic FLOPs per sample: MLP f-eval
