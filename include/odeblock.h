@@ -108,7 +108,14 @@ typedef struct {
   int32_t nc;             /* revolve slots                                         */
   int32_t loss;           /* OB_LOSS_*                                             */
   const double* times;    /* HOST array, n_steps+1 boundary times (integrators.py:276) */
+  int32_t flags;          /* OB_FLAG_* */
+  int32_t _pad;
 } ob_problem;
+
+/* flags: accumulate per-phase SM cycles of the persistent kernels (profiling aid;
+   read with ob_debug_phase_cycles) */
+enum { OB_FLAG_PHASE_TIMING = 1 };
+#define OB_NPHASES 16
 
 /* Device buffers of one gradient call. */
 typedef struct {
@@ -164,6 +171,9 @@ int ob_revolve_schedule(int32_t nt, int32_t nc, int32_t* actions, int64_t capaci
    loss_and_grad_seed (losses.py:78-107) + backward_sweep (:235-253). */
 int ob_grad_workspace_size(const ob_problem* p, size_t* bytes);
 int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream);
+
+/* ---- profiling aid: per-phase cycle totals summed over CTAs (reset: zero them) */
+int ob_debug_phase_cycles(uint64_t* out, int32_t n, int32_t reset);
 
 /* ---- the Field protocol, batched (integrators.py:53-102) -----------------
    eval: f(u,t); jvp: (df/du) w; vjp: ((df/du)^T v, sum_b (df/dtheta)^T v);

@@ -33,7 +33,7 @@ OB_NSTATS = 5
 
 EXPORTS = (
     "ob_version", "ob_last_error", "ob_device_count", "ob_revolve_count", "ob_revolve_schedule",
-    "ob_grad_workspace_size", "ob_grad", "ob_field_eval", "ob_field_jvp", "ob_field_vjp",
+    "ob_grad_workspace_size", "ob_grad", "ob_debug_phase_cycles", "ob_field_eval", "ob_field_jvp", "ob_field_vjp",
     "ob_field_vjp_u",
 )
 
@@ -59,7 +59,7 @@ class Problem(C.Structure):
     _fields_ = [("field", FieldDesc), ("scheme", SchemeDesc), ("solver", SolverDesc),
                 ("batch", C.c_int64), ("batch_global", C.c_int64), ("n_steps", C.c_int32),
                 ("policy", C.c_int32), ("nc", C.c_int32), ("loss", C.c_int32),
-                ("times", C.POINTER(C.c_double))]
+                ("times", C.POINTER(C.c_double)), ("flags", C.c_int32), ("_pad", C.c_int32)]
 
 
 class Buffers(C.Structure):
@@ -110,6 +110,7 @@ def load():
         lib.ob_revolve_schedule.argtypes = [i32, i32, C.POINTER(i32), i64, C.POINTER(i64)]
         lib.ob_grad_workspace_size.argtypes = [C.POINTER(Problem), C.POINTER(C.c_size_t)]
         lib.ob_grad.argtypes = [C.POINTER(Problem), C.POINTER(Buffers), C.POINTER(Counters), vp]
+        lib.ob_debug_phase_cycles.argtypes = [C.POINTER(C.c_uint64), C.c_int32, C.c_int32]
         fd = C.POINTER(FieldDesc)
         lib.ob_field_eval.argtypes = [fd, i64, vp, vp, vp, C.c_double, vp, vp]
         lib.ob_field_jvp.argtypes = [fd, i64, vp, vp, vp, C.c_double, vp, vp, vp]

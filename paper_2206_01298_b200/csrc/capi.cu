@@ -81,6 +81,31 @@ static int fail(int code, const std::string& msg) {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static int pad4i(int n) { return (n + 3) & ~3; }
 
+static unsigned long long* g_phase = nullptr;   // device [OB_NPHASES] (profiling aid)
+
+static unsigned long long* phase_buffer() {
+  if (!g_phase) {
+    if (cudaMalloc(&g_phase, sizeof(unsigned long long) * OB_NPHASES) != cudaSuccess) {
+      g_phase = nullptr;
+      return nullptr;
+    }
+    cudaMemset(g_phase, 0, sizeof(unsigned long long) * OB_NPHASES);
+  }
+  return g_phase;
+}
+
+extern "C" int ob_debug_phase_cycles(uint64_t* out, int32_t n, int32_t reset) {
+  unsigned long long h[OB_NPHASES] = {};
+  unsigned long long* d = phase_buffer();
+  if (!d) return fail(OB_ERR_CUDA, "no device");
+  cudaError_t e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(OB_ERR_CUDA, cudaGetErrorString(e));
+  for (int i = 0; i < n && i < OB_NPHASES; ++i) out[i] = h[i];
+  if (reset && (e = cudaMemset(d, 0, sizeof(h))) != cudaSuccess)
+    return fail(OB_ERR_CUDA, cudaGetErrorString(e));
+  return OB_OK;
+}
+
 extern "C" const char* ob_version(void) { return "odeblock-b200 0.1.0 (sm_100a)"; }
 extern "C" const char* ob_last_error(void) { return g_err.c_str(); }
 
@@ -551,7 +576,9 @@ int plan_problem(const ob_problem& p, Plan& P) {
   P.off_state = o;
   if (P.sm.u < 0) o = align_up(o + P.esz * (size_t)P.tiles * 5 * P.Rt * P.d.ldn, 256);
   P.off_head = o;
-  if (p.loss == OB_LOSS_CE_HEAD) o = align_up(o + P.esz * (size_t)P.tiles * (10 * 64 + 10), 256);
+  if (p.loss == OB_LOSS_CE_HEAD)   // partials + fp64 scratch (gap|dl|loss rows, dgap rows)
+    o = align_up(o + P.esz * (size_t)P.tiles * (10 * 64 + 10) + 16 +
+                     sizeof(double) * (size_t)P.tiles * 8 * (81 + 64), 256);
   P.off_lp = o;
   o = align_up(o + sizeof(double) * P.tiles, 256);
   P.total = o;
@@ -614,6 +641,8 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   rp.loss_part = reinterpret_cast<double*>(ws + P.off_lp);
   int* status = reinterpret_cast<int*>(ws + P.off_blob + o_stat);
   rp.status = status;
+  rp.prof = (p.flags & OB_FLAG_PHASE_TIMING) ? 1 : 0;
+  rp.phase = rp.prof ? phase_buffer() : nullptr;
   rp.theta = p.scheme.theta;
   rp.newton_tol = p.solver.newton_tol;
   rp.gmres_tol = p.solver.gmres_tol;
@@ -633,6 +662,7 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   rp.labels = b.labels;
   rp.n_classes = b.n_classes;
   rp.head_part = reinterpret_cast<T*>(ws + P.off_head);
+  rp.tiles_total = P.tiles;
   CU(cudaMemsetAsync(stats, 0, sizeof(int) * (size_t)p.batch * OB_NSTATS, st));
 
   // per-phase CUDA events on the launch stream (bench roofline timing)

@@ -122,6 +122,9 @@ OB_DEV void conv_wgrad(const T* Dh, const T* Xh, int Kc, T scale, T* M, T* mb, W
   for (int it = tid; it < items; it += nth) {
     const int co0 = (it % 16) * 4, rest = it / 16, s = rest / kq, ci0 = (rest % kq) * 4;
     const int dy = s / 3, dx = s % 3;
+    T cur[4][4];   // prefetch the slot (L2) so its latency overlaps the pixel loop
+#pragma unroll
+    for (int i = 0; i < 4; ++i) Vec4<T>::ld(M + (long long)(co0 + i) * (9 * kCP) + s * kCP + ci0, cur[i]);
     T acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -138,12 +141,9 @@ OB_DEV void conv_wgrad(const T* Dh, const T* Xh, int Kc, T scale, T* M, T* mb, W
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      T* m = M + (long long)(co0 + i) * (9 * kCP) + s * kCP + ci0;
-      T cur[4];
-      Vec4<T>::ld(m, cur);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) cur[j] = Num<T>::add(cur[j], Num<T>::mul(scale, acc[i][j]));
-      Vec4<T>::st(m, cur);
+      for (int j = 0; j < 4; ++j) cur[i][j] = Num<T>::add(cur[i][j], Num<T>::mul(scale, acc[i][j]));
+      Vec4<T>::st(M + (long long)(co0 + i) * (9 * kCP) + s * kCP + ci0, cur[i]);
     }
   }
   for (int co = tid; co < 64; co += nth) {

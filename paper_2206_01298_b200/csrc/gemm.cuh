@@ -210,6 +210,11 @@ OB_DEV void gemm_tn_accum(const T* D, int ldd, const T* X, int ldx, int R, int N
   const uint32_t ds = smem_addr(D), xs = smem_addr(X);
   for (int it = tid; it < items; it += nth) {
     const int n0 = (it / kq) * 4, k0 = (it % kq) * 4;
+    // the slot's current values are fetched first so their L2 latency overlaps the R-loop
+    T cur[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (n0 + i < N) Vec4<T>::ld(M + (long long)(n0 + i) * ldm + k0, cur[i]);
     T acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -227,12 +232,9 @@ OB_DEV void gemm_tn_accum(const T* D, int ldd, const T* X, int ldx, int R, int N
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (n0 + i < N) {
-        T* m = M + (long long)(n0 + i) * ldm + k0;
-        T cur[4];
-        Vec4<T>::ld(m, cur);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cur[j] = Num<T>::add(cur[j], Num<T>::mul(scale, acc[i][j]));
-        Vec4<T>::st(m, cur);
+        for (int j = 0; j < 4; ++j) cur[i][j] = Num<T>::add(cur[i][j], Num<T>::mul(scale, acc[i][j]));
+        Vec4<T>::st(M + (long long)(n0 + i) * ldm + k0, cur[i]);
       }
     }
   }

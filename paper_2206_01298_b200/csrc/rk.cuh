@@ -57,6 +57,8 @@ struct RkParams {
   long long n_params;
   double* loss_part;      // [tiles]
   int* status;            // [2] first error code, step
+  int prof;               // OB_FLAG_PHASE_TIMING
+  unsigned long long* phase;  // [OB_NPHASES] cycle accumulators (prof only)
   // theta methods (integrators.py:225-244, linalg.py:37-142)
   double theta;
   double newton_tol, gmres_tol;
@@ -71,7 +73,8 @@ struct RkParams {
   const T* head;
   const int* labels;
   int n_classes;
-  T* head_part;           // [tiles][n_head] per-tile head-gradient partials
+  T* head_part;           // [tiles][n_head] head-gradient partials, then fp64 scratch
+  int tiles_total;
   // CNF (config C4)
   const T* eps;           // Hutchinson probes [B][D]
   T* cnf_pre;             // per tile [L-1][2Rt][lda] pre-activations (forward | raw tangent)
@@ -84,5 +87,10 @@ struct PackParams {
   const T* theta;
   T* packed;
 };
+
+// per-phase SM-cycle counters (profiling aid, OB_FLAG_PHASE_TIMING)
+enum { kPhElem = 0, kPhRecompute = 1, kPhVjp = 2, kPhLam = 3, kPhReplay = 4, kPhFwdStep = 5,
+       kPhGmres = 6, kPhOther = 7 };
+
 
 }  // namespace ob

@@ -65,7 +65,9 @@ struct MlpAdapter {
   const RkParams<T>& p;
   MlpTile<T, LR, WS> mt;
   OB_DEV MlpAdapter(const RkParams<T>& p_, const Weights<T>& W, MlpSmem<T>& ms, T*, int, int)
-      : p(p_), mt(p_.d, W, ms, p_.Rt) {}
+      : p(p_), mt(p_.d, W, ms, p_.Rt) {
+    mt.prof_acc = p.prof ? p.phase : nullptr;
+  }
   OB_DEV MlpAdapter(const RkParams<T>& p_, const MlpTile<T, LR, WS>& m) : p(p_), mt(m) {}
   OB_DEV T* x0() { return mt.s.x0; }
   OB_DEV int nin() const { return p.d.N; }
@@ -109,7 +111,9 @@ struct MlpAdapter {
 
   // ((df/du)^T w, mu += h * (df/dtheta)^T w) at the state in x0
   OB_DEV void vjp(const T* w, T* jtv, T* mu, double h, int Rv) {
+    PhaseTimer pt(p.prof ? p.phase : nullptr);
     mt.forward(nullptr, 0, p.d.L - 1);  // hidden layers only: the output value is not needed
+    pt.mark(kPhRecompute);
     const int ldn = p.d.ldn;
     if (p.field_kind == OB_FIELD_STIFF) {
       mt.vjp(w, ldn, Rv, jtv, ldn, mu, T(h * double(p.out_scale)));
@@ -136,6 +140,7 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
   const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, nin = f.nin();
   const long long kst = (long long)Rt * ldn;
   const long long vec = (long long)p.B * N;
+  PhaseTimer pt(p.prof ? p.phase : nullptr);
   for (int i = 0; i < s; ++i) {
     for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
       const int r = idx / N, j = idx % N;
@@ -149,12 +154,14 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
     }
     f.put_time(t + p.c[i] * h);
     __syncthreads();
+    pt.mark(8);   // stage combination + record write
     if (i == 0 && carry) {  // FSAL: k_0 of this step is k_{s-1} of the previous one
       for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) ks[idx] = ks[(s - 1) * kst + idx];
       __syncthreads();
     } else {
       f.eval(ks + i * kst);
     }
+    pt.mark(9);   // field eval
   }
   int bad = 0;
   for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
@@ -235,23 +242,27 @@ OB_DEV void ce_head_row(const RkParams<T>& p, const T* urow, int label, double* 
 template <typename T>
 OB_DEV void loss_partial(const RkParams<T>& p, const T* u, int row0, int Rv, int tile) {
   if (p.loss_kind == OB_LOSS_CE_HEAD) {
-    // per-tile loss sum and head-gradient partial (dWh = dl gap^T / B, dbh = dl / B)
-    __shared__ double gap[8][64], dl[8][16], lrow[8];
+    // per-tile loss sum and head-gradient partial (dWh = dl gap^T / B, dbh = dl / B);
+    // scratch rows (gap | dl | loss, fp64) live after this tile's head partial
     const int C = p.d.w[2], K = p.n_classes;
     const int ldn = p.d.ldn;
+    double* scr = reinterpret_cast<double*>(p.head_part + (long long)p.tiles_total * (K * C + K)) +
+                  (long long)tile * 8 * (64 + 16 + 1);
+    auto gap = [&](int r) { return scr + r * 81; };
+    auto dl = [&](int r) { return scr + r * 81 + 64; };
     for (int r = warp_id(); r < Rv && r < 8; r += n_warps())
-      ce_head_row(p, u + r * ldn, p.labels[row0 + r], gap[r], dl[r], &lrow[r]);
+      ce_head_row(p, u + r * ldn, p.labels[row0 + r], gap(r), dl(r), scr + r * 81 + 80);
     __syncthreads();
     T* hp = p.head_part + (long long)tile * (K * C + K);
     const double ib = 1.0 / p.batch_global;
     for (int i = threadIdx.x; i < K * C + K; i += blockDim.x) {
       double acc = 0.0;
-      for (int r = 0; r < Rv; ++r) acc += (i < K * C ? dl[r][i / C] * gap[r][i % C] : dl[r][i - K * C]);
+      for (int r = 0; r < Rv; ++r) acc += (i < K * C ? dl(r)[i / C] * gap(r)[i % C] : dl(r)[i - K * C]);
       hp[i] = T(acc * ib);
     }
     if (threadIdx.x == 0) {
       double acc = 0.0;
-      for (int r = 0; r < Rv; ++r) acc += lrow[r];
+      for (int r = 0; r < Rv; ++r) acc += scr[r * 81 + 80];
       p.loss_part[tile] = acc;
     }
     return;
@@ -285,22 +296,25 @@ OB_DEV void loss_seed(const RkParams<T>& p, T* lam, int row0, int Rv) {
   const int N = p.d.N, ldn = p.d.ldn;
   if (p.loss_kind == OB_LOSS_CE_HEAD) {
     // lambda = d CE / du(T) = (dl Wh) / (P * B) broadcast over the pixels
-    __shared__ double gap[8][64], dl[8][16], lrow[8], dg[8][64];
     const int C = p.d.w[2], K = p.n_classes, P = N / C;
+    double* scr = reinterpret_cast<double*>(p.head_part + (long long)p.tiles_total * (K * C + K)) +
+                  (long long)blockIdx.x * 8 * (64 + 16 + 1);
+    double* dg = reinterpret_cast<double*>(p.head_part + (long long)p.tiles_total * (K * C + K)) +
+                 (long long)p.tiles_total * 8 * 81 + (long long)blockIdx.x * 8 * 64;
     for (int r = warp_id(); r < Rv && r < 8; r += n_warps())
-      ce_head_row(p, p.u_final + (long long)(row0 + r) * N, p.labels[row0 + r], gap[r], dl[r],
-                  &lrow[r]);
+      ce_head_row(p, p.u_final + (long long)(row0 + r) * N, p.labels[row0 + r], scr + r * 81,
+                  scr + r * 81 + 64, scr + r * 81 + 80);
     __syncthreads();
     for (int i = threadIdx.x; i < Rv * C; i += blockDim.x) {
       const int r = i / C, c = i % C;
       double s = 0.0;
-      for (int k = 0; k < K; ++k) s += dl[r][k] * double(p.head[k * C + c]);
-      dg[r][c] = s / (double(P) * p.batch_global);
+      for (int k = 0; k < K; ++k) s += scr[r * 81 + 64 + k] * double(p.head[k * C + c]);
+      dg[r * 64 + c] = s / (double(P) * p.batch_global);
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
       const int r = idx / N, j = idx % N;
-      lam[(long long)r * ldn + j] = T(dg[r][j % C]);
+      lam[(long long)r * ldn + j] = T(dg[r * 64 + j % C]);
     }
     return;
   }
@@ -351,7 +365,9 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
       __syncthreads();
     }
     T* rec = p.fwd_rec[n] >= 0 ? p.rec + (long long)p.fwd_rec[n] * (p.s + 1) * vec : nullptr;
+    PhaseTimer pt(p.prof ? p.phase : nullptr);
     const bool ok = rk_step_tile<T, F>(p, f, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv);
+    pt.mark(kPhFwdStep);
     if (!ok) {  // integrators.py:219-220
       if (threadIdx.x == 0) set_status(p.status, OB_ERR_INTEGRATION, n);
       return;
@@ -391,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
 
   loss_seed(p, lam, row0, Rv);
   __syncthreads();
+  PhaseTimer pt(p.prof ? p.phase : nullptr);
 
   for (int pc = 0; pc < p.prog_len; ++pc) {
     const int4 op = p.prog[pc];
@@ -407,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       __syncthreads();
       T* rec = p.rec + (long long)op.w * (s + 1) * vec;
       rk_step_tile<T, F>(p, f, u, ks, t, h, false, rec, row0, Rv);
+      pt.mark(kPhReplay);
       continue;
     }
     // REVERSE(n) from record buffer op.w: rk_adjoint_step (adjoint.py:67-94)
@@ -435,7 +453,9 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       }
       f.put_time(t + p.c[i] * h);
       __syncthreads();
+      pt.mark(kPhElem);
       f.vjp(w, jtv, mu, h, Rv);
+      pt.mark(kPhVjp);
       // Lam_i = h * jtv; lam_n += Lam_i
       for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
         const int o = (idx / N) * ldn + idx % N;
@@ -444,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
         lamn[o] = Num<T>::add(lamn[o], li);
       }
       __syncthreads();
+      pt.mark(kPhLam);
     }
     int bad = 0;
     for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) {

@@ -76,9 +76,19 @@ def workspace_size(prob) -> int:
     return int(n.value)
 
 
+def phase_cycles(reset=True):
+    """Per-phase SM-cycle totals of the last profiled calls (grad(..., profile=True))."""
+    buf = (C.c_uint64 * 16)()
+    raise_status(_lib.load().ob_debug_phase_cycles(buf, 16, int(reset)), _lib.last_error())
+    names = ["elementwise", "recompute", "vjp", "lam_update", "replay", "fwd_step", "gmres",
+             "other", "step_combine", "step_eval", "fwd_hidden", "fwd_out", "fwd_out_split",
+             "fwd_out_reduce", "p14", "p15"]
+    return {n: int(buf[i]) for i, n in enumerate(names)}
+
+
 def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
          policy=CheckpointPolicy("store_all"), solver_cfg=None, counters=None, *,
-         batch_global=None) -> GradResult:
+         batch_global=None, profile=False) -> GradResult:
     """Loss, dL/dtheta and dL/du0 by forward solve + discrete adjoint sweep."""
     solver_cfg = solver_cfg or SolverConfig()
     counters = counters if counters is not None else NfeCounters()
@@ -101,6 +111,7 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
         raise ValueError(f"expected length {field.n}, got {N}")
     bg = int(batch_global) if batch_global is not None else B
     prob, _times = build_problem(field, scheme, loss, B, ts, policy, solver_cfg, bg)
+    prob.flags = 1 if profile else 0
     nbytes = workspace_size(prob)
     dev = u0d.device
     ws = _workspace(nbytes, dev)

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--policy", default=None)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--phases", action="store_true")
     a = ap.parse_args()
     import torch
 
@@ -26,10 +27,22 @@ def main():
 
     ci = make_config(a.config) if a.batch is None else make_config(a.config).subset(a.batch)
     fld = field_from_config(ci)
-    u0 = torch.as_tensor(ci.u0, dtype=fld.torch_dtype, device="cuda")
+    from paper_2206_01298_b200.workloads import initial_state
+    u0 = torch.as_tensor(initial_state(ci), dtype=fld.torch_dtype, device="cuda")
     for _ in range(a.iters):
         res = run_config(ci, a.policy, field=fld, u0=u0)
     torch.cuda.synchronize()
+    if a.phases:
+        from paper_2206_01298_b200.engine import phase_cycles
+        phase_cycles(reset=True)
+        res = run_config(ci, a.policy, field=fld, u0=u0, profile=True)
+        cyc = phase_cycles(reset=True)
+        tot = sum(cyc.values())
+        tiles = res.device["tiles"]
+        print("phase cycles per CTA (and share):")
+        for k, v in cyc.items():
+            if v:
+                print(f"  {k:12s} {v / tiles / 1e6:8.3f} Mcyc  {100 * v / max(tot, 1):5.1f}%")
     print({k: v for k, v in res.device.items() if k.startswith("ms_") or k in ("tiles", "tile_rows")})
 
 
