@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -153,6 +154,7 @@ struct Plan {
   int R = 1, Rt = 4, LR = 1, tiles = 1;
   bool need_jvp = false;
   bool theta = false;
+  int gmres_m = 0;
   size_t off_kry = 0, off_stats = 0, off_cnf = 0, off_state = 0, off_head = 0;
   long long cnf_stride = 0;
   long long krylov_stride = 0;
@@ -289,6 +291,10 @@ void make_dims(const ob_field_desc& f, int LR, Dims& d) {
 // shared-memory layout for Rt rows; weights staged in smem when they fit
 void layout_smem(Plan& P) {
   const Dims& d = P.d;
+  if (P.theta) {   // Krylov workspace of the tile: Q | H | cs | sn | g | y per row
+    const long long m = P.gmres_m;
+    P.krylov_stride = (long long)P.R * ((m + 1) * d.ldn + (m + 1) * m + 2 * m + (m + 1) + m);
+  }
   SmemLayout& s = P.sm;
   int o = 0;
   auto take = [&](long long n) { int r = o; o += (int)((n + 7) & ~7LL); return r; };  // 32 B aligned
@@ -318,11 +324,21 @@ void layout_smem(Plan& P) {
   s.w = take((long long)P.Rt * d.ldn);
   s.jtv = take((long long)P.Rt * d.ldn);
   for (int i = 0; i < 8; ++i) s.vec[i] = P.theta ? take((long long)P.Rt * d.ldn) : -1;
+  s.scr = s.kry = -1;
+  s.scr_elems = 0;
+  if (P.theta) {
+    s.scr_elems = 8 * P.Rt * d.ldn;     // up to 8 split-K partials of a state-wide product
+    s.scr = take(s.scr_elems);
+    // The Krylov basis stays in global memory by default: the L1 capacity it would
+    // take caches the streamed weights, which matters more (measured on C5)
+    if ((size_t)(o + P.krylov_stride) * P.esz <= kSmemLimit && getenv("OB_KRYLOV_SMEM"))
+      s.kry = take(P.krylov_stride);
+  }
   s.total = o;
   s.wts = -1;
   // fp32 weights are staged in shared memory when they fit (fp64 kernels
   // always read L1/L2-resident weights: halves the kernel instantiations)
-  if (P.esz == 4 && (size_t)(o + d.n_packed) * P.esz <= kSmemLimit) {
+  if (P.esz == 4 && (size_t)(o + d.n_packed) * P.esz <= kSmemLimit && !getenv("OB_NO_SMEM_WEIGHTS")) {
     s.wts = take(d.n_packed);
     s.total = o;
   }
@@ -352,6 +368,7 @@ void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
     P.tiles = (int)((B + P.R - 1) / P.R);
     return;
   }
+  if (const char* e = getenv("OB_TILE_ROWS")) R = std::max(1, atoi(e));   // experiments
   R = std::min(R, P.esz == 8 ? 8 : 32);   // fp64 kernels are built for tiles of <= 8 rows
   for (;;) {
     P.R = R;
@@ -509,6 +526,7 @@ int plan_problem(const ob_problem& p, Plan& P) {
   } else {
     cudaGetLastError();
   }
+  P.gmres_m = P.theta ? std::min(p.solver.gmres_restart, p.field.widths[p.field.n_layers]) : 0;
   choose_tiles(P, p.field, p.batch, sms);
   if (P.smem_bytes > kSmemLimit) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   st = compile_policy(p, P);
@@ -558,11 +576,7 @@ int plan_problem(const ob_problem& p, Plan& P) {
   P.off_mu = o;
   o = align_up(o + P.esz * (size_t)P.tiles * P.d.n_mu, 256);
   P.off_kry = o;
-  if (P.theta) {
-    const long long m = std::min(p.solver.gmres_restart, P.d.N);
-    P.krylov_stride = (long long)P.Rt * ((m + 1) * P.d.ldn + (m + 1) * m + 2 * m + (m + 1) + m);
-    o = align_up(o + P.esz * (size_t)P.tiles * P.krylov_stride, 256);
-  }
+  if (P.theta && P.sm.kry < 0) o = align_up(o + P.esz * (size_t)P.tiles * P.krylov_stride, 256);
   P.off_stats = o;
   o = align_up(o + sizeof(int) * (size_t)p.batch * OB_NSTATS, 256);
   P.off_cnf = o;

@@ -129,7 +129,7 @@ struct CnfAdapter {
       }
       T* H = mt.s.hid[l - 1];
       const int ldh = d.lda[l];
-      mt.nn(aux, lo, l, d.w[l], Warps::all(), [&](int r, int k, T acc) { H[r * ldh + k] = acc; });
+      mt.nn(aux, lo, l, d.w[l], Warps::all(), [&](int r, int k, T acc, int) { H[r * ldh + k] = acc; });
       __syncthreads();
     }
     for (int l = d.L - 2; l >= 0; --l) {
@@ -153,7 +153,7 @@ struct CnfAdapter {
         }
         T* Hn = mt.s.hid[l - 1];
         const int ldn2 = d.lda[l];
-        mt.nn(H, ldh, l, d.w[l], Warps::all(), [&](int r, int k, T acc) { Hn[r * ldn2 + k] = acc; });
+        mt.nn(H, ldh, l, d.w[l], Warps::all(), [&](int r, int k, T acc, int) { Hn[r * ldn2 + k] = acc; });
         __syncthreads();
       } else {
         const int nw = n_warps();
@@ -161,7 +161,7 @@ struct CnfAdapter {
         const Warps wn = both ? Warps{0, nw / 2} : Warps::all();
         const Warps wa = both ? Warps{nw / 2, nw - nw / 2} : Warps::all();
         if (jtv)
-          mt.nn(H, ldh, 0, D, wn, [&](int r, int k, T acc) { if (r < rt) jtv[r * ldn + k] = acc; });
+          mt.nn(H, ldh, 0, D, wn, [&](int r, int k, T acc, int) { if (r < rt) jtv[r * ldn + k] = acc; });
         if (mu)
           gemm_tn_accum<T>(H, ldh, mt.s.x0, ld0, R2, N, d.w[0], hs, mu + d.mwoff[0], d.ldm[0],
                            mu + d.mboff[0], wa, Rt);

@@ -158,21 +158,24 @@ OB_DEV void gemm_nt(const T* X, int ldx, int Rt, const T* W, int ldw, int N, int
 // columns here are contiguous (k = c0 + TC*lc + j) so W rows load as vectors.
 template <typename T, int TR, int LR, bool WS, class Epi>
 OB_DEV void gemm_nn(const T* D, int ldd, int Rt, const T* W, int ldw, int Np, int K, Warps ws,
-                    Epi epi) {
+                    Epi epi, int split = 1) {
   constexpr int TC = 4, LC = 32 / LR, RT = TR * LR, CT = TC * LC;
   if (!ws.mine()) return;
   const int lr = lane_id() % LR, lc = lane_id() / LR;
   const int rtiles = Rt / RT, ctiles = (K + CT - 1) / CT;
+  const int nq = Np / 4, per = (nq + split - 1) / split;
   const uint32_t ds = smem_addr(D);
   const WOp<T, WS> wo(W);
-  for (int task = ws.me(); task < rtiles * ctiles; task += ws.nw) {
-    const int r0 = (task % rtiles) * RT + lr, k0 = (task / rtiles) * CT + TC * lc;
+  for (int task = ws.me(); task < rtiles * ctiles * split; task += ws.nw) {
+    const int sl = task / (rtiles * ctiles), rc = task % (rtiles * ctiles);
+    const int r0 = (rc % rtiles) * RT + lr, k0 = (rc / rtiles) * CT + TC * lc;
+    const int nb = sl * per * 4, ne = min(Np, (sl + 1) * per * 4);
     T acc[TR][TC];
 #pragma unroll
     for (int i = 0; i < TR; ++i)
 #pragma unroll
       for (int j = 0; j < TC; ++j) acc[i][j] = T(0);
-    for (int n = 0; n < Np; n += 4) {
+    for (int n = nb; n < ne; n += 4) {
       T d[TR][4], w[4][4];
 #pragma unroll
       for (int i = 0; i < TR; ++i)
@@ -190,7 +193,7 @@ OB_DEV void gemm_nn(const T* D, int ldd, int Rt, const T* W, int ldw, int Np, in
     for (int i = 0; i < TR; ++i)
 #pragma unroll
       for (int j = 0; j < TC; ++j)
-        if (k0 + j < K) epi(r0 + i * LR, k0 + j, acc[i][j]);
+        if (k0 + j < K) epi(r0 + i * LR, k0 + j, acc[i][j], sl);
   }
 }
 
@@ -210,11 +213,15 @@ OB_DEV void gemm_tn_accum(const T* D, int ldd, const T* X, int ldx, int R, int N
   const uint32_t ds = smem_addr(D), xs = smem_addr(X);
   for (int it = tid; it < items; it += nth) {
     const int n0 = (it / kq) * 4, k0 = (it % kq) * 4;
-    // the slot's current values are fetched first so their L2 latency overlaps the R-loop
+    // fp32: the slot's current values are fetched first so their L2 latency
+    // overlaps the R-loop; fp64 reads them after (register budget)
+    constexpr bool kPre = sizeof(T) == 4;
     T cur[4][4];
+    if (kPre) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (n0 + i < N) Vec4<T>::ld(M + (long long)(n0 + i) * ldm + k0, cur[i]);
+      for (int i = 0; i < 4; ++i)
+        if (n0 + i < N) Vec4<T>::ld(M + (long long)(n0 + i) * ldm + k0, cur[i]);
+    }
     T acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -232,6 +239,7 @@ OB_DEV void gemm_tn_accum(const T* D, int ldd, const T* X, int ldx, int R, int N
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (n0 + i < N) {
+        if (!kPre) Vec4<T>::ld(M + (long long)(n0 + i) * ldm + k0, cur[i]);
 #pragma unroll
         for (int j = 0; j < 4; ++j) cur[i][j] = Num<T>::add(cur[i][j], Num<T>::mul(scale, acc[i][j]));
         Vec4<T>::st(M + (long long)(n0 + i) * ldm + k0, cur[i]);

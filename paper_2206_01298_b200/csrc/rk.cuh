@@ -16,6 +16,8 @@ struct SmemLayout {      // offsets in elements of T (-1: not allocated)
   int u, lam, lamn, w, jtv;
   int vec[8];             // theta-method work vectors [Rt][ldn] (-1 when unused)
   int aux;                // CNF: output-layer buffer [2Rt][lda_L]
+  int scr, scr_elems;     // theta: split-K scratch for narrow JVP / VJP products
+  int kry;                // theta: Krylov workspace in shared memory (or -1: global)
   int wts;                // packed weights staged in shared memory, or -1
   int total;
 };

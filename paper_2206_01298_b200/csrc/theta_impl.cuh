@@ -73,12 +73,14 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
   const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt;
   const int m = min(p.gmres_restart, N);
   const long long qs = (long long)(m + 1) * ldn, hs = (long long)(m + 1) * m;
+  // per-sample Krylov workspace, one block per valid row (p.R rows per tile)
+  const int Rk = p.R;
   T* Qb = kry;
-  T* Hb = Qb + (long long)Rt * qs;
-  T* csb = Hb + (long long)Rt * hs;
-  T* snb = csb + (long long)Rt * m;
-  T* gb = snb + (long long)Rt * m;
-  T* yb = gb + (long long)Rt * (m + 1);
+  T* Hb = Qb + (long long)Rk * qs;
+  T* csb = Hb + (long long)Rk * hs;
+  T* snb = csb + (long long)Rk * m;
+  T* gb = snb + (long long)Rk * m;
+  T* yb = gb + (long long)Rk * (m + 1);
   const int w = warp_id();
   if (w < Rv) {
     // warp-uniform local copy of the sample state; lane 0 writes it back
@@ -103,6 +105,7 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
   }
   __syncthreads();
   bool ok = true;
+  PhaseTimer pt(p.prof ? p.phase : nullptr);
   for (;;) {
     // operator input of every row from its own state machine
     int any = 0;
@@ -116,7 +119,9 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
       c.vin[r * ldn + j] = v;
     }
     if (!__syncthreads_or(any)) break;
+    pt.mark(14);   // operator-input assembly
     op.apply(c.vin, c.vout);
+    pt.mark(kPhGmres);   // operator products (JVP / transposed VJP)
     if (w < Rv) {
       SampleState S = c.st[w];           // warp-uniform copy, written back by lane 0
       const int lane = lane_id();
@@ -227,6 +232,7 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
       if (S.phase == kPhFail) ok = false;
     }
     __syncthreads();
+    pt.mark(kPhOther);   // per-sample Arnoldi / Givens / update work
   }
   if (w < Rv && lane_id() == 0 && c.active[w]) c.cnt[w * OB_NSTATS + cnt_col] += c.st[w].total;
   return __syncthreads_and(ok) != 0;
@@ -392,9 +398,10 @@ theta_forward_kernel(const __grid_constant__ RkParams<T> p) {
   Weights<T> W;
   setup_tile(p, sm, ms, W);
   MlpTile<T, LR, WS> mt(p.d, W, ms, p.Rt);
+  if (p.sm.scr >= 0) { mt.scratch = sm + p.sm.scr; mt.scratch_elems = p.sm.scr_elems; }
   ThetaCtx<T> c = theta_ctx(p, sm);
   T* u = sm + p.sm.u;
-  T* kry = p.krylov + tile * p.krylov_stride;
+  T* kry = p.sm.kry >= 0 ? sm + p.sm.kry : p.krylov + tile * p.krylov_stride;
   const int N = p.d.N, ldn = p.d.ldn;
   const long long vec = (long long)p.B * N;
   load_rows(u, ldn, p.u0, N, row0, Rv);
@@ -440,13 +447,14 @@ theta_reverse_kernel(const __grid_constant__ RkParams<T> p) {
   Weights<T> W;
   setup_tile(p, sm, ms, W);
   MlpTile<T, LR, WS> mt(p.d, W, ms, p.Rt);
+  if (p.sm.scr >= 0) { mt.scratch = sm + p.sm.scr; mt.scratch_elems = p.sm.scr_elems; }
   ThetaCtx<T> c = theta_ctx(p, sm);
   const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt;
   const long long vec = (long long)p.B * N;
   T* u = sm + p.sm.u;
   T* lam = sm + p.sm.lam;
   T* jtv = sm + p.sm.jtv;
-  T* kry = p.krylov + tile * p.krylov_stride;
+  T* kry = p.sm.kry >= 0 ? sm + p.sm.kry : p.krylov + tile * p.krylov_stride;
   T* mu = p.mu + tile * p.d.n_mu;
   const double th = p.theta;
   loss_seed(p, lam, row0, Rv);

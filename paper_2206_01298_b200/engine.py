@@ -80,9 +80,9 @@ def phase_cycles(reset=True):
     """Per-phase SM-cycle totals of the last profiled calls (grad(..., profile=True))."""
     buf = (C.c_uint64 * 16)()
     raise_status(_lib.load().ob_debug_phase_cycles(buf, 16, int(reset)), _lib.last_error())
-    names = ["elementwise", "recompute", "vjp", "lam_update", "replay", "fwd_step", "gmres",
-             "other", "step_combine", "step_eval", "fwd_hidden", "fwd_out", "fwd_out_split",
-             "fwd_out_reduce", "p14", "p15"]
+    names = ["elementwise", "recompute", "vjp", "lam_update", "replay", "fwd_step", "gmres_apply",
+             "gmres_scalar", "step_combine", "step_eval", "fwd_hidden", "fwd_out", "fwd_out_split",
+             "fwd_out_reduce", "gmres_input", "p15"]
     return {n: int(buf[i]) for i, n in enumerate(names)}
 
 
