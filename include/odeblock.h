@@ -52,9 +52,13 @@ enum { OB_FIELD_MLP = 0, OB_FIELD_STIFF = 1, OB_FIELD_CNF = 2, OB_FIELD_CONV = 3
 enum { OB_SCHEME_RK = 0, OB_SCHEME_THETA = 1 };
 /* CheckpointPolicy kinds (checkpointing.py:173-190) */
 enum { OB_POLICY_STORE_ALL = 0, OB_POLICY_STORE_SOLUTIONS = 1, OB_POLICY_REVOLVE = 2 };
-/* terminal losses: 0.5*mean||u||^2 (BASELINE C1/C2/C5), per-sample MSE vs
-   targets (losses.py:78-107, K=1), CE head (C3), CNF NLL (C4) */
-enum { OB_LOSS_HALF_SQNORM = 0, OB_LOSS_MSE = 1, OB_LOSS_CE_HEAD = 2, OB_LOSS_CNF_NLL = 3 };
+/* losses: 0.5*mean||u||^2 (BASELINE C1/C2/C5), per-sample MSE vs terminal
+   targets (losses.py:78-107, K=1), CE head (C3), CNF NLL (C4), and the
+   reference's observation losses (LossSpec mse/mae over K observation times
+   with optional min-max scaling, losses.py:10-107; seeds injected at step
+   boundaries as in backward_sweep, adjoint.py:235-253) for MLP / stiff fields */
+enum { OB_LOSS_HALF_SQNORM = 0, OB_LOSS_MSE = 1, OB_LOSS_CE_HEAD = 2, OB_LOSS_CNF_NLL = 3,
+       OB_LOSS_OBS_MSE = 4, OB_LOSS_OBS_MAE = 5 };
 /* revolve action kinds (checkpointing.py:70-80) */
 enum { OB_ACT_ADVANCE = 0, OB_ACT_STORE = 1, OB_ACT_RESTORE = 2, OB_ACT_REVERSE = 3 };
 
@@ -109,7 +113,9 @@ typedef struct {
   int32_t loss;           /* OB_LOSS_*                                             */
   const double* times;    /* HOST array, n_steps+1 boundary times (integrators.py:276) */
   int32_t flags;          /* OB_FLAG_* */
-  int32_t _pad;
+  int32_t n_obs;          /* OB_LOSS_OBS_*: observation count K >= 1           */
+  const int32_t* obs_steps; /* HOST [n_obs] boundary index of each observation, strictly
+                             increasing in [0, n_steps] (_match_boundaries, adjoint.py:213) */
 } ob_problem;
 
 /* flags: accumulate per-phase SM cycles of the persistent kernels (profiling aid;
@@ -136,6 +142,11 @@ typedef struct {
   void* dhead;            /* out [n_classes*C + n_classes] head gradient (this batch) */
   int32_t n_classes;
   int32_t _pad;
+  /* OB_LOSS_OBS_*: observations and the optional min-max scaling (losses.py:10-37) */
+  const void* obs_values; /* [n_obs, B, N] observed states (scaled space when scaling) */
+  const void* scale_lo;   /* [N] or NULL (no scaling); components with hi <= lo pass through */
+  const void* scale_hi;   /* [N] or NULL                                          */
+  void* predictions;      /* out [n_obs, B, N]: states at the observation boundaries */
 } ob_buffers;
 
 /* per-sample stats columns (implicit schemes; explicit: fixed by the schedule) */

@@ -647,11 +647,15 @@ class Run:
 
 
 def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", seed_fn=None,
-                  cfg: SolverCfg = None, times=None):
+                  cfg: SolverCfg = None, times=None, obs=None):
     """forward_pass + terminal seed + backward_sweep for a batch of samples.
 
     ``seed_fn(u_final) -> (loss, lam_N)``; default is the BASELINE loss
     L = 0.5 * mean_b ||u_b(T)||^2 with seed lam_N = u_b(T) / B.
+    ``obs`` (an obs_losses.ObsLoss) replaces the terminal loss by observations
+    at step boundaries: states captured in the forward (adjoint.py:196-210),
+    seeds injected into lambda before reversing the step that ends at each
+    observed boundary and at boundary 0 last (adjoint.py:235-253).
     Returns a dict with u_final, du0, dtheta (batch sum of per-sample mu),
     loss, counters, store counters, per-sample counters and solver stats.
     """
@@ -676,9 +680,15 @@ def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", see
     final = None
     U = U0.copy()
     k_carry = None
+    capture = {}
+    want = set(obs.steps) if obs is not None else set()
+    if 0 in want:
+        capture[0] = U0.copy()
     for n in range(n_steps):
         t, h = ts[n], ts[n + 1] - ts[n]
         rec, k_carry = run.step(U, t, h, k_carry)
+        if n + 1 in want:
+            capture[n + 1] = rec.u_next.copy()
         rec.n = n
         run.c.steps_accepted += 1
         last = n == n_steps - 1
@@ -709,7 +719,15 @@ def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", see
         run.sc.max_live_slots = max(len(slots), len(sols))
     u_final = U
 
-    if seed_fn is None:
+    inj = {}
+    preds = None
+    if obs is not None:
+        preds = np.stack([capture[j] for j in obs.steps])
+        loss, seeds = obs.loss_and_seeds(preds)
+        for j, sd in zip(obs.steps, seeds):
+            inj[j] = inj.get(j, 0.0) + sd
+        lam = np.zeros_like(U0)
+    elif seed_fn is None:
         loss = float(np.mean(0.5 * np.sum(u_final * u_final, axis=1)))
         lam = u_final / B
     else:
@@ -754,9 +772,13 @@ def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", see
                     yield rec
 
     for rec in records():
+        if rec.n + 1 in inj:
+            lam = lam + inj[rec.n + 1]
         lam, mu = run.adjoint(rec, lam, mu)
+    if 0 in inj:
+        lam = lam + inj[0]
     return {
-        "u_final": u_final, "du0": lam, "dtheta": mu, "loss": loss,
+        "u_final": u_final, "du0": lam, "dtheta": mu, "loss": loss, "predictions": preds,
         "counters": run.c, "store": run.sc, "sample_counters": run.sample,
         "stats": run.stats,
     }

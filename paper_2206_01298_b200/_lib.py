@@ -26,7 +26,9 @@ OB_F32, OB_F64 = 0, 1
 OB_FIELD_MLP, OB_FIELD_STIFF, OB_FIELD_CNF, OB_FIELD_CONV = 0, 1, 2, 3
 OB_SCHEME_RK, OB_SCHEME_THETA = 0, 1
 OB_POLICY = {"store_all": 0, "store_solutions": 1, "revolve": 2}
-OB_LOSS = {"half_sqnorm": 0, "mse": 1, "ce_head": 2, "cnf_nll": 3}
+OB_LOSS = {"half_sqnorm": 0, "mse": 4, "mae": 5, "ce_head": 2, "cnf_nll": 3}
+# (code 1 = the ABI's K=1 terminal MSE; the host routes mse through the general
+#  observation path, code 4)
 OB_MAX_LAYERS = 8
 OB_MAX_STAGES = 8
 OB_NSTATS = 5
@@ -59,7 +61,8 @@ class Problem(C.Structure):
     _fields_ = [("field", FieldDesc), ("scheme", SchemeDesc), ("solver", SolverDesc),
                 ("batch", C.c_int64), ("batch_global", C.c_int64), ("n_steps", C.c_int32),
                 ("policy", C.c_int32), ("nc", C.c_int32), ("loss", C.c_int32),
-                ("times", C.POINTER(C.c_double)), ("flags", C.c_int32), ("_pad", C.c_int32)]
+                ("times", C.POINTER(C.c_double)), ("flags", C.c_int32), ("n_obs", C.c_int32),
+                ("obs_steps", C.POINTER(C.c_int32))]
 
 
 class Buffers(C.Structure):
@@ -68,7 +71,9 @@ class Buffers(C.Structure):
                 ("dtheta", C.c_void_p), ("loss", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("sample_stats", C.c_void_p),
                 ("head", C.c_void_p), ("labels", C.c_void_p), ("dhead", C.c_void_p),
-                ("n_classes", C.c_int32), ("_pad", C.c_int32)]
+                ("n_classes", C.c_int32), ("_pad", C.c_int32),
+                ("obs_values", C.c_void_p), ("scale_lo", C.c_void_p), ("scale_hi", C.c_void_p),
+                ("predictions", C.c_void_p)]
 
 
 class Counters(C.Structure):

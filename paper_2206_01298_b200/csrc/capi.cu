@@ -162,12 +162,12 @@ struct Plan {
   size_t smem_bytes = 0;
   // checkpoint program
   int nbuf = 0, nsol = 0;
-  std::vector<int> fwd_rec, fwd_sol;
+  std::vector<int> fwd_rec, fwd_sol, obs_k;
   std::vector<int4> prog;
   unsigned skip_vjp = 0;
   ob_counters cnt{};
   // workspace layout (byte offsets)
-  size_t o_ts = 0, o_fr = 0, o_fs = 0, o_pg = 0, o_stat = 0;
+  size_t o_ts = 0, o_fr = 0, o_fs = 0, o_pg = 0, o_stat = 0, o_obs = 0;
   size_t off_blob = 0, blob_bytes = 0, off_w = 0, off_rec = 0, off_sol = 0, off_scr = 0,
          off_mu = 0, off_lp = 0, total = 0;
   size_t off_pk = 0;
@@ -336,9 +336,11 @@ void layout_smem(Plan& P) {
   }
   s.total = o;
   s.wts = -1;
-  // fp32 weights are staged in shared memory when they fit (fp64 kernels
-  // always read L1/L2-resident weights: halves the kernel instantiations)
-  if (P.esz == 4 && (size_t)(o + d.n_packed) * P.esz <= kSmemLimit && !getenv("OB_NO_SMEM_WEIGHTS")) {
+  // fp32 explicit-RK MLP / stiff weights are staged in shared memory when
+  // they fit; fp64, theta-method and CNF kernels read L1/L2-resident weights
+  // (only rk_f32s.cu instantiates the shared-memory-weight variants)
+  const bool ws_variant = P.esz == 4 && !P.theta && !d.cnf && !d.conv;
+  if (ws_variant && (size_t)(o + d.n_packed) * P.esz <= kSmemLimit && !getenv("OB_NO_SMEM_WEIGHTS")) {
     s.wts = take(d.n_packed);
     s.total = o;
   }
@@ -511,10 +513,24 @@ int plan_problem(const ob_problem& p, Plan& P) {
   if (!p.times) return fail(OB_ERR_VALUE, "times array is required");
   for (int i = 0; i < p.n_steps; ++i)
     if (!(p.times[i + 1] > p.times[i])) return fail(OB_ERR_VALUE, "step size must be positive");
-  if (p.loss != OB_LOSS_HALF_SQNORM && p.loss != OB_LOSS_MSE &&
+  const bool obs = p.loss == OB_LOSS_OBS_MSE || p.loss == OB_LOSS_OBS_MAE;
+  const bool vec_field = p.field.kind == OB_FIELD_MLP || p.field.kind == OB_FIELD_STIFF;
+  if (p.loss != OB_LOSS_HALF_SQNORM && p.loss != OB_LOSS_MSE && !(obs && vec_field) &&
       !(p.loss == OB_LOSS_CNF_NLL && p.field.kind == OB_FIELD_CNF) &&
       !(p.loss == OB_LOSS_CE_HEAD && p.field.kind == OB_FIELD_CONV))
     return fail(OB_ERR_UNSUPPORTED, "loss kind not supported for this field");
+  P.obs_k.clear();
+  if (obs) {  // LossSpec validation (losses.py:54-69) on boundary indices
+    if (p.n_obs < 1 || !p.obs_steps) return fail(OB_ERR_VALUE, "need one observation vector per time");
+    P.obs_k.assign(p.n_steps + 1, -1);
+    for (int k = 0; k < p.n_obs; ++k) {
+      const int j = p.obs_steps[k];
+      if (j < 0 || j > p.n_steps) return fail(OB_ERR_VALUE, "observation boundary out of range");
+      if (k > 0 && j <= p.obs_steps[k - 1])
+        return fail(OB_ERR_VALUE, "observation times must be strictly increasing");
+      P.obs_k[j] = k;
+    }
+  }
   if ((p.field.kind == OB_FIELD_CNF || p.field.kind == OB_FIELD_CONV) &&
       p.scheme.kind != OB_SCHEME_RK)
     return fail(OB_ERR_UNSUPPORTED, "CNF / conv fields are built for explicit schemes");
@@ -562,7 +578,8 @@ int plan_problem(const ob_problem& p, Plan& P) {
   P.o_fs = P.o_fr + sizeof(int) * nt;
   P.o_pg = align_up(P.o_fs + sizeof(int) * nt, 16);
   P.o_stat = P.o_pg + sizeof(int4) * P.prog.size();
-  P.blob_bytes = P.o_stat + sizeof(int) * 4;
+  P.o_obs = P.o_stat + sizeof(int) * 4;
+  P.blob_bytes = P.o_obs + sizeof(int) * P.obs_k.size();
   o = align_up(o + P.blob_bytes, 256);
   P.off_pk = o;
   o = align_up(o + P.esz * (size_t)P.d.n_packed, 256);
@@ -609,6 +626,7 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   std::memcpy(blob.data() + P.o_fr, P.fwd_rec.data(), sizeof(int) * nt);
   std::memcpy(blob.data() + P.o_fs, P.fwd_sol.data(), sizeof(int) * nt);
   if (!P.prog.empty()) std::memcpy(blob.data() + P.o_pg, P.prog.data(), sizeof(int4) * P.prog.size());
+  if (!P.obs_k.empty()) std::memcpy(blob.data() + P.o_obs, P.obs_k.data(), sizeof(int) * P.obs_k.size());
   const size_t o_ts = P.o_ts, o_fr = P.o_fr, o_fs = P.o_fs, o_pg = P.o_pg, o_stat = P.o_stat;
   CU(cudaMemcpyAsync(ws + P.off_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
 
@@ -637,6 +655,14 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   rp.ts = reinterpret_cast<const double*>(ws + P.off_blob + o_ts);
   rp.loss_kind = p.loss;
   rp.targets = static_cast<const T*>(b.targets);
+  if (!P.obs_k.empty()) {
+    rp.obs_k = reinterpret_cast<const int*>(ws + P.off_blob + P.o_obs);
+    rp.n_obs = p.n_obs;
+    rp.obs_values = static_cast<const T*>(b.obs_values);
+    rp.scale_lo = static_cast<const T*>(b.scale_lo);
+    rp.scale_hi = static_cast<const T*>(b.scale_hi);
+    rp.preds = static_cast<T*>(b.predictions);
+  }
   rp.batch_global = double(p.batch_global > 0 ? p.batch_global : p.batch);
   rp.inv_batch_global = 1.0 / rp.batch_global;
   rp.u0 = static_cast<const T*>(b.u0);
@@ -785,6 +811,10 @@ extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* ou
   if (p->loss == OB_LOSS_CE_HEAD && (!b->head || !b->labels || b->n_classes != 10))
     return fail(OB_ERR_VALUE, "cross-entropy head needs head parameters, labels and 10 classes");
   if (p->loss == OB_LOSS_MSE && !b->targets) return fail(OB_ERR_VALUE, "mse loss needs targets");
+  if ((p->loss == OB_LOSS_OBS_MSE || p->loss == OB_LOSS_OBS_MAE) &&
+      (!b->obs_values || !b->predictions || (!b->scale_lo) != (!b->scale_hi)))
+    return fail(OB_ERR_VALUE, "observation loss needs observations, a predictions buffer and "
+                              "both or neither scaling bounds");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   st = P.dtype == OB_F32 ? run_grad<float>(*p, *b, P, s) : run_grad<double>(*p, *b, P, s);
   if (out) *out = P.cnt;

@@ -40,6 +40,13 @@ struct RkParams {
   const double* ts;       // [n_steps+1]
   int loss_kind;
   const T* targets;
+  // observation losses (OB_LOSS_OBS_*): obs_k[n] = observation index at boundary n or -1
+  const int* obs_k;
+  int n_obs;
+  const T* obs_values;             // [n_obs][B][N]
+  const T* scale_lo;               // [N] or null
+  const T* scale_hi;
+  T* preds;                        // [n_obs][B][N]
   double inv_batch_global;
   double batch_global;
   // buffers

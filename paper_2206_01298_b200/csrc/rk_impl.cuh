@@ -205,6 +205,94 @@ OB_DEV T* state_buf(const RkParams<T>& p, T* sm, int k) {
   return p.state_glob + blockIdx.x * p.state_stride + (long long)k * p.Rt * p.d.ldn;
 }
 
+// --------------------------------------------------------------- observation losses
+// Reference LossSpec mse/mae over K observations with optional min-max scaling
+// (losses.py:10-107), batched as the mean over samples: states captured at the
+// observed boundaries in the forward (adjoint.py:196-210), seeds injected into
+// lambda before reversing the step that ends at each observed boundary and at
+// boundary 0 last (backward_sweep, adjoint.py:235-253).
+template <typename T>
+OB_DEV bool is_obs_loss(const RkParams<T>& p) {
+  return p.loss_kind == OB_LOSS_OBS_MSE || p.loss_kind == OB_LOSS_OBS_MAE;
+}
+
+// rows of boundary n -> predictions[k] when boundary n is observed
+template <typename T>
+OB_DEV void obs_capture(const RkParams<T>& p, const T* u, int n, int row0, int Rv) {
+  if (!p.obs_k) return;
+  const int k = p.obs_k[n];
+  if (k < 0) return;
+  store_rows(p.preds + (long long)k * p.B * p.d.N, p.d.N, u, p.d.ldn, row0, Rv);
+  __syncthreads();
+}
+
+// r = scale(pred) - obs for one element, and the scaling span (1 when unscaled
+// or degenerate: MinMaxScaling.apply / .chain, losses.py:26-37)
+template <typename T>
+OB_DEV double obs_residual(const RkParams<T>& p, int k, int row, int j, double& span) {
+  const long long g = ((long long)k * p.B + row) * p.d.N + j;
+  double v = double(p.preds[g]);
+  span = 1.0;
+  if (p.scale_lo) {
+    const double lo = double(p.scale_lo[j]), hi = double(p.scale_hi[j]);
+    if (hi > lo) {
+      span = hi - lo;
+      v = (v - lo) / span;
+    }
+  }
+  return v - double(p.obs_values[g]);
+}
+
+// deterministic block sum (fixed shuffle tree, then warps in order); result on thread 0
+OB_DEV double block_sum_fixed(double v) {
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane_id() == 0) red[warp_id()] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < n_warps(); ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+// per-tile sum over samples of the per-sample loss mean over K*N (losses.py:94-107)
+template <typename T>
+OB_DEV void obs_loss_partial(const RkParams<T>& p, int row0, int Rv, int tile) {
+  const int N = p.d.N;
+  const int per = Rv * N;
+  double acc = 0.0;
+  for (int k = 0; k < p.n_obs; ++k)
+    for (int i = threadIdx.x; i < per; i += blockDim.x) {
+      double span;
+      const double r = obs_residual(p, k, row0 + i / N, i % N, span);
+      acc += p.loss_kind == OB_LOSS_OBS_MAE ? fabs(r) : r * r;
+    }
+  acc = block_sum_fixed(acc);
+  if (threadIdx.x == 0) p.loss_part[tile] = acc / (double(p.n_obs) * N);
+}
+
+// lambda += dL/du at boundary n (inject_observation, adjoint.py:135-140):
+// seed = {sign(r) | 2r} / (K N), chained through the scaling, / B
+template <typename T>
+OB_DEV void obs_inject(const RkParams<T>& p, T* lam, int n, int row0, int Rv) {
+  if (!p.obs_k) return;
+  const int k = p.obs_k[n];
+  if (k < 0) return;
+  const int N = p.d.N, ldn = p.d.ldn;
+  const double denom = double(p.n_obs) * N;
+  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+    const int r = idx / N, j = idx % N;
+    double span;
+    const double rr = obs_residual(p, k, row0 + r, j, span);
+    double sd = p.loss_kind == OB_LOSS_OBS_MAE ? double((rr > 0.0) - (rr < 0.0)) / denom
+                                                : 2.0 * rr / denom;
+    sd = sd / span / p.batch_global;
+    lam[r * ldn + j] = T(double(lam[r * ldn + j]) + sd);
+  }
+  __syncthreads();
+}
+
 // --------------------------------------------------------------- losses
 // Terminal losses (losses.py:78-107 with the batch mean; BASELINE configs):
 // per-tile fp64 partial sums in fixed order, and the seed lambda_N = dL/du(T).
@@ -241,6 +329,10 @@ OB_DEV void ce_head_row(const RkParams<T>& p, const T* urow, int label, double* 
 
 template <typename T>
 OB_DEV void loss_partial(const RkParams<T>& p, const T* u, int row0, int Rv, int tile) {
+  if (is_obs_loss(p)) {
+    obs_loss_partial(p, row0, Rv, tile);
+    return;
+  }
   if (p.loss_kind == OB_LOSS_CE_HEAD) {
     // per-tile loss sum and head-gradient partial (dWh = dl gap^T / B, dbh = dl / B);
     // scratch rows (gap | dl | loss, fp64) live after this tile's head partial
@@ -294,6 +386,10 @@ OB_DEV void loss_partial(const RkParams<T>& p, const T* u, int row0, int Rv, int
 template <typename T>
 OB_DEV void loss_seed(const RkParams<T>& p, T* lam, int row0, int Rv) {
   const int N = p.d.N, ldn = p.d.ldn;
+  if (is_obs_loss(p)) {  // lambda starts at zero; seeds arrive by injection
+    for (int i = threadIdx.x; i < p.Rt * ldn; i += blockDim.x) lam[i] = T(0);
+    return;
+  }
   if (p.loss_kind == OB_LOSS_CE_HEAD) {
     // lambda = d CE / du(T) = (dl Wh) / (P * B) broadcast over the pixels
     const int C = p.d.w[2], K = p.n_classes, P = N / C;
@@ -360,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
   }
   for (int n = 0; n < p.n_steps; ++n) {
     const double t = p.ts[n], h = p.ts[n + 1] - p.ts[n];
+    obs_capture(p, u, n, row0, Rv);
     if (p.fwd_sol[n] >= 0) {
       store_rows(p.sol + p.fwd_sol[n] * vec, N, u, ldn, row0, Rv);
       __syncthreads();
@@ -374,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
     }
   }
   store_rows(p.u_final, N, u, ldn, row0, Rv);
+  obs_capture(p, u, p.n_steps, row0, Rv);
   loss_partial(p, u, row0, Rv, tile);
 }
 
@@ -428,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       continue;
     }
     // REVERSE(n) from record buffer op.w: rk_adjoint_step (adjoint.py:67-94)
+    obs_inject(p, lam, n + 1, row0, Rv);
     const T* rec = p.rec + (long long)op.w * (s + 1) * vec;
     for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) lamn[idx] = lam[idx];
     __syncthreads();
@@ -476,6 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       return;
     }
   }
+  obs_inject(p, lam, 0, row0, Rv);
   store_rows(p.du0, N, lam, ldn, row0, Rv);
 }
 

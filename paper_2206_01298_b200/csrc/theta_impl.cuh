@@ -415,6 +415,7 @@ theta_forward_kernel(const __grid_constant__ RkParams<T> p) {
   }
   for (int n = 0; n < p.n_steps; ++n) {
     const double t = p.ts[n], h = p.ts[n + 1] - p.ts[n];
+    obs_capture(p, u, n, row0, Rv);
     if (p.fwd_sol[n] >= 0) {
       store_rows(p.sol + p.fwd_sol[n] * vec, N, u, ldn, row0, Rv);
       __syncthreads();
@@ -428,6 +429,7 @@ theta_forward_kernel(const __grid_constant__ RkParams<T> p) {
     }
   }
   store_rows(p.u_final, N, u, ldn, row0, Rv);
+  obs_capture(p, u, p.n_steps, row0, Rv);
   flush_stats(p, c, row0, Rv);
   loss_partial(p, u, row0, Rv, tile);
 }
@@ -480,6 +482,7 @@ theta_reverse_kernel(const __grid_constant__ RkParams<T> p) {
       continue;
     }
     // theta_adjoint_step (adjoint.py:97-126)
+    obs_inject(p, lam, n + 1, row0, Rv);
     const T* rec = p.rec + (long long)op.w * 3 * vec;
     const double t1 = t + h;
     const T hth = T(h * th), h1 = T(h * (1.0 - th));
@@ -533,6 +536,7 @@ theta_reverse_kernel(const __grid_constant__ RkParams<T> p) {
       return;
     }
   }
+  obs_inject(p, lam, 0, row0, Rv);
   store_rows(p.du0, N, lam, ldn, row0, Rv);
   flush_stats(p, c, row0, Rv);
 }

@@ -211,12 +211,33 @@ struct MlpTile {
                                                          split, epi);
   }
   template <class Epi>
-  OB_DEV void nn(const T* D, int ldD, int l, int K, Warps ws, Epi epi) {
+  OB_DEV void nn(const T* D, int ldD, int l, int K, Warps ws, Epi epi, int split = 1) {
     const int Np = (d.w[l + 1] + 3) & ~3;
-    if (tasks_wide(K) >= ws.nw || 2 * LR > 32)
-      gemm_nn<T, 4, LR, WS>(D, ldD, Rt, W.W[l], d.ldw[l], Np, K, ws, epi);
+    if (tasks_wide(K) * split >= ws.nw || 2 * LR > 32)
+      gemm_nn<T, 4, LR, WS>(D, ldD, Rt, W.W[l], d.ldw[l], Np, K, ws, epi, split);
     else
-      gemm_nn<T, 2, (2 * LR > 32 ? 32 : 2 * LR), WS>(D, ldD, Rt, W.W[l], d.ldw[l], Np, K, ws, epi);
+      gemm_nn<T, 2, (2 * LR > 32 ? 32 : 2 * LR), WS>(D, ldD, Rt, W.W[l], d.ldw[l], Np, K, ws, epi,
+                                                      split);
+  }
+
+  // split-K factor for a narrow output product of n columns reducing over kred
+  // (deterministic: partials in `scratch`, summed in slice order)
+  OB_DEV int narrow_split(int n, int kred) const {
+    if (!scratch) return 1;
+    const int tn = tasks_narrow(n);
+    if (tn >= n_warps()) return 1;
+    int split = min(n_warps() / max(tn, 1), scratch_elems / (Rt * n));
+    return max(1, min(split, kred / 4));
+  }
+  // reduce split partials [split][Rt][n] -> dst[r*ldo + c] (+ bias when given)
+  OB_DEV void split_reduce(int split, int n, T* dst, int ldo, const T* bias) {
+    const int pst = Rt * n;
+    for (int i = threadIdx.x; i < Rt * n; i += blockDim.x) {
+      T acc = scratch[i];
+      for (int sl = 1; sl < split; ++sl) acc = Num<T>::add(acc, scratch[sl * pst + i]);
+      dst[(i / n) * ldo + i % n] = bias ? Num<T>::add(acc, bias[i % n]) : acc;
+    }
+    __syncthreads();
   }
 
   // Layers [0, nl) from x0; when nl == L the last writes z = W a + b to
@@ -288,7 +309,7 @@ struct MlpTile {
         T* h = s.hid[l - 1];
         const T* z = d.need_pre ? s.pre[l - 1] : nullptr;
         const int ldh = d.lda[l], act = d.act;
-        nn(D, ldD, l, d.w[l], Warps::all(), [&](int r, int k, T acc) {
+        nn(D, ldD, l, d.w[l], Warps::all(), [&](int r, int k, T acc, int) {
           const T a = h[r * ldh + k];
           h[r * ldh + k] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + k] : a, act));
         });
@@ -300,7 +321,7 @@ struct MlpTile {
         const bool both = mu && jtv;
         const Warps wn = both ? Warps{0, nw / 2} : Warps::all();
         const Warps wa = both ? Warps{nw / 2, nw - nw / 2} : Warps::all();
-        if (jtv) nn(D, ldD, 0, d.N, wn, [&](int r, int k, T acc) { jtv[r * ldo + k] = acc; });
+        if (jtv) nn(D, ldD, 0, d.N, wn, [&](int r, int k, T acc, int) { jtv[r * ldo + k] = acc; });
         if (mu)
           gemm_tn_accum<T>(D, ldD, s.x0, d.lda[0], Rv, d.w[1], d.w[0], scale, mu + d.mwoff[0],
                            d.ldm[0], mu + d.mboff[0], wa);
@@ -328,12 +349,22 @@ struct MlpTile {
         const T* h = s.hid[l - 1];
         const T* z = d.need_pre ? s.pre[l - 1] : nullptr;
         const int ldh = d.lda[l], ldt = d.ldt, act = d.act;
-        nn(cur, ldc, l, d.w[l], wn, [&](int r, int k, T acc) {
+        nn(cur, ldc, l, d.w[l], wn, [&](int r, int k, T acc, int) {
           const T a = h[r * ldh + k];
           dst[r * ldt + k] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + k] : a, act));
         });
       } else if (jtv) {
-        nn(cur, ldc, 0, d.N, wn, [&](int r, int k, T acc) { jtv[r * ldo + k] = acc; });
+        const int split = mu ? 1 : narrow_split(d.N, d.w[1]);
+        if (split > 1) {
+          T* part = scratch;
+          const int pst = Rt * d.N, nn_ = d.N;
+          nn(cur, ldc, 0, d.N, wn,
+             [&](int r, int k, T acc, int sl) { part[sl * pst + r * nn_ + k] = acc; }, split);
+          __syncthreads();
+          split_reduce(split, d.N, jtv, ldo, nullptr);
+        } else {
+          nn(cur, ldc, 0, d.N, wn, [&](int r, int k, T acc, int) { jtv[r * ldo + k] = acc; });
+        }
       }
       if (mu)
         gemm_tn_accum<T>(cur, ldc, in(l), d.lda[l], Rv, d.w[l + 1], d.w[l], scale,
@@ -362,15 +393,25 @@ struct MlpTile {
       const T* z = (last || !d.need_pre) ? nullptr : s.pre[l];
       const int ldh = d.lda[l + 1], ldt = d.ldt, act = d.act;
       T* dst = last ? out : nxt;
-      nt(cur, ldt, l, 1, Warps::all(), [&](int r, int n, T acc, int) {
-        if (last) {
-          dst[r * ldo + n] = acc;
-        } else {
-          const T a = h[r * ldh + n];
-          dst[r * ldt + n] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + n] : a, act));
-        }
-      });
-      __syncthreads();
+      const int split = last ? narrow_split(d.w[l + 1], d.w[l]) : 1;
+      if (split > 1) {
+        T* part = scratch;
+        const int nn_ = d.w[l + 1], pst = Rt * nn_;
+        nt(cur, ldt, l, split, Warps::all(),
+           [&](int r, int n, T acc, int sl) { part[sl * pst + r * nn_ + n] = acc; });
+        __syncthreads();
+        split_reduce(split, nn_, out, ldo, nullptr);
+      } else {
+        nt(cur, ldt, l, 1, Warps::all(), [&](int r, int n, T acc, int) {
+          if (last) {
+            dst[r * ldo + n] = acc;
+          } else {
+            const T a = h[r * ldh + n];
+            dst[r * ldt + n] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + n] : a, act));
+          }
+        });
+        __syncthreads();
+      }
       T* tmp = cur; cur = nxt; nxt = tmp;
     }
   }

@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from .controls import (NfeCounters, SolverConfig, StoreCounters, boundary_times, raise_status)
 from .fields import Field, stream_ptr, to_device
-from .losses import LossSpec
+from .losses import OBSERVATION_KINDS, LossSpec, match_boundaries
 from .policies import CheckpointPolicy
 from .schemes import Scheme, to_desc
 
@@ -94,9 +94,11 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     counters = counters if counters is not None else NfeCounters()
     if loss.times[-1] > tF + 1e-9 * max(1.0, abs(tF)):
         raise ValueError("observations extend past the final time")
-    if abs(loss.times[-1] - tF) > 1e-9 * max(1.0, abs(tF)):
-        raise NotImplementedError("observations before tF are not built (SURVEY 8f row 3)")
+    obs = loss.kind in OBSERVATION_KINDS
+    if not obs and abs(loss.times[-1] - tF) > 1e-9 * max(1.0, abs(tF)):
+        raise ValueError(f"{loss.kind} is a terminal loss at tF")
     ts = boundary_times(ctrl, t0, tF)
+    obs_steps = match_boundaries(loss.times, ts) if obs else None
     host_io = not (isinstance(u0, torch.Tensor) and u0.is_cuda)
     dt = field.torch_dtype
     if isinstance(u0, torch.Tensor) and not u0.is_cuda:
@@ -112,6 +114,10 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     bg = int(batch_global) if batch_global is not None else B
     prob, _times = build_problem(field, scheme, loss, B, ts, policy, solver_cfg, bg)
     prob.flags = 1 if profile else 0
+    if obs:
+        steps_c = (C.c_int32 * len(obs_steps))(*obs_steps)
+        prob.n_obs = len(obs_steps)
+        prob.obs_steps = C.cast(steps_c, C.POINTER(C.c_int32))
     nbytes = workspace_size(prob)
     dev = u0d.device
     ws = _workspace(nbytes, dev)
@@ -119,15 +125,34 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     du0 = torch.empty_like(u0d)
     dtheta = torch.empty(field.n_params, dtype=dt, device=dev)
     loss_t = torch.zeros(1, dtype=torch.float64, device=dev)
-    targets = to_device(loss.values, dt) if loss.kind == "mse" else None
-    if targets is not None and tuple(targets.shape) != (B, N):
-        raise ValueError("targets must be [B, N]")
+    preds = obs_vals = lo = hi = None
+    if obs:
+        vals = []
+        for v in loss.values:
+            v = to_device(v, dt)
+            if v.dim() == 1:
+                v = v.unsqueeze(0).expand(B, -1)
+            if tuple(v.shape) != (B, N):
+                raise ValueError("observations must be [B, N] or [N]")
+            vals.append(v)
+        obs_vals = torch.stack(vals).contiguous()
+        preds = torch.empty_like(obs_vals)
+        if loss.scaling is not None:
+            if loss.scaling.lo.shape != (N,):
+                raise ValueError("scaling bounds must have the state dimension")
+            lo = to_device(loss.scaling.lo, dt)
+            hi = to_device(loss.scaling.hi, dt)
     aux = field.aux()
     bufs = _lib.Buffers()
     bufs.theta = field.theta_tensor().data_ptr()
     bufs.aux = aux.data_ptr() if aux is not None else None
     bufs.u0 = u0d.data_ptr()
-    bufs.targets = targets.data_ptr() if targets is not None else None
+    bufs.targets = None
+    if obs:
+        bufs.obs_values = obs_vals.data_ptr()
+        bufs.predictions = preds.data_ptr()
+        bufs.scale_lo = lo.data_ptr() if lo is not None else None
+        bufs.scale_hi = hi.data_ptr() if hi is not None else None
     bufs.u_final = u_final.data_ptr()
     bufs.du0 = du0.data_ptr()
     bufs.dtheta = dtheta.data_ptr()
@@ -169,6 +194,11 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
         dtheta_o, du0_o, uf_o = dtheta, du0, u_final
     if dhead is not None and host_io:
         dhead = dhead.cpu().numpy()
+    if obs:
+        pr = preds.cpu().numpy() if host_io else preds
+        predictions = [pr[k] for k in range(pr.shape[0])]
+    else:
+        predictions = [uf_o]
     return GradResult(dtheta=dtheta_o, du0=du0_o, loss=loss_v, counters=counters,
-                      predictions=[uf_o], u_final=uf_o, store_counters=sc, device=c,
+                      predictions=predictions, u_final=uf_o, store_counters=sc, device=c,
                       sample_counters=samp, dtheta_head=dhead)

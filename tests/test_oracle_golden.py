@@ -247,3 +247,41 @@ def test_kat_gmres():
     with pytest.raises(oc.ConvergenceError):
         oc.gmres(lambda v: a @ v, rng.standard_normal(40),
                  oc.SolverCfg(gmres_maxit=2, gmres_restart=2))
+
+
+OBS_CASES = ("mse_rk4", "mae_dopri5", "mse_cn", "mae_rk4_tF")
+
+
+def obs_case(g, name):
+    """Oracle ObsLoss + field for one obs_losses.npz case (reference grad() per sample)."""
+    from oracle import obs_losses as ol
+    kind, sch, pol, tin = (str(x) for x in g[f"{name}/meta"])
+    tin = tin == "1"
+    N = g[f"{name}/u0"].shape[1]
+    mlp = oc.Mlp((N + int(tin), 8, 8, N), "tanh", g[f"{name}/theta"], time_input=tin)
+    ts = np.linspace(0.0, 1.0, 9)
+    steps = ol.match_boundaries(g[f"{name}/times"], ts)
+    scaling = ol.MinMax(g[f"{name}/lo"], g[f"{name}/hi"]) if f"{name}/lo" in g else None
+    return mlp, sch, pol, ol.ObsLoss(kind, steps, g[f"{name}/values"], scaling)
+
+
+@pytest.mark.parametrize("name", OBS_CASES)
+def test_observation_losses_match_reference(golden, name):
+    g = golden("obs_losses.npz")
+    mlp, sch, pol, obs = obs_case(g, name)
+    res = oc.grad_terminal(oc.MlpField(mlp), sch, g[f"{name}/u0"], 0.0, 1.0, 8, pol, obs=obs)
+    assert abs(res["loss"] - float(g[f"{name}/loss"])) <= 1e-12 * max(1.0, abs(float(g[f"{name}/loss"])))
+    assert oc.rel_error(res["predictions"], g[f"{name}/predictions"]) < 1e-12
+    assert oc.rel_error(res["dtheta"], g[f"{name}/dtheta"]) < 1e-10
+    assert oc.rel_error(res["du0"], g[f"{name}/du0"]) < 1e-10
+
+
+def test_observation_alignment_and_scaling_rules():
+    from oracle import obs_losses as ol
+    ts = np.linspace(0.0, 1.0, 5)
+    assert ol.match_boundaries([0.0, 0.5, 1.0], ts) == [0, 2, 4]
+    with pytest.raises(ValueError):
+        ol.match_boundaries([0.3], ts)
+    sc = ol.MinMax([0.0, 1.0], [2.0, 1.0])        # second component degenerate
+    np.testing.assert_allclose(sc.apply(np.array([1.0, 5.0])), [0.5, 5.0])
+    np.testing.assert_allclose(sc.chain(np.array([1.0, 1.0])), [0.5, 1.0])

@@ -170,6 +170,56 @@ def gen_config(name, nsub, policies, solver=None, suffix=""):
     save(f"{name.lower()}_sub{suffix}.npz", **out)
 
 
+def gen_obs():
+    """Multi-observation MAE/MSE losses with min-max scaling (losses.py:10-107,
+    adjoint.py:143-279) through the reference's own grad(), per sample; the batch
+    result is the sample mean (loss, dtheta) and du0_b / B."""
+    out = {}
+    rng = np.random.default_rng(424242)
+    cases = [
+        ("mse_rk4", "mse", "rk4", "store_all", (0.25, 0.5, 1.0), False, False),
+        ("mae_dopri5", "mae", "dopri5", "revolve:3", (0.0, 0.5, 0.75), True, True),
+        ("mse_cn", "mse", "cn", "store_solutions", (0.5, 1.0), True, False),
+        ("mae_rk4_tF", "mae", "rk4", "store_all", (1.0,), False, False),
+    ]
+    n_steps, B, N = 8, 3, 3
+    for name, kind, sch, pol, times, scaled, tin in cases:
+        model = og.init_model(og.mlp_spec(N, 8, 2, "tanh", time_input=tin), seed=5)
+        U0 = rng.uniform(-1, 1, (B, N))
+        vals = rng.uniform(-0.5, 0.5, (len(times), B, N))
+        lo = hi = None
+        scaling = None
+        if scaled:
+            lo = np.array([-1.0, 0.3, -2.0])
+            hi = np.array([1.5, 0.3, 0.5])       # component 1 degenerate (hi <= lo)
+            scaling = og.losses.MinMaxScaling(lo, hi)
+        scheme = og.tableau_catalog(sch)
+        ctrl = og.FixedController(n_steps)
+        loss, dth, du0, preds = 0.0, np.zeros(model.n_params), [], []
+        for b in range(B):
+            spec = og.losses.LossSpec(kind, times, tuple(vals[:, b]), scaling)
+            r = og.grad(og.MlpField(model), scheme, spec, U0[b], 0.0, 1.0, ctrl,
+                        og.CheckpointPolicy.parse(pol))
+            loss += r.loss / B
+            dth = dth + r.dtheta / B
+            du0.append(r.du0 / B)
+            preds.append(np.array(r.predictions))
+        pre = f"{name}/"
+        out[pre + "theta"] = model.theta
+        out[pre + "u0"] = U0
+        out[pre + "values"] = vals
+        out[pre + "times"] = np.array(times)
+        out[pre + "meta"] = np.array([kind, sch, pol, str(int(tin))])
+        if scaled:
+            out[pre + "lo"] = lo
+            out[pre + "hi"] = hi
+        out[pre + "loss"] = np.float64(loss)
+        out[pre + "dtheta"] = dth
+        out[pre + "du0"] = np.array(du0)
+        out[pre + "predictions"] = np.transpose(np.array(preds), (1, 0, 2))   # [K, B, N]
+    save("obs_losses.npz", **out)
+
+
 def gen_revolve():
     out = {}
     counts = np.zeros((61, 21), np.int64)
@@ -197,9 +247,13 @@ if __name__ == "__main__":
                    suffix="_numpy")
         sys.exit(0)
     og.kernels.warmup()
+    if len(sys.argv) > 1 and sys.argv[1] == "obs":
+        gen_obs()
+        sys.exit(0)
     gen_revolve()
     gen_kernels()
     gen_small()
+    gen_obs()
     gen_config("C1", 4, ["store_all", "store_solutions", "revolve:3"])
     gen_config("C2", 3, ["store_all", "revolve:8"])
     gen_config("C5", 2, ["store_all"], solver=configs.make_c5(batch=1).extras["solver"])
