@@ -87,6 +87,9 @@ typedef struct {
   double a[OB_MAX_STAGES * OB_MAX_STAGES];  /* row-major s x s */
   double b[OB_MAX_STAGES];
   double c[OB_MAX_STAGES];
+  double b_emb[OB_MAX_STAGES]; /* embedded weights (adaptive stepping), when has_emb */
+  int32_t order;               /* order p of b: PI exponents 0.7/p, 0.4/p (integrators.py:300-302) */
+  int32_t has_emb;
 } ob_scheme_desc;
 
 /* SolverConfig (linalg.py:22-34). */
@@ -116,6 +119,15 @@ typedef struct {
   int32_t n_obs;          /* OB_LOSS_OBS_*: observation count K >= 1           */
   const int32_t* obs_steps; /* HOST [n_obs] boundary index of each observation, strictly
                              increasing in [0, n_steps] (_match_boundaries, adjoint.py:213) */
+  /* AdaptiveController (integrators.py:178-193): adaptive = 1 replaces the fixed
+     grid (times / n_steps unused) by per-sample error-controlled steps on [t0, tF],
+     one integration per observation interval (adjoint.py:162-186) */
+  int32_t adaptive;
+  int32_t max_accepted;   /* per-sample capacity of accepted steps (workspace sizing) */
+  double abstol, reltol, h_init, h_min, h_max, safety;
+  int64_t max_steps;      /* per integrate() call, trials included               */
+  double t0, tF;
+  const double* obs_times; /* HOST [n_obs] observation times (adaptive + OB_LOSS_OBS_*) */
 } ob_problem;
 
 /* flags: accumulate per-phase SM cycles of the persistent kernels (profiling aid;
@@ -147,11 +159,15 @@ typedef struct {
   const void* scale_lo;   /* [N] or NULL (no scaling); components with hi <= lo pass through */
   const void* scale_hi;   /* [N] or NULL                                          */
   void* predictions;      /* out [n_obs, B, N]: states at the observation boundaries */
+  /* adaptive: optional outputs of the per-sample grids */
+  double* grid;           /* out [B, max_accepted + 1] boundary times (NaN past the end) or NULL */
+  int32_t* n_accepted;    /* out [B] accepted steps per sample, or NULL                 */
 } ob_buffers;
 
 /* per-sample stats columns (implicit schemes; explicit: fixed by the schedule) */
 enum { OB_STAT_NFE_F = 0, OB_STAT_NFE_B = 1, OB_STAT_NEWTON = 2, OB_STAT_GMRES_F = 3,
-       OB_STAT_GMRES_B = 4, OB_NSTATS = 5 };
+       OB_STAT_GMRES_B = 4, OB_STAT_ACCEPTED = 5, OB_STAT_REJECTED = 6, OB_STAT_RECOMPUTED = 7,
+       OB_NSTATS = 8 };
 
 /* NfeCounters (integrators.py:28-50) + StoreCounters (checkpointing.py:193-198),
    reference semantics per sample trajectory, plus what the device really ran. */

@@ -8,7 +8,7 @@ samples and executed by hand-written sm_100a kernels behind a C ABI
 """
 
 from .configs import ConfigInputs, make_config
-from .controls import (ConvergenceError, DeviceError, FixedController, FixedGridController,
+from .controls import (AdaptiveController, ConvergenceError, DeviceError, FixedController, FixedGridController,
                        GradientExplosionError, IntegrationError, NfeCounters, SolverConfig,
                        StiffnessError, StoreCounters)
 from .engine import GradResult, grad
@@ -21,7 +21,7 @@ from .schemes import SCHEME_NAMES, ButcherTableau, Scheme, tableau_catalog
 __version__ = "0.1.0"
 
 __all__ = [
-    "ACTIVATION_IDS", "ButcherTableau", "CnfField", "CheckpointPolicy", "ConvField", "ConfigInputs", "ConvergenceError",
+    "ACTIVATION_IDS", "AdaptiveController", "ButcherTableau", "CnfField", "CheckpointPolicy", "ConvField", "ConfigInputs", "ConvergenceError",
     "DeviceError", "Field", "FixedController", "FixedGridController", "GradResult",
     "GradientExplosionError", "IntegrationError", "LossSpec", "MlpField", "MlpModel", "MlpSpec",
     "NfeCounters", "SCHEME_NAMES", "ScheduleAction", "Scheme", "SolverConfig", "StiffMlpField",

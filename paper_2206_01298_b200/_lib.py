@@ -31,7 +31,7 @@ OB_LOSS = {"half_sqnorm": 0, "mse": 4, "mae": 5, "ce_head": 2, "cnf_nll": 3}
 #  observation path, code 4)
 OB_MAX_LAYERS = 8
 OB_MAX_STAGES = 8
-OB_NSTATS = 5
+OB_NSTATS = 8   # nfe_f, nfe_b, newton, gmres_f, gmres_b, accepted, rejected, recomputed
 
 EXPORTS = (
     "ob_version", "ob_last_error", "ob_device_count", "ob_revolve_count", "ob_revolve_schedule",
@@ -49,7 +49,8 @@ class FieldDesc(C.Structure):
 class SchemeDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("stages", C.c_int32), ("fsal", C.c_int32), ("_pad", C.c_int32),
                 ("theta", C.c_double), ("a", C.c_double * (OB_MAX_STAGES * OB_MAX_STAGES)),
-                ("b", C.c_double * OB_MAX_STAGES), ("c", C.c_double * OB_MAX_STAGES)]
+                ("b", C.c_double * OB_MAX_STAGES), ("c", C.c_double * OB_MAX_STAGES),
+                ("b_emb", C.c_double * OB_MAX_STAGES), ("order", C.c_int32), ("has_emb", C.c_int32)]
 
 
 class SolverDesc(C.Structure):
@@ -62,7 +63,12 @@ class Problem(C.Structure):
                 ("batch", C.c_int64), ("batch_global", C.c_int64), ("n_steps", C.c_int32),
                 ("policy", C.c_int32), ("nc", C.c_int32), ("loss", C.c_int32),
                 ("times", C.POINTER(C.c_double)), ("flags", C.c_int32), ("n_obs", C.c_int32),
-                ("obs_steps", C.POINTER(C.c_int32))]
+                ("obs_steps", C.POINTER(C.c_int32)),
+                ("adaptive", C.c_int32), ("max_accepted", C.c_int32),
+                ("abstol", C.c_double), ("reltol", C.c_double), ("h_init", C.c_double),
+                ("h_min", C.c_double), ("h_max", C.c_double), ("safety", C.c_double),
+                ("max_steps", C.c_int64), ("t0", C.c_double), ("tF", C.c_double),
+                ("obs_times", C.POINTER(C.c_double))]
 
 
 class Buffers(C.Structure):
@@ -73,7 +79,7 @@ class Buffers(C.Structure):
                 ("head", C.c_void_p), ("labels", C.c_void_p), ("dhead", C.c_void_p),
                 ("n_classes", C.c_int32), ("_pad", C.c_int32),
                 ("obs_values", C.c_void_p), ("scale_lo", C.c_void_p), ("scale_hi", C.c_void_p),
-                ("predictions", C.c_void_p)]
+                ("predictions", C.c_void_p), ("grid", C.c_void_p), ("n_accepted", C.c_void_p)]
 
 
 class Counters(C.Structure):

@@ -101,6 +101,31 @@ class FixedGridController:
             raise ValueError("times must be strictly increasing, length >= 2")
 
 
+@dataclass(frozen=True)
+class AdaptiveController:
+    """Error-controlled stepping with an embedded pair (integrators.py:178-193):
+    WRMS norm, PI controller, per-sample step sizes.  ``max_accepted`` is this
+    build's per-sample capacity of accepted steps (device record storage);
+    exceeding it raises NotImplementedError naming the sample."""
+
+    abstol: float = 1e-6
+    reltol: float = 1e-6
+    h_init: float = 1e-3
+    h_min: float = 1e-14
+    h_max: float = np.inf
+    safety: float = 0.9
+    max_steps: int = 1_000_000
+    max_accepted: int = 1000
+
+    def __post_init__(self):
+        if self.abstol <= 0 or self.reltol <= 0:
+            raise ValueError("tolerances must be positive")
+        if not (self.h_min <= self.h_init <= self.h_max):
+            raise ValueError("need h_min <= h_init <= h_max")
+        if self.max_accepted < 1:
+            raise ValueError("max_accepted must be >= 1")
+
+
 def boundary_times(ctrl, t0, tF) -> np.ndarray:
     """The fp64 step grid (integrators.py:274-280): np.linspace for a fixed
     step count, the explicit grid (checked to span [t0, tF]) otherwise."""
@@ -113,9 +138,7 @@ def boundary_times(ctrl, t0, tF) -> np.ndarray:
         if abs(ts[0] - t0) > 1e-12 * max(1.0, abs(t0)) or abs(ts[-1] - tF) > 1e-12 * max(1.0, abs(tF)):
             raise ValueError("time grid must span [t0, tF]")
         return ts
-    raise NotImplementedError(
-        f"controller {type(ctrl).__name__} is not built: adaptive stepping is the next "
-        "component (SURVEY 8f row 1)")
+    raise TypeError(f"unknown controller {ctrl!r}")
 
 
 @dataclass(frozen=True)

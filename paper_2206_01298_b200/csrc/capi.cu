@@ -43,6 +43,8 @@ template <typename T>
 cudaError_t launch_conv_field(const RkParams<T>&, int, size_t, int, double, const T*, const T*, T*,
                               cudaStream_t);
 template <typename T> cudaError_t launch_pack_conv(const PackParams<T>&, cudaStream_t);
+template <typename T, bool WS>
+cudaError_t launch_adaptive_ws(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
 template <typename T>
 cudaError_t launch_reduce_plain(const T*, int, long long, long long, T*, cudaStream_t);
 
@@ -53,6 +55,13 @@ cudaError_t launch_rk(const RkParams<T>& p, int lr, int tiles, size_t smem, cuda
   if constexpr (sizeof(T) == 4)
     if (p.sm.wts >= 0) return launch_rk_ws<T, true>(p, lr, tiles, smem, st, forward);
   return launch_rk_ws<T, false>(p, lr, tiles, smem, st, forward);
+}
+template <typename T>
+cudaError_t launch_adaptive(const RkParams<T>& p, int lr, int tiles, size_t smem, cudaStream_t st,
+                            bool forward) {
+  if constexpr (sizeof(T) == 4)
+    if (p.sm.wts >= 0) return launch_adaptive_ws<T, true>(p, lr, tiles, smem, st, forward);
+  return launch_adaptive_ws<T, false>(p, lr, tiles, smem, st, forward);
 }
 template <typename T>
 cudaError_t launch_field_op(const RkParams<T>& p, int lr, int tiles, size_t smem, int mode,
@@ -172,9 +181,17 @@ struct Plan {
          off_mu = 0, off_lp = 0, total = 0;
   size_t off_pk = 0;
   long long scratch_stride = 0;
+  size_t smem_reserve = 0;        // static shared memory of the kernel family
+  // adaptive stepping
+  bool adaptive = false;
+  int cap = 0, nseg = 0, obs0 = 0;
+  std::vector<double> pts;
+  size_t off_grid = 0, off_nacc = 0, off_ostep = 0;
 };
 
 constexpr size_t kSmemLimit = 227 * 1024;
+constexpr size_t kAdaptiveStaticSmem = 6 * 1024;   // per-row controller state + reductions
+inline size_t smem_cap(const Plan& P) { return kSmemLimit - P.smem_reserve; }
 
 int check_field(const ob_field_desc& f) {
   if (f.dtype != OB_F32 && f.dtype != OB_F64) return fail(OB_ERR_VALUE, "dtype must be f32 or f64");
@@ -331,7 +348,7 @@ void layout_smem(Plan& P) {
     s.scr = take(s.scr_elems);
     // The Krylov basis stays in global memory by default: the L1 capacity it would
     // take caches the streamed weights, which matters more (measured on C5)
-    if ((size_t)(o + P.krylov_stride) * P.esz <= kSmemLimit && getenv("OB_KRYLOV_SMEM"))
+    if ((size_t)(o + P.krylov_stride) * P.esz <= smem_cap(P) && getenv("OB_KRYLOV_SMEM"))
       s.kry = take(P.krylov_stride);
   }
   s.total = o;
@@ -340,7 +357,7 @@ void layout_smem(Plan& P) {
   // they fit; fp64, theta-method and CNF kernels read L1/L2-resident weights
   // (only rk_f32s.cu instantiates the shared-memory-weight variants)
   const bool ws_variant = P.esz == 4 && !P.theta && !d.cnf && !d.conv;
-  if (ws_variant && (size_t)(o + d.n_packed) * P.esz <= kSmemLimit && !getenv("OB_NO_SMEM_WEIGHTS")) {
+  if (ws_variant && (size_t)(o + d.n_packed) * P.esz <= smem_cap(P) && !getenv("OB_NO_SMEM_WEIGHTS")) {
     s.wts = take(d.n_packed);
     s.total = o;
   }
@@ -365,7 +382,7 @@ void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
       P.R = std::min(R, P.Rt);
       make_dims(f, P.LR, P.d);
       layout_smem(P);
-      if (P.smem_bytes <= kSmemLimit || R == 1) break;
+      if (P.smem_bytes <= smem_cap(P) || R == 1) break;
     }
     P.tiles = (int)((B + P.R - 1) / P.R);
     return;
@@ -378,7 +395,7 @@ void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
     P.Rt = round_up(R, 4 * P.LR);
     make_dims(f, P.LR, P.d);
     layout_smem(P);
-    if (P.smem_bytes <= kSmemLimit || R == 1) break;
+    if (P.smem_bytes <= smem_cap(P) || R == 1) break;
     R = std::max(1, R * 3 / 4);
   }
   P.tiles = (int)((B + P.R - 1) / P.R);
@@ -508,11 +525,8 @@ int plan_problem(const ob_problem& p, Plan& P) {
     return fail(OB_ERR_VALUE, "unknown scheme kind");
   }
   if (p.scheme.stages < 1 || p.scheme.stages > OB_MAX_STAGES) return fail(OB_ERR_VALUE, "bad stage count");
-  if (p.n_steps < 1) return fail(OB_ERR_VALUE, "fixed mode requires at least one step");
+  P.adaptive = p.adaptive != 0;
   if (p.batch < 1) return fail(OB_ERR_VALUE, "batch must be >= 1");
-  if (!p.times) return fail(OB_ERR_VALUE, "times array is required");
-  for (int i = 0; i < p.n_steps; ++i)
-    if (!(p.times[i + 1] > p.times[i])) return fail(OB_ERR_VALUE, "step size must be positive");
   const bool obs = p.loss == OB_LOSS_OBS_MSE || p.loss == OB_LOSS_OBS_MAE;
   const bool vec_field = p.field.kind == OB_FIELD_MLP || p.field.kind == OB_FIELD_STIFF;
   if (p.loss != OB_LOSS_HALF_SQNORM && p.loss != OB_LOSS_MSE && !(obs && vec_field) &&
@@ -520,15 +534,69 @@ int plan_problem(const ob_problem& p, Plan& P) {
       !(p.loss == OB_LOSS_CE_HEAD && p.field.kind == OB_FIELD_CONV))
     return fail(OB_ERR_UNSUPPORTED, "loss kind not supported for this field");
   P.obs_k.clear();
-  if (obs) {  // LossSpec validation (losses.py:54-69) on boundary indices
-    if (p.n_obs < 1 || !p.obs_steps) return fail(OB_ERR_VALUE, "need one observation vector per time");
-    P.obs_k.assign(p.n_steps + 1, -1);
-    for (int k = 0; k < p.n_obs; ++k) {
-      const int j = p.obs_steps[k];
-      if (j < 0 || j > p.n_steps) return fail(OB_ERR_VALUE, "observation boundary out of range");
-      if (k > 0 && j <= p.obs_steps[k - 1])
-        return fail(OB_ERR_VALUE, "observation times must be strictly increasing");
-      P.obs_k[j] = k;
+  if (P.adaptive) {
+    // AdaptiveController / integrate / forward_pass checks (integrators.py:187-193,
+    // :297-299; adjoint.py:165-166; checkpointing.py:218-220)
+    if (!(p.abstol > 0 && p.reltol > 0)) return fail(OB_ERR_VALUE, "tolerances must be positive");
+    if (!(p.h_min <= p.h_init && p.h_init <= p.h_max))
+      return fail(OB_ERR_VALUE, "need h_min <= h_init <= h_max");
+    if (!(p.tF > p.t0)) return fail(OB_ERR_VALUE, "tF must exceed t0");
+    if (p.policy == OB_POLICY_REVOLVE)
+      return fail(OB_ERR_VALUE, "revolve checkpointing needs fixed stepping");
+    if (P.theta || !p.scheme.has_emb || p.scheme.order < 1)
+      return fail(OB_ERR_INTEGRATION, "adaptive mode needs an embedded explicit scheme");
+    if (!vec_field) return fail(OB_ERR_UNSUPPORTED, "adaptive stepping is built for MLP / stiff fields");
+    if (p.max_accepted < 1) return fail(OB_ERR_VALUE, "max_accepted must be >= 1");
+    if (p.max_steps < 1) return fail(OB_ERR_VALUE, "max_steps must be >= 1");
+    P.cap = p.max_accepted;
+    // observation intervals: [t0] + obs > t0 (+ tF)
+    std::vector<double> ot;
+    if (obs) {
+      if (p.n_obs < 1 || !p.obs_times) return fail(OB_ERR_VALUE, "need one observation vector per time");
+      for (int k = 0; k < p.n_obs; ++k) {
+        if (k > 0 && !(p.obs_times[k] > p.obs_times[k - 1]))
+          return fail(OB_ERR_VALUE, "observation times must be strictly increasing");
+        if (p.obs_times[k] > p.tF + 1e-9 * std::max(1.0, std::fabs(p.tF)))
+          return fail(OB_ERR_VALUE, "observations extend past the final time");
+        ot.push_back(p.obs_times[k]);
+      }
+    }
+    P.pts.assign(1, p.t0);
+    for (double t : ot)
+      if (t > p.t0) P.pts.push_back(t);
+    if (std::fabs(P.pts.back() - p.tF) > 1e-12 * std::max(1.0, std::fabs(p.tF))) P.pts.push_back(p.tF);
+    P.nseg = (int)P.pts.size() - 1;
+    P.obs0 = !ot.empty() && ot[0] == p.t0;
+    if (obs) {
+      P.obs_k.assign(P.nseg, -1);
+      std::vector<int> seen(ot.size(), 0);
+      if (P.obs0) seen[0] = 1;
+      for (int sgm = 0; sgm < P.nseg; ++sgm) {
+        const double b = P.pts[sgm + 1];
+        for (size_t k = 0; k < ot.size(); ++k)
+          if (std::fabs(b - ot[k]) <= 1e-9 * std::max(1.0, std::fabs(ot[k]))) {
+            if (P.obs_k[sgm] < 0) P.obs_k[sgm] = (int)k;
+            seen[k] = 1;
+          }
+      }
+      for (int v : seen)   // loss_and_grad_seed (losses.py:85-86)
+        if (!v) return fail(OB_ERR_VALUE, "one prediction per observation required");
+    }
+  } else {
+    if (p.n_steps < 1) return fail(OB_ERR_VALUE, "fixed mode requires at least one step");
+    if (!p.times) return fail(OB_ERR_VALUE, "times array is required");
+    for (int i = 0; i < p.n_steps; ++i)
+      if (!(p.times[i + 1] > p.times[i])) return fail(OB_ERR_VALUE, "step size must be positive");
+    if (obs) {  // LossSpec validation (losses.py:54-69) on boundary indices
+      if (p.n_obs < 1 || !p.obs_steps) return fail(OB_ERR_VALUE, "need one observation vector per time");
+      P.obs_k.assign(p.n_steps + 1, -1);
+      for (int k = 0; k < p.n_obs; ++k) {
+        const int j = p.obs_steps[k];
+        if (j < 0 || j > p.n_steps) return fail(OB_ERR_VALUE, "observation boundary out of range");
+        if (k > 0 && j <= p.obs_steps[k - 1])
+          return fail(OB_ERR_VALUE, "observation times must be strictly increasing");
+        P.obs_k[j] = k;
+      }
     }
   }
   if ((p.field.kind == OB_FIELD_CNF || p.field.kind == OB_FIELD_CONV) &&
@@ -543,10 +611,26 @@ int plan_problem(const ob_problem& p, Plan& P) {
     cudaGetLastError();
   }
   P.gmres_m = P.theta ? std::min(p.solver.gmres_restart, p.field.widths[p.field.n_layers]) : 0;
+  P.smem_reserve = P.adaptive ? kAdaptiveStaticSmem : 0;
   choose_tiles(P, p.field, p.batch, sms);
-  if (P.smem_bytes > kSmemLimit) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
-  st = compile_policy(p, P);
-  if (st) return st;
+  if (P.smem_bytes > smem_cap(P)) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
+  if (P.adaptive) {
+    P.prog.clear();
+    P.fwd_rec.assign(P.nseg, -1);
+    P.fwd_sol.assign(P.nseg, -1);
+    if (p.policy == OB_POLICY_STORE_ALL) {
+      P.nbuf = P.cap;
+      P.nsol = 0;
+    } else if (p.policy == OB_POLICY_STORE_SOLUTIONS) {
+      P.nbuf = 3;          // final-record ping-pong + replay slot
+      P.nsol = P.cap;
+    } else {
+      return fail(OB_ERR_VALUE, "unknown checkpoint policy");
+    }
+  } else {
+    st = compile_policy(p, P);
+    if (st) return st;
+  }
   // zero-cotangent stages: b_i == 0 and a_ji == 0 for all j > i  (dopri5 stage 7)
   const int s = p.scheme.stages;
   P.skip_vjp = 0;
@@ -557,7 +641,7 @@ int plan_problem(const ob_problem& p, Plan& P) {
   }
   // reference-semantics NFE counters, per trajectory (integrators.py:83-102)
   ob_counters& c = P.cnt;
-  const long long nt = p.n_steps;
+  const long long nt = P.adaptive ? P.nseg : p.n_steps;   // blob: fixed grid | interval ends
   c.nfe_forward = s * nt - (p.scheme.fsal ? nt - 1 : 0) + c.steps_recomputed * s;
   c.nfe_backward = s * nt;
   c.steps_accepted = nt;
@@ -566,6 +650,7 @@ int plan_problem(const ob_problem& p, Plan& P) {
   if (P.theta) {  // data dependent: filled from the per-sample device counters after the run
     c.nfe_forward = c.nfe_backward = c.device_rhs_evals = c.device_vjp_evals = 0;
   }
+  if (P.adaptive) c = ob_counters{};   // per-sample grids: filled after the run
   c.tile_rows = P.R;
   c.tiles = P.tiles;
   c.kernel_launches = 4;
@@ -612,6 +697,14 @@ int plan_problem(const ob_problem& p, Plan& P) {
                      sizeof(double) * (size_t)P.tiles * 8 * (81 + 64), 256);
   P.off_lp = o;
   o = align_up(o + sizeof(double) * P.tiles, 256);
+  if (P.adaptive) {
+    P.off_grid = o;
+    o = align_up(o + sizeof(double) * 2 * (size_t)B * P.cap, 256);
+    P.off_nacc = o;
+    o = align_up(o + sizeof(int) * (size_t)B, 256);
+    P.off_ostep = o;
+    o = align_up(o + sizeof(int) * (size_t)B * std::max(p.n_obs, 1), 256);
+  }
   P.total = o;
   return OB_OK;
 }
@@ -619,10 +712,10 @@ int plan_problem(const ob_problem& p, Plan& P) {
 template <typename T>
 int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st) {
   char* ws = static_cast<char*>(b.workspace);
-  const int nt = p.n_steps, s = p.scheme.stages;
-  // ---- control blob: ts | fwd_rec | fwd_sol | prog | status
+  const int nt = P.adaptive ? P.nseg : p.n_steps, s = p.scheme.stages;
+  // ---- control blob: ts (adaptive: interval ends) | fwd_rec | fwd_sol | prog | status | obs
   std::vector<char> blob(P.blob_bytes, 0);
-  std::memcpy(blob.data() + P.o_ts, p.times, sizeof(double) * (nt + 1));
+  std::memcpy(blob.data() + P.o_ts, P.adaptive ? P.pts.data() : p.times, sizeof(double) * (nt + 1));
   std::memcpy(blob.data() + P.o_fr, P.fwd_rec.data(), sizeof(int) * nt);
   std::memcpy(blob.data() + P.o_fs, P.fwd_sol.data(), sizeof(int) * nt);
   if (!P.prog.empty()) std::memcpy(blob.data() + P.o_pg, P.prog.data(), sizeof(int4) * P.prog.size());
@@ -703,6 +796,28 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   rp.n_classes = b.n_classes;
   rp.head_part = reinterpret_cast<T*>(ws + P.off_head);
   rp.tiles_total = P.tiles;
+  if (P.adaptive) {
+    rp.ad_policy = p.policy == OB_POLICY_STORE_ALL ? 0 : 1;
+    rp.ad_abstol = p.abstol;
+    rp.ad_reltol = p.reltol;
+    rp.ad_hinit = p.h_init;
+    rp.ad_hmin = p.h_min;
+    rp.ad_hmax = p.h_max;
+    rp.ad_safety = p.safety;
+    rp.ad_alpha = 0.7 / p.scheme.order;   // PI exponents (integrators.py:300-302)
+    rp.ad_beta = 0.4 / p.scheme.order;
+    rp.ad_max_steps = p.max_steps;
+    rp.ad_cap = P.cap;
+    for (int i = 0; i < s; ++i) rp.ad_d[i] = p.scheme.b[i] - p.scheme.b_emb[i];
+    rp.ad_pts = reinterpret_cast<const double*>(ws + P.off_blob + o_ts);
+    rp.ad_nseg = P.nseg;
+    rp.ad_seg_obs = rp.obs_k;
+    rp.ad_obs0 = P.obs0;
+    rp.ad_grid = reinterpret_cast<double*>(ws + P.off_grid);
+    rp.ad_nacc = reinterpret_cast<int*>(ws + P.off_nacc);
+    rp.obs_step = reinterpret_cast<int*>(ws + P.off_ostep);
+    CU(cudaMemsetAsync(rp.obs_step, 0xff, sizeof(int) * (size_t)p.batch * std::max(p.n_obs, 1), st));
+  }
   CU(cudaMemsetAsync(stats, 0, sizeof(int) * (size_t)p.batch * OB_NSTATS, st));
 
   // per-phase CUDA events on the launch stream (bench roofline timing)
@@ -718,6 +833,7 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   }
   CU(cudaEventRecord(ev[1], st));
   auto sweep = [&](bool fwd) -> cudaError_t {
+    if (P.adaptive) return launch_adaptive<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
     if (P.theta) return launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
     if (P.d.cnf || P.d.conv) {
       if constexpr (sizeof(T) == 4) {
@@ -743,7 +859,7 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
   int hs[2] = {0, 0};
   CU(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
   std::vector<int> hstats;
-  if (P.theta) {
+  if (P.theta || P.adaptive) {
     hstats.resize((size_t)p.batch * OB_NSTATS);
     CU(cudaMemcpyAsync(hstats.data(), stats, sizeof(int) * hstats.size(), cudaMemcpyDeviceToHost, st));
   }
@@ -751,14 +867,49 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
     CU(cudaMemcpyAsync(b.sample_stats, stats, sizeof(int) * (size_t)p.batch * OB_NSTATS,
                        cudaMemcpyDeviceToDevice, st));
   CU(cudaStreamSynchronize(st));
-  if (P.theta) {  // reference-semantics NFE of the critical-path trajectory (max over samples)
-    long long mf = 0, mb = 0;
+  if (P.theta || P.adaptive) {  // reference-semantics counters of the critical-path trajectory
+    long long mf = 0, mb = 0, ma = 0, mr = 0, mc = 0;
     for (long long i = 0; i < p.batch; ++i) {
-      mf = std::max<long long>(mf, hstats[i * OB_NSTATS + OB_STAT_NFE_F]);
-      mb = std::max<long long>(mb, hstats[i * OB_NSTATS + OB_STAT_NFE_B]);
+      const int* r = &hstats[i * OB_NSTATS];
+      mf = std::max<long long>(mf, r[OB_STAT_NFE_F]);
+      mb = std::max<long long>(mb, r[OB_STAT_NFE_B]);
+      ma = std::max<long long>(ma, r[OB_STAT_ACCEPTED]);
+      mr = std::max<long long>(mr, r[OB_STAT_REJECTED]);
+      mc = std::max<long long>(mc, r[OB_STAT_RECOMPUTED]);
     }
     P.cnt.nfe_forward = P.cnt.device_rhs_evals = mf;
     P.cnt.nfe_backward = P.cnt.device_vjp_evals = mb;
+    if (P.adaptive) {   // per trajectory, max over samples (checkpointing.py:193-198, :272-284)
+      P.cnt.steps_accepted = ma;
+      P.cnt.steps_rejected = mr;
+      P.cnt.steps_recomputed = P.cnt.recomputed_steps = mc;
+      P.cnt.stored_states = ma > 0 ? ma - 1 : 0;
+      P.cnt.stored_stage_vectors = p.policy == OB_POLICY_STORE_ALL ? (ma > 0 ? ma - 1 : 0) * s : 0;
+      P.cnt.max_live_slots = P.cnt.stored_states;
+      P.cnt.tile_rows = P.R;
+      P.cnt.tiles = P.tiles;
+      P.cnt.kernel_launches = 4;
+    }
+  }
+  if (P.adaptive && hs[0] == 0 && (b.grid || b.n_accepted)) {
+    // per-sample boundary times t_0, t_n + h_n (adjoint.py:171-173)
+    std::vector<double> g((size_t)p.batch * P.cap * 2);
+    std::vector<int> na((size_t)p.batch);
+    CU(cudaMemcpy(g.data(), rp.ad_grid, sizeof(double) * g.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(na.data(), rp.ad_nacc, sizeof(int) * na.size(), cudaMemcpyDeviceToHost));
+    if (b.n_accepted)
+      CU(cudaMemcpyAsync(b.n_accepted, na.data(), sizeof(int) * na.size(), cudaMemcpyHostToDevice, st));
+    if (b.grid) {
+      const size_t w = (size_t)P.cap + 1;
+      std::vector<double> bt((size_t)p.batch * w, std::nan(""));
+      for (long long i = 0; i < p.batch; ++i) {
+        bt[i * w] = p.t0;
+        for (int n = 0; n < na[i]; ++n)
+          bt[i * w + n + 1] = g[((size_t)i * P.cap + n) * 2] + g[((size_t)i * P.cap + n) * 2 + 1];
+      }
+      CU(cudaMemcpyAsync(b.grid, bt.data(), sizeof(double) * bt.size(), cudaMemcpyHostToDevice, st));
+    }
+    CU(cudaStreamSynchronize(st));
   }
   float ms[4] = {0, 0, 0, 0};
   for (int i = 0; i < 4; ++i) CU(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
@@ -778,6 +929,15 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
       snprintf(msg, sizeof msg, "implicit step at t=%.17g failed: Newton/GMRES did not converge", t);
     } else if (hs[0] == OB_ERR_VALUE) {
       snprintf(msg, sizeof msg, "vector contains non-finite entries");
+    } else if (hs[0] == OB_ERR_STIFFNESS) {   // integrators.py:309-311, :322-323, :342-343
+      if (hs[1] & 1)
+        snprintf(msg, sizeof msg, "adaptive integration exceeded %lld steps (sample %d)",
+                 (long long)p.max_steps, hs[1] >> 1);
+      else
+        snprintf(msg, sizeof msg, "step size underflow (sample %d): stiffness suspected", hs[1] >> 1);
+    } else if (hs[0] == OB_ERR_UNSUPPORTED && P.adaptive) {
+      snprintf(msg, sizeof msg, "sample %d needs more than max_accepted = %d accepted steps", hs[1],
+               P.cap);
     } else {
       snprintf(msg, sizeof msg, "device status %d (%d)", hs[0], hs[1]);
     }

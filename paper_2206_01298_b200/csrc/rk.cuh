@@ -47,6 +47,19 @@ struct RkParams {
   const T* scale_lo;               // [N] or null
   const T* scale_hi;
   T* preds;                        // [n_obs][B][N]
+  int* obs_step;                   // adaptive: [n_obs][B] boundary index of each observation
+  // adaptive stepping (integrators.py:294-349)
+  int ad_policy;                   // 0 store_all, 1 store_solutions
+  double ad_abstol, ad_reltol, ad_hinit, ad_hmin, ad_hmax, ad_safety, ad_alpha, ad_beta;
+  long long ad_max_steps;
+  int ad_cap;                      // accepted-step capacity per sample
+  double ad_d[OB_MAX_STAGES];      // b - b_emb
+  const double* ad_pts;            // interval end points [ad_nseg + 1]
+  int ad_nseg;
+  const int* ad_seg_obs;           // observation index at the end of interval seg, or -1
+  int ad_obs0;                     // observation 0 at t0 (initial state)
+  double* ad_grid;                 // [B][cap][2] (t_n, h_n)
+  int* ad_nacc;                    // [B]
   double inv_batch_global;
   double batch_global;
   // buffers

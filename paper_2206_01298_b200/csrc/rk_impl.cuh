@@ -77,6 +77,9 @@ struct MlpAdapter {
     if (p.d.time_input)
       for (int r = threadIdx.x; r < p.Rt; r += blockDim.x) mt.s.x0[r * p.d.lda[0] + p.d.N] = T(t);
   }
+  OB_DEV void put_time_row(int r, double t) {   // per-row time (adaptive stepping)
+    if (p.d.time_input) mt.s.x0[r * p.d.lda[0] + p.d.N] = T(t);
+  }
   OB_DEV void set_scratch(T* s, int n) { mt.scratch = s; mt.scratch_elems = n; }
   static constexpr bool kHasJvp = true;
 

@@ -17,7 +17,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .controls import (NfeCounters, SolverConfig, StoreCounters, boundary_times, raise_status)
+from .controls import (AdaptiveController, NfeCounters, SolverConfig, StoreCounters, boundary_times,
+                       raise_status)
 from .fields import Field, stream_ptr, to_device
 from .losses import OBSERVATION_KINDS, LossSpec, match_boundaries
 from .policies import CheckpointPolicy
@@ -39,6 +40,8 @@ class GradResult:
     # (implicit schemes; explicit ones repeat the schedule-fixed counts)
     sample_counters: dict = None
     dtheta_head: object = None      # ce_head loss: gradient of the classification head
+    # adaptive stepping: per-sample boundary times (t0, t_n + h_n; adjoint.py:171-173)
+    grids: list = None
 
 
 _WS_CACHE = {}
@@ -97,8 +100,15 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     obs = loss.kind in OBSERVATION_KINDS
     if not obs and abs(loss.times[-1] - tF) > 1e-9 * max(1.0, abs(tF)):
         raise ValueError(f"{loss.kind} is a terminal loss at tF")
-    ts = boundary_times(ctrl, t0, tF)
-    obs_steps = match_boundaries(loss.times, ts) if obs else None
+    adaptive = isinstance(ctrl, AdaptiveController)
+    if adaptive:
+        if tF <= t0:
+            raise ValueError("tF must exceed t0")
+        ts = np.array([t0, tF], dtype=np.float64)
+        obs_steps = None
+    else:
+        ts = boundary_times(ctrl, t0, tF)
+        obs_steps = match_boundaries(loss.times, ts) if obs else None
     host_io = not (isinstance(u0, torch.Tensor) and u0.is_cuda)
     dt = field.torch_dtype
     if isinstance(u0, torch.Tensor) and not u0.is_cuda:
@@ -114,7 +124,20 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     bg = int(batch_global) if batch_global is not None else B
     prob, _times = build_problem(field, scheme, loss, B, ts, policy, solver_cfg, bg)
     prob.flags = 1 if profile else 0
-    if obs:
+    if adaptive:
+        prob.adaptive = 1
+        prob.n_steps = 0
+        prob.max_accepted = int(ctrl.max_accepted)
+        prob.abstol, prob.reltol = float(ctrl.abstol), float(ctrl.reltol)
+        prob.h_init, prob.h_min = float(ctrl.h_init), float(ctrl.h_min)
+        prob.h_max, prob.safety = float(ctrl.h_max), float(ctrl.safety)
+        prob.max_steps = int(ctrl.max_steps)
+        prob.t0, prob.tF = float(t0), float(tF)
+        if obs:
+            otimes = (C.c_double * len(loss.times))(*loss.times)
+            prob.n_obs = len(loss.times)
+            prob.obs_times = C.cast(otimes, C.POINTER(C.c_double))
+    elif obs:
         steps_c = (C.c_int32 * len(obs_steps))(*obs_steps)
         prob.n_obs = len(obs_steps)
         prob.obs_steps = C.cast(steps_c, C.POINTER(C.c_int32))
@@ -170,6 +193,11 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
         dhead = torch.empty_like(head)
         bufs.head, bufs.labels, bufs.dhead = head.data_ptr(), labels.data_ptr(), dhead.data_ptr()
         bufs.n_classes = 10
+    grid_t = nacc_t = None
+    if adaptive:
+        grid_t = torch.empty((B, ctrl.max_accepted + 1), dtype=torch.float64, device=dev)
+        nacc_t = torch.empty(B, dtype=torch.int32, device=dev)
+        bufs.grid, bufs.n_accepted = grid_t.data_ptr(), nacc_t.data_ptr()
     cnt = _lib.Counters()
     rc = _lib.load().ob_grad(C.byref(prob), C.byref(bufs), C.byref(cnt), stream_ptr())
     raise_status(rc, _lib.last_error())
@@ -184,6 +212,11 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
         st = stats.cpu().numpy().astype(np.int64)
         samp = {"nfe_forward": st[:, 0], "nfe_backward": st[:, 1], "newton_iters": st[:, 2],
                 "gmres_iters_forward": st[:, 3], "gmres_iters_adjoint": st[:, 4]}
+    elif adaptive:
+        st = stats.cpu().numpy().astype(np.int64)
+        samp = {"nfe_forward": st[:, 0], "nfe_backward": st[:, 1], "steps_accepted": st[:, 5],
+                "steps_rejected": st[:, 6], "steps_recomputed": st[:, 7]}
+        counters.steps_rejected += c["steps_rejected"]
     else:
         samp = {"nfe_forward": np.full(B, c["nfe_forward"]),
                 "nfe_backward": np.full(B, c["nfe_backward"])}
@@ -199,6 +232,11 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
         predictions = [pr[k] for k in range(pr.shape[0])]
     else:
         predictions = [uf_o]
+    grids = None
+    if adaptive:
+        g = grid_t.cpu().numpy()
+        na = nacc_t.cpu().numpy()
+        grids = [g[b, :na[b] + 1].copy() for b in range(B)]
     return GradResult(dtheta=dtheta_o, du0=du0_o, loss=loss_v, counters=counters,
                       predictions=predictions, u_final=uf_o, store_counters=sc, device=c,
-                      sample_counters=samp, dtheta_head=dhead)
+                      sample_counters=samp, dtheta_head=dhead, grids=grids)

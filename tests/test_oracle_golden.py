@@ -285,3 +285,51 @@ def test_observation_alignment_and_scaling_rules():
     sc = ol.MinMax([0.0, 1.0], [2.0, 1.0])        # second component degenerate
     np.testing.assert_allclose(sc.apply(np.array([1.0, 5.0])), [0.5, 5.0])
     np.testing.assert_allclose(sc.chain(np.array([1.0, 1.0])), [0.5, 1.0])
+
+
+ADAPTIVE_CASES = ("dopri5_term", "bosh3_obs", "dopri5_obs0")
+
+
+def adaptive_case(g, name):
+    """Oracle field / ctrl / ObsLoss for one adaptive.npz case (reference grad per sample)."""
+    from oracle import adaptive as oa
+    from oracle import obs_losses as ol
+    sch, kind, pol = (str(x) for x in g[f"{name}/meta"])
+    tol, _, h0 = (float(x) for x in g[f"{name}/ctrl"])
+    N = g[f"{name}/u0"].shape[1]
+    mlp = oc.Mlp((N + 1, 16, 16, N), "tanh", g[f"{name}/theta"], time_input=True)
+    scaling = ol.MinMax(g[f"{name}/lo"], g[f"{name}/hi"]) if f"{name}/lo" in g else None
+    times = tuple(float(t) for t in g[f"{name}/times"])
+    obs = ol.ObsLoss(kind, range(len(times)), g[f"{name}/values"], scaling)
+    return mlp, sch, pol, oa.AdaptiveCtrl(abstol=tol, reltol=tol, h_init=h0), obs, times
+
+
+@pytest.mark.parametrize("name", ADAPTIVE_CASES)
+def test_adaptive_stepping_matches_reference(golden, name):
+    from oracle import adaptive as oa
+    g = golden("adaptive.npz")
+    mlp, sch, pol, ctrl, obs, times = adaptive_case(g, name)
+    res = oa.grad_adaptive(oc.MlpField(mlp), sch, g[f"{name}/u0"], 0.0, 1.0, ctrl, pol,
+                           obs=obs, obs_times=times)
+    for k in ("accepted", "rejected", "nfe_forward", "nfe_backward", "steps_recomputed"):
+        assert list(res[k]) == list(g[f"{name}/{k}"]), k
+    for b, grid in enumerate(res["grids"]):
+        ref = g[f"{name}/grids"][b]
+        ref = ref[~np.isnan(ref)]
+        # the embedded error estimate cancels ~8 digits (err ~ 1e-9 from O(1) stages),
+        # so ulp-level field differences move the step sizes at the 1e-11 level
+        assert len(grid) == len(ref) and np.max(np.abs(grid - ref)) <= 1e-9
+    assert abs(res["loss"] - float(g[f"{name}/loss"])) <= 1e-12 * abs(float(g[f"{name}/loss"]))
+    assert oc.rel_error(res["predictions"], g[f"{name}/predictions"]) <= 1e-12
+    assert oc.rel_error(res["dtheta"], g[f"{name}/dtheta"]) <= 1e-10
+    assert oc.rel_error(res["du0"], g[f"{name}/du0"]) <= 1e-10
+
+
+def test_adaptive_rules():
+    from oracle import adaptive as oa
+    mlp = oc.Mlp((3, 4, 2), "tanh", np.zeros(4 * 3 + 4 + 2 * 4 + 2), time_input=True)
+    with pytest.raises(ValueError):
+        oa.grad_adaptive(oc.MlpField(mlp), "dopri5", np.ones((1, 2)), 0.0, 1.0, oa.AdaptiveCtrl(),
+                         "revolve:2")
+    with pytest.raises(oc.IntegrationError):
+        oa.grad_adaptive(oc.MlpField(mlp), "rk4", np.ones((1, 2)), 0.0, 1.0, oa.AdaptiveCtrl())

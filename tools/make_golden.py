@@ -220,6 +220,70 @@ def gen_obs():
     save("obs_losses.npz", **out)
 
 
+def gen_adaptive():
+    """Adaptive Dopri5 / Bosh3 stepping (integrators.py:294-349, adjoint.py:162-186)
+    through the reference's grad() per sample; batch = sample mean."""
+    from odegrad.integrators import AdaptiveController
+    out = {}
+    rng = np.random.default_rng(777)
+    cases = [
+        ("dopri5_term", "dopri5", "mse", "store_all", (1.0,), False, 1e-8, 0.5),
+        ("bosh3_obs", "bosh3", "mae", "store_solutions", (0.3, 0.7, 1.0), True, 1e-6, 0.3),
+        ("dopri5_obs0", "dopri5", "mse", "store_all", (0.0, 0.5), False, 1e-9, 0.4),
+    ]
+    B, N = 3, 3
+    for name, sch, kind, pol, times, scaled, tol, h0 in cases:
+        model = og.init_model(og.mlp_spec(N, 16, 2, "tanh", time_input=True), seed=9)
+        model = og.MlpModel(model.spec, 2.5 * model.theta)     # livelier dynamics
+        U0 = rng.uniform(-1.5, 1.5, (B, N))
+        vals = rng.uniform(-0.5, 0.5, (len(times), B, N))
+        scaling = og.losses.MinMaxScaling(np.array([-1.0, 0.2, -2.0]),
+                                          np.array([1.5, 0.2, 0.5])) if scaled else None
+        ctrl = AdaptiveController(abstol=tol, reltol=tol, h_init=h0)
+        loss, dth, du0, preds, grids = 0.0, np.zeros(model.n_params), [], [], []
+        acc, rej, nff, nfb, rec = [], [], [], [], []
+        for b in range(B):
+            spec = og.losses.LossSpec(kind, times, tuple(vals[:, b]), scaling)
+            c = og.NfeCounters()
+            r = og.grad(og.MlpField(model), og.tableau_catalog(sch), spec, U0[b], 0.0, 1.0, ctrl,
+                        og.CheckpointPolicy.parse(pol), counters=c)
+            fwd = og.adjoint.forward_pass(og.MlpField(model), og.tableau_catalog(sch), U0[b], 0.0,
+                                          1.0, ctrl, og.CheckpointPolicy.parse(pol),
+                                          og.SolverConfig(), og.NfeCounters(), obs_times=times)
+            loss += r.loss / B
+            dth = dth + r.dtheta / B
+            du0.append(r.du0 / B)
+            preds.append(np.array(r.predictions))
+            grids.append(np.array(fwd.boundary_times))
+            acc.append(c.steps_accepted)
+            rej.append(c.steps_rejected)
+            nff.append(c.nfe_forward)
+            nfb.append(c.nfe_backward)
+            rec.append(c.steps_recomputed)
+        L = max(len(g) for g in grids)
+        pre = f"{name}/"
+        out[pre + "theta"] = model.theta
+        out[pre + "u0"] = U0
+        out[pre + "values"] = vals
+        out[pre + "times"] = np.array(times)
+        out[pre + "meta"] = np.array([sch, kind, pol])
+        out[pre + "ctrl"] = np.array([tol, tol, h0])
+        if scaled:
+            out[pre + "lo"] = scaling.lo
+            out[pre + "hi"] = scaling.hi
+        out[pre + "loss"] = np.float64(loss)
+        out[pre + "dtheta"] = dth
+        out[pre + "du0"] = np.array(du0)
+        out[pre + "predictions"] = np.transpose(np.array(preds), (1, 0, 2))
+        out[pre + "grids"] = np.array([np.pad(g, (0, L - len(g)), constant_values=np.nan) for g in grids])
+        out[pre + "accepted"] = np.array(acc)
+        out[pre + "rejected"] = np.array(rej)
+        out[pre + "nfe_forward"] = np.array(nff)
+        out[pre + "nfe_backward"] = np.array(nfb)
+        out[pre + "steps_recomputed"] = np.array(rec)
+    save("adaptive.npz", **out)
+
+
 def gen_revolve():
     out = {}
     counts = np.zeros((61, 21), np.int64)
@@ -250,10 +314,14 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "obs":
         gen_obs()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "adaptive":
+        gen_adaptive()
+        sys.exit(0)
     gen_revolve()
     gen_kernels()
     gen_small()
     gen_obs()
+    gen_adaptive()
     gen_config("C1", 4, ["store_all", "store_solutions", "revolve:3"])
     gen_config("C2", 3, ["store_all", "revolve:8"])
     gen_config("C5", 2, ["store_all"], solver=configs.make_c5(batch=1).extras["solver"])
