@@ -199,6 +199,19 @@ int ob_revolve_schedule(int32_t nt, int32_t nc, int32_t* actions, int64_t capaci
 int ob_grad_workspace_size(const ob_problem* p, size_t* bytes);
 int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream);
 
+/* ---- training-loop optimizer (training.py:156-190, :276-277) ------------------
+   ob_adamw_step: one AdamW update of device vectors theta/m/v (n params, dtype
+   OB_F32|OB_F64) with gradient g; step = the new step count t >= 1.  Bit-identical
+   to the reference's numpy update in fp64.  A non-finite g returns
+   OB_ERR_GRADIENT_EXPLOSION and leaves theta/m/v untouched.
+   ob_grad_norm: ||g||_2 in fp64 (fixed reduction order) into *norm (host).
+   Errors of these two calls are reported by ob_optim_last_error(). */
+int ob_adamw_step(int32_t dtype, void* theta, const void* g, void* m, void* v, int64_t n,
+                  int64_t step, double lr, double beta1, double beta2, double eps,
+                  double weight_decay, void* stream);
+int ob_grad_norm(int32_t dtype, const void* g, int64_t n, double* norm, void* stream);
+const char* ob_optim_last_error(void);
+
 /* ---- profiling aid: per-phase cycle totals summed over CTAs (reset: zero them) */
 int ob_debug_phase_cycles(uint64_t* out, int32_t n, int32_t reset);
 

@@ -17,6 +17,9 @@ from .fields import (ACTIVATION_IDS, CnfField, ConvField, Field, MlpField, MlpMo
 from .losses import LossSpec, terminal_loss
 from .policies import CheckpointPolicy, ScheduleAction, revolve_count, revolve_schedule
 from .schemes import SCHEME_NAMES, ButcherTableau, Scheme, tableau_catalog
+from .formats import load_model, model_from_json, model_to_json, read_dataset_csv, save_model, write_dataset_csv
+from .training import (AdamWConfig, Dataset, OptimizerState, TrainConfig, TrainingRecord, adamw_step,
+                       geometric_grid, minmax_normalize, train)
 
 __version__ = "0.1.0"
 
@@ -27,4 +30,7 @@ __all__ = [
     "NfeCounters", "SCHEME_NAMES", "ScheduleAction", "Scheme", "SolverConfig", "StiffMlpField",
     "StiffnessError", "StoreCounters", "grad", "init_model", "make_config", "mlp_spec",
     "revolve_count", "revolve_schedule", "tableau_catalog", "terminal_loss",
+    "AdamWConfig", "Dataset", "OptimizerState", "TrainConfig", "TrainingRecord", "adamw_step",
+    "geometric_grid", "minmax_normalize", "train", "load_model", "model_from_json", "model_to_json",
+    "read_dataset_csv", "save_model", "write_dataset_csv",
 ]

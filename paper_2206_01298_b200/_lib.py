@@ -36,7 +36,7 @@ OB_NSTATS = 8   # nfe_f, nfe_b, newton, gmres_f, gmres_b, accepted, rejected, re
 EXPORTS = (
     "ob_version", "ob_last_error", "ob_device_count", "ob_revolve_count", "ob_revolve_schedule",
     "ob_grad_workspace_size", "ob_grad", "ob_debug_phase_cycles", "ob_field_eval", "ob_field_jvp", "ob_field_vjp",
-    "ob_field_vjp_u",
+    "ob_field_vjp_u", "ob_adamw_step", "ob_grad_norm", "ob_optim_last_error",
 )
 
 
@@ -122,20 +122,27 @@ def load():
         lib.ob_grad_workspace_size.argtypes = [C.POINTER(Problem), C.POINTER(C.c_size_t)]
         lib.ob_grad.argtypes = [C.POINTER(Problem), C.POINTER(Buffers), C.POINTER(Counters), vp]
         lib.ob_debug_phase_cycles.argtypes = [C.POINTER(C.c_uint64), C.c_int32, C.c_int32]
+        dbl = C.c_double
+        lib.ob_adamw_step.argtypes = [i32, vp, vp, vp, vp, i64, i64, dbl, dbl, dbl, dbl, dbl, vp]
+        lib.ob_grad_norm.argtypes = [i32, vp, i64, C.POINTER(dbl), vp]
         fd = C.POINTER(FieldDesc)
         lib.ob_field_eval.argtypes = [fd, i64, vp, vp, vp, C.c_double, vp, vp]
         lib.ob_field_jvp.argtypes = [fd, i64, vp, vp, vp, C.c_double, vp, vp, vp]
         lib.ob_field_vjp.argtypes = [fd, i64, vp, vp, vp, C.c_double, vp, vp, vp, vp]
         lib.ob_field_vjp_u.argtypes = [fd, i64, vp, vp, vp, C.c_double, vp, vp, vp]
         for name in EXPORTS:
-            getattr(lib, name).restype = C.c_int if name not in ("ob_version", "ob_last_error") \
-                else C.c_char_p
+            getattr(lib, name).restype = C.c_int if name not in (
+                "ob_version", "ob_last_error", "ob_optim_last_error") else C.c_char_p
         _lib = lib
         return lib
 
 
 def last_error() -> str:
     return load().ob_last_error().decode()
+
+
+def optim_last_error() -> str:
+    return load().ob_optim_last_error().decode()
 
 
 def version() -> str:

@@ -333,3 +333,32 @@ def test_adaptive_rules():
                          "revolve:2")
     with pytest.raises(oc.IntegrationError):
         oa.grad_adaptive(oc.MlpField(mlp), "rk4", np.ones((1, 2)), 0.0, 1.0, oa.AdaptiveCtrl())
+
+
+def test_adamw_restatement_matches_reference(golden):
+    from oracle import training as otr
+    g = golden("training.npz")
+    theta, m, v, t = g["adamw/theta0"], np.zeros(50), np.zeros(50), 0
+    for k in range(4):
+        theta, m, v, t = otr.adamw_step(theta, g[f"adamw/g{k}"], m, v, t, lr=0.01, weight_decay=0.1)
+        assert np.array_equal(theta, g[f"adamw/theta{k + 1}"])
+        assert np.array_equal(m, g[f"adamw/m{k + 1}"]) and np.array_equal(v, g[f"adamw/v{k + 1}"])
+
+
+def test_dataset_formats_roundtrip(tmp_path, golden):
+    from paper_2206_01298_b200.formats import read_dataset_csv, write_dataset_csv
+    from paper_2206_01298_b200.training import Dataset, geometric_grid, minmax_normalize
+    g = golden("training.npz")
+    ds = Dataset(g["data/times"], list(g["data/obs"]))
+    p = tmp_path / "d.csv"
+    write_dataset_csv(ds, p)
+    back = read_dataset_csv(p)
+    assert np.array_equal(back.times, ds.times) and np.array_equal(back.matrix(), ds.matrix())
+    assert open(p).readline().strip() == "t,u1,u2,u3"
+    grid = geometric_grid(ds.times, 3)
+    assert len(grid) == 3 * (len(ds.times) - 1) + 1
+    assert all(np.min(np.abs(grid - t)) <= 1e-9 * t for t in ds.times)
+    nd = minmax_normalize(ds)
+    assert np.allclose(nd.matrix().min(axis=0), 0.0) and np.allclose(nd.matrix().max(axis=0), 1.0)
+    with pytest.raises(ValueError):
+        Dataset([0.0, 0.0], [np.zeros(2), np.zeros(2)])

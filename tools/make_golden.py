@@ -284,6 +284,47 @@ def gen_adaptive():
     save("adaptive.npz", **out)
 
 
+def gen_training():
+    """AdamW steps (training.py:175-190), a reference Robertson dataset
+    (training.py:86-129, minmax-normalised :132-137) and short train() runs
+    (training.py:233-329): CN on the geometric grid and adaptive Dopri5; plus the
+    reference's model JSON / dataset CSV text (nn.py:190-220, training.py:140-152)."""
+    from odegrad import training as tr
+    from odegrad import nn as rnn
+    out = {}
+    rng = np.random.default_rng(99)
+    theta = rng.standard_normal(50)
+    st = tr.OptimizerState.zeros(50)
+    cfg = tr.AdamWConfig(lr=0.01, weight_decay=0.1)
+    out["adamw/theta0"] = theta.copy()
+    for k in range(4):
+        g = rng.standard_normal(50) * (10.0 ** (k - 2))
+        theta, st = tr.adamw_step(theta, g, st, cfg)
+        out[f"adamw/g{k}"] = g
+        out[f"adamw/theta{k + 1}"] = theta.copy()
+        out[f"adamw/m{k + 1}"] = st.m.copy()
+        out[f"adamw/v{k + 1}"] = st.v.copy()
+    ds = tr.minmax_normalize(tr.generate_robertson_dataset(n_points=6, span=(1e-5, 1e-1), n_sub=12))
+    out["data/times"] = ds.times
+    out["data/obs"] = ds.matrix()
+    model = og.init_model(og.mlp_spec(3, 8, 1, "tanh"), seed=3)
+    out["model/theta"] = model.theta
+    out["model/json"] = np.array(rnn.model_to_json(model))
+    runs = [("cn", tr.TrainConfig(epochs=4, n_sub=3, loss_kind="mae",
+                                  optimizer=tr.AdamWConfig(lr=0.01))),
+            ("dopri5", tr.TrainConfig(epochs=3, loss_kind="mse", abstol=1e-6, reltol=1e-6,
+                                      optimizer=tr.AdamWConfig(lr=0.02, weight_decay=0.01)))]
+    for sch, tc in runs:
+        trained, rec = tr.train(model, og.tableau_catalog(sch), ds, tc)
+        pre = f"train_{sch}/"
+        out[pre + "loss"] = np.array(rec.loss)
+        out[pre + "grad_norm"] = np.array(rec.grad_norm)
+        out[pre + "nfe_forward"] = np.array(rec.nfe_forward)
+        out[pre + "nfe_backward"] = np.array(rec.nfe_backward)
+        out[pre + "final_theta"] = rec.final_theta
+    save("training.npz", **out)
+
+
 def gen_revolve():
     out = {}
     counts = np.zeros((61, 21), np.int64)
@@ -317,11 +358,15 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "adaptive":
         gen_adaptive()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "training":
+        gen_training()
+        sys.exit(0)
     gen_revolve()
     gen_kernels()
     gen_small()
     gen_obs()
     gen_adaptive()
+    gen_training()
     gen_config("C1", 4, ["store_all", "store_solutions", "revolve:3"])
     gen_config("C2", 3, ["store_all", "revolve:8"])
     gen_config("C5", 2, ["store_all"], solver=configs.make_c5(batch=1).extras["solver"])
