@@ -199,6 +199,16 @@ int ob_revolve_schedule(int32_t nt, int32_t nc, int32_t* actions, int64_t capaci
 int ob_grad_workspace_size(const ob_problem* p, size_t* bytes);
 int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream);
 
+/* ---- continuous-adjoint baseline (continuous_adjoint_solve, adjoint.py:294-331) ----
+   Integrates the augmented reverse-time system (u, lambda, mu) with p's explicit
+   scheme over the tau grid p->times (n_steps + 1 points from 0 to tF - t0; p->tF
+   sets t = tF - tau) from u_final [B,N] and dphi_du [B,N]: lam0 [B,N] =
+   lambda(t0), mu0 [n_params] = sum over samples of the integral of P^T lambda.
+   Workspace: >= ob_grad_workspace_size(p).  Explicit schemes, MLP / stiff fields. */
+int ob_continuous_adjoint(const ob_problem* p, const void* theta, const void* aux,
+                          const void* u_final, const void* dphi_du, void* lam0, void* mu0,
+                          void* workspace, size_t workspace_bytes, ob_counters* out, void* stream);
+
 /* ---- training-loop optimizer (training.py:156-190, :276-277) ------------------
    ob_adamw_step: one AdamW update of device vectors theta/m/v (n params, dtype
    OB_F32|OB_F64) with gradient g; step = the new step count t >= 1.  Bit-identical

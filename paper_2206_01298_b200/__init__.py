@@ -11,7 +11,7 @@ from .configs import ConfigInputs, make_config
 from .controls import (AdaptiveController, ConvergenceError, DeviceError, FixedController, FixedGridController,
                        GradientExplosionError, IntegrationError, NfeCounters, SolverConfig,
                        StiffnessError, StoreCounters)
-from .engine import GradResult, grad
+from .engine import GradResult, continuous_adjoint_solve, grad
 from .fields import (ACTIVATION_IDS, CnfField, ConvField, Field, MlpField, MlpModel, MlpSpec, StiffMlpField, init_model,
                      mlp_spec)
 from .losses import LossSpec, terminal_loss
@@ -32,5 +32,5 @@ __all__ = [
     "revolve_count", "revolve_schedule", "tableau_catalog", "terminal_loss",
     "AdamWConfig", "Dataset", "OptimizerState", "TrainConfig", "TrainingRecord", "adamw_step",
     "geometric_grid", "minmax_normalize", "train", "load_model", "model_from_json", "model_to_json",
-    "read_dataset_csv", "save_model", "write_dataset_csv",
+    "read_dataset_csv", "save_model", "write_dataset_csv", "continuous_adjoint_solve",
 ]

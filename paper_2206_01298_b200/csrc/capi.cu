@@ -45,6 +45,8 @@ cudaError_t launch_conv_field(const RkParams<T>&, int, size_t, int, double, cons
 template <typename T> cudaError_t launch_pack_conv(const PackParams<T>&, cudaStream_t);
 template <typename T, bool WS>
 cudaError_t launch_adaptive_ws(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
+template <typename T, bool WS>
+cudaError_t launch_cadj_ws(const RkParams<T>&, int, int, size_t, double, const T*, cudaStream_t);
 template <typename T>
 cudaError_t launch_reduce_plain(const T*, int, long long, long long, T*, cudaStream_t);
 
@@ -62,6 +64,13 @@ cudaError_t launch_adaptive(const RkParams<T>& p, int lr, int tiles, size_t smem
   if constexpr (sizeof(T) == 4)
     if (p.sm.wts >= 0) return launch_adaptive_ws<T, true>(p, lr, tiles, smem, st, forward);
   return launch_adaptive_ws<T, false>(p, lr, tiles, smem, st, forward);
+}
+template <typename T>
+cudaError_t launch_cadj(const RkParams<T>& p, int lr, int tiles, size_t smem, double tF, const T* dphi,
+                        cudaStream_t st) {
+  if constexpr (sizeof(T) == 4)
+    if (p.sm.wts >= 0) return launch_cadj_ws<T, true>(p, lr, tiles, smem, tF, dphi, st);
+  return launch_cadj_ws<T, false>(p, lr, tiles, smem, tF, dphi, st);
 }
 template <typename T>
 cudaError_t launch_field_op(const RkParams<T>& p, int lr, int tiles, size_t smem, int mode,
@@ -710,7 +719,8 @@ int plan_problem(const ob_problem& p, Plan& P) {
 }
 
 template <typename T>
-int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st) {
+int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
+             const void* cadj_dphi = nullptr) {
   char* ws = static_cast<char*>(b.workspace);
   const int nt = P.adaptive ? P.nseg : p.n_steps, s = p.scheme.stages;
   // ---- control blob: ts (adaptive: interval ends) | fwd_rec | fwd_sol | prog | status | obs
@@ -844,9 +854,14 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st)
     }
     return launch_rk<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
   };
-  CU(sweep(true));
-  CU(cudaEventRecord(ev[2], st));
-  CU(sweep(false));
+  if (cadj_dphi) {   // continuous-adjoint baseline: one augmented reverse-time sweep
+    CU(launch_cadj<T>(rp, P.LR, P.tiles, P.smem_bytes, p.tF, static_cast<const T*>(cadj_dphi), st));
+    CU(cudaEventRecord(ev[2], st));
+  } else {
+    CU(sweep(true));
+    CU(cudaEventRecord(ev[2], st));
+    CU(sweep(false));
+  }
   CU(cudaEventRecord(ev[3], st));
   CU(launch_reduce<T>(P.d, rp.mu, P.tiles, p.field.n_params, static_cast<T*>(b.dtheta),
                       rp.loss_part, rp.inv_batch_global, b.loss, st));
@@ -977,6 +992,53 @@ extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* ou
                               "both or neither scaling bounds");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   st = P.dtype == OB_F32 ? run_grad<float>(*p, *b, P, s) : run_grad<double>(*p, *b, P, s);
+  if (out) *out = P.cnt;
+  return st;
+}
+
+// Continuous-adjoint baseline (continuous_adjoint_solve, adjoint.py:314-331):
+// lambda(t0) and the integral of P^T lambda from the terminal state u(tF) and
+// seed dphi/du, integrating the augmented reverse-time system with the
+// problem's explicit scheme over p->times (the tau grid, 0 .. tF - t0).
+extern "C" int ob_continuous_adjoint(const ob_problem* p, const void* theta, const void* aux,
+                                     const void* u_final, const void* dphi_du, void* lam0,
+                                     void* mu0, void* workspace, size_t workspace_bytes,
+                                     ob_counters* out, void* stream) {
+  if (!p || !theta || !u_final || !dphi_du || !lam0 || !mu0) return fail(OB_ERR_VALUE, "null argument");
+  if (p->scheme.kind != OB_SCHEME_RK)
+    return fail(OB_ERR_VALUE, "the continuous-adjoint baseline supports explicit schemes");
+  if (p->field.kind != OB_FIELD_MLP && p->field.kind != OB_FIELD_STIFF)
+    return fail(OB_ERR_UNSUPPORTED, "the continuous-adjoint baseline is built for MLP / stiff fields");
+  if (p->field.kind == OB_FIELD_STIFF && !aux) return fail(OB_ERR_VALUE, "stiff field needs diag");
+  ob_problem q = *p;
+  q.policy = OB_POLICY_STORE_SOLUTIONS;
+  q.loss = OB_LOSS_HALF_SQNORM;
+  q.n_obs = 0;
+  q.adaptive = 0;
+  Plan P;
+  int st = plan_problem(q, P);
+  if (st) return st;
+  if (!workspace || workspace_bytes < P.total)
+    return fail(OB_ERR_VALUE, "workspace too small (need " + std::to_string(P.total) + " bytes)");
+  ob_buffers b{};
+  b.theta = theta;
+  b.aux = aux;
+  b.u0 = u_final;
+  b.u_final = const_cast<void*>(u_final);
+  b.du0 = lam0;
+  b.dtheta = mu0;
+  b.loss = nullptr;
+  b.workspace = workspace;
+  b.workspace_bytes = workspace_bytes;
+  const long long s = q.scheme.stages, n = q.n_steps;
+  P.cnt = ob_counters{};
+  P.cnt.nfe_forward = P.cnt.nfe_backward = s * n - (q.scheme.fsal ? n - 1 : 0);
+  P.cnt.steps_accepted = n;
+  P.cnt.tile_rows = P.R;
+  P.cnt.tiles = P.tiles;
+  P.cnt.kernel_launches = 3;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  st = P.dtype == OB_F32 ? run_grad<float>(q, b, P, cs, dphi_du) : run_grad<double>(q, b, P, cs, dphi_du);
   if (out) *out = P.cnt;
   return st;
 }

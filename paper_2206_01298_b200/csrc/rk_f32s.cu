@@ -8,4 +8,6 @@ template cudaError_t launch_rk_ws<float, true>(const RkParams<float>&, int, int,
 template cudaError_t launch_field_ws<float, true>(const RkParams<float>&, int, int, size_t, int,
                                                   double, const float*, const float*, float*,
                                                   cudaStream_t);
+template cudaError_t launch_cadj_ws<float, true>(const RkParams<float>&, int, int, size_t, double,
+                                                   const float*, cudaStream_t);
 }  // namespace ob

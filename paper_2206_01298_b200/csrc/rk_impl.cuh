@@ -618,6 +618,101 @@ field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const
   store_rows(out, N, res, ldn, row0, Rv);
 }
 
+// ------------------------------------------------------ continuous adjoint
+// Vanilla continuous-adjoint baseline (continuous_adjoint_solve, adjoint.py:294-331):
+// the augmented reverse-time system y = (u, lambda, mu), dy/dtau = (-f, J^T lam,
+// P^T lam) at t = tF - tau, integrated with the same explicit tableau and FSAL
+// carry on the fixed tau grid p.ts.  mu never feeds back into the derivatives,
+// so its stage derivatives go straight into the CTA's mu slot scaled by h b_i;
+// with FSAL the reused stage's contribution is added when it is computed, with
+// the next step's h b_0 folded into its scale.
+template <typename T, class F>
+__global__ void __launch_bounds__(kThreads, 1) cadj_kernel(const __grid_constant__ RkParams<T> p, double tF,
+                                                           const T* dphi) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  zero_smem(sm, p.sm.wts >= 0 ? p.sm.wts : p.sm.total);
+  const int tile = blockIdx.x;
+  const int row0 = tile * p.R;
+  const int Rv = min(p.R, p.B - row0);
+  MlpSmem<T> ms;
+  Weights<T> W;
+  setup_tile(p, sm, ms, W);
+  F f(p, W, ms, sm, row0, Rv);
+  // no split-K scratch here: the stage cotangent lives in the lamn slot
+
+  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, nin = f.nin();
+  const long long kst = (long long)Rt * ldn;
+  T* u = state_buf(p, sm, 0);
+  T* lam = state_buf(p, sm, 1);
+  T* li = state_buf(p, sm, 2);     // stage lambda (the VJP cotangent)
+  T* jtv = state_buf(p, sm, 4);
+  T* kU = p.scratch + tile * p.scratch_stride;
+  T* kL = kU + s * kst;
+  T* mu = p.mu + tile * p.d.n_mu;
+  load_rows(u, ldn, p.u_final, N, row0, Rv);
+  load_rows(lam, ldn, dphi, N, row0, Rv);
+  __syncthreads();
+  for (int n = 0; n < p.n_steps; ++n) {
+    const double tau = p.ts[n], h = p.ts[n + 1] - p.ts[n];
+    const bool has_next = n + 1 < p.n_steps;
+    const double hn = has_next ? p.ts[n + 2] - p.ts[n + 1] : 0.0;
+    for (int i = 0; i < s; ++i) {
+      if (i == 0 && p.fsal && n > 0) {   // k_first = k_last (integrators.py:210-211)
+        for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) {
+          kU[idx] = kU[(s - 1) * kst + idx];
+          kL[idx] = kL[(s - 1) * kst + idx];
+        }
+        __syncthreads();
+        continue;
+      }
+      for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
+        const int r = idx / N, j = idx % N, o = r * ldn + j;
+        T vu = u[o], vl = lam[o];
+        for (int q = 0; q < i; ++q) {
+          const double aiq = p.a[i * OB_MAX_STAGES + q];
+          if (aiq != 0.0) {
+            vu = Num<T>::add(vu, Num<T>::mul(T(h * aiq), kU[q * kst + o]));
+            vl = Num<T>::add(vl, Num<T>::mul(T(h * aiq), kL[q * kst + o]));
+          }
+        }
+        if (j < nin) f.put(r, j, vu);
+        li[o] = r < Rv ? vl : T(0);
+      }
+      f.put_time(tF - (tau + p.c[i] * h));
+      __syncthreads();
+      f.eval(kU + i * kst);                 // f(U_i); negated below
+      double sc = h * p.b[i];
+      if (i == s - 1 && p.fsal && has_next) sc += hn * p.b[0];
+      f.vjp(li, jtv, sc != 0.0 ? mu : nullptr, sc, Rv);
+      for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
+        const int o = (idx / N) * ldn + idx % N;
+        kU[i * kst + o] = -kU[i * kst + o];
+        kL[i * kst + o] = jtv[o];
+      }
+      __syncthreads();
+    }
+    int bad = 0;
+    for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
+      const int r = idx / N, o = r * ldn + idx % N;
+      T vu = u[o], vl = lam[o];
+      for (int i = 0; i < s; ++i)
+        if (p.b[i] != 0.0) {
+          vu = Num<T>::add(vu, Num<T>::mul(T(h * p.b[i]), kU[i * kst + o]));
+          vl = Num<T>::add(vl, Num<T>::mul(T(h * p.b[i]), kL[i * kst + o]));
+        }
+      u[o] = vu;
+      lam[o] = vl;
+      if (r < Rv && !(Num<T>::finite(vu) && Num<T>::finite(vl))) bad = 1;
+    }
+    if (__syncthreads_or(bad)) {   // explicit_rk_step overflow (integrators.py:219-220)
+      if (threadIdx.x == 0) set_status(p.status, OB_ERR_INTEGRATION, n);
+      return;
+    }
+  }
+  store_rows(p.du0, N, lam, ldn, row0, Rv);
+}
+
 // --------------------------------------------------------------- helpers
 // packed W_l: [nrow_l][ldw_l] row-major copy of theta's W_l, zero padded
 template <typename T>
@@ -701,6 +796,19 @@ cudaError_t launch_rk_ws(const RkParams<T>& p, int lr, int tiles, size_t smem, c
     case 2: return launch_rk_lr<T, 2, WS>(p, tiles, smem, st, forward);
     default:
       if constexpr (sizeof(T) == 4) return launch_rk_lr<T, 8, WS>(p, tiles, smem, st, forward);
+      return cudaErrorInvalidConfiguration;
+  }
+}
+
+template <typename T, bool WS>
+cudaError_t launch_cadj_ws(const RkParams<T>& p, int lr, int tiles, size_t smem, double tF,
+                           const T* dphi, cudaStream_t st) {
+  switch (lr) {
+    case 1: return launch_smem(cadj_kernel<T, MlpAdapter<T, 1, WS>>, tiles, smem, st, p, tF, dphi);
+    case 2: return launch_smem(cadj_kernel<T, MlpAdapter<T, 2, WS>>, tiles, smem, st, p, tF, dphi);
+    default:
+      if constexpr (sizeof(T) == 4)
+        return launch_smem(cadj_kernel<T, MlpAdapter<T, 8, WS>>, tiles, smem, st, p, tF, dphi);
       return cudaErrorInvalidConfiguration;
   }
 }

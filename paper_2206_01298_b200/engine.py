@@ -240,3 +240,44 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     return GradResult(dtheta=dtheta_o, du0=du0_o, loss=loss_v, counters=counters,
                       predictions=predictions, u_final=uf_o, store_counters=sc, device=c,
                       sample_counters=samp, dtheta_head=dhead, grids=grids)
+
+
+def continuous_adjoint_solve(field: Field, scheme: Scheme, dphi_du, u_final, t0, tF, n_steps,
+                             counters=None):
+    """Vanilla continuous-adjoint baseline (adjoint.py:314-331): integrate
+    du/dtau = -f, dlam/dtau = J^T lam, dmu/dtau = P^T lam backward from
+    (u_final, dphi_du) with the same explicit scheme on n_steps fixed steps.
+    Batched: returns (lam0 [B, N], mu0 = sum over samples, counters)."""
+    if scheme.kind != "rk":
+        raise ValueError("the continuous-adjoint baseline supports explicit schemes")
+    counters = counters if counters is not None else NfeCounters()
+    dt = field.torch_dtype
+    host_io = not (isinstance(u_final, torch.Tensor) and u_final.is_cuda)
+    uf = to_device(u_final, dt)
+    lamT = to_device(dphi_du, dt)
+    if uf.dim() == 1:
+        uf, lamT = uf.unsqueeze(0), lamT.unsqueeze(0)
+    B, N = uf.shape
+    if N != field.n or tuple(lamT.shape) != (B, N):
+        raise ValueError(f"expected [B, {field.n}] terminal state and seed")
+    ts = np.linspace(0.0, tF - t0, int(n_steps) + 1)
+    prob, _times = build_problem(field, scheme, LossSpec("half_sqnorm", (tF,)), B, ts,
+                                 CheckpointPolicy("store_solutions"), SolverConfig(), B)
+    prob.tF = float(tF)
+    ws = _workspace(workspace_size(prob), uf.device)
+    lam0 = torch.empty_like(uf)
+    mu0 = torch.empty(field.n_params, dtype=dt, device=uf.device)
+    aux = field.aux()
+    cnt = _lib.Counters()
+    rc = _lib.load().ob_continuous_adjoint(
+        C.byref(prob), field.theta_tensor().data_ptr(), aux.data_ptr() if aux is not None else None,
+        uf.data_ptr(), lamT.data_ptr(), lam0.data_ptr(), mu0.data_ptr(), ws.data_ptr(), ws.numel(),
+        C.byref(cnt), stream_ptr())
+    raise_status(rc, _lib.last_error())
+    c = cnt.as_dict()
+    counters.nfe_forward += c["nfe_forward"]
+    counters.nfe_backward += c["nfe_backward"]
+    counters.steps_accepted += c["steps_accepted"]
+    if host_io:
+        return lam0.cpu().numpy(), mu0.cpu().numpy(), counters
+    return lam0, mu0, counters

@@ -362,3 +362,16 @@ def test_dataset_formats_roundtrip(tmp_path, golden):
     assert np.allclose(nd.matrix().min(axis=0), 0.0) and np.allclose(nd.matrix().max(axis=0), 1.0)
     with pytest.raises(ValueError):
         Dataset([0.0, 0.0], [np.zeros(2), np.zeros(2)])
+
+
+@pytest.mark.parametrize("sch", ["euler", "rk4", "dopri5"])
+def test_continuous_adjoint_matches_reference(golden, sch):
+    from oracle import cadj
+    g = golden("cadj.npz")
+    n_steps, tin = (int(x) for x in g[f"{sch}/meta"])
+    mlp = oc.Mlp((3 + tin, 8, 8, 3), "tanh", g[f"{sch}/theta"], time_input=bool(tin))
+    uf = g[f"{sch}/u_final"]
+    lam0, mu0 = cadj.continuous_adjoint_solve(oc.MlpField(mlp), sch, uf / uf.shape[0], uf, 0.0, 1.0,
+                                              n_steps)
+    assert oc.rel_error(lam0, g[f"{sch}/lam0"]) <= 1e-12
+    assert oc.rel_error(mu0, g[f"{sch}/mu0"]) <= 1e-12

@@ -325,6 +325,39 @@ def gen_training():
     save("training.npz", **out)
 
 
+def gen_cadj():
+    """Continuous-adjoint baseline (adjoint.py:294-331) per sample: terminal state
+    from the reference integrate, seed u(tF)/B; batch mu = sum over samples."""
+    out = {}
+    rng = np.random.default_rng(1234)
+    B = 3
+    for sch, n_steps, tin in (("euler", 12, False), ("rk4", 6, True), ("dopri5", 5, True)):
+        model = og.init_model(og.mlp_spec(3, 8, 2, "tanh", time_input=tin), seed=21)
+        U0 = rng.uniform(-1, 1, (B, 3))
+        fld = og.MlpField(model)
+        scheme = og.tableau_catalog(sch)
+        lam0, mu0, uf, nff, nfb = [], np.zeros(model.n_params), [], [], []
+        for b in range(B):
+            u1, _ = og.integrators.integrate(scheme, fld, U0[b], 0.0, 1.0, og.FixedController(n_steps))
+            c = og.NfeCounters()
+            lam, mu, _ = og.adjoint.continuous_adjoint_solve(fld, scheme, u1 / B, u1, 0.0, 1.0,
+                                                             n_steps, counters=c)
+            lam0.append(lam)
+            mu0 = mu0 + mu
+            uf.append(u1)
+            nff.append(c.nfe_forward)
+            nfb.append(c.nfe_backward)
+        pre = f"{sch}/"
+        out[pre + "theta"] = model.theta
+        out[pre + "u0"] = U0
+        out[pre + "u_final"] = np.array(uf)
+        out[pre + "lam0"] = np.array(lam0)
+        out[pre + "mu0"] = mu0
+        out[pre + "meta"] = np.array([n_steps, int(tin)])
+        out[pre + "nfe"] = np.array([nff, nfb])
+    save("cadj.npz", **out)
+
+
 def gen_revolve():
     out = {}
     counts = np.zeros((61, 21), np.int64)
@@ -361,12 +394,16 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "training":
         gen_training()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "cadj":
+        gen_cadj()
+        sys.exit(0)
     gen_revolve()
     gen_kernels()
     gen_small()
     gen_obs()
     gen_adaptive()
     gen_training()
+    gen_cadj()
     gen_config("C1", 4, ["store_all", "store_solutions", "revolve:3"])
     gen_config("C2", 3, ["store_all", "revolve:8"])
     gen_config("C5", 2, ["store_all"], solver=configs.make_c5(batch=1).extras["solver"])
