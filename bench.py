@@ -249,6 +249,17 @@ def fp_peak(dtype):
         return nominal, "nominal 148 SM x FMA lanes x 2 x 1.965 GHz"
 
 
+def bf16_peak():
+    """Driver-measured dense bf16 tensor throughput (MEASURED_PEAKS.json): the
+    sustained figure, since the dominant kernel runs inside a multi-ms step."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["bf16_tflops_sustained"]), "MEASURED_PEAKS.json bf16_tflops_sustained"
+    except (OSError, KeyError, ValueError):
+        return 2250.0, "nominal B200 dense bf16 (2.25 PFLOP/s)"
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -372,6 +383,25 @@ def main():
     dms, dfl = kern[dom]
     peak, peak_src = fp_peak(ci.dtype)
     achieved = dfl / (dms / 1e3) / 1e12
+    pipe, bound, tc_extra = f"{ci.dtype} FMA (SIMT)", "compute", {}
+    if dev.get("tensor_cores"):
+        # tcgen05 kind::f16 tile: each fp32 product is 3 bf16 MMAs (hi*hi + hi*lo + lo*hi),
+        # so the fp32-equivalent ceiling is the measured dense bf16 peak / 3; the executed
+        # tensor-pipe FLOPs (split passes and the 32-column sample padding included) are
+        # reported beside it
+        bf16, bf16_src = bf16_peak()
+        peak, peak_src = bf16 / 3.0, f"{bf16_src} / 3 (3-pass bf16 split)"
+        pipe, bound = "tcgen05 kind::f16 (bf16 3-pass split, fp32 accumulate in TMEM)", "tensor"
+        D0, H = ci.widths[-1], ci.widths[1]
+        nmb, t = H // 128, dev["tiles"]
+        ev = 2 * 3 * (128 * 32 * D0 * nmb + 64 * 32 * H)                    # one f-eval
+        vj = 2 * 3 * (4 * 128 * 32 * D0 * nmb + 64 * 32 * H)   # z, dW2^T, dH, dW1 + dX
+        dev_fwd = t * (dev["device_rhs_evals"] - replays * s) * ev
+        dev_rev = t * (replays * s * ev + dev["device_vjp_evals"] * vj)
+        ex = dev_rev if dom == "reverse" else dev_fwd
+        tc_extra = {"tensor_pipe_flops_per_launch": ex,
+                    "tensor_pipe_tflops": ex / (dms / 1e3) / 1e12,
+                    "tensor_pipe_frac": ex / (dms / 1e3) / 1e12 / bf16}
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
@@ -403,11 +433,12 @@ def main():
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "roofline": {"bound": "compute", "pipe": f"{ci.dtype} FMA (SIMT)", "kernel": dom,
+            "roofline": {"bound": bound, "pipe": pipe, "kernel": dom,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_flops_per_launch": dfl, "ms_per_launch": dms,
-                         "phase_ms_per_step": {k: v / K for k, v in phases.items()}},
+                         "phase_ms_per_step": {k: v / K for k, v in phases.items()},
+                         **tc_extra},
             "cpu_baseline": cpu,
             "clocks": clocks,
             "counters": {k: dev[k] for k in ("nfe_forward", "nfe_backward", "steps_recomputed",

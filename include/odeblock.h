@@ -132,7 +132,9 @@ typedef struct {
 
 /* flags: accumulate per-phase SM cycles of the persistent kernels (profiling aid;
    read with ob_debug_phase_cycles) */
-enum { OB_FLAG_PHASE_TIMING = 1 };
+enum { OB_FLAG_PHASE_TIMING = 1,
+       /* force the SIMT (FMA) MLP tile even where the tcgen05 tensor-core tile applies */
+       OB_FLAG_NO_TENSOR_CORES = 2 };
 #define OB_NPHASES 16
 
 /* Device buffers of one gradient call. */
@@ -179,6 +181,7 @@ typedef struct {
   int64_t device_vjp_evals;      /* VJP pairs the device executed (zero cotangents skipped) */
   int64_t tile_rows;             /* samples per CTA tile                                 */
   int64_t tiles;                 /* CTAs per persistent launch                           */
+  int64_t tensor_cores;          /* 1: the MLP contractions ran on tcgen05 (3-pass bf16 split) */
   double ms_pack, ms_forward, ms_reverse, ms_reduce;  /* CUDA-event device times of this call */
 } ob_counters;
 

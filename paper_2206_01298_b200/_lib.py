@@ -86,7 +86,8 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "nfe_forward", "nfe_backward", "steps_accepted", "steps_rejected", "steps_recomputed",
         "stored_states", "stored_stage_vectors", "max_live_slots", "recomputed_steps",
-        "kernel_launches", "device_rhs_evals", "device_vjp_evals", "tile_rows", "tiles")] + [
+        "kernel_launches", "device_rhs_evals", "device_vjp_evals", "tile_rows", "tiles",
+        "tensor_cores")] + [
         (n, C.c_double) for n in ("ms_pack", "ms_forward", "ms_reverse", "ms_reduce")]
 
     def as_dict(self):

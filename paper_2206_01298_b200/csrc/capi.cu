@@ -49,6 +49,12 @@ template <typename T, bool WS>
 cudaError_t launch_cadj_ws(const RkParams<T>&, int, int, size_t, double, const T*, cudaStream_t);
 template <typename T>
 cudaError_t launch_reduce_plain(const T*, int, long long, long long, T*, cudaStream_t);
+// tcgen05 tensor-core MLP tile (rk_tc.cu)
+void tc_sizes(int D0, int H, int D2, unsigned* packed_bytes, unsigned* total_bytes);
+bool tc_shape_supported(int D0, int H, int D2);
+cudaError_t launch_pack_tc(const Dims& d, const float* theta, float* packed, cudaStream_t st);
+cudaError_t launch_rk_tc(const RkParams<float>& p, int tiles, size_t smem, cudaStream_t st,
+                         bool forward);
 
 // dispatch on where the weights live (fp32 only stages them in shared memory)
 template <typename T>
@@ -172,6 +178,7 @@ struct Plan {
   int R = 1, Rt = 4, LR = 1, tiles = 1;
   bool need_jvp = false;
   bool theta = false;
+  bool tc = false;                // tcgen05 tensor-core MLP tile (rk_tc.cu)
   int gmres_m = 0;
   size_t off_kry = 0, off_stats = 0, off_cnf = 0, off_state = 0, off_head = 0;
   long long cnf_stride = 0;
@@ -410,6 +417,55 @@ void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   P.tiles = (int)((B + P.R - 1) / P.R);
 }
 
+// Tensor-core tile: fp32 two-layer MLP field on an explicit fixed-step scheme.
+// Tiles of <= 32 samples (the MMA N), generic state buffers then the tcgen05
+// region (staged weights + operand tiles) in shared memory.
+bool tc_eligible(const ob_problem& p, const Plan& P) {
+  const ob_field_desc& f = p.field;
+  if (P.esz != 4 || P.theta || P.adaptive || f.kind != OB_FIELD_MLP || f.n_layers != 2) return false;
+  // smooth activations only: ReLU' jumps at 0 and the ~2^-16 split-product error moves
+  // pre-activations across it (measured 3.7e-4 on du0), so ReLU keeps the fp32 SIMT tile
+  if (f.activation != OB_ACT_TANH && f.activation != OB_ACT_IDENTITY) return false;
+  if ((p.flags & OB_FLAG_NO_TENSOR_CORES) || getenv("OB_NO_TC")) return false;
+  const int N = f.widths[2];
+  return tc_shape_supported(N, f.widths[1], N);
+}
+
+bool plan_tc(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
+  Plan Q = P;
+  int R = (int)std::max<long long>(1, (B + sm_count - 1) / sm_count);
+  if (const char* e = getenv("OB_TILE_ROWS")) R = std::max(1, atoi(e));
+  R = std::min(R, 32);
+  Q.R = Q.Rt = R;
+  Q.LR = 8;
+  make_dims(f, Q.LR, Q.d);
+  unsigned packed = 0, total = 0;
+  tc_sizes(Q.d.N, f.widths[1], Q.d.N, &packed, &total);
+  Q.d.n_packed = packed / 4;
+  for (int l = 0; l < OB_MAX_LAYERS; ++l) Q.d.pwoff[l] = 0;
+  SmemLayout& s = Q.sm;
+  s = SmemLayout{};
+  int o = 0;
+  auto take = [&](long long n) { int r = o; o += (int)((n + 7) & ~7LL); return r; };
+  s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = -1;
+  for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
+  for (int i = 0; i < 8; ++i) s.vec[i] = -1;
+  s.scr_elems = 0;
+  s.u = take((long long)Q.Rt * Q.d.ldn);
+  s.lam = take((long long)Q.Rt * Q.d.ldn);
+  s.lamn = take((long long)Q.Rt * Q.d.ldn);
+  s.w = take((long long)Q.Rt * Q.d.ldn);
+  s.jtv = take((long long)Q.Rt * Q.d.ldn);
+  s.wts = take(total / 4);
+  s.total = o;
+  Q.smem_bytes = (size_t)o * 4;
+  if (Q.smem_bytes > smem_cap(Q)) return false;
+  Q.tiles = (int)((B + R - 1) / R);
+  Q.tc = true;
+  P = Q;
+  return true;
+}
+
 // compile the checkpoint policy into forward store directives + a reverse
 // program (checkpointing.py:242-340), with reference-semantics counters.
 int compile_policy(const ob_problem& p, Plan& P) {
@@ -517,7 +573,7 @@ int compile_policy(const ob_problem& p, Plan& P) {
   return OB_OK;
 }
 
-int plan_problem(const ob_problem& p, Plan& P) {
+int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   int st = check_field(p.field);
   if (st) return st;
   P.theta = (p.scheme.kind == OB_SCHEME_THETA);
@@ -622,6 +678,7 @@ int plan_problem(const ob_problem& p, Plan& P) {
   P.gmres_m = P.theta ? std::min(p.solver.gmres_restart, p.field.widths[p.field.n_layers]) : 0;
   P.smem_reserve = P.adaptive ? kAdaptiveStaticSmem : 0;
   choose_tiles(P, p.field, p.batch, sms);
+  if (allow_tc && tc_eligible(p, P)) plan_tc(P, p.field, p.batch, sms);
   if (P.smem_bytes > smem_cap(P)) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   if (P.adaptive) {
     P.prog.clear();
@@ -662,6 +719,7 @@ int plan_problem(const ob_problem& p, Plan& P) {
   if (P.adaptive) c = ob_counters{};   // per-sample grids: filled after the run
   c.tile_rows = P.R;
   c.tiles = P.tiles;
+  c.tensor_cores = P.tc ? 1 : 0;
   c.kernel_launches = 4;
   // workspace
   const long long B = p.batch, N = P.d.N;
@@ -838,6 +896,10 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
   CU(cudaEventRecord(ev[0], st));
   if (P.d.conv) {
     if constexpr (sizeof(T) == 4) CU(launch_pack_conv<T>(pp, st));
+  } else if (P.tc) {
+    if constexpr (sizeof(T) == 4)
+      CU(launch_pack_tc(P.d, reinterpret_cast<const float*>(pp.theta),
+                        reinterpret_cast<float*>(pp.packed), st));
   } else {
     CU(launch_pack<T>(pp, st));
   }
@@ -845,6 +907,12 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
   auto sweep = [&](bool fwd) -> cudaError_t {
     if (P.adaptive) return launch_adaptive<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
     if (P.theta) return launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
+    if (P.tc) {
+      if constexpr (sizeof(T) == 4)
+        return launch_rk_tc(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.smem_bytes, st,
+                            fwd);
+      return cudaErrorNotSupported;
+    }
     if (P.d.cnf || P.d.conv) {
       if constexpr (sizeof(T) == 4) {
         if (P.d.conv) return launch_conv<T>(rp, P.tiles, P.smem_bytes, st, fwd);
@@ -966,7 +1034,7 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
 extern "C" int ob_grad_workspace_size(const ob_problem* p, size_t* bytes) {
   if (!p || !bytes) return fail(OB_ERR_VALUE, "null argument");
   Plan P;
-  int st = plan_problem(*p, P);
+  int st = plan_problem(*p, P, true);
   if (st) return st;
   *bytes = P.total;
   return OB_OK;
@@ -975,7 +1043,7 @@ extern "C" int ob_grad_workspace_size(const ob_problem* p, size_t* bytes) {
 extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream) {
   if (!p || !b) return fail(OB_ERR_VALUE, "null argument");
   Plan P;
-  int st = plan_problem(*p, P);
+  int st = plan_problem(*p, P, true);
   if (st) return st;
   if (!b->workspace || b->workspace_bytes < P.total)
     return fail(OB_ERR_VALUE, "workspace too small (need " + std::to_string(P.total) + " bytes)");

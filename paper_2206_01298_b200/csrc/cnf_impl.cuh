@@ -27,6 +27,9 @@ struct CnfAdapter {
   T* aux;                     // [2Rt][lda_L]
   int Rt, R2, D;
   static constexpr bool kHasJvp = false;
+  static constexpr bool kScaledVjp = false;  // vjp returns J^T w; the caller scales by h
+  OB_DEV void finish(T*) {}   // flush device-resident parameter cotangents (none here)
+  OB_DEV void release() {}    // free per-CTA hardware resources (none here)
 
   OB_DEV CnfAdapter(const RkParams<T>& p_, const Weights<T>& W, MlpSmem<T>& ms, T* sm, int row0,
                     int Rv)

@@ -23,6 +23,9 @@ struct ConvAdapter {
   T* xsave;    // global parking slot for A
   const T *W1f, *W2f, *W1b, *W2b, *b1, *b2;
   static constexpr bool kHasJvp = false;
+  static constexpr bool kScaledVjp = false;  // vjp returns J^T w; the caller scales by h
+  OB_DEV void finish(T*) {}   // flush device-resident parameter cotangents (none here)
+  OB_DEV void release() {}    // free per-CTA hardware resources (none here)
 
   OB_DEV ConvAdapter(const RkParams<T>& p_, const Weights<T>& W, MlpSmem<T>&, T* sm, int, int)
       : p(p_) {

@@ -82,6 +82,9 @@ struct MlpAdapter {
   }
   OB_DEV void set_scratch(T* s, int n) { mt.scratch = s; mt.scratch_elems = n; }
   static constexpr bool kHasJvp = true;
+  static constexpr bool kScaledVjp = false;  // vjp returns J^T w; the caller scales by h
+  OB_DEV void finish(T*) {}   // flush device-resident parameter cotangents (none here)
+  OB_DEV void release() {}    // free per-CTA hardware resources (none here)
 
   // (df/du) w at x0 (integrators.py:88-92)
   OB_DEV void jvp(const T* w, T* out) {
@@ -455,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
     if (!Num<T>::finite(u[(idx / N) * ldn + idx % N])) bad = 1;
   if (__syncthreads_or(bad)) {
     if (threadIdx.x == 0) set_status(p.status, OB_ERR_VALUE, -1);
+    f.release();
     return;
   }
   for (int n = 0; n < p.n_steps; ++n) {
@@ -470,9 +474,11 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
     pt.mark(kPhFwdStep);
     if (!ok) {  // integrators.py:219-220
       if (threadIdx.x == 0) set_status(p.status, OB_ERR_INTEGRATION, n);
+      f.release();
       return;
     }
   }
+  f.release();
   store_rows(p.u_final, N, u, ldn, row0, Rv);
   obs_capture(p, u, p.n_steps, row0, Rv);
   loss_partial(p, u, row0, Rv, tile);
@@ -558,10 +564,10 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       pt.mark(kPhElem);
       f.vjp(w, jtv, mu, h, Rv);
       pt.mark(kPhVjp);
-      // Lam_i = h * jtv; lam_n += Lam_i
+      // Lam_i = h * jtv; lam_n += Lam_i  (scaled-VJP adapters return J^T (h w) directly)
       for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
         const int o = (idx / N) * ldn + idx % N;
-        const T li = Num<T>::mul(T(h), jtv[o]);
+        const T li = F::kScaledVjp ? jtv[o] : Num<T>::mul(T(h), jtv[o]);
         Lam[i * kst + o] = li;
         lamn[o] = Num<T>::add(lamn[o], li);
       }
@@ -575,9 +581,12 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
     }
     if (__syncthreads_or(bad)) {  // AdjointState.check_finite (adjoint.py:42-44)
       if (threadIdx.x == 0) set_status(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
+      f.release();
       return;
     }
   }
+  f.finish(mu);
+  f.release();
   obs_inject(p, lam, 0, row0, Rv);
   store_rows(p.du0, N, lam, ldn, row0, Rv);
 }

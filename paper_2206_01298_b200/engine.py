@@ -84,15 +84,19 @@ def phase_cycles(reset=True):
     buf = (C.c_uint64 * 16)()
     raise_status(_lib.load().ob_debug_phase_cycles(buf, 16, int(reset)), _lib.last_error())
     names = ["elementwise", "recompute", "vjp", "lam_update", "replay", "fwd_step", "gmres_apply",
-             "gmres_scalar", "step_combine", "step_eval", "fwd_hidden", "fwd_out", "fwd_out_split",
-             "fwd_out_reduce", "gmres_input", "p15"]
+             "gmres_scalar", "step_combine", "step_eval", "fwd_hidden|tc_mma", "fwd_out|tc_epilogue",
+             "fwd_out_split", "fwd_out_reduce", "gmres_input|tc_prep", "p15"]
     return {n: int(buf[i]) for i, n in enumerate(names)}
 
 
 def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
          policy=CheckpointPolicy("store_all"), solver_cfg=None, counters=None, *,
-         batch_global=None, profile=False) -> GradResult:
-    """Loss, dL/dtheta and dL/du0 by forward solve + discrete adjoint sweep."""
+         batch_global=None, profile=False, tensor_cores=True) -> GradResult:
+    """Loss, dL/dtheta and dL/du0 by forward solve + discrete adjoint sweep.
+
+    ``tensor_cores=False`` forces the SIMT (FMA) MLP tile where the tcgen05
+    tile would apply (fp32 two-layer MLP fields on explicit fixed-step schemes).
+    """
     solver_cfg = solver_cfg or SolverConfig()
     counters = counters if counters is not None else NfeCounters()
     if loss.times[-1] > tF + 1e-9 * max(1.0, abs(tF)):
@@ -123,7 +127,7 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
         raise ValueError(f"expected length {field.n}, got {N}")
     bg = int(batch_global) if batch_global is not None else B
     prob, _times = build_problem(field, scheme, loss, B, ts, policy, solver_cfg, bg)
-    prob.flags = 1 if profile else 0
+    prob.flags = (1 if profile else 0) | (0 if tensor_cores else 2)
     if adaptive:
         prob.adaptive = 1
         prob.n_steps = 0

@@ -1,0 +1,135 @@
+"""GPU parity of the tcgen05 tensor-core MLP tile (csrc/tc_mlp.cuh).
+
+fp32 two-layer MLP fields on explicit fixed-step schemes run their
+contractions on the 5th-gen tensor cores as a 3-pass bf16 split (A_hi B_hi +
+A_hi B_lo + A_lo B_hi, fp32 accumulation in TMEM).  The bar is the fp32 one of
+north_star: rel_error <= 1e-4 (inf-norm relative, adjoint.py:368-373) against
+the fp64 oracle fed the same fp32-rounded inputs, for every shape, activation,
+scheme and checkpoint policy the tile accepts, with ragged and single-sample
+batches; the SIMT tile (tensor_cores=False) is held to the same bar, and
+shapes the tile does not take must fall back to the SIMT tile.  ReLU stays on
+the SIMT tile: its derivative jumps at 0, and the split products move
+pre-activations near 0 across the jump often enough to cost ~4e-4 on du0.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import core as oc
+from paper_2206_01298_b200 import (CheckpointPolicy, FixedController, MlpField, MlpModel, MlpSpec,
+                                   grad, tableau_catalog, terminal_loss)
+from paper_2206_01298_b200.configs import make_config
+from paper_2206_01298_b200.workloads import field_from_config, run_config
+
+pytestmark = pytest.mark.gpu
+TOL32 = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2206_01298_b200 import _lib as L
+    L.load()
+
+
+def np_(x):
+    return x.detach().cpu().numpy().astype(np.float64) if isinstance(x, torch.Tensor) else x
+
+
+def f32(x):
+    return np.asarray(x, np.float32).astype(np.float64)
+
+
+def make_mlp(rng, n, hidden, act, time_input):
+    widths = (n + int(time_input), hidden, n)
+    parts = []
+    for l in range(2):
+        b = np.sqrt(6.0 / (widths[l] + widths[l + 1]))
+        parts += [rng.uniform(-b, b, widths[l + 1] * widths[l]), rng.normal(0, 0.1, widths[l + 1])]
+    return widths, f32(np.concatenate(parts))
+
+
+def run_both(widths, act, time_input, theta, u0, scheme, n_steps, policy, tc=True):
+    model = MlpModel(MlpSpec(widths, act, time_input=time_input, dtype="f32"), theta)
+    fld = MlpField(model)
+    res = grad(fld, tableau_catalog(scheme), terminal_loss("half_sqnorm", 1.0),
+               torch.as_tensor(u0, dtype=torch.float32, device="cuda"), 0.0, 1.0,
+               FixedController(n_steps), CheckpointPolicy.parse(policy), tensor_cores=tc)
+    ref = oc.grad_terminal(oc.MlpField(oc.Mlp(widths, act, theta, time_input)), scheme, u0, 0.0, 1.0,
+                           n_steps, policy)
+    return res, ref
+
+
+def errs(res, ref):
+    e = {k: oc.rel_error(np_(getattr(res, k)), ref[k]) for k in ("u_final", "du0", "dtheta")}
+    e["loss"] = abs(res.loss - ref["loss"]) / abs(ref["loss"])
+    return e
+
+
+def test_c2_full_batch_on_tensor_cores_matches_oracle_and_simt():
+    ci = make_config("C2")
+    fld = field_from_config(ci)
+    u0 = torch.as_tensor(ci.u0, dtype=torch.float32, device="cuda")
+    tc = run_config(ci, "revolve:8", field=fld, u0=u0)
+    simt = run_config(ci, "revolve:8", field=fld, u0=u0, tensor_cores=False)
+    assert tc.device["tensor_cores"] == 1 and simt.device["tensor_cores"] == 0
+    mlp = oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input)
+    ref = oc.grad_terminal(oc.MlpField(mlp), ci.scheme, ci.u0, ci.t0, ci.tF, ci.n_steps, "store_all")
+    e_tc, e_simt = errs(tc, ref), errs(simt, ref)
+    assert max(e_tc.values()) <= TOL32, e_tc
+    assert max(e_simt.values()) <= TOL32, e_simt
+    assert tc.counters.nfe_forward == 241 + 31 * 7 and tc.counters.nfe_backward == 280
+
+
+def test_c2_policies_bit_identical_on_tensor_cores():
+    ci = make_config("C2", batch=600)
+    fld = field_from_config(ci)
+    u0 = torch.as_tensor(ci.u0, dtype=torch.float32, device="cuda")
+    runs = [run_config(ci, pol, field=fld, u0=u0) for pol in ("revolve:8", "store_all",
+                                                               "store_solutions", "revolve:8")]
+    for r in runs[1:]:
+        assert r.device["tensor_cores"] == 1
+        assert torch.equal(r.dtheta, runs[0].dtheta)
+        assert torch.equal(r.du0, runs[0].du0)
+        assert r.loss == runs[0].loss
+
+
+@pytest.mark.parametrize("n,hidden,act,time_input", [
+    (64, 256, "tanh", True), (64, 128, "tanh", False), (32, 256, "tanh", True),
+    (16, 128, "identity", True), (48, 256, "tanh", False)])
+@pytest.mark.parametrize("batch", [1, 37, 333])
+def test_shapes_activations_ragged_batches(n, hidden, act, time_input, batch):
+    rng = np.random.default_rng(1000 + n + hidden + batch)
+    widths, theta = make_mlp(rng, n, hidden, act, time_input)
+    u0 = f32(rng.normal(size=(batch, n)))
+    res, ref = run_both(widths, act, time_input, theta, u0, "dopri5", 6, "store_all")
+    assert res.device["tensor_cores"] == 1
+    e = errs(res, ref)
+    assert max(e.values()) <= TOL32, e
+
+
+@pytest.mark.parametrize("scheme", ["euler", "midpoint", "bosh3", "rk4", "dopri5"])
+@pytest.mark.parametrize("policy", ["store_all", "store_solutions", "revolve:3"])
+def test_schemes_and_policies_on_tensor_cores(scheme, policy):
+    rng = np.random.default_rng(7)
+    widths, theta = make_mlp(rng, 64, 256, "tanh", True)
+    u0 = f32(rng.normal(size=(300, 64)))
+    res, ref = run_both(widths, "tanh", True, theta, u0, scheme, 9, policy)
+    assert res.device["tensor_cores"] == 1
+    e = errs(res, ref)
+    assert max(e.values()) <= TOL32, e
+    assert res.counters.nfe_forward == ref["counters"].nfe_forward
+    assert res.counters.nfe_backward == ref["counters"].nfe_backward
+
+
+def test_ineligible_shapes_fall_back_to_simt():
+    rng = np.random.default_rng(3)
+    for n, hidden, act in ((64, 256, "gelu"), (64, 256, "relu"), (64, 200, "tanh"), (100, 256, "tanh")):
+        widths, theta = make_mlp(rng, n, hidden, act, True)
+        u0 = f32(rng.normal(size=(40, n)))
+        res, ref = run_both(widths, act, True, theta, u0, "rk4", 4, "store_all")
+        assert res.device["tensor_cores"] == 0, (n, hidden, act)
+        e = errs(res, ref)
+        assert max(e.values()) <= TOL32, e
