@@ -451,12 +451,12 @@ bool plan_tc(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
   for (int i = 0; i < 8; ++i) s.vec[i] = -1;
   s.scr_elems = 0;
+  s.wts = take(total / 4);   // the tcgen05 region first: constant operand addresses
   s.u = take((long long)Q.Rt * Q.d.ldn);
   s.lam = take((long long)Q.Rt * Q.d.ldn);
   s.lamn = take((long long)Q.Rt * Q.d.ldn);
   s.w = take((long long)Q.Rt * Q.d.ldn);
   s.jtv = take((long long)Q.Rt * Q.d.ldn);
-  s.wts = take(total / 4);
   s.total = o;
   Q.smem_bytes = (size_t)o * 4;
   if (Q.smem_bytes > smem_cap(Q)) return false;

@@ -1,5 +1,6 @@
 // rk_tc.cu -- persistent explicit-RK kernels instantiated with the tcgen05
-// tensor-core MLP tile (tc_mlp.cuh), its weight packer and host geometry.
+// tensor-core MLP tile (tc_mlp.cuh) for each supported (state, hidden) shape,
+// its weight packer and host geometry.
 #include "tc_mlp.cuh"
 
 namespace ob {
@@ -17,11 +18,23 @@ cudaError_t launch_pack_tc(const Dims& d, const float* theta, float* packed, cud
   return cudaGetLastError();
 }
 
-cudaError_t launch_rk_tc(const RkParams<float>& p, int tiles, size_t smem, cudaStream_t st,
-                         bool forward) {
-  using F = TcMlpAdapter<float>;
+template <int D, int H>
+static cudaError_t launch_shape(const RkParams<float>& p, int tiles, size_t smem, cudaStream_t st,
+                               bool forward) {
+  using F = TcMlpAdapter<float, D, H, D>;
   return forward ? launch_smem(rk_forward_kernel<float, F>, tiles, smem, st, p)
                  : launch_smem(rk_reverse_kernel<float, F>, tiles, smem, st, p);
+}
+
+cudaError_t launch_rk_tc(const RkParams<float>& p, int tiles, size_t smem, cudaStream_t st,
+                         bool forward) {
+  const int D = p.d.N, H = p.d.w[1];
+#define OB_TC_CASE(d, h) \
+  if (D == d && H == h) return launch_shape<d, h>(p, tiles, smem, st, forward);
+  OB_TC_CASE(64, 256) OB_TC_CASE(64, 128) OB_TC_CASE(48, 256) OB_TC_CASE(48, 128)
+  OB_TC_CASE(32, 256) OB_TC_CASE(32, 128) OB_TC_CASE(16, 256) OB_TC_CASE(16, 128)
+#undef OB_TC_CASE
+  return cudaErrorInvalidConfiguration;
 }
 
 }  // namespace ob

@@ -35,8 +35,9 @@ namespace ob {
 constexpr int kTcNS = 32;       // sample columns (MMA N) per tile
 constexpr uint32_t kTcLB = 144; // activation block-column stride (128 + 16: conflict-free stores)
 
-// shared-memory geometry of the tensor-core tile (bytes from the region base);
-// used by the host planner and the device adapter alike
+// shared-memory geometry of the tensor-core tile (bytes from the start of dynamic
+// shared memory, where the region sits); used by the host planner and, as
+// compile-time constants, by the device adapter
 struct TcGeom {
   int D0, H, D2, nmb;
   uint32_t SA1, SA2, SAx, SAh, SAv;
@@ -44,7 +45,7 @@ struct TcGeom {
   uint32_t X0h, X0l, Hh, Hl, Vh, Vl, vec, bar, slot, total;
 };
 
-__host__ __device__ inline TcGeom tc_geom(int D0, int H, int D2) {
+__host__ __device__ constexpr TcGeom tc_geom(int D0, int H, int D2) {
   TcGeom g{};
   g.D0 = D0; g.H = H; g.D2 = D2; g.nmb = H / 128;
   g.SA1 = (uint32_t)(D0 / 8) * 128u;
@@ -71,89 +72,95 @@ __host__ __device__ inline TcGeom tc_geom(int D0, int H, int D2) {
   o = (o + 15) & ~15u;
   g.bar = o; o += 8;
   g.slot = o; o += 8;
+  o = (o + 31) & ~31u;
   g.total = o;
   return g;
 }
 
-// eligibility (host): fp32 two-layer MLP field, explicit fixed-step scheme
+// shapes with an instantiated tile (D0 = D2 = state dim, H hidden)
 __host__ inline bool tc_shape_ok(int D0, int H, int D2) {
-  return D0 % 16 == 0 && D0 >= 16 && D0 <= 64 && D2 % 16 == 0 && D2 >= 16 && D2 <= 64 &&
-         (H == 128 || H == 256);
+  return D0 == D2 && (D0 == 16 || D0 == 32 || D0 == 48 || D0 == 64) && (H == 128 || H == 256);
 }
 
-template <typename T>
+// dynamic shared memory (aliases every kernel's extern smem_raw); the tile's
+// region starts at offset 0, so all operand addresses are link-time constants
+extern __shared__ __align__(128) unsigned char ob_tc_smem[];
+
+// 3-pass split product D (+)= A B over KS K-slices of 16, all geometry constant:
+// (AH, AL) / (BH, BL): byte offsets of the hi / lo copies, *LB / *SB: the
+// descriptor's leading / stride byte offsets, *ST: address step per K-slice
+template <uint32_t D, uint32_t AH, uint32_t AL, uint32_t ALB, uint32_t ASB, uint32_t AST,
+          uint32_t BH, uint32_t BL, uint32_t BLB, uint32_t BSB, uint32_t BST, int KS, uint32_t ID>
+OB_DEV void tc_mma3(uint32_t first_acc) {
+  const uint32_t sb = tc::smem_u32(ob_tc_smem);
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const uint64_t Ah = tc::sdesc(sb + AH + k * AST, ALB, ASB), Al = tc::sdesc(sb + AL + k * AST, ALB, ASB);
+    const uint64_t Bh = tc::sdesc(sb + BH + k * BST, BLB, BSB), Bl = tc::sdesc(sb + BL + k * BST, BLB, BSB);
+    tc::mma_bf16(D, Ah, Bh, ID, k > 0 ? 1u : first_acc);
+    tc::mma_bf16(D, Ah, Bl, ID, 1u);
+    tc::mma_bf16(D, Al, Bh, ID, 1u);
+  }
+}
+
+template <typename T, int D0, int H, int D2>
 struct TcMlpAdapter {
   static_assert(sizeof(T) == 4, "tensor-core MLP tile is fp32");
   static constexpr bool kHasJvp = false;
   static constexpr bool kScaledVjp = true;   // vjp returns J^T (h w)
-  static constexpr uint32_t kCols = 512;
+  static constexpr uint32_t kCols = 512;     // whole TMEM: one CTA per SM, base column 0
+  static constexpr TcGeom G = tc_geom(D0, H, D2);
+  static constexpr int NMB = H / 128;
+  static constexpr int CW = 8 * NMB;         // hidden-epilogue columns per thread
+  // TMEM columns (lane 0 base = 0: 512 columns allocated by the only CTA on the SM)
+  static constexpr uint32_t T_ACC1 = 0, T_ACC2 = 64, T_W2 = 128, T_W1 = 256;
 
   const RkParams<T>& p;
-  TcGeom g;
-  unsigned char* base;
-  uint32_t sbase;       // shared address of base
-  uint32_t tmem;        // TMEM base (lane 0, column 0)
   uint32_t phase;       // mbarrier parity
   float tcur;           // stage time (CTA-wide, set by put_time)
   int Rv, act;
   bool started;         // parameter-cotangent accumulators hold data
-  uint64_t* bar;
 
-  OB_DEV const float* w1t() const { return reinterpret_cast<const float*>(base + g.fv); }
-  OB_DEV const float* b1() const { return w1t() + g.H; }
-  OB_DEV const float* b2() const { return w1t() + 2 * g.H; }
-  OB_DEV float* db1() const { return reinterpret_cast<float*>(base + g.vec); }
-  OB_DEV float* dwt() const { return db1() + g.H; }
-  OB_DEV float* db2() const { return db1() + 2 * g.H; }
-  OB_DEV uint32_t t_acc1() const { return tmem; }
-  OB_DEV uint32_t t_acc2() const { return tmem + 64; }
-  OB_DEV uint32_t t_w2() const { return tmem + 128; }
-  OB_DEV uint32_t t_w1() const { return tmem + 256; }
+  OB_DEV unsigned char* base() const { return ob_tc_smem; }
+  OB_DEV uint64_t* bar() const { return reinterpret_cast<uint64_t*>(ob_tc_smem + G.bar); }
+  OB_DEV const float* w1t() const { return reinterpret_cast<const float*>(ob_tc_smem + G.fv); }
+  OB_DEV const float* b1() const { return w1t() + H; }
+  OB_DEV const float* b2() const { return w1t() + 2 * H; }
+  OB_DEV float* db1() const { return reinterpret_cast<float*>(ob_tc_smem + G.vec); }
+  OB_DEV float* dwt() const { return db1() + H; }
+  OB_DEV float* db2() const { return db1() + 2 * H; }
 
   OB_DEV TcMlpAdapter(const RkParams<T>& p_, const Weights<T>&, MlpSmem<T>&, T* sm, int, int Rv_)
       : p(p_), phase(0), tcur(0.f), Rv(Rv_), act(p_.d.act), started(false) {
-    g = tc_geom(p.d.N, p.d.w[1], p.d.w[2]);
-    base = reinterpret_cast<unsigned char*>(sm + p.sm.wts);
-    sbase = tc::smem_u32(base);
-    bar = reinterpret_cast<uint64_t*>(base + g.bar);
-    // activation operands and accumulator vectors start at zero (padded samples stay 0)
-    uint4* z = reinterpret_cast<uint4*>(base + g.X0h);
-    const int n16 = (int)((g.bar - g.X0h) / 16);
-    for (int i = threadIdx.x; i < n16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-    if (threadIdx.x < 32) tc::tmem_alloc(reinterpret_cast<uint32_t*>(base + g.slot), kCols);
-    if (threadIdx.x == 0) tc::bar_init(bar, 1);
+    // operand tiles, accumulator vectors and the generic state buffers after the
+    // region start at zero (padded samples stay 0)
+    uint4* z = reinterpret_cast<uint4*>(ob_tc_smem + G.packed);
+    const int n16 = (int)(((size_t)p.sm.total * sizeof(T) - G.packed) / 16);
+    for (int i = threadIdx.x; i < n16; i += blockDim.x)
+      if (i < (int)((G.bar - G.packed) / 16) || i >= (int)((G.total - G.packed) / 16))
+        z[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x < 32) tc::tmem_alloc(reinterpret_cast<uint32_t*>(ob_tc_smem + G.slot), kCols);
+    if (threadIdx.x == 0) tc::bar_init(bar(), 1);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    tmem = *reinterpret_cast<volatile uint32_t*>(base + g.slot);
+    if (threadIdx.x == 0 && *reinterpret_cast<volatile uint32_t*>(ob_tc_smem + G.slot) != 0u)
+      set_status(p.status, OB_ERR_UNSUPPORTED, -2);   // TMEM not at column 0: shared SM
   }
 
   OB_DEV T* x0() { return nullptr; }
-  OB_DEV int nin() const { return p.d.N; }
+  OB_DEV int nin() const { return D0; }
   OB_DEV void set_scratch(T*, int) {}
   // stage state element j of row r (rows >= Rv are padding: kept at zero)
   OB_DEV void put(int r, int j, T v) {
     uint16_t hi, lo;
     tc::split_bf16(r < Rv ? v : 0.f, hi, lo);
-    const uint32_t off = tc::blk(r, j, g.SAx, kTcLB);
-    *reinterpret_cast<uint16_t*>(base + g.X0h + off) = hi;
-    *reinterpret_cast<uint16_t*>(base + g.X0l + off) = lo;
+    const uint32_t off = tc::blk(r, j, G.SAx, kTcLB);
+    *reinterpret_cast<uint16_t*>(ob_tc_smem + G.X0h + off) = hi;
+    *reinterpret_cast<uint16_t*>(ob_tc_smem + G.X0l + off) = lo;
   }
   OB_DEV void put_time(double t) { tcur = p.d.time_input ? float(t) : 0.f; }
 
-  // ---- MMA issue (one thread) and completion wait (all threads)
-  // 3-pass split product over ksteps K-slices of 16; a/b: (hi, lo) shared addresses
-  OB_DEV void mma3(uint32_t d, uint32_t ah, uint32_t al, uint32_t alb, uint32_t asb, uint32_t ast,
-                   uint32_t bh, uint32_t bl, uint32_t blb, uint32_t bsb, uint32_t bst, int ksteps,
-                   uint32_t idesc, bool acc) {
-    for (int k = 0; k < ksteps; ++k) {
-      const uint64_t Ah = tc::sdesc(ah + k * ast, alb, asb), Al = tc::sdesc(al + k * ast, alb, asb);
-      const uint64_t Bh = tc::sdesc(bh + k * bst, blb, bsb), Bl = tc::sdesc(bl + k * bst, blb, bsb);
-      tc::mma_bf16(d, Ah, Bh, idesc, (acc || k > 0) ? 1u : 0u);
-      tc::mma_bf16(d, Ah, Bl, idesc, 1u);
-      tc::mma_bf16(d, Al, Bh, idesc, 1u);
-    }
-  }
   // operands written by the generic proxy -> visible to the MMA; accumulator reads retired
   OB_DEV void sync_issue() {
     tc::fence_async_smem();
@@ -162,78 +169,100 @@ struct TcMlpAdapter {
     tc::fence_after();
   }
   OB_DEV void wait() {
-    tc::bar_wait(bar, phase);
+    tc::bar_wait(bar(), phase);
     phase ^= 1u;
     tc::fence_after();
   }
 
-  // hidden layer: z = W1 x + b1 + t w1t  (rows o of the hidden layer = MMA M)
+  // ---- products (issued by warp 0; one elected lane)
+  // z[o][s] = sum_i W1[o][i] X0[s][i]           (A = W1 K-major, B = X0 K-major)
   OB_DEV void issue_hidden() {
-    const uint32_t id = tc::idesc_bf16(128, kTcNS, false, false);
-    for (int mb = 0; mb < g.nmb; ++mb)
-      mma3(t_acc1() + 32 * mb, sbase + g.W1h + mb * 16 * g.SA1, sbase + g.W1l + mb * 16 * g.SA1,
-           128, g.SA1, 256, sbase + g.X0h, sbase + g.X0l, kTcLB, g.SAx, 2 * kTcLB, g.D0 / 16, id,
-           false);
+    constexpr uint32_t id = tc::idesc_bf16(128, kTcNS, false, false);
+    tc_mma3<T_ACC1, G.W1h, G.W1l, 128, G.SA1, 256, G.X0h, G.X0l, kTcLB, G.SAx, 2 * kTcLB, D0 / 16, id>(0);
+    if constexpr (NMB == 2)
+      tc_mma3<T_ACC1 + 32, G.W1h + 16 * G.SA1, G.W1l + 16 * G.SA1, 128, G.SA1, 256, G.X0h, G.X0l,
+              kTcLB, G.SAx, 2 * kTcLB, D0 / 16, id>(0);
   }
-  // epilogue of the hidden layer: act -> H (hi, lo); act' kept in registers for a VJP
-  // warp w: lane quarter q = w % 4, column group cg = w / 4
-  OB_DEV int hid_cols() const { return 8 * g.nmb; }
+  // out[o2][s] = sum_i2 W2[o2][i2] H[s][i2]      (M = 64)
+  OB_DEV void issue_out() {
+    constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, false, false);
+    tc_mma3<T_ACC2, G.W2h, G.W2l, 128, G.SA2, 256, G.Hh, G.Hl, kTcLB, G.SAh, 2 * kTcLB, H / 16, id>(0);
+  }
+  // dW2^T[i2][o2] += sum_s H[s][i2] V[s][o2]     (A = H MN-major, B = V MN-major)
+  OB_DEV void issue_dw2(uint32_t acc) {
+    constexpr uint32_t id = tc::idesc_bf16(128, D2, true, true);
+    tc_mma3<T_W2, G.Hh, G.Hl, G.SAh, kTcLB, 2 * G.SAh, G.Vh, G.Vl, G.SAv, kTcLB, 2 * G.SAv,
+            kTcNS / 16, id>(acc);
+    if constexpr (NMB == 2)
+      tc_mma3<T_W2 + D2, G.Hh + 16 * kTcLB, G.Hl + 16 * kTcLB, G.SAh, kTcLB, 2 * G.SAh, G.Vh, G.Vl,
+              G.SAv, kTcLB, 2 * G.SAv, kTcNS / 16, id>(acc);
+  }
+  // dH[i2][s] = sum_o2 W2[o2][i2] V[s][o2]       (A = W2 MN-major, B = V K-major)
+  OB_DEV void issue_dh() {
+    constexpr uint32_t id = tc::idesc_bf16(128, kTcNS, true, false);
+    tc_mma3<T_ACC1, G.W2h, G.W2l, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl, kTcLB, G.SAv, 2 * kTcLB,
+            D2 / 16, id>(0);
+    if constexpr (NMB == 2)
+      tc_mma3<T_ACC1 + 32, G.W2h + 16 * 128, G.W2l + 16 * 128, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl,
+              kTcLB, G.SAv, 2 * kTcLB, D2 / 16, id>(0);
+  }
+  // dW1[o][i] += sum_s dZ[s][o] X0[s][i]          (A = dZ MN-major, B = X0 MN-major)
+  OB_DEV void issue_dw1(uint32_t acc) {
+    constexpr uint32_t id = tc::idesc_bf16(128, D0, true, true);
+    tc_mma3<T_W1, G.Hh, G.Hl, G.SAh, kTcLB, 2 * G.SAh, G.X0h, G.X0l, G.SAx, kTcLB, 2 * G.SAx,
+            kTcNS / 16, id>(acc);
+    if constexpr (NMB == 2)
+      tc_mma3<T_W1 + D0, G.Hh + 16 * kTcLB, G.Hl + 16 * kTcLB, G.SAh, kTcLB, 2 * G.SAh, G.X0h,
+              G.X0l, G.SAx, kTcLB, 2 * G.SAx, kTcNS / 16, id>(acc);
+  }
+  // dX[i][s] = sum_o W1[o][i] dZ[s][o]            (A = W1 MN-major, B = dZ K-major, M = 64)
+  OB_DEV void issue_dx() {
+    constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, true, false);
+    tc_mma3<T_ACC2, G.W1h, G.W1l, G.SA1, 128, 2 * G.SA1, G.Hh, G.Hl, kTcLB, G.SAh, 2 * kTcLB,
+            H / 16, id>(0);
+  }
+
+  // ---- epilogues (warp w: TMEM lane quarter q = w % 4, column group cg = w / 4)
+  OB_DEV void ld_hidden(float v[16], int& o, int& c0, int& cg) const {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3;
+    cg = w >> 2;
+    const int f0 = cg * CW, mb = f0 >> 5;
+    c0 = f0 & 31;
+    o = mb * 128 + q * 32 + lane;
+    const uint32_t ta = T_ACC1 + ((uint32_t)(q * 32) << 16) + 32 * mb + c0;
+    if constexpr (CW == 16) tc::ld16(ta, v); else tc::ld8(ta, v);
+  }
+  OB_DEV void put_hid(int s, int o, float a) {
+    uint16_t hi, lo;
+    tc::split_bf16(a, hi, lo);
+    const uint32_t off = tc::blk(s, o, G.SAh, kTcLB);
+    *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Hh + off) = hi;
+    *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Hl + off) = lo;
+  }
+  // act(z + b1 + t w1t) -> H (hi, lo); act' kept in registers for a VJP
   template <bool kVjp>
   OB_DEV void epi_hidden(float ap[16]) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3, cg = w >> 2;
-    const int cw = hid_cols(), f0 = cg * cw, mb = f0 >> 5, c0 = f0 & 31;
-    const int o = mb * 128 + q * 32 + lane;
     float v[16];
-    const uint32_t ta = t_acc1() + ((uint32_t)(q * 32) << 16) + 32 * mb + c0;
-    if (cw == 16) tc::ld16(ta, v); else tc::ld8(ta, v);
+    int o, c0, cg;
+    ld_hidden(v, o, c0, cg);
     const float bo = b1()[o], wt = w1t()[o];
-    for (int j = 0; j < cw; ++j) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
       const float z = v[j] + bo + tcur * wt;
-      float a;
-      if (act == OB_ACT_TANH) a = fast_tanh(z);
-      else if (act == OB_ACT_RELU) a = z > 0.f ? z : 0.f;
-      else a = z;
-      if (kVjp) ap[j] = act == OB_ACT_TANH ? 1.f - a * a : act == OB_ACT_RELU ? (a > 0.f ? 1.f : 0.f) : 1.f;
-      uint16_t hi, lo;
-      tc::split_bf16(a, hi, lo);
-      const uint32_t off = tc::blk(c0 + j, o, g.SAh, kTcLB);
-      *reinterpret_cast<uint16_t*>(base + g.Hh + off) = hi;
-      *reinterpret_cast<uint16_t*>(base + g.Hl + off) = lo;
+      const float a = act == OB_ACT_TANH ? fast_tanh(z) : z;
+      if (kVjp) ap[j] = act == OB_ACT_TANH ? 1.f - a * a : 1.f;
+      put_hid(c0 + j, o, a);
     }
   }
-
-  // f(x0) -> out [Rt][ldn] (global or shared), columns >= N untouched
-  OB_DEV void eval(T* out) {
-    PhaseTimer pt(p.prof ? p.phase : nullptr);   // 10: MMA issue + wait, 11: epilogues
-    sync_issue();
-    if (threadIdx.x == 0) { issue_hidden(); tc::commit(bar); }
-    wait();
-    pt.mark(10);
-    float ap[16];
-    epi_hidden<false>(ap);
-    sync_issue();
-    pt.mark(11);
-    if (threadIdx.x == 0) {
-      mma3(t_acc2(), sbase + g.W2h, sbase + g.W2l, 128, g.SA2, 256, sbase + g.Hh, sbase + g.Hl,
-           kTcLB, g.SAh, 2 * kTcLB, g.H / 16, tc::idesc_bf16(64, kTcNS, false, false), false);
-      tc::commit(bar);
-    }
-    wait();
-    pt.mark(10);
-    epi_state(out, p.d.ldn, g.D2, true);
-    tc::fence_before();
-    __syncthreads();
-    pt.mark(11);
-  }
-
-  // M = 64 accumulator (state-sized rows m = 16 q + lane, lanes < 16) -> dst[s][m]
-  OB_DEV void epi_state(T* dst, int ldo, int rows, bool bias) {
+  // M = 64 accumulator (rows m = 16 q + lane for lanes < 16) -> dst[s][m] (+ b2)
+  OB_DEV void epi_state(T* dst, int ldo, bool bias) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3, cg = w >> 2;
     float v[8];
-    tc::ld8(t_acc2() + ((uint32_t)(q * 32) << 16) + 8 * cg, v);
+    tc::ld8(T_ACC2 + ((uint32_t)(q * 32) << 16) + 8 * cg, v);
     const int m = 16 * q + lane;
-    if (lane < 16 && m < rows) {
+    if (lane < 16 && m < D0) {
       const float bm = bias ? b2()[m] : 0.f;
+#pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int s = 8 * cg + j;
         if (s < p.Rt) dst[s * ldo + m] = v[j] + bm;
@@ -241,9 +270,29 @@ struct TcMlpAdapter {
     }
   }
 
+  // f(x0) -> out [Rt][ldn] (global or shared), columns >= N untouched
+  OB_DEV void eval(T* out) {
+    PhaseTimer pt(p.prof ? p.phase : nullptr);   // 10: MMA issue + wait, 11: epilogues
+    sync_issue();
+    if (tc::uniform_warp() == 0) { issue_hidden(); tc::commit(bar()); }
+    wait();
+    pt.mark(10);
+    float ap[16];
+    epi_hidden<false>(ap);
+    sync_issue();
+    pt.mark(11);
+    if (tc::uniform_warp() == 0) { issue_out(); tc::commit(bar()); }
+    wait();
+    pt.mark(10);
+    epi_state(out, p.d.ldn, true);
+    tc::fence_before();
+    __syncthreads();
+    pt.mark(11);
+  }
+
   // jtv = J^T (h w); mu (nullable) += h P^T w, accumulated on chip until finish()
   OB_DEV void vjp(const T* wv, T* jtv, T* mu, double h, int) {
-    const int N = p.d.N, ldn = p.d.ldn, D2 = g.D2, H = g.H;
+    const int ldn = p.d.ldn;
     const float hf = float(h);
     PhaseTimer pt(p.prof ? p.phase : nullptr);   // 14: operand prep, 10: MMA waits, 11: epilogues
     // V = h w (rows >= Rv zero) as (hi, lo)
@@ -252,13 +301,13 @@ struct TcMlpAdapter {
       const float v = s < Rv ? hf * wv[s * ldn + o2] : 0.f;
       uint16_t hi, lo;
       tc::split_bf16(v, hi, lo);
-      const uint32_t off = tc::blk(s, o2, g.SAv, kTcLB);
-      *reinterpret_cast<uint16_t*>(base + g.Vh + off) = hi;
-      *reinterpret_cast<uint16_t*>(base + g.Vl + off) = lo;
+      const uint32_t off = tc::blk(s, o2, G.SAv, kTcLB);
+      *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vh + off) = hi;
+      *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vl + off) = lo;
     }
     sync_issue();
     pt.mark(14);
-    if (threadIdx.x == 0) { issue_hidden(); tc::commit(bar); }
+    if (tc::uniform_warp() == 0) { issue_hidden(); tc::commit(bar()); }
     if (mu && threadIdx.x < D2) {   // db2 += sum_s h w[s]
       float acc = 0.f;
       for (int s = 0; s < Rv; ++s) acc += hf * wv[s * ldn + threadIdx.x];
@@ -270,72 +319,48 @@ struct TcMlpAdapter {
     epi_hidden<true>(ap);
     sync_issue();
     pt.mark(11);
-    if (threadIdx.x == 0) {
-      if (mu) {   // dW2^T[i2][o2] += sum_s H[s][i2] V[s][o2]
-        const uint32_t id = tc::idesc_bf16(128, D2, true, true);
-        for (int mb = 0; mb < g.nmb; ++mb)
-          mma3(t_w2() + D2 * mb, sbase + g.Hh + mb * 16 * kTcLB, sbase + g.Hl + mb * 16 * kTcLB,
-               g.SAh, kTcLB, 2 * g.SAh, sbase + g.Vh, sbase + g.Vl, g.SAv, kTcLB, 2 * g.SAv,
-               kTcNS / 16, id, started);
-      }
-      // dH[i2][s] = sum_o2 W2[o2][i2] V[s][o2]
-      const uint32_t id = tc::idesc_bf16(128, kTcNS, true, false);
-      for (int mb = 0; mb < g.nmb; ++mb)
-        mma3(t_acc1() + 32 * mb, sbase + g.W2h + mb * 16 * 128, sbase + g.W2l + mb * 16 * 128,
-             g.SA2, 128, 2 * g.SA2, sbase + g.Vh, sbase + g.Vl, kTcLB, g.SAv, 2 * kTcLB, D2 / 16,
-             id, false);
-      tc::commit(bar);
+    const uint32_t acc = started ? 1u : 0u;
+    if (tc::uniform_warp() == 0) {
+      if (mu) issue_dw2(acc);
+      issue_dh();
+      tc::commit(bar());
     }
     wait();
     pt.mark(10);
     // dZ = dH * act'(z) overwrites H (its MMAs have completed); per-row partial sums
     {
-      const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3, cg = w >> 2;
-      const int cw = hid_cols(), f0 = cg * cw, mb = f0 >> 5, c0 = f0 & 31;
-      const int o = mb * 128 + q * 32 + lane;
       float v[16];
-      const uint32_t ta = t_acc1() + ((uint32_t)(q * 32) << 16) + 32 * mb + c0;
-      if (cw == 16) tc::ld16(ta, v); else tc::ld8(ta, v);
+      int o, c0, cg;
+      ld_hidden(v, o, c0, cg);
       float ps = 0.f;
-      for (int j = 0; j < cw; ++j) {
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
         const float dz = v[j] * ap[j];
         ps += dz;
-        uint16_t hi, lo;
-        tc::split_bf16(dz, hi, lo);
-        const uint32_t off = tc::blk(c0 + j, o, g.SAh, kTcLB);
-        *reinterpret_cast<uint16_t*>(base + g.Hh + off) = hi;
-        *reinterpret_cast<uint16_t*>(base + g.Hl + off) = lo;
+        put_hid(c0 + j, o, dz);
       }
       // V is free now: partial sums part[k][o], k = column group within the row
-      float* part = reinterpret_cast<float*>(base + g.Vh);
-      part[(cg % (4 / g.nmb)) * H + o] = ps;
+      float* part = reinterpret_cast<float*>(ob_tc_smem + G.Vh);
+      part[(cg % (4 / NMB)) * H + o] = ps;
     }
     sync_issue();
     pt.mark(11);
-    if (threadIdx.x == 0) {
-      if (mu) {   // dW1[o][i] += sum_s dZ[s][o] X0[s][i]
-        const uint32_t id = tc::idesc_bf16(128, g.D0, true, true);
-        for (int mb = 0; mb < g.nmb; ++mb)
-          mma3(t_w1() + g.D0 * mb, sbase + g.Hh + mb * 16 * kTcLB, sbase + g.Hl + mb * 16 * kTcLB,
-               g.SAh, kTcLB, 2 * g.SAh, sbase + g.X0h, sbase + g.X0l, g.SAx, kTcLB, 2 * g.SAx,
-               kTcNS / 16, id, started);
-      }
-      // dX[i][s] = sum_o W1[o][i] dZ[s][o]
-      mma3(t_acc2(), sbase + g.W1h, sbase + g.W1l, g.SA1, 128, 2 * g.SA1, sbase + g.Hh,
-           sbase + g.Hl, kTcLB, g.SAh, 2 * kTcLB, H / 16, tc::idesc_bf16(64, kTcNS, true, false),
-           false);
-      tc::commit(bar);
+    if (tc::uniform_warp() == 0) {
+      if (mu) issue_dw1(acc);
+      issue_dx();
+      tc::commit(bar());
     }
     if (mu && threadIdx.x < H) {   // db1 += sum_s dZ, time column += t sum_s dZ
-      const float* part = reinterpret_cast<const float*>(base + g.Vh);
+      const float* part = reinterpret_cast<const float*>(ob_tc_smem + G.Vh);
       float s = 0.f;
-      for (int k = 0; k < 4 / g.nmb; ++k) s += part[k * H + threadIdx.x];
+#pragma unroll
+      for (int k = 0; k < 4 / NMB; ++k) s += part[k * H + threadIdx.x];
       db1()[threadIdx.x] += s;
       dwt()[threadIdx.x] += tcur * s;
     }
     wait();
     pt.mark(10);
-    epi_state(jtv, ldn, N, false);
+    epi_state(jtv, ldn, false);
     if (mu) started = true;
     tc::fence_before();
     __syncthreads();
@@ -347,32 +372,33 @@ struct TcMlpAdapter {
     if (!started || !mu) return;
     const Dims& d = p.d;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3, cg = w >> 2;
-    for (int mb = 0; mb < g.nmb; ++mb) {
-      for (int c8 = cg; c8 < g.D2 / 8; c8 += 4) {   // dW2^T: lanes i2, columns o2
+#pragma unroll
+    for (int mb = 0; mb < NMB; ++mb) {
+      for (int c8 = cg; c8 < D2 / 8; c8 += 4) {   // dW2^T: lanes i2, columns o2
         float v[8];
-        tc::ld8(t_w2() + ((uint32_t)(q * 32) << 16) + g.D2 * mb + 8 * c8, v);
+        tc::ld8(T_W2 + ((uint32_t)(q * 32) << 16) + D2 * mb + 8 * c8, v);
         const int i2 = mb * 128 + q * 32 + lane;
         for (int j = 0; j < 8; ++j) mu[d.mwoff[1] + (long long)(8 * c8 + j) * d.ldm[1] + i2] += v[j];
       }
-      for (int c8 = cg; c8 < g.D0 / 8; c8 += 4) {   // dW1: lanes o, columns i
+      for (int c8 = cg; c8 < D0 / 8; c8 += 4) {   // dW1: lanes o, columns i
         float v[8];
-        tc::ld8(t_w1() + ((uint32_t)(q * 32) << 16) + g.D0 * mb + 8 * c8, v);
+        tc::ld8(T_W1 + ((uint32_t)(q * 32) << 16) + D0 * mb + 8 * c8, v);
         const int o = mb * 128 + q * 32 + lane;
         for (int j = 0; j < 8; ++j) mu[d.mwoff[0] + (long long)o * d.ldm[0] + 8 * c8 + j] += v[j];
       }
     }
-    for (int o = threadIdx.x; o < g.H; o += blockDim.x) {
+    for (int o = threadIdx.x; o < H; o += blockDim.x) {
       mu[d.mboff[0] + o] += db1()[o];
-      if (d.time_input) mu[d.mwoff[0] + (long long)o * d.ldm[0] + g.D0] += dwt()[o];
+      if (d.time_input) mu[d.mwoff[0] + (long long)o * d.ldm[0] + D0] += dwt()[o];
     }
-    for (int o = threadIdx.x; o < g.D2; o += blockDim.x) mu[d.mboff[1] + o] += db2()[o];
+    for (int o = threadIdx.x; o < D2; o += blockDim.x) mu[d.mboff[1] + o] += db2()[o];
     __syncthreads();
   }
 
   OB_DEV void release() {
     tc::fence_before();
     __syncthreads();
-    if (threadIdx.x < 32) tc::tmem_free(tmem, kCols);
+    if (threadIdx.x < 32) tc::tmem_free(0u, kCols);
   }
 };
 
