@@ -83,6 +83,7 @@ struct MlpAdapter {
   OB_DEV void set_scratch(T* s, int n) { mt.scratch = s; mt.scratch_elems = n; }
   static constexpr bool kHasJvp = true;
   static constexpr bool kScaledVjp = false;  // vjp returns J^T w; the caller scales by h
+  static constexpr int kCombineBatch = 4;    // stage loads in flight per ordered sum (registers)
   OB_DEV void finish(T*) {}   // flush device-resident parameter cotangents (none here)
   OB_DEV void release() {}    // free per-CTA hardware resources (none here)
 
@@ -150,10 +151,20 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
   for (int i = 0; i < s; ++i) {
     for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
       const int r = idx / N, j = idx % N;
+      // issue every stage-derivative load (L2-resident scratch) before the dependent
+      // sum so they overlap; the sum keeps the reference order
       T v = u[r * ldn + j];
-      for (int q = 0; q < i; ++q) {
-        const double aiq = p.a[i * OB_MAX_STAGES + q];
-        if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), ks[q * kst + r * ldn + j]));
+#pragma unroll
+      for (int q0 = 0; q0 < OB_MAX_STAGES; q0 += F::kCombineBatch) {
+        T kv[F::kCombineBatch];
+#pragma unroll
+        for (int t = 0; t < F::kCombineBatch; ++t)
+          kv[t] = q0 + t < i ? ks[(q0 + t) * kst + r * ldn + j] : T(0);
+#pragma unroll
+        for (int t = 0; t < F::kCombineBatch; ++t) {
+          const double aiq = q0 + t < i ? p.a[i * OB_MAX_STAGES + q0 + t] : 0.0;
+          if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), kv[t]));
+        }
       }
       if (j < nin) f.put(r, j, v);
       if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * N + j] = v;
@@ -173,8 +184,18 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
   for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
     T v = u[r * ldn + j];
-    for (int i = 0; i < s; ++i)
-      if (p.b[i] != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * p.b[i]), ks[i * kst + r * ldn + j]));
+#pragma unroll
+    for (int i0 = 0; i0 < OB_MAX_STAGES; i0 += F::kCombineBatch) {
+      T kv[F::kCombineBatch];
+#pragma unroll
+      for (int t = 0; t < F::kCombineBatch; ++t)
+        kv[t] = i0 + t < s ? ks[(i0 + t) * kst + r * ldn + j] : T(0);
+#pragma unroll
+      for (int t = 0; t < F::kCombineBatch; ++t) {
+        const double bi = i0 + t < s ? p.b[i0 + t] : 0.0;
+        if (bi != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * bi), kv[t]));
+      }
+    }
     u[r * ldn + j] = v;
     if (r < Rv) {
       if (!Num<T>::finite(v)) bad = 1;
@@ -548,9 +569,17 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
         const int o = (idx / N) * ldn + idx % N;
         T v = Num<T>::mul(T(p.b[i]), lam[o]);
-        for (int j = i + 1; j < s; ++j) {
-          const double aji = p.a[j * OB_MAX_STAGES + i];
-          if (aji != 0.0) v = Num<T>::add(v, Num<T>::mul(T(aji), Lam[j * kst + o]));
+#pragma unroll
+        for (int j0 = 0; j0 < OB_MAX_STAGES; j0 += F::kCombineBatch) {   // loads in flight first
+          T lv[F::kCombineBatch];
+#pragma unroll
+          for (int t = 0; t < F::kCombineBatch; ++t)
+            lv[t] = (j0 + t > i && j0 + t < s) ? Lam[(j0 + t) * kst + o] : T(0);
+#pragma unroll
+          for (int t = 0; t < F::kCombineBatch; ++t) {
+            const double aji = (j0 + t > i && j0 + t < s) ? p.a[(j0 + t) * OB_MAX_STAGES + i] : 0.0;
+            if (aji != 0.0) v = Num<T>::add(v, Num<T>::mul(T(aji), lv[t]));
+          }
         }
         w[o] = v;
       }

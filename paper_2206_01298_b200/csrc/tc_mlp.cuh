@@ -108,6 +108,7 @@ struct TcMlpAdapter {
   static_assert(sizeof(T) == 4, "tensor-core MLP tile is fp32");
   static constexpr bool kHasJvp = false;
   static constexpr bool kScaledVjp = true;   // vjp returns J^T (h w)
+  static constexpr int kCombineBatch = 8;    // all stage loads in flight (no register pressure)
   static constexpr uint32_t kCols = 512;     // whole TMEM: one CTA per SM, base column 0
   static constexpr TcGeom G = tc_geom(D0, H, D2);
   static constexpr int NMB = H / 128;
