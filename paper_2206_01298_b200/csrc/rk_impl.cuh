@@ -84,6 +84,7 @@ struct MlpAdapter {
   static constexpr bool kHasJvp = true;
   static constexpr bool kScaledVjp = false;  // vjp returns J^T w; the caller scales by h
   static constexpr int kCombineBatch = 4;    // stage loads in flight per ordered sum (registers)
+  static constexpr int kCombineElems = 1;    // elements per thread combined together
   OB_DEV void finish(T*) {}   // flush device-resident parameter cotangents (none here)
   OB_DEV void release() {}    // free per-CTA hardware resources (none here)
 
@@ -149,6 +150,34 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
   const long long vec = (long long)p.B * N;
   PhaseTimer pt(p.prof ? p.phase : nullptr);
   for (int i = 0; i < s; ++i) {
+    if constexpr (F::kCombineElems > 1) {
+      // E elements per thread at once: every stage-derivative load of all of them in
+      // flight before the ordered sums (L2 latency paid once per stage)
+      constexpr int E = F::kCombineElems;
+      for (int b0 = threadIdx.x; b0 < Rt * N; b0 += E * blockDim.x) {
+        T kv[E][OB_MAX_STAGES];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int idx = b0 + e * blockDim.x, r = idx / N, j = idx % N;
+#pragma unroll
+          for (int q = 0; q < OB_MAX_STAGES; ++q)
+            kv[e][q] = (idx < Rt * N && q < i) ? ks[q * kst + r * ldn + j] : T(0);
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int idx = b0 + e * blockDim.x, r = idx / N, j = idx % N;
+          if (idx >= Rt * N) continue;
+          T v = u[r * ldn + j];
+#pragma unroll
+          for (int q = 0; q < OB_MAX_STAGES; ++q) {
+            const double aiq = q < i ? p.a[i * OB_MAX_STAGES + q] : 0.0;
+            if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), kv[e][q]));
+          }
+          if (j < nin) f.put(r, j, v);
+          if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * N + j] = v;
+        }
+      }
+    } else
     for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
       const int r = idx / N, j = idx % N;
       // issue every stage-derivative load (L2-resident scratch) before the dependent
@@ -181,6 +210,36 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
     pt.mark(9);   // field eval
   }
   int bad = 0;
+  if constexpr (F::kCombineElems > 1) {
+    constexpr int E = F::kCombineElems;
+    for (int b0 = threadIdx.x; b0 < Rt * N; b0 += E * blockDim.x) {
+      T kv[E][OB_MAX_STAGES];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int idx = b0 + e * blockDim.x, r = idx / N, j = idx % N;
+#pragma unroll
+        for (int q = 0; q < OB_MAX_STAGES; ++q)
+          kv[e][q] = (idx < Rt * N && q < s) ? ks[q * kst + r * ldn + j] : T(0);
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int idx = b0 + e * blockDim.x, r = idx / N, j = idx % N;
+        if (idx >= Rt * N) continue;
+        T v = u[r * ldn + j];
+#pragma unroll
+        for (int q = 0; q < OB_MAX_STAGES; ++q) {
+          const double bq = q < s ? p.b[q] : 0.0;
+          if (bq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * bq), kv[e][q]));
+        }
+        u[r * ldn + j] = v;
+        if (r < Rv) {
+          if (!Num<T>::finite(v)) bad = 1;
+          if (rec) rec[s * vec + (long long)(row0 + r) * N + j] = v;
+        }
+      }
+    }
+    return __syncthreads_or(bad) == 0;
+  }
   for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
     T v = u[r * ldn + j];
@@ -566,6 +625,35 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
         continue;
       }
       // w_i = b_i lam_{n+1} + sum_{j>i, a_ji != 0} a_ji Lam_j   (pad rows stay 0)
+      if constexpr (F::kCombineElems > 1) {
+        constexpr int E = F::kCombineElems;
+        for (int b0 = threadIdx.x; b0 < Rt * N; b0 += E * blockDim.x) {
+          T lv[E][OB_MAX_STAGES];
+          T xs[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int idx = b0 + e * blockDim.x, r = idx / N, jj = idx % N, o = r * ldn + jj;
+#pragma unroll
+            for (int j = 0; j < OB_MAX_STAGES; ++j)
+              lv[e][j] = (idx < Rt * N && j > i && j < s) ? Lam[j * kst + o] : T(0);
+            xs[e] = (idx < Rt * N && r < Rv && jj < nin) ? rec[i * vec + (long long)(row0 + r) * N + jj]
+                                                         : T(0);
+          }
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int idx = b0 + e * blockDim.x, r = idx / N, jj = idx % N, o = r * ldn + jj;
+            if (idx >= Rt * N) continue;
+            T v = Num<T>::mul(T(p.b[i]), lam[o]);
+#pragma unroll
+            for (int j = 0; j < OB_MAX_STAGES; ++j) {
+              const double aji = (j > i && j < s) ? p.a[j * OB_MAX_STAGES + i] : 0.0;
+              if (aji != 0.0) v = Num<T>::add(v, Num<T>::mul(T(aji), lv[e][j]));
+            }
+            w[o] = v;
+            if (r < Rv && jj < nin) f.put(r, jj, xs[e]);   // stage state U_i into the field input
+          }
+        }
+      } else {
       for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
         const int o = (idx / N) * ldn + idx % N;
         T v = Num<T>::mul(T(p.b[i]), lam[o]);
@@ -587,6 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       for (int idx = threadIdx.x; idx < Rv * nin; idx += blockDim.x) {
         const int r = idx / nin, j = idx % nin;
         f.put(r, j, rec[i * vec + (long long)(row0 + r) * N + j]);
+      }
       }
       f.put_time(t + p.c[i] * h);
       __syncthreads();

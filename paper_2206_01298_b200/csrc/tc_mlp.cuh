@@ -51,7 +51,7 @@ __host__ __device__ constexpr TcGeom tc_geom(int D0, int H, int D2) {
   g.SA1 = (uint32_t)(D0 / 8) * 128u;
   g.SA2 = (uint32_t)(H / 8) * 128u;
   g.SAx = (uint32_t)(D0 / 8) * kTcLB;
-  g.SAh = (uint32_t)(H / 8) * kTcLB;
+  g.SAh = (uint32_t)(kTcNS / 8) * 128u;             // H^T [o][s]: o-block stride
   g.SAv = (uint32_t)(D2 / 8) * kTcLB;
   uint32_t o = 0;
   g.W2h = o; o += (uint32_t)D2 * H * 2;
@@ -64,8 +64,8 @@ __host__ __device__ constexpr TcGeom tc_geom(int D0, int H, int D2) {
   const uint32_t rb = kTcNS / 8;
   g.X0h = o; o += rb * g.SAx;
   g.X0l = o; o += rb * g.SAx;
-  g.Hh = o;  o += rb * g.SAh;
-  g.Hl = o;  o += rb * g.SAh;
+  g.Hh = o;  o += (uint32_t)(H / 8) * g.SAh;
+  g.Hl = o;  o += (uint32_t)(H / 8) * g.SAh;
   g.Vh = o;  o += rb * g.SAv;
   g.Vl = o;  o += rb * g.SAv;
   g.vec = o; o += (uint32_t)(2 * H + D2) * 4;       // db1[H] | dwt[H] | db2[D2]
@@ -109,6 +109,7 @@ struct TcMlpAdapter {
   static constexpr bool kHasJvp = false;
   static constexpr bool kScaledVjp = true;   // vjp returns J^T (h w)
   static constexpr int kCombineBatch = 8;    // all stage loads in flight (no register pressure)
+  static constexpr int kCombineElems = 4;    // ... for 4 elements per thread at once
   static constexpr uint32_t kCols = 512;     // whole TMEM: one CTA per SM, base column 0
   static constexpr TcGeom G = tc_geom(D0, H, D2);
   static constexpr int NMB = H / 128;
@@ -184,18 +185,18 @@ struct TcMlpAdapter {
       tc_mma3<T_ACC1 + 32, G.W1h + 16 * G.SA1, G.W1l + 16 * G.SA1, 128, G.SA1, 256, G.X0h, G.X0l,
               kTcLB, G.SAx, 2 * kTcLB, D0 / 16, id>(0);
   }
-  // out[o2][s] = sum_i2 W2[o2][i2] H[s][i2]      (M = 64)
+  // out[o2][s] = sum_i2 W2[o2][i2] H[s][i2]      (M = 64; B = H^T MN-major)
   OB_DEV void issue_out() {
-    constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, false, false);
-    tc_mma3<T_ACC2, G.W2h, G.W2l, 128, G.SA2, 256, G.Hh, G.Hl, kTcLB, G.SAh, 2 * kTcLB, H / 16, id>(0);
+    constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, false, true);
+    tc_mma3<T_ACC2, G.W2h, G.W2l, 128, G.SA2, 256, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh, H / 16, id>(0);
   }
-  // dW2^T[i2][o2] += sum_s H[s][i2] V[s][o2]     (A = H MN-major, B = V MN-major)
+  // dW2^T[i2][o2] += sum_s H[s][i2] V[s][o2]     (A = H^T K-major, B = V MN-major)
   OB_DEV void issue_dw2(uint32_t acc) {
-    constexpr uint32_t id = tc::idesc_bf16(128, D2, true, true);
-    tc_mma3<T_W2, G.Hh, G.Hl, G.SAh, kTcLB, 2 * G.SAh, G.Vh, G.Vl, G.SAv, kTcLB, 2 * G.SAv,
+    constexpr uint32_t id = tc::idesc_bf16(128, D2, false, true);
+    tc_mma3<T_W2, G.Hh, G.Hl, 128, G.SAh, 256, G.Vh, G.Vl, G.SAv, kTcLB, 2 * G.SAv,
             kTcNS / 16, id>(acc);
     if constexpr (NMB == 2)
-      tc_mma3<T_W2 + D2, G.Hh + 16 * kTcLB, G.Hl + 16 * kTcLB, G.SAh, kTcLB, 2 * G.SAh, G.Vh, G.Vl,
+      tc_mma3<T_W2 + D2, G.Hh + 16 * G.SAh, G.Hl + 16 * G.SAh, 128, G.SAh, 256, G.Vh, G.Vl,
               G.SAv, kTcLB, 2 * G.SAv, kTcNS / 16, id>(acc);
   }
   // dH[i2][s] = sum_o2 W2[o2][i2] V[s][o2]       (A = W2 MN-major, B = V K-major)
@@ -207,19 +208,19 @@ struct TcMlpAdapter {
       tc_mma3<T_ACC1 + 32, G.W2h + 16 * 128, G.W2l + 16 * 128, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl,
               kTcLB, G.SAv, 2 * kTcLB, D2 / 16, id>(0);
   }
-  // dW1[o][i] += sum_s dZ[s][o] X0[s][i]          (A = dZ MN-major, B = X0 MN-major)
+  // dW1[o][i] += sum_s dZ[s][o] X0[s][i]          (A = dZ^T K-major, B = X0 MN-major)
   OB_DEV void issue_dw1(uint32_t acc) {
-    constexpr uint32_t id = tc::idesc_bf16(128, D0, true, true);
-    tc_mma3<T_W1, G.Hh, G.Hl, G.SAh, kTcLB, 2 * G.SAh, G.X0h, G.X0l, G.SAx, kTcLB, 2 * G.SAx,
+    constexpr uint32_t id = tc::idesc_bf16(128, D0, false, true);
+    tc_mma3<T_W1, G.Hh, G.Hl, 128, G.SAh, 256, G.X0h, G.X0l, G.SAx, kTcLB, 2 * G.SAx,
             kTcNS / 16, id>(acc);
     if constexpr (NMB == 2)
-      tc_mma3<T_W1 + D0, G.Hh + 16 * kTcLB, G.Hl + 16 * kTcLB, G.SAh, kTcLB, 2 * G.SAh, G.X0h,
+      tc_mma3<T_W1 + D0, G.Hh + 16 * G.SAh, G.Hl + 16 * G.SAh, 128, G.SAh, 256, G.X0h,
               G.X0l, G.SAx, kTcLB, 2 * G.SAx, kTcNS / 16, id>(acc);
   }
-  // dX[i][s] = sum_o W1[o][i] dZ[s][o]            (A = W1 MN-major, B = dZ K-major, M = 64)
+  // dX[i][s] = sum_o W1[o][i] dZ[s][o]            (A = W1 MN-major, B = dZ^T MN-major, M = 64)
   OB_DEV void issue_dx() {
-    constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, true, false);
-    tc_mma3<T_ACC2, G.W1h, G.W1l, G.SA1, 128, 2 * G.SA1, G.Hh, G.Hl, kTcLB, G.SAh, 2 * kTcLB,
+    constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, true, true);
+    tc_mma3<T_ACC2, G.W1h, G.W1l, G.SA1, 128, 2 * G.SA1, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh,
             H / 16, id>(0);
   }
 
@@ -233,12 +234,23 @@ struct TcMlpAdapter {
     const uint32_t ta = T_ACC1 + ((uint32_t)(q * 32) << 16) + 32 * mb + c0;
     if constexpr (CW == 16) tc::ld16(ta, v); else tc::ld8(ta, v);
   }
-  OB_DEV void put_hid(int s, int o, float a) {
-    uint16_t hi, lo;
-    tc::split_bf16(a, hi, lo);
-    const uint32_t off = tc::blk(s, o, G.SAh, kTcLB);
-    *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Hh + off) = hi;
-    *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Hl + off) = lo;
+  // CW consecutive samples c0.. of hidden unit o -> H^T (hi, lo): 16-byte vector stores
+  OB_DEV void put_hid(int c0, int o, const float* a) {
+    const uint32_t off = tc::blk(o, c0, G.SAh, 128);
+#pragma unroll
+    for (int g8 = 0; g8 < CW / 8; ++g8) {
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint16_t h0, l0, h1, l1;
+        tc::split_bf16(a[8 * g8 + 2 * q], h0, l0);
+        tc::split_bf16(a[8 * g8 + 2 * q + 1], h1, l1);
+        hw[q] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+        lw[q] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+      }
+      *reinterpret_cast<uint4*>(ob_tc_smem + G.Hh + off + 128 * g8) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(ob_tc_smem + G.Hl + off + 128 * g8) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
   }
   // act(z + b1 + t w1t) -> H (hi, lo); act' kept in registers for a VJP
   template <bool kVjp>
@@ -247,13 +259,14 @@ struct TcMlpAdapter {
     int o, c0, cg;
     ld_hidden(v, o, c0, cg);
     const float bo = b1()[o], wt = w1t()[o];
+    float a[16];
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
       const float z = v[j] + bo + tcur * wt;
-      const float a = act == OB_ACT_TANH ? fast_tanh(z) : z;
-      if (kVjp) ap[j] = act == OB_ACT_TANH ? 1.f - a * a : 1.f;
-      put_hid(c0 + j, o, a);
+      a[j] = act == OB_ACT_TANH ? fast_tanh(z) : z;
+      if (kVjp) ap[j] = act == OB_ACT_TANH ? 1.f - a[j] * a[j] : 1.f;
     }
+    put_hid(c0, o, a);
   }
   // M = 64 accumulator (rows m = 16 q + lane for lanes < 16) -> dst[s][m] (+ b2)
   OB_DEV void epi_state(T* dst, int ldo, bool bias) {
@@ -336,10 +349,10 @@ struct TcMlpAdapter {
       float ps = 0.f;
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
-        const float dz = v[j] * ap[j];
-        ps += dz;
-        put_hid(c0 + j, o, dz);
+        v[j] *= ap[j];
+        ps += v[j];
       }
+      put_hid(c0, o, v);
       // V is free now: partial sums part[k][o], k = column group within the row
       float* part = reinterpret_cast<float*>(ob_tc_smem + G.Vh);
       part[(cg % (4 / NMB)) * H + o] = ps;
