@@ -154,6 +154,14 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
       // E elements per thread at once: every stage-derivative load of all of them in
       // flight before the ordered sums (L2 latency paid once per stage)
       constexpr int E = F::kCombineElems;
+      T ca[OB_MAX_STAGES];   // T(h a_iq) once per stage (uniform), exact zeros skipped
+      bool nz[OB_MAX_STAGES];
+#pragma unroll
+      for (int q = 0; q < OB_MAX_STAGES; ++q) {
+        const double aiq = q < i ? p.a[i * OB_MAX_STAGES + q] : 0.0;
+        nz[q] = aiq != 0.0;
+        ca[q] = T(h * aiq);
+      }
       for (int b0 = threadIdx.x; b0 < Rt * N; b0 += E * blockDim.x) {
         T kv[E][OB_MAX_STAGES];
 #pragma unroll
@@ -169,10 +177,8 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
           if (idx >= Rt * N) continue;
           T v = u[r * ldn + j];
 #pragma unroll
-          for (int q = 0; q < OB_MAX_STAGES; ++q) {
-            const double aiq = q < i ? p.a[i * OB_MAX_STAGES + q] : 0.0;
-            if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), kv[e][q]));
-          }
+          for (int q = 0; q < OB_MAX_STAGES; ++q)
+            if (nz[q]) v = Num<T>::add(v, Num<T>::mul(ca[q], kv[e][q]));
           if (j < nin) f.put(r, j, v);
           if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * N + j] = v;
         }
@@ -212,6 +218,14 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
   int bad = 0;
   if constexpr (F::kCombineElems > 1) {
     constexpr int E = F::kCombineElems;
+    T cb[OB_MAX_STAGES];
+    bool nz[OB_MAX_STAGES];
+#pragma unroll
+    for (int q = 0; q < OB_MAX_STAGES; ++q) {
+      const double bq = q < s ? p.b[q] : 0.0;
+      nz[q] = bq != 0.0;
+      cb[q] = T(h * bq);
+    }
     for (int b0 = threadIdx.x; b0 < Rt * N; b0 += E * blockDim.x) {
       T kv[E][OB_MAX_STAGES];
 #pragma unroll
@@ -227,10 +241,8 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
         if (idx >= Rt * N) continue;
         T v = u[r * ldn + j];
 #pragma unroll
-        for (int q = 0; q < OB_MAX_STAGES; ++q) {
-          const double bq = q < s ? p.b[q] : 0.0;
-          if (bq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * bq), kv[e][q]));
-        }
+        for (int q = 0; q < OB_MAX_STAGES; ++q)
+          if (nz[q]) v = Num<T>::add(v, Num<T>::mul(cb[q], kv[e][q]));
         u[r * ldn + j] = v;
         if (r < Rv) {
           if (!Num<T>::finite(v)) bad = 1;
@@ -627,6 +639,15 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       // w_i = b_i lam_{n+1} + sum_{j>i, a_ji != 0} a_ji Lam_j   (pad rows stay 0)
       if constexpr (F::kCombineElems > 1) {
         constexpr int E = F::kCombineElems;
+        T ca[OB_MAX_STAGES];
+        bool nz[OB_MAX_STAGES];
+#pragma unroll
+        for (int j = 0; j < OB_MAX_STAGES; ++j) {
+          const double aji = (j > i && j < s) ? p.a[j * OB_MAX_STAGES + i] : 0.0;
+          nz[j] = aji != 0.0;
+          ca[j] = T(aji);
+        }
+        const T bi = T(p.b[i]);
         for (int b0 = threadIdx.x; b0 < Rt * N; b0 += E * blockDim.x) {
           T lv[E][OB_MAX_STAGES];
           T xs[E];
@@ -643,12 +664,10 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
           for (int e = 0; e < E; ++e) {
             const int idx = b0 + e * blockDim.x, r = idx / N, jj = idx % N, o = r * ldn + jj;
             if (idx >= Rt * N) continue;
-            T v = Num<T>::mul(T(p.b[i]), lam[o]);
+            T v = Num<T>::mul(bi, lam[o]);
 #pragma unroll
-            for (int j = 0; j < OB_MAX_STAGES; ++j) {
-              const double aji = (j > i && j < s) ? p.a[j * OB_MAX_STAGES + i] : 0.0;
-              if (aji != 0.0) v = Num<T>::add(v, Num<T>::mul(T(aji), lv[e][j]));
-            }
+            for (int j = 0; j < OB_MAX_STAGES; ++j)
+              if (nz[j]) v = Num<T>::add(v, Num<T>::mul(ca[j], lv[e][j]));
             w[o] = v;
             if (r < Rv && jj < nin) f.put(r, jj, xs[e]);   // stage state U_i into the field input
           }

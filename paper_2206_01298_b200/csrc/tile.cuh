@@ -106,7 +106,7 @@ struct PhaseTimer {
   unsigned long long* acc;
   __device__ __forceinline__ explicit PhaseTimer(unsigned long long* a) : t0(0), acc(a) {
 #ifdef __CUDA_ARCH__
-    t0 = clock64();
+    if (acc) t0 = clock64();   // no clock read when profiling is off
 #endif
   }
   __device__ __forceinline__ void mark(int ph) {   // call right after a __syncthreads
