@@ -133,3 +133,53 @@ def test_ineligible_shapes_fall_back_to_simt():
         assert res.device["tensor_cores"] == 0, (n, hidden, act)
         e = errs(res, ref)
         assert max(e.values()) <= TOL32, e
+
+
+@pytest.mark.parametrize("kind,scaled", [("mse", False), ("mae", True)])
+def test_observation_losses_on_tensor_cores(kind, scaled):
+    """Observation seeds injected between reversed steps (adjoint.py:235-253) with the
+    tensor-core tile's h-prescaled VJP and TMEM-resident parameter cotangent."""
+    from oracle import obs_losses as ol
+    from paper_2206_01298_b200.losses import LossSpec, MinMaxScaling
+    rng = np.random.default_rng(11)
+    widths, theta = make_mlp(rng, 64, 256, "tanh", True)
+    B, n_steps = 200, 8
+    u0 = f32(rng.normal(size=(B, 64)))
+    times = (0.25, 0.5, 1.0)
+    vals = [f32(rng.normal(size=(B, 64))) for _ in times]
+    lo = hi = None
+    if scaled:
+        lo, hi = f32(rng.uniform(-2, -1, 64)), f32(rng.uniform(1, 2, 64))
+        hi[3] = lo[3]   # a degenerate component passes through (losses.py:27-33)
+    loss = LossSpec(kind, times, tuple(vals), MinMaxScaling(lo, hi) if scaled else None)
+    model = MlpModel(MlpSpec(widths, "tanh", time_input=True, dtype="f32"), theta)
+    res = grad(MlpField(model), tableau_catalog("dopri5"), loss,
+               torch.as_tensor(u0, dtype=torch.float32, device="cuda"), 0.0, 1.0,
+               FixedController(n_steps), CheckpointPolicy.parse("revolve:3"))
+    assert res.device["tensor_cores"] == 1
+    obs = ol.ObsLoss(kind, ol.match_boundaries(times, np.linspace(0, 1, n_steps + 1)),
+                     np.stack(vals), ol.MinMax(lo, hi) if scaled else None)
+    ref = oc.grad_terminal(oc.MlpField(oc.Mlp(widths, "tanh", theta, True)), "dopri5", u0, 0.0, 1.0,
+                           n_steps, "revolve:3", obs=obs)
+    assert abs(res.loss - ref["loss"]) <= 1e-4 * abs(ref["loss"])
+    assert oc.rel_error(np_(res.dtheta), ref["dtheta"]) <= TOL32
+    assert oc.rel_error(np_(res.du0), ref["du0"]) <= TOL32
+    assert oc.rel_error(np.stack([np_(p) for p in res.predictions]), np.stack(ref["predictions"])) <= TOL32
+
+
+def test_mse_target_loss_on_tensor_cores():
+    rng = np.random.default_rng(5)
+    widths, theta = make_mlp(rng, 32, 128, "tanh", False)
+    u0 = f32(rng.normal(size=(150, 32)))
+    target = f32(rng.normal(size=(150, 32)))
+    model = MlpModel(MlpSpec(widths, "tanh", time_input=False, dtype="f32"), theta)
+    res = grad(MlpField(model), tableau_catalog("rk4"), terminal_loss("mse", 1.0, target),
+               torch.as_tensor(u0, dtype=torch.float32, device="cuda"), 0.0, 1.0,
+               FixedController(10), CheckpointPolicy.parse("store_all"))
+    res64 = grad(MlpField(MlpModel(MlpSpec(widths, "tanh", time_input=False), theta)),
+                 tableau_catalog("rk4"), terminal_loss("mse", 1.0, target), u0, 0.0, 1.0,
+                 FixedController(10), CheckpointPolicy.parse("store_all"))
+    assert res.device["tensor_cores"] == 1 and res64.device["tensor_cores"] == 0
+    assert abs(res.loss - res64.loss) <= 1e-4 * abs(res64.loss)
+    assert oc.rel_error(np_(res.dtheta), np_(res64.dtheta)) <= TOL32
+    assert oc.rel_error(np_(res.du0), np_(res64.du0)) <= TOL32
