@@ -396,8 +396,11 @@ def main():
         nmb, t = H // 128, dev["tiles"]
         ev = 2 * 3 * (128 * 32 * D0 * nmb + 64 * 32 * H)                    # one f-eval
         vj = 2 * 3 * (4 * 128 * 32 * D0 * nmb + 64 * 32 * H)   # z, dW2^T, dH, dW1 + dX
-        dev_fwd = t * (dev["device_rhs_evals"] - replays * s) * ev
-        dev_rev = t * (replays * s * ev + dev["device_vjp_evals"] * vj)
+        tab = scheme.tableau
+        unused = sum(1 for i in range(s) if tab.b[i] == 0.0 and not np.any(tab.a[i + 1:, i]))
+        rs = replays * (s - unused)          # replayed stage evaluations the device executes
+        dev_fwd = t * (dev["device_rhs_evals"] - rs) * ev
+        dev_rev = t * (rs * ev + dev["device_vjp_evals"] * vj)
         ex = dev_rev if dom == "reverse" else dev_fwd
         tc_extra = {"tensor_pipe_flops_per_launch": ex,
                     "tensor_pipe_tflops": ex / (dms / 1e3) / 1e12,

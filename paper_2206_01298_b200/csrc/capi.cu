@@ -712,6 +712,14 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   c.nfe_backward = s * nt;
   c.steps_accepted = nt;
   c.device_rhs_evals = c.nfe_forward;
+  if (!P.theta && !P.adaptive) {
+    // stages whose derivative no later stage and no update uses are not evaluated on the
+    // device (dopri5 stage 7 outside the FSAL carry: replays and the final forward step)
+    const long long unused = __builtin_popcount(P.skip_vjp);
+    const bool carried = p.scheme.fsal && (P.skip_vjp >> (s - 1) & 1u);
+    c.device_rhs_evals -= c.steps_recomputed * unused + (nt - 1) * (unused - (carried ? 1 : 0)) +
+                          (nt > 0 ? unused : 0);
+  }
   c.device_vjp_evals = (s - __builtin_popcount(P.skip_vjp)) * nt;
   if (P.theta) {  // data dependent: filled from the per-sample device counters after the run
     c.nfe_forward = c.nfe_backward = c.device_rhs_evals = c.device_vjp_evals = 0;

@@ -142,9 +142,12 @@ struct MlpAdapter {
 // ks: this tile's stage-derivative scratch [s][Rt][ldn].  rec (nullable):
 // record base for this step ([s+1][B][N]).  On return `u` holds u_next.
 // Returns false (block-uniform) if u_next has a non-finite entry.
+// keep_last: k_{s-1} feeds the next step (FSAL carry); otherwise stages whose
+// derivative nothing uses (p.skip_vjp: b_i = 0 and a_ji = 0 for j > i) are not
+// evaluated (their stage state is still recorded).
 template <typename T, class F>
 OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, double h, bool carry,
-                         T* rec, int row0, int Rv) {
+                         T* rec, int row0, int Rv, bool keep_last = false) {
   const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt, s = p.s, nin = f.nin();
   const long long kst = (long long)Rt * ldn;
   const long long vec = (long long)p.B * N;
@@ -210,7 +213,7 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
     if (i == 0 && carry) {  // FSAL: k_0 of this step is k_{s-1} of the previous one
       for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) ks[idx] = ks[(s - 1) * kst + idx];
       __syncthreads();
-    } else {
+    } else if (!((p.skip_vjp >> i) & 1u) || (keep_last && i == s - 1)) {
       f.eval(ks + i * kst);
     }
     pt.mark(9);   // field eval
@@ -562,7 +565,8 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
     }
     T* rec = p.fwd_rec[n] >= 0 ? p.rec + (long long)p.fwd_rec[n] * (p.s + 1) * vec : nullptr;
     PhaseTimer pt(p.prof ? p.phase : nullptr);
-    const bool ok = rk_step_tile<T, F>(p, f, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv);
+    const bool ok = rk_step_tile<T, F>(p, f, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv,
+                                       p.fsal && n + 1 < p.n_steps);
     pt.mark(kPhFwdStep);
     if (!ok) {  // integrators.py:219-220
       if (threadIdx.x == 0) set_status(p.status, OB_ERR_INTEGRATION, n);
