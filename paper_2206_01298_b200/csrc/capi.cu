@@ -17,6 +17,9 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
+#include <cstdio>
+
 #include "../../include/odeblock.h"
 #include "revolve.h"
 #include "rk.cuh"
@@ -784,6 +787,8 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   return OB_OK;
 }
 
+thread_local std::chrono::steady_clock::time_point g_t_entry;   // OB_HOST_TIMING
+
 template <typename T>
 int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
              const void* cadj_dphi = nullptr) {
@@ -947,6 +952,7 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
                                 static_cast<T*>(b.dhead), st));
   }
   CU(cudaEventRecord(ev[4], st));
+  const auto t_issued = std::chrono::steady_clock::now();
   int hs[2] = {0, 0};
   CU(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
   std::vector<int> hstats;
@@ -958,6 +964,12 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
     CU(cudaMemcpyAsync(b.sample_stats, stats, sizeof(int) * (size_t)p.batch * OB_NSTATS,
                        cudaMemcpyDeviceToDevice, st));
   CU(cudaStreamSynchronize(st));
+  if (getenv("OB_HOST_TIMING")) {
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "ob_grad host: issue %.1f us, sync wait %.1f us\n",
+            std::chrono::duration<double, std::micro>(t_issued - g_t_entry).count(),
+            std::chrono::duration<double, std::micro>(now - t_issued).count());
+  }
   if (P.theta || P.adaptive) {  // reference-semantics counters of the critical-path trajectory
     long long mf = 0, mb = 0, ma = 0, mr = 0, mc = 0;
     for (long long i = 0; i < p.batch; ++i) {
@@ -1039,19 +1051,67 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
 
 }  // namespace
 
+// The plan of the last gradient problem, reused while the problem (struct and the host
+// arrays it points to) and the device are unchanged: ob_grad_workspace_size + ob_grad
+// on a training / benchmark loop then plan once.
+namespace {
+std::vector<char> plan_key(const ob_problem& p) {
+  ob_problem q = p;
+  q.times = nullptr;
+  q.obs_steps = nullptr;
+  q.obs_times = nullptr;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) cudaGetLastError();
+  std::vector<char> k(sizeof(q) + sizeof(dev));
+  std::memcpy(k.data(), &q, sizeof(q));
+  std::memcpy(k.data() + sizeof(q), &dev, sizeof(dev));
+  auto app = [&](const void* src, size_t n) {
+    if (!src || !n) return;
+    const size_t o = k.size();
+    k.resize(o + n);
+    std::memcpy(k.data() + o, src, n);
+  };
+  if (!p.adaptive && p.n_steps >= 0) app(p.times, sizeof(double) * (size_t)(p.n_steps + 1));
+  if (p.n_obs > 0) {
+    app(p.obs_steps, sizeof(int32_t) * (size_t)p.n_obs);
+    app(p.obs_times, sizeof(double) * (size_t)p.n_obs);
+  }
+  return k;
+}
+
+int cached_plan(const ob_problem& p, Plan& P) {
+  static thread_local std::vector<char> key;
+  static thread_local Plan plan;
+  static thread_local bool valid = false;
+  std::vector<char> k = plan_key(p);
+  if (valid && k == key) {
+    P = plan;
+    return OB_OK;
+  }
+  valid = false;
+  int st = plan_problem(p, P, true);
+  if (st) return st;
+  key = std::move(k);
+  plan = P;
+  valid = true;
+  return OB_OK;
+}
+}  // namespace
+
 extern "C" int ob_grad_workspace_size(const ob_problem* p, size_t* bytes) {
   if (!p || !bytes) return fail(OB_ERR_VALUE, "null argument");
   Plan P;
-  int st = plan_problem(*p, P, true);
+  int st = cached_plan(*p, P);
   if (st) return st;
   *bytes = P.total;
   return OB_OK;
 }
 
 extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream) {
+  g_t_entry = std::chrono::steady_clock::now();
   if (!p || !b) return fail(OB_ERR_VALUE, "null argument");
   Plan P;
-  int st = plan_problem(*p, P, true);
+  int st = cached_plan(*p, P);
   if (st) return st;
   if (!b->workspace || b->workspace_bytes < P.total)
     return fail(OB_ERR_VALUE, "workspace too small (need " + std::to_string(P.total) + " bytes)");

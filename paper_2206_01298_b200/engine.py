@@ -151,7 +151,7 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     u_final = torch.empty_like(u0d)
     du0 = torch.empty_like(u0d)
     dtheta = torch.empty(field.n_params, dtype=dt, device=dev)
-    loss_t = torch.zeros(1, dtype=torch.float64, device=dev)
+    loss_t = torch.empty(1, dtype=torch.float64, device=dev)   # written by the reduction
     preds = obs_vals = lo = hi = None
     if obs:
         vals = []
@@ -186,7 +186,7 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     bufs.loss = loss_t.data_ptr()
     bufs.workspace = ws.data_ptr()
     bufs.workspace_bytes = ws.numel()
-    stats = torch.zeros((B, _lib.OB_NSTATS), dtype=torch.int32, device=dev)
+    stats = torch.empty((B, _lib.OB_NSTATS), dtype=torch.int32, device=dev)   # copied from the zeroed device stats
     bufs.sample_stats = stats.data_ptr()
     dhead = None
     if loss.kind == "ce_head":
