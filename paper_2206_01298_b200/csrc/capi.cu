@@ -430,6 +430,14 @@ bool tc_eligible(const ob_problem& p, const Plan& P) {
   // pre-activations across it (measured 3.7e-4 on du0), so ReLU keeps the fp32 SIMT tile
   if (f.activation != OB_ACT_TANH && f.activation != OB_ACT_IDENTITY) return false;
   if ((p.flags & OB_FLAG_NO_TENSOR_CORES) || getenv("OB_NO_TC")) return false;
+  // stage derivatives live in TMEM slots 0..5 during reverse-sweep replays: stages >= 6
+  // must be ones a replay never evaluates (b_i = 0 and a_ji = 0 for j > i; dopri5's 7th)
+  const int s = p.scheme.stages;
+  for (int i = 6; i < s; ++i) {
+    bool unused = p.scheme.b[i] == 0.0;
+    for (int j = i + 1; j < s && unused; ++j) unused = p.scheme.a[j * OB_MAX_STAGES + i] == 0.0;
+    if (!unused) return false;
+  }
   const int N = f.widths[2];
   return tc_shape_supported(N, f.widths[1], N);
 }

@@ -85,6 +85,7 @@ struct MlpAdapter {
   static constexpr bool kScaledVjp = false;  // vjp returns J^T w; the caller scales by h
   static constexpr int kCombineBatch = 4;    // stage loads in flight per ordered sum (registers)
   static constexpr int kCombineElems = 1;    // elements per thread combined together
+  static constexpr bool kOwnsStep = false;   // the adapter runs whole RK steps itself
   OB_DEV void finish(T*) {}   // flush device-resident parameter cotangents (none here)
   OB_DEV void release() {}    // free per-CTA hardware resources (none here)
 
@@ -565,8 +566,12 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
     }
     T* rec = p.fwd_rec[n] >= 0 ? p.rec + (long long)p.fwd_rec[n] * (p.s + 1) * vec : nullptr;
     PhaseTimer pt(p.prof ? p.phase : nullptr);
-    const bool ok = rk_step_tile<T, F>(p, f, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv,
-                                       p.fsal && n + 1 < p.n_steps);
+    bool ok;
+    if constexpr (F::kOwnsStep)
+      ok = f.step(u, t, h, p.fsal && n > 0, rec, row0, p.fsal && n + 1 < p.n_steps);
+    else
+      ok = rk_step_tile<T, F>(p, f, u, ks, t, h, p.fsal && n > 0, rec, row0, Rv,
+                              p.fsal && n + 1 < p.n_steps);
     pt.mark(kPhFwdStep);
     if (!ok) {  // integrators.py:219-220
       if (threadIdx.x == 0) set_status(p.status, OB_ERR_INTEGRATION, n);
@@ -626,7 +631,10 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       load_rows(u, ldn, srcp, N, row0, Rv);
       __syncthreads();
       T* rec = p.rec + (long long)op.w * (s + 1) * vec;
-      rk_step_tile<T, F>(p, f, u, ks, t, h, false, rec, row0, Rv);
+      if constexpr (F::kOwnsStep)
+        f.step(u, t, h, false, rec, row0, false);
+      else
+        rk_step_tile<T, F>(p, f, u, ks, t, h, false, rec, row0, Rv);
       pt.mark(kPhReplay);
       continue;
     }

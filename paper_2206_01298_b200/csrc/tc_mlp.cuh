@@ -89,9 +89,9 @@ extern __shared__ __align__(128) unsigned char ob_tc_smem[];
 // 3-pass split product D (+)= A B over KS K-slices of 16, all geometry constant:
 // (AH, AL) / (BH, BL): byte offsets of the hi / lo copies, *LB / *SB: the
 // descriptor's leading / stride byte offsets, *ST: address step per K-slice
-template <uint32_t D, uint32_t AH, uint32_t AL, uint32_t ALB, uint32_t ASB, uint32_t AST,
+template <uint32_t AH, uint32_t AL, uint32_t ALB, uint32_t ASB, uint32_t AST,
           uint32_t BH, uint32_t BL, uint32_t BLB, uint32_t BSB, uint32_t BST, int KS, uint32_t ID>
-OB_DEV void tc_mma3(uint32_t first_acc) {
+OB_DEV void tc_mma3(uint32_t D, uint32_t first_acc) {
   const uint32_t sb = tc::smem_u32(ob_tc_smem);
 #pragma unroll
   for (int k = 0; k < KS; ++k) {
@@ -110,12 +110,17 @@ struct TcMlpAdapter {
   static constexpr bool kScaledVjp = true;   // vjp returns J^T (h w)
   static constexpr int kCombineBatch = 8;    // all stage loads in flight (no register pressure)
   static constexpr int kCombineElems = 4;    // ... for 4 elements per thread at once
+  static constexpr bool kOwnsStep = true;    // step(): stage derivatives stay in TMEM
   static constexpr uint32_t kCols = 512;     // whole TMEM: one CTA per SM, base column 0
   static constexpr TcGeom G = tc_geom(D0, H, D2);
   static constexpr int NMB = H / 128;
   static constexpr int CW = 8 * NMB;         // hidden-epilogue columns per thread
   // TMEM columns (lane 0 base = 0: 512 columns allocated by the only CTA on the SM)
-  static constexpr uint32_t T_ACC1 = 0, T_ACC2 = 64, T_W2 = 128, T_W1 = 256;
+  // acc1: hidden accumulator; stage slots k (M = 64 out accumulators, the step's stage
+  // derivatives kept on chip) at 64 + 32 k; acc2 (the VJP's dX) shares slot 0; dW2^T, dW1
+  // of the reverse sweep.  The reverse kernel's replays use slots 0..5 only (see tc_eligible).
+  static constexpr uint32_t T_ACC1 = 0, T_ACC2 = 64, T_W2 = 256, T_W1 = 384;
+  static constexpr uint32_t slot_col(int k) { return 64u + 32u * (uint32_t)k; }
 
   const RkParams<T>& p;
   uint32_t phase;       // mbarrier parity
@@ -180,48 +185,48 @@ struct TcMlpAdapter {
   // z[o][s] = sum_i W1[o][i] X0[s][i]           (A = W1 K-major, B = X0 K-major)
   OB_DEV void issue_hidden() {
     constexpr uint32_t id = tc::idesc_bf16(128, kTcNS, false, false);
-    tc_mma3<T_ACC1, G.W1h, G.W1l, 128, G.SA1, 256, G.X0h, G.X0l, kTcLB, G.SAx, 2 * kTcLB, D0 / 16, id>(0);
+    tc_mma3<G.W1h, G.W1l, 128, G.SA1, 256, G.X0h, G.X0l, kTcLB, G.SAx, 2 * kTcLB, D0 / 16, id>(T_ACC1, 0);
     if constexpr (NMB == 2)
-      tc_mma3<T_ACC1 + 32, G.W1h + 16 * G.SA1, G.W1l + 16 * G.SA1, 128, G.SA1, 256, G.X0h, G.X0l,
-              kTcLB, G.SAx, 2 * kTcLB, D0 / 16, id>(0);
+      tc_mma3<G.W1h + 16 * G.SA1, G.W1l + 16 * G.SA1, 128, G.SA1, 256, G.X0h, G.X0l,
+              kTcLB, G.SAx, 2 * kTcLB, D0 / 16, id>(T_ACC1 + 32, 0);
   }
   // out[o2][s] = sum_i2 W2[o2][i2] H[s][i2]      (M = 64; B = H^T MN-major)
-  OB_DEV void issue_out() {
+  OB_DEV void issue_out(uint32_t dst = T_ACC2) {
     constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, false, true);
-    tc_mma3<T_ACC2, G.W2h, G.W2l, 128, G.SA2, 256, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh, H / 16, id>(0);
+    tc_mma3<G.W2h, G.W2l, 128, G.SA2, 256, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh, H / 16, id>(dst, 0);
   }
   // dW2^T[i2][o2] += sum_s H[s][i2] V[s][o2]     (A = H^T K-major, B = V MN-major)
   OB_DEV void issue_dw2(uint32_t acc) {
     constexpr uint32_t id = tc::idesc_bf16(128, D2, false, true);
-    tc_mma3<T_W2, G.Hh, G.Hl, 128, G.SAh, 256, G.Vh, G.Vl, G.SAv, kTcLB, 2 * G.SAv,
-            kTcNS / 16, id>(acc);
+    tc_mma3<G.Hh, G.Hl, 128, G.SAh, 256, G.Vh, G.Vl, G.SAv, kTcLB, 2 * G.SAv,
+            kTcNS / 16, id>(T_W2, acc);
     if constexpr (NMB == 2)
-      tc_mma3<T_W2 + D2, G.Hh + 16 * G.SAh, G.Hl + 16 * G.SAh, 128, G.SAh, 256, G.Vh, G.Vl,
-              G.SAv, kTcLB, 2 * G.SAv, kTcNS / 16, id>(acc);
+      tc_mma3<G.Hh + 16 * G.SAh, G.Hl + 16 * G.SAh, 128, G.SAh, 256, G.Vh, G.Vl,
+              G.SAv, kTcLB, 2 * G.SAv, kTcNS / 16, id>(T_W2 + D2, acc);
   }
   // dH[i2][s] = sum_o2 W2[o2][i2] V[s][o2]       (A = W2 MN-major, B = V K-major)
   OB_DEV void issue_dh() {
     constexpr uint32_t id = tc::idesc_bf16(128, kTcNS, true, false);
-    tc_mma3<T_ACC1, G.W2h, G.W2l, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl, kTcLB, G.SAv, 2 * kTcLB,
-            D2 / 16, id>(0);
+    tc_mma3<G.W2h, G.W2l, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl, kTcLB, G.SAv, 2 * kTcLB,
+            D2 / 16, id>(T_ACC1, 0);
     if constexpr (NMB == 2)
-      tc_mma3<T_ACC1 + 32, G.W2h + 16 * 128, G.W2l + 16 * 128, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl,
-              kTcLB, G.SAv, 2 * kTcLB, D2 / 16, id>(0);
+      tc_mma3<G.W2h + 16 * 128, G.W2l + 16 * 128, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl,
+              kTcLB, G.SAv, 2 * kTcLB, D2 / 16, id>(T_ACC1 + 32, 0);
   }
   // dW1[o][i] += sum_s dZ[s][o] X0[s][i]          (A = dZ^T K-major, B = X0 MN-major)
   OB_DEV void issue_dw1(uint32_t acc) {
     constexpr uint32_t id = tc::idesc_bf16(128, D0, false, true);
-    tc_mma3<T_W1, G.Hh, G.Hl, 128, G.SAh, 256, G.X0h, G.X0l, G.SAx, kTcLB, 2 * G.SAx,
-            kTcNS / 16, id>(acc);
+    tc_mma3<G.Hh, G.Hl, 128, G.SAh, 256, G.X0h, G.X0l, G.SAx, kTcLB, 2 * G.SAx,
+            kTcNS / 16, id>(T_W1, acc);
     if constexpr (NMB == 2)
-      tc_mma3<T_W1 + D0, G.Hh + 16 * G.SAh, G.Hl + 16 * G.SAh, 128, G.SAh, 256, G.X0h,
-              G.X0l, G.SAx, kTcLB, 2 * G.SAx, kTcNS / 16, id>(acc);
+      tc_mma3<G.Hh + 16 * G.SAh, G.Hl + 16 * G.SAh, 128, G.SAh, 256, G.X0h,
+              G.X0l, G.SAx, kTcLB, 2 * G.SAx, kTcNS / 16, id>(T_W1 + D0, acc);
   }
   // dX[i][s] = sum_o W1[o][i] dZ[s][o]            (A = W1 MN-major, B = dZ^T MN-major, M = 64)
   OB_DEV void issue_dx() {
     constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, true, true);
-    tc_mma3<T_ACC2, G.W1h, G.W1l, G.SA1, 128, 2 * G.SA1, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh,
-            H / 16, id>(0);
+    tc_mma3<G.W1h, G.W1l, G.SA1, 128, 2 * G.SA1, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh,
+            H / 16, id>(T_ACC2, 0);
   }
 
   // ---- epilogues (warp w: TMEM lane quarter q = w % 4, column group cg = w / 4)
@@ -302,6 +307,114 @@ struct TcMlpAdapter {
     tc::fence_before();
     __syncthreads();
     pt.mark(11);
+  }
+
+  // f(x0) into stage slot k (TMEM, bias b2 not yet added); no epilogue
+  OB_DEV void eval_slot(int k) {
+    PhaseTimer pt(p.prof ? p.phase : nullptr);
+    sync_issue();
+    if (tc::uniform_warp() == 0) { issue_hidden(); tc::commit(bar()); }
+    wait();
+    pt.mark(10);
+    float ap[16];
+    epi_hidden<false>(ap);
+    sync_issue();
+    pt.mark(11);
+    if (tc::uniform_warp() == 0) { issue_out(slot_col(k)); tc::commit(bar()); }
+    wait();
+    pt.mark(10);
+  }
+
+  // One explicit RK step of the tile (explicit_rk_step, integrators.py:196-222) with the
+  // stage derivatives k_q = f(U_q) held in TMEM slots: the stage sums read them with
+  // tcgen05.ld in the accumulator layout (warp w: state rows 16 (w%4) + lane for lanes < 16,
+  // samples 8 (w/4) ..+7) -- same order and roundings as rk_step_tile (k = acc + b2, then
+  // v + (h a_iq) k).  carry: FSAL (k_0 = previous k_{s-1}); keep_last: k_{s-1} is carried on.
+  OB_DEV bool step(T* u, double t, double h, bool carry, T* rec, int row0, bool keep_last) {
+    const int s = p.s, ldn = p.d.ldn, Rt = p.Rt;
+    const long long vec = (long long)p.B * D0;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q4 = w & 3, cg = w >> 2;
+    const int m = 16 * q4 + lane, s0 = 8 * cg;
+    const bool mine = lane < 16 && m < D0;
+    const uint32_t lrow = (uint32_t)(32 * q4) << 16;
+    const float b2m = mine ? b2()[m] : 0.f;
+    PhaseTimer pt(p.prof ? p.phase : nullptr);
+    if (carry) {   // FSAL: this step's k_0 is the previous k_{s-1}
+      float v[8];
+      tc::ld8(slot_col(s - 1) + lrow + s0, v);
+      tc::st8(slot_col(0) + lrow + s0, v);
+      tc::wait_st();
+    }
+    for (int i = 0; i < s; ++i) {
+      float ca[OB_MAX_STAGES];
+      bool nz[OB_MAX_STAGES];
+#pragma unroll
+      for (int q = 0; q < OB_MAX_STAGES; ++q) {
+        const double a = q < i ? p.a[i * OB_MAX_STAGES + q] : 0.0;
+        nz[q] = a != 0.0;
+        ca[q] = float(h * a);
+      }
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (mine && s0 + j < Rt) ? u[(s0 + j) * ldn + m] : 0.f;
+#pragma unroll
+      for (int q = 0; q < OB_MAX_STAGES; ++q) {
+        if (!nz[q]) continue;
+        float k[8];
+        tc::ld8(slot_col(q) + lrow + s0, k);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          v[j] = Num<float>::add(v[j], Num<float>::mul(ca[q], Num<float>::add(k[j], b2m)));
+      }
+      if (mine) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = s0 + j;
+          if (r < Rt) put(r, m, v[j]);
+          if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * D0 + m] = v[j];
+        }
+      }
+      put_time(t + p.c[i] * h);
+      pt.mark(8);
+      if (i == 0 && carry) continue;
+      if (!((p.skip_vjp >> i) & 1u) || (keep_last && i == s - 1)) eval_slot(i);
+      pt.mark(9);
+    }
+    // u_next = u + sum_i (h b_i) k_i
+    float cb[OB_MAX_STAGES];
+    bool nzb[OB_MAX_STAGES];
+#pragma unroll
+    for (int q = 0; q < OB_MAX_STAGES; ++q) {
+      const double b = q < s ? p.b[q] : 0.0;
+      nzb[q] = b != 0.0;
+      cb[q] = float(h * b);
+    }
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (mine && s0 + j < Rt) ? u[(s0 + j) * ldn + m] : 0.f;
+#pragma unroll
+    for (int q = 0; q < OB_MAX_STAGES; ++q) {
+      if (!nzb[q]) continue;
+      float k[8];
+      tc::ld8(slot_col(q) + lrow + s0, k);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        v[j] = Num<float>::add(v[j], Num<float>::mul(cb[q], Num<float>::add(k[j], b2m)));
+    }
+    int bad = 0;
+    if (mine) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = s0 + j;
+        if (r < Rt) u[r * ldn + m] = v[j];
+        if (r < Rv) {
+          if (!Num<float>::finite(v[j])) bad = 1;
+          if (rec) rec[s * vec + (long long)(row0 + r) * D0 + m] = v[j];
+        }
+      }
+    }
+    tc::fence_before();
+    return __syncthreads_or(bad) == 0;
   }
 
   // jtv = J^T (h w); mu (nullable) += h P^T w, accumulated on chip until finish()
