@@ -641,6 +641,15 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
     // REVERSE(n) from record buffer op.w: rk_adjoint_step (adjoint.py:67-94)
     obs_inject(p, lam, n + 1, row0, Rv);
     const T* rec = p.rec + (long long)op.w * (s + 1) * vec;
+    if constexpr (F::kOwnsStep) {
+      if (!f.reverse_step(lam, t, h, rec, row0, mu)) {
+        if (threadIdx.x == 0) set_status(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
+        f.release();
+        return;
+      }
+      pt.mark(kPhVjp);
+      continue;
+    }
     for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) lamn[idx] = lam[idx];
     __syncthreads();
     for (int i = s - 1; i >= 0; --i) {

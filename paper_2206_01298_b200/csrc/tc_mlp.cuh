@@ -42,7 +42,7 @@ struct TcGeom {
   int D0, H, D2, nmb;
   uint32_t SA1, SA2, SAx, SAh, SAv;
   uint32_t W2h, W2l, W1h, W1l, fv, packed;
-  uint32_t X0h, X0l, Hh, Hl, Vh, Vl, vec, bar, slot, total;
+  uint32_t X0h, X0l, Hh, Hl, Vh, Vl, vec, pw, bar, slot, total;
 };
 
 __host__ __device__ constexpr TcGeom tc_geom(int D0, int H, int D2) {
@@ -69,6 +69,7 @@ __host__ __device__ constexpr TcGeom tc_geom(int D0, int H, int D2) {
   g.Vh = o;  o += rb * g.SAv;
   g.Vl = o;  o += rb * g.SAv;
   g.vec = o; o += (uint32_t)(2 * H + D2) * 4;       // db1[H] | dwt[H] | db2[D2]
+  g.pw = o;  o += (uint32_t)(4 * D2) * 4;           // db2 partials [4][D2] (reverse_step)
   o = (o + 15) & ~15u;
   g.bar = o; o += 8;
   g.slot = o; o += 8;
@@ -410,6 +411,166 @@ struct TcMlpAdapter {
         if (r < Rv) {
           if (!Num<float>::finite(v[j])) bad = 1;
           if (rec) rec[s * vec + (long long)(row0 + r) * D0 + m] = v[j];
+        }
+      }
+    }
+    tc::fence_before();
+    return __syncthreads_or(bad) == 0;
+  }
+
+  // The VJP pair on the operands already staged (V = h w split, X0 = stage state):
+  // dX (= J^T (h w)) lands in TMEM column dx; parameter cotangents accumulate on chip.
+  // db2_part: add the [4][D2] partial sums of h w in pw to db2 (reverse_step).
+  OB_DEV void vjp_core(T* mu, uint32_t dx, bool db2_part) {
+    PhaseTimer pt(p.prof ? p.phase : nullptr);
+    sync_issue();
+    pt.mark(14);
+    if (tc::uniform_warp() == 0) { issue_hidden(); tc::commit(bar()); }
+    if (mu && db2_part && threadIdx.x < D2) {
+      const float* pw = reinterpret_cast<const float*>(ob_tc_smem + G.pw);
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc += pw[k * D2 + threadIdx.x];
+      db2()[threadIdx.x] += acc;
+    }
+    wait();
+    pt.mark(10);
+    float ap[16];
+    epi_hidden<true>(ap);
+    sync_issue();
+    pt.mark(11);
+    const uint32_t acc = started ? 1u : 0u;
+    if (tc::uniform_warp() == 0) {
+      if (mu) issue_dw2(acc);
+      issue_dh();
+      tc::commit(bar());
+    }
+    wait();
+    pt.mark(10);
+    {
+      float v[16];
+      int o, c0, cg;
+      ld_hidden(v, o, c0, cg);
+      float ps = 0.f;
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        v[j] *= ap[j];
+        ps += v[j];
+      }
+      put_hid(c0, o, v);
+      float* part = reinterpret_cast<float*>(ob_tc_smem + G.Vh);
+      part[(cg % (4 / NMB)) * H + o] = ps;
+    }
+    sync_issue();
+    pt.mark(11);
+    if (tc::uniform_warp() == 0) {
+      if (mu) issue_dw1(acc);
+      constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, true, true);
+      tc_mma3<G.W1h, G.W1l, G.SA1, 128, 2 * G.SA1, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh, H / 16, id>(dx, 0);
+      tc::commit(bar());
+    }
+    if (mu && threadIdx.x < H) {
+      const float* part = reinterpret_cast<const float*>(ob_tc_smem + G.Vh);
+      float sm = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4 / NMB; ++k) sm += part[k * H + threadIdx.x];
+      db1()[threadIdx.x] += sm;
+      dwt()[threadIdx.x] += tcur * sm;
+    }
+    wait();
+    pt.mark(10);
+    if (mu) started = true;
+  }
+
+  // One reverse step (rk_adjoint_step, adjoint.py:67-94) with the stage cotangents
+  // Lambda_i = J^T (h w_i) held in TMEM slots: w_i = b_i lam + sum_{j>i} a_ji Lambda_j is
+  // formed from tcgen05.ld in the accumulator layout, split straight into V; the
+  // stage state U_i comes from the record (prefetched one stage ahead); at the end
+  // lam += Lambda_{s-1} + ... + Lambda_0 (the reference's order).  Returns false on a
+  // non-finite adjoint state (AdjointState.check_finite, adjoint.py:42-44).
+  OB_DEV bool reverse_step(T* lam, double t, double h, const T* rec, int row0, T* mu) {
+    const int s = p.s, ldn = p.d.ldn, Rt = p.Rt;
+    const long long vec = (long long)p.B * D0;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q4 = w & 3, cg = w >> 2;
+    const int m = 16 * q4 + lane, s0 = 8 * cg;
+    const bool mine = lane < 16 && m < D0;
+    const uint32_t lrow = (uint32_t)(32 * q4) << 16;
+    const float hf = float(h);
+    float lv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) lv[j] = (mine && s0 + j < Rt) ? lam[(s0 + j) * ldn + m] : 0.f;
+    float un[8];   // stage state of the next stage to reverse (prefetched)
+    auto load_u = [&](int i) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        un[j] = (mine && s0 + j < Rv) ? rec[i * vec + (long long)(row0 + s0 + j) * D0 + m] : 0.f;
+    };
+    load_u(s - 1);
+    unsigned live = 0;   // slots holding a nonzero Lambda_i
+    for (int i = s - 1; i >= 0; --i) {
+      if ((p.skip_vjp >> i) & 1u) {   // w_i == 0 exactly: Lambda_i = 0 (still counted, B8)
+        if (i > 0) load_u(i - 1);
+        continue;
+      }
+      float ca[OB_MAX_STAGES];
+      bool nz[OB_MAX_STAGES];
+#pragma unroll
+      for (int j = 0; j < OB_MAX_STAGES; ++j) {
+        const double a = (j > i && j < s && ((live >> j) & 1u)) ? p.a[j * OB_MAX_STAGES + i] : 0.0;
+        nz[j] = a != 0.0;
+        ca[j] = float(a);
+      }
+      const float bi = float(p.b[i]);
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = Num<float>::mul(bi, lv[j]);
+#pragma unroll
+      for (int j = 0; j < OB_MAX_STAGES; ++j) {
+        if (!nz[j]) continue;
+        float k[8];
+        tc::ld8(slot_col(j) + lrow + s0, k);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = Num<float>::add(v[e], Num<float>::mul(ca[j], k[e]));
+      }
+      // V = h w (padded samples zero), db2 partial, U_i into X0
+      float ps = 0.f;
+      if (mine) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int r = s0 + e;
+          const float hv = r < Rv ? hf * v[e] : 0.f;
+          ps += hv;
+          uint16_t hi, lo;
+          tc::split_bf16(hv, hi, lo);
+          const uint32_t off = tc::blk(r, m, G.SAv, kTcLB);
+          *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vh + off) = hi;
+          *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vl + off) = lo;
+          if (r < Rt) put(r, m, un[e]);
+        }
+        reinterpret_cast<float*>(ob_tc_smem + G.pw)[cg * D2 + m] = ps;
+      }
+      if (i > 0) load_u(i - 1);
+      put_time(t + p.c[i] * h);
+      vjp_core(mu, slot_col(i), true);
+      live |= 1u << i;
+    }
+    // lam_n = lam_{n+1} + Lambda_{s-1} + ... + Lambda_0
+    int bad = 0;
+#pragma unroll
+    for (int i = OB_MAX_STAGES - 1; i >= 0; --i) {
+      if (i >= s || !((live >> i) & 1u)) continue;
+      float k[8];
+      tc::ld8(slot_col(i) + lrow + s0, k);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) lv[e] = Num<float>::add(lv[e], k[e]);
+    }
+    if (mine) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int r = s0 + e;
+        if (r < Rt) {
+          lam[r * ldn + m] = lv[e];
+          if (!Num<float>::finite(lv[e])) bad = 1;
         }
       }
     }
