@@ -182,6 +182,7 @@ struct Plan {
   bool need_jvp = false;
   bool theta = false;
   bool tc = false;                // tcgen05 tensor-core MLP tile (rk_tc.cu)
+  int s_stages = 0;               // scheme stages (stage scratch sizing)
   int gmres_m = 0;
   size_t off_kry = 0, off_stats = 0, off_cnf = 0, off_state = 0, off_head = 0;
   long long cnf_stride = 0;
@@ -339,7 +340,7 @@ void layout_smem(Plan& P) {
     s.x0 = take(18 * 18 * 68);
     for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
     s.hid[0] = take(18 * 18 * 68);
-    s.tA = s.tB = s.u = s.lam = s.lamn = s.w = s.jtv = s.aux = s.wts = -1;
+    s.tA = s.tB = s.u = s.lam = s.lamn = s.w = s.jtv = s.aux = s.wts = s.ks = -1;
     for (int i = 0; i < 8; ++i) s.vec[i] = -1;
     s.total = o;
     P.smem_bytes = (size_t)o * P.esz;
@@ -378,6 +379,14 @@ void layout_smem(Plan& P) {
   const bool ws_variant = P.esz == 4 && !P.theta && !d.cnf && !d.conv;
   if (ws_variant && (size_t)(o + d.n_packed) * P.esz <= smem_cap(P) && !getenv("OB_NO_SMEM_WEIGHTS")) {
     s.wts = take(d.n_packed);
+    s.total = o;
+  }
+  // explicit-RK stage scratch (k_i forward, Lambda_i reverse) in shared memory when it
+  // fits beside everything else: the stage sums then read it without L2 latency
+  s.ks = -1;
+  const long long kscr = 2LL * P.s_stages * P.Rt * d.ldn;
+  if (!P.theta && P.s_stages > 0 && (size_t)(o + kscr) * P.esz <= smem_cap(P) && !getenv("OB_KS_GLOBAL")) {
+    s.ks = take(kscr);
     s.total = o;
   }
   P.smem_bytes = (size_t)s.total * P.esz;
@@ -458,7 +467,7 @@ bool plan_tc(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   s = SmemLayout{};
   int o = 0;
   auto take = [&](long long n) { int r = o; o += (int)((n + 7) & ~7LL); return r; };
-  s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = -1;
+  s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = s.ks = -1;
   for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
   for (int i = 0; i < 8; ++i) s.vec[i] = -1;
   s.scr_elems = 0;
@@ -688,6 +697,7 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   }
   P.gmres_m = P.theta ? std::min(p.solver.gmres_restart, p.field.widths[p.field.n_layers]) : 0;
   P.smem_reserve = P.adaptive ? kAdaptiveStaticSmem : 0;
+  P.s_stages = (P.adaptive || P.theta) ? 0 : p.scheme.stages;   // fixed explicit: smem stage scratch
   choose_tiles(P, p.field, p.batch, sms);
   if (allow_tc && tc_eligible(p, P)) plan_tc(P, p.field, p.batch, sms);
   if (P.smem_bytes > smem_cap(P)) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");

@@ -19,6 +19,7 @@ struct SmemLayout {      // offsets in elements of T (-1: not allocated)
   int scr, scr_elems;     // theta: split-K scratch for narrow JVP / VJP products
   int kry;                // theta: Krylov workspace in shared memory (or -1: global)
   int wts;                // packed weights staged in shared memory, or -1
+  int ks;                 // per-tile stage scratch [2][s][Rt][ldn] in shared memory, or -1 (global)
   int total;
 };
 

@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
   // replays, so forward and replayed steps sum identically (bit-identical records)
   if (p.sm.u >= 0) f.set_scratch(sm + p.sm.lamn, p.sm.jtv + p.Rt * p.d.ldn - p.sm.lamn);
   T* u = state_buf(p, sm, 0);
-  T* ks = p.scratch + tile * p.scratch_stride;
+  T* ks = p.sm.ks >= 0 ? sm + p.sm.ks : p.scratch + tile * p.scratch_stride;
   const int N = p.d.N, ldn = p.d.ldn;
   const long long vec = (long long)p.B * N;
 
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
   T* lamn = state_buf(p, sm, 2);
   T* w = state_buf(p, sm, 3);
   T* jtv = state_buf(p, sm, 4);
-  T* ks = p.scratch + tile * p.scratch_stride;
+  T* ks = p.sm.ks >= 0 ? sm + p.sm.ks : p.scratch + tile * p.scratch_stride;
   T* Lam = ks + s * kst;
   T* mu = p.mu + tile * p.d.n_mu;
 
@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, 1) cadj_kernel(const __grid_constant
   T* lam = state_buf(p, sm, 1);
   T* li = state_buf(p, sm, 2);     // stage lambda (the VJP cotangent)
   T* jtv = state_buf(p, sm, 4);
-  T* kU = p.scratch + tile * p.scratch_stride;
+  T* kU = p.sm.ks >= 0 ? sm + p.sm.ks : p.scratch + tile * p.scratch_stride;
   T* kL = kU + s * kst;
   T* mu = p.mu + tile * p.d.n_mu;
   load_rows(u, ldn, p.u_final, N, row0, Rv);
