@@ -149,6 +149,32 @@ __device__ __forceinline__ void split_bf16(float x, uint16_t& hi, uint16_t& lo) 
   lo = __bfloat16_as_ushort(l);
 }
 
+// two fp32 -> two (hi, lo) bf16 pairs, packed (element a in the low half): one
+// cvt.rn.bf16x2 per pair for hi and for lo
+__device__ __forceinline__ void split2_bf16(float a, float b, uint32_t& hi2, uint32_t& lo2) {
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi2) : "f"(b), "f"(a));
+  const float ha = __uint_as_float(hi2 << 16), hb = __uint_as_float(hi2 & 0xffff0000u);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo2) : "f"(b - hb), "f"(a - ha));
+}
+
+// tanh with one MUFU op: e = 2^(-2|x| log2 e) on the SFU, 1/(1 + e) by a linear guess
+// and two Newton steps on the FMA pipe (1 + e lies in (1, 2]); |rel err| ~1e-6, well
+// below the 3-pass split's 2^-16 (series near 0 avoids 1 - (1 - eps) cancellation)
+__device__ __forceinline__ float tanh_1sfu(float x) {
+  const float ax = fabsf(x);
+  if (ax < 0.0625f) {
+    const float x2 = x * x;
+    return x * (1.0f + x2 * (-0.33333334f + x2 * (0.13333334f + x2 * -0.053968254f)));
+  }
+  const float e = exp2f(-2.8853900817779268f * ax);
+  const float d = 1.0f + e;
+  float r = fmaf(-0.5f, d, 1.4571068f);      // minimax-ish guess of 1/d on [1, 2] (~3 %)
+  r = fmaf(r, fmaf(-d, r, 1.0f), r);
+  r = fmaf(r, fmaf(-d, r, 1.0f), r);
+  r = fmaf(r, fmaf(-d, r, 1.0f), r);
+  return copysignf((1.0f - e) * r, x);
+}
+
 // byte offset of element (a, b) in a core-blocked operand (see the header comment)
 __host__ __device__ __forceinline__ uint32_t blk(int a, int b, uint32_t SA, uint32_t SB) {
   return (uint32_t)(a >> 3) * SA + (uint32_t)(b >> 3) * SB + (uint32_t)(a & 7) * 16u +

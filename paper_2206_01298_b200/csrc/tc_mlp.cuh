@@ -247,13 +247,7 @@ struct TcMlpAdapter {
     for (int g8 = 0; g8 < CW / 8; ++g8) {
       uint32_t hw[4], lw[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint16_t h0, l0, h1, l1;
-        tc::split_bf16(a[8 * g8 + 2 * q], h0, l0);
-        tc::split_bf16(a[8 * g8 + 2 * q + 1], h1, l1);
-        hw[q] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-        lw[q] = (uint32_t)l0 | ((uint32_t)l1 << 16);
-      }
+      for (int q = 0; q < 4; ++q) tc::split2_bf16(a[8 * g8 + 2 * q], a[8 * g8 + 2 * q + 1], hw[q], lw[q]);
       *reinterpret_cast<uint4*>(ob_tc_smem + G.Hh + off + 128 * g8) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
       *reinterpret_cast<uint4*>(ob_tc_smem + G.Hl + off + 128 * g8) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
@@ -269,7 +263,7 @@ struct TcMlpAdapter {
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
       const float z = v[j] + bo + tcur * wt;
-      a[j] = act == OB_ACT_TANH ? fast_tanh(z) : z;
+      a[j] = act == OB_ACT_TANH ? tc::tanh_1sfu(z) : z;
       if (kVjp) ap[j] = act == OB_ACT_TANH ? 1.f - a[j] * a[j] : 1.f;
     }
     put_hid(c0, o, a);
