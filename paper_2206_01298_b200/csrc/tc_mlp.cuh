@@ -33,7 +33,7 @@
 namespace ob {
 
 constexpr int kTcNS = 32;       // sample columns (MMA N) per tile
-constexpr uint32_t kTcLB = 144; // activation block-column stride (128 + 16: conflict-free stores)
+constexpr uint32_t kTcRow = (kTcNS / 8) * 128u;   // activation tiles stored transposed [feature][sample]
 
 // shared-memory geometry of the tensor-core tile (bytes from the start of dynamic
 // shared memory, where the region sits); used by the host planner and, as
@@ -50,9 +50,9 @@ __host__ __device__ constexpr TcGeom tc_geom(int D0, int H, int D2) {
   g.D0 = D0; g.H = H; g.D2 = D2; g.nmb = H / 128;
   g.SA1 = (uint32_t)(D0 / 8) * 128u;
   g.SA2 = (uint32_t)(H / 8) * 128u;
-  g.SAx = (uint32_t)(D0 / 8) * kTcLB;
+  g.SAx = kTcRow;                                   // X0^T [i][s]: i-block stride
   g.SAh = (uint32_t)(kTcNS / 8) * 128u;             // H^T [o][s]: o-block stride
-  g.SAv = (uint32_t)(D2 / 8) * kTcLB;
+  g.SAv = kTcRow;                                   // V^T  [o2][s]
   uint32_t o = 0;
   g.W2h = o; o += (uint32_t)D2 * H * 2;
   g.W2l = o; o += (uint32_t)D2 * H * 2;
@@ -61,13 +61,12 @@ __host__ __device__ constexpr TcGeom tc_geom(int D0, int H, int D2) {
   g.fv = o;  o += (uint32_t)(2 * H + D2) * 4;      // w1t[H] | b1[H] | b2[D2]
   o = (o + 127) & ~127u;
   g.packed = o;                                     // staged from global by setup_tile
-  const uint32_t rb = kTcNS / 8;
-  g.X0h = o; o += rb * g.SAx;
-  g.X0l = o; o += rb * g.SAx;
+  g.X0h = o; o += (uint32_t)(D0 / 8) * g.SAx;
+  g.X0l = o; o += (uint32_t)(D0 / 8) * g.SAx;
   g.Hh = o;  o += (uint32_t)(H / 8) * g.SAh;
   g.Hl = o;  o += (uint32_t)(H / 8) * g.SAh;
-  g.Vh = o;  o += rb * g.SAv;
-  g.Vl = o;  o += rb * g.SAv;
+  g.Vh = o;  o += (uint32_t)(D2 / 8) * g.SAv;
+  g.Vl = o;  o += (uint32_t)(D2 / 8) * g.SAv;
   g.vec = o; o += (uint32_t)(2 * H + D2) * 4;       // db1[H] | dwt[H] | db2[D2]
   g.pw = o;  o += (uint32_t)(4 * D2) * 4;           // db2 partials [4][D2] (reverse_step)
   o = (o + 15) & ~15u;
@@ -163,9 +162,20 @@ struct TcMlpAdapter {
   OB_DEV void put(int r, int j, T v) {
     uint16_t hi, lo;
     tc::split_bf16(r < Rv ? v : 0.f, hi, lo);
-    const uint32_t off = tc::blk(r, j, G.SAx, kTcLB);
+    const uint32_t off = tc::blk(j, r, G.SAx, 128);
     *reinterpret_cast<uint16_t*>(ob_tc_smem + G.X0h + off) = hi;
     *reinterpret_cast<uint16_t*>(ob_tc_smem + G.X0l + off) = lo;
+  }
+  // samples s0..s0+7 of state component m (rows >= Rv zero): two 16-byte stores
+  OB_DEV void put8(int m, int s0, const float* v) {
+    uint32_t hw[4], lw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      tc::split2_bf16(s0 + 2 * q < Rv ? v[2 * q] : 0.f, s0 + 2 * q + 1 < Rv ? v[2 * q + 1] : 0.f, hw[q],
+                      lw[q]);
+    const uint32_t off = tc::blk(m, s0, G.SAx, 128);
+    *reinterpret_cast<uint4*>(ob_tc_smem + G.X0h + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(ob_tc_smem + G.X0l + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
   OB_DEV void put_time(double t) { tcur = p.d.time_input ? float(t) : 0.f; }
 
@@ -183,45 +193,45 @@ struct TcMlpAdapter {
   }
 
   // ---- products (issued by warp 0; one elected lane)
-  // z[o][s] = sum_i W1[o][i] X0[s][i]           (A = W1 K-major, B = X0 K-major)
+  // z[o][s] = sum_i W1[o][i] X0[s][i]           (A = W1 K-major, B = X0^T MN-major)
   OB_DEV void issue_hidden() {
-    constexpr uint32_t id = tc::idesc_bf16(128, kTcNS, false, false);
-    tc_mma3<G.W1h, G.W1l, 128, G.SA1, 256, G.X0h, G.X0l, kTcLB, G.SAx, 2 * kTcLB, D0 / 16, id>(T_ACC1, 0);
+    constexpr uint32_t id = tc::idesc_bf16(128, kTcNS, false, true);
+    tc_mma3<G.W1h, G.W1l, 128, G.SA1, 256, G.X0h, G.X0l, G.SAx, 128, 2 * G.SAx, D0 / 16, id>(T_ACC1, 0);
     if constexpr (NMB == 2)
       tc_mma3<G.W1h + 16 * G.SA1, G.W1l + 16 * G.SA1, 128, G.SA1, 256, G.X0h, G.X0l,
-              kTcLB, G.SAx, 2 * kTcLB, D0 / 16, id>(T_ACC1 + 32, 0);
+              G.SAx, 128, 2 * G.SAx, D0 / 16, id>(T_ACC1 + 32, 0);
   }
   // out[o2][s] = sum_i2 W2[o2][i2] H[s][i2]      (M = 64; B = H^T MN-major)
   OB_DEV void issue_out(uint32_t dst = T_ACC2) {
     constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, false, true);
     tc_mma3<G.W2h, G.W2l, 128, G.SA2, 256, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh, H / 16, id>(dst, 0);
   }
-  // dW2^T[i2][o2] += sum_s H[s][i2] V[s][o2]     (A = H^T K-major, B = V MN-major)
+  // dW2^T[i2][o2] += sum_s H[s][i2] V[s][o2]     (A = H^T K-major, B = V^T K-major)
   OB_DEV void issue_dw2(uint32_t acc) {
-    constexpr uint32_t id = tc::idesc_bf16(128, D2, false, true);
-    tc_mma3<G.Hh, G.Hl, 128, G.SAh, 256, G.Vh, G.Vl, G.SAv, kTcLB, 2 * G.SAv,
+    constexpr uint32_t id = tc::idesc_bf16(128, D2, false, false);
+    tc_mma3<G.Hh, G.Hl, 128, G.SAh, 256, G.Vh, G.Vl, 128, G.SAv, 256,
             kTcNS / 16, id>(T_W2, acc);
     if constexpr (NMB == 2)
       tc_mma3<G.Hh + 16 * G.SAh, G.Hl + 16 * G.SAh, 128, G.SAh, 256, G.Vh, G.Vl,
-              G.SAv, kTcLB, 2 * G.SAv, kTcNS / 16, id>(T_W2 + D2, acc);
+              128, G.SAv, 256, kTcNS / 16, id>(T_W2 + D2, acc);
   }
-  // dH[i2][s] = sum_o2 W2[o2][i2] V[s][o2]       (A = W2 MN-major, B = V K-major)
+  // dH[i2][s] = sum_o2 W2[o2][i2] V[s][o2]       (A = W2 MN-major, B = V^T MN-major)
   OB_DEV void issue_dh() {
-    constexpr uint32_t id = tc::idesc_bf16(128, kTcNS, true, false);
-    tc_mma3<G.W2h, G.W2l, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl, kTcLB, G.SAv, 2 * kTcLB,
+    constexpr uint32_t id = tc::idesc_bf16(128, kTcNS, true, true);
+    tc_mma3<G.W2h, G.W2l, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl, G.SAv, 128, 2 * G.SAv,
             D2 / 16, id>(T_ACC1, 0);
     if constexpr (NMB == 2)
       tc_mma3<G.W2h + 16 * 128, G.W2l + 16 * 128, G.SA2, 128, 2 * G.SA2, G.Vh, G.Vl,
-              kTcLB, G.SAv, 2 * kTcLB, D2 / 16, id>(T_ACC1 + 32, 0);
+              G.SAv, 128, 2 * G.SAv, D2 / 16, id>(T_ACC1 + 32, 0);
   }
-  // dW1[o][i] += sum_s dZ[s][o] X0[s][i]          (A = dZ^T K-major, B = X0 MN-major)
+  // dW1[o][i] += sum_s dZ[s][o] X0[s][i]          (A = dZ^T K-major, B = X0^T K-major)
   OB_DEV void issue_dw1(uint32_t acc) {
-    constexpr uint32_t id = tc::idesc_bf16(128, D0, false, true);
-    tc_mma3<G.Hh, G.Hl, 128, G.SAh, 256, G.X0h, G.X0l, G.SAx, kTcLB, 2 * G.SAx,
+    constexpr uint32_t id = tc::idesc_bf16(128, D0, false, false);
+    tc_mma3<G.Hh, G.Hl, 128, G.SAh, 256, G.X0h, G.X0l, 128, G.SAx, 256,
             kTcNS / 16, id>(T_W1, acc);
     if constexpr (NMB == 2)
       tc_mma3<G.Hh + 16 * G.SAh, G.Hl + 16 * G.SAh, 128, G.SAh, 256, G.X0h,
-              G.X0l, G.SAx, kTcLB, 2 * G.SAx, kTcNS / 16, id>(T_W1 + D0, acc);
+              G.X0l, 128, G.SAx, 256, kTcNS / 16, id>(T_W1 + D0, acc);
   }
   // dX[i][s] = sum_o W1[o][i] dZ[s][o]            (A = W1 MN-major, B = dZ^T MN-major, M = 64)
   OB_DEV void issue_dx() {
@@ -362,10 +372,10 @@ struct TcMlpAdapter {
           v[j] = Num<float>::add(v[j], Num<float>::mul(ca[q], Num<float>::add(k[j], b2m)));
       }
       if (mine) {
+        put8(m, s0, v);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int r = s0 + j;
-          if (r < Rt) put(r, m, v[j]);
           if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * D0 + m] = v[j];
         }
       }
@@ -529,18 +539,19 @@ struct TcMlpAdapter {
       // V = h w (padded samples zero), db2 partial, U_i into X0
       float ps = 0.f;
       if (mine) {
+        float hv[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int r = s0 + e;
-          const float hv = r < Rv ? hf * v[e] : 0.f;
-          ps += hv;
-          uint16_t hi, lo;
-          tc::split_bf16(hv, hi, lo);
-          const uint32_t off = tc::blk(r, m, G.SAv, kTcLB);
-          *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vh + off) = hi;
-          *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vl + off) = lo;
-          if (r < Rt) put(r, m, un[e]);
+          hv[e] = s0 + e < Rv ? hf * v[e] : 0.f;
+          ps += hv[e];
         }
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tc::split2_bf16(hv[2 * q], hv[2 * q + 1], hw[q], lw[q]);
+        const uint32_t off = tc::blk(m, s0, G.SAv, 128);
+        *reinterpret_cast<uint4*>(ob_tc_smem + G.Vh + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(ob_tc_smem + G.Vl + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        put8(m, s0, un);
         reinterpret_cast<float*>(ob_tc_smem + G.pw)[cg * D2 + m] = ps;
       }
       if (i > 0) load_u(i - 1);
@@ -583,7 +594,7 @@ struct TcMlpAdapter {
       const float v = s < Rv ? hf * wv[s * ldn + o2] : 0.f;
       uint16_t hi, lo;
       tc::split_bf16(v, hi, lo);
-      const uint32_t off = tc::blk(s, o2, G.SAv, kTcLB);
+      const uint32_t off = tc::blk(o2, s, G.SAv, 128);
       *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vh + off) = hi;
       *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vl + off) = lo;
     }
