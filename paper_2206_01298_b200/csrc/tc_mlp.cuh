@@ -97,8 +97,9 @@ OB_DEV void tc_mma3(uint32_t D, uint32_t first_acc) {
   for (int k = 0; k < KS; ++k) {
     const uint64_t Ah = tc::sdesc(sb + AH + k * AST, ALB, ASB), Al = tc::sdesc(sb + AL + k * AST, ALB, ASB);
     const uint64_t Bh = tc::sdesc(sb + BH + k * BST, BLB, BSB), Bl = tc::sdesc(sb + BL + k * BST, BLB, BSB);
-    tc::mma_bf16(D, Ah, Bh, ID, k > 0 ? 1u : first_acc);
-    tc::mma_bf16(D, Ah, Bl, ID, 1u);
+    // A_hi feeds two products: read once, reused from the collector buffer
+    tc::mma_bf16_keep_a(D, Ah, Bh, ID, k > 0 ? 1u : first_acc);
+    tc::mma_bf16_reuse_a(D, Ah, Bl, ID, 1u);
     tc::mma_bf16(D, Al, Bh, ID, 1u);
   }
 }
