@@ -224,9 +224,17 @@ def grad(field: Field, scheme: Scheme, loss: LossSpec, u0, t0, tF, ctrl,
     else:
         samp = {"nfe_forward": np.full(B, c["nfe_forward"]),
                 "nfe_backward": np.full(B, c["nfe_backward"])}
+    if host_io:
+        # pinned staging (torch's caching host allocator) + async copies: one stream
+        # synchronisation (the loss read below) instead of three pageable round trips
+        staged = []
+        for x in (dtheta, du0, u_final):
+            h = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+            h.copy_(x, non_blocking=True)
+            staged.append(h)
     loss_v = float(loss_t.item())
     if host_io:
-        dtheta_o, du0_o, uf_o = dtheta.cpu().numpy(), du0.cpu().numpy(), u_final.cpu().numpy()
+        dtheta_o, du0_o, uf_o = (h.numpy() for h in staged)
     else:
         dtheta_o, du0_o, uf_o = dtheta, du0, u_final
     if dhead is not None and host_io:
