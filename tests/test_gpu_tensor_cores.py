@@ -183,3 +183,35 @@ def test_mse_target_loss_on_tensor_cores():
     assert abs(res.loss - res64.loss) <= 1e-4 * abs(res64.loss)
     assert oc.rel_error(np_(res.dtheta), np_(res64.dtheta)) <= TOL32
     assert oc.rel_error(np_(res.du0), np_(res64.du0)) <= TOL32
+
+
+@pytest.mark.parametrize("scheme,n_steps", [("dopri5", 1), ("bosh3", 1), ("dopri5", 2)])
+def test_fsal_edges_on_tensor_cores(scheme, n_steps):
+    """FSAL carry and the skipped unused last stage at the sweep's edges (one and two
+    steps), revolve with a single slot."""
+    rng = np.random.default_rng(21 + n_steps)
+    widths, theta = make_mlp(rng, 64, 256, "tanh", True)
+    u0 = f32(rng.normal(size=(90, 64)))
+    for pol in ("store_all", "revolve:1"):
+        res, ref = run_both(widths, "tanh", True, theta, u0, scheme, n_steps, pol)
+        assert res.device["tensor_cores"] == 1
+        e = errs(res, ref)
+        assert max(e.values()) <= TOL32, (pol, e)
+        assert res.counters.nfe_forward == ref["counters"].nfe_forward
+
+
+def test_nonuniform_grid_on_tensor_cores():
+    from paper_2206_01298_b200 import FixedGridController
+    rng = np.random.default_rng(8)
+    widths, theta = make_mlp(rng, 48, 128, "tanh", True)
+    u0 = f32(rng.normal(size=(120, 48)))
+    times = (0.0, 0.05, 0.2, 0.3, 0.65, 1.0)
+    model = MlpModel(MlpSpec(widths, "tanh", time_input=True, dtype="f32"), theta)
+    res = grad(MlpField(model), tableau_catalog("dopri5"), terminal_loss("half_sqnorm", 1.0),
+               torch.as_tensor(u0, dtype=torch.float32, device="cuda"), 0.0, 1.0,
+               FixedGridController(times), CheckpointPolicy.parse("revolve:2"))
+    assert res.device["tensor_cores"] == 1
+    ref = oc.grad_terminal(oc.MlpField(oc.Mlp(widths, "tanh", theta, True)), "dopri5", u0, 0.0, 1.0,
+                           len(times) - 1, "revolve:2", times=np.array(times))
+    e = errs(res, ref)
+    assert max(e.values()) <= TOL32, e
