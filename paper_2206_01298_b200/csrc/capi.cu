@@ -342,6 +342,8 @@ void layout_smem(Plan& P) {
     s.hid[0] = take(18 * 18 * 68);
     s.tA = s.tB = s.u = s.lam = s.lamn = s.w = s.jtv = s.aux = s.wts = s.ks = -1;
     for (int i = 0; i < 8; ++i) s.vec[i] = -1;
+    // double-buffered tap weights (2 x 64 x 68) for the staged conv GEMMs, when they fit
+    if ((size_t)(o + 2 * 64 * 68) * P.esz <= smem_cap(P) && !getenv("OB_CONV_UNSTAGED")) s.tA = take(2 * 64 * 68);
     s.total = o;
     P.smem_bytes = (size_t)o * P.esz;
     return;

@@ -24,6 +24,113 @@ OB_DEV int halo_idx(int p, int dy, int dx) {   // pixel p shifted by (dy, dx) in
   return ((p / kImg) + dy) * kHalo + (p % kImg) + dx;
 }
 
+// ---- tap-staged variants: one tap's 64 weight rows (64 x kCP, 17 KB) are copied to
+// shared memory with cp.async while the previous tap is consumed (double buffer), so
+// the inner loops read weights with ld.shared instead of waiting on L2.  The warps of
+// `ws` synchronise with a named barrier (ws may be half the CTA).
+OB_DEV void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+OB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> OB_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+OB_DEV void warps_sync(const Warps& ws) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + (ws.w0 != 0 ? 1 : 0)), "r"(ws.nw * 32) : "memory");
+}
+template <typename T>
+OB_DEV void stage_tap(T* dst, const T* src, long long rowstride, const Warps& ws) {
+  constexpr int kV = 16 / sizeof(T), kChunks = kCP / kV;
+  const int tid = ws.me() * 32 + lane_id(), nth = ws.nw * 32;
+  for (int c = tid; c < 64 * kChunks; c += nth) {
+    const int r = c / kChunks, q = c % kChunks;
+    cp_async16(dst + r * kCP + q * kV, src + r * rowstride + q * kV);
+  }
+  cp_async_commit();
+}
+
+// out[p][co] = epi(sum_{s, k < K} X[p + off(s)][k] * Wt_s[co][k]) with Wt_s the staged tap
+// rows (tap s at src + s * tapstride, row co at + co * rowstride).  bwd: D read at the
+// flipped tap (transposed conv), thread columns contiguous (k0 + j) as in conv_bwd.
+template <typename T, bool kBwd, class Epi>
+OB_DEV void conv_staged(const T* Xh, const T* W, long long rowstride, long long tapstride, int Cout,
+                        int K, Warps ws, T* stage, Epi epi) {
+  constexpr int LR = 8, LC = 4, kMaxT = 2;
+  if (!ws.mine()) return;
+  const int lr = lane_id() % LR, lc = lane_id() / LR;
+  const int ctiles = (Cout + 15) / 16, ntask = (kPix / 32) * ctiles;
+  const int per = (ntask + ws.nw - 1) / ws.nw, groups = (per + kMaxT - 1) / kMaxT;
+  const uint32_t xs = smem_addr(Xh);
+  for (int g = 0; g < groups; ++g) {
+    T acc[kMaxT][4][4];
+#pragma unroll
+    for (int t = 0; t < kMaxT; ++t)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[t][i][j] = T(0);
+    stage_tap(stage, W, rowstride, ws);
+    for (int s = 0; s < 9; ++s) {
+      if (s + 1 < 9) {
+        stage_tap(stage + ((s + 1) & 1) * 64 * kCP, W + (s + 1) * tapstride, rowstride, ws);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      warps_sync(ws);
+      const uint32_t wsm = smem_addr(stage + (s & 1) * 64 * kCP);
+      const int dy = kBwd ? 2 - s / 3 : s / 3, dx = kBwd ? 2 - s % 3 : s % 3;
+#pragma unroll
+      for (int t = 0; t < kMaxT; ++t) {
+        const int task = ws.me() + (g * kMaxT + t) * ws.nw;
+        if (task >= ntask) continue;
+        const int p0 = (task % (kPix / 32)) * 32 + lr;
+        const int c0 = kBwd ? (task / (kPix / 32)) * 16 + 4 * lc : (task / (kPix / 32)) * 16 + lc;
+        int hx[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hx[i] = halo_idx(p0 + i * LR, dy, dx) * kCP;
+        for (int k = 0; k < K; k += 4) {
+          T x[4][4], w[4][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) Ld<T>::s4(xs + (uint32_t)((hx[i] + k) * sizeof(T)), x[i]);
+          if constexpr (kBwd) {   // w[q][j] = Wt[k + q][c0 + j]
+#pragma unroll
+            for (int q = 0; q < 4; ++q) Ld<T>::s4(wsm + (uint32_t)(((k + q) * kCP + c0) * sizeof(T)), w[q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[t][i][j] = Num<T>::fma(x[i][q], w[q][j], acc[t][i][j]);
+          } else {                // w[j][q] = Wt[c0 + j LC][k + q]
+#pragma unroll
+            for (int j = 0; j < 4; ++j) Ld<T>::s4(wsm + (uint32_t)(((c0 + j * LC) * kCP + k) * sizeof(T)), w[j]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[t][i][j] = Num<T>::fma(x[i][q], w[j][q], acc[t][i][j]);
+          }
+        }
+      }
+      warps_sync(ws);   // every warp is done with this buffer before it is refilled
+    }
+#pragma unroll
+    for (int t = 0; t < kMaxT; ++t) {
+      const int task = ws.me() + (g * kMaxT + t) * ws.nw;
+      if (task >= ntask) continue;
+      const int p0 = (task % (kPix / 32)) * 32 + lr;
+      const int c0 = kBwd ? (task / (kPix / 32)) * 16 + 4 * lc : (task / (kPix / 32)) * 16 + lc;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = kBwd ? c0 + j : c0 + j * LC;
+          if (c < Cout) epi(p0 + i * LR, c, acc[t][i][j]);
+        }
+    }
+  }
+}
+
 // out[p][co] (co < Cout) = sum over taps and ci < Kc of X[...] * Wf[co][s*kCP + ci]
 template <typename T, class Epi>
 OB_DEV void conv_fwd(const T* Xh, const T* Wf, int Cout, int Kc, Warps ws, Epi epi) {

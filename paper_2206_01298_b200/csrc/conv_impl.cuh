@@ -22,6 +22,7 @@ struct ConvAdapter {
   T* Bh;       // hidden halo tile
   T* xsave;    // global parking slot for A
   const T *W1f, *W2f, *W1b, *W2b, *b1, *b2;
+  T* stage;    // double-buffered tap weights in shared memory (nullptr: read through L1/L2)
   static constexpr bool kHasJvp = false;
   static constexpr bool kScaledVjp = false;  // vjp returns J^T w; the caller scales by h
   static constexpr int kCombineBatch = 4;    // stage loads in flight per ordered sum (registers)
@@ -41,6 +42,17 @@ struct ConvAdapter {
     W2b = p.packed + p.d.pwoff[3];
     b1 = W.bias[0];
     b2 = W.bias[1];
+    stage = p.sm.tA >= 0 ? sm + p.sm.tA : nullptr;
+  }
+  template <class Epi>
+  OB_DEV void fwd(const T* X, const T* Wf, int Kc, Warps ws, Epi epi) {
+    if (stage) conv_staged<T, false>(X, Wf, 9 * kCP, kCP, 64, Kc, ws, stage, epi);
+    else conv_fwd<T>(X, Wf, 64, Kc, ws, epi);
+  }
+  template <class Epi>
+  OB_DEV void bwd(const T* D, const T* Wb, Warps ws, Epi epi) {
+    if (stage) conv_staged<T, true>(D, Wb, kCP, 64LL * kCP, 64, 64, ws, stage, epi);
+    else conv_bwd<T>(D, Wb, kCP, 64, ws, epi);
   }
   OB_DEV T* x0() { return A; }
   OB_DEV int nin() const { return p.d.N; }
@@ -54,7 +66,7 @@ struct ConvAdapter {
   OB_DEV void hidden() {   // Bh = relu(conv1(A) + b1)
     T* H = Bh;
     const T* bb = b1;
-    conv_fwd<T>(A, W1f, 64, kCP, Warps::all(), [&](int q, int co, T acc) {
+    fwd(A, W1f, kCP, Warps::all(), [&](int q, int co, T acc) {
       const T z = Num<T>::add(acc, bb[co]);
       H[halo_idx(q, 1, 1) * kCP + co] = z > T(0) ? z : T(0);
     });
@@ -64,8 +76,8 @@ struct ConvAdapter {
   OB_DEV void eval(T* out) {
     hidden();
     const T* bb = b2;
-    conv_fwd<T>(Bh, W2f, 64, 64, Warps::all(),
-                [&](int q, int co, T acc) { out[q * 64 + co] = Num<T>::add(acc, bb[co]); });
+    fwd(Bh, W2f, 64, Warps::all(),
+        [&](int q, int co, T acc) { out[q * 64 + co] = Num<T>::add(acc, bb[co]); });
     __syncthreads();
   }
 
@@ -85,7 +97,7 @@ struct ConvAdapter {
       __syncthreads();
     }
     T* H = Bh;
-    conv_bwd<T>(A, W2b, kCP, 64, Warps::all(), [&](int q, int ci, T acc) {   // dz1 in place
+    bwd(A, W2b, Warps::all(), [&](int q, int ci, T acc) {   // dz1 in place
       const int o = halo_idx(q, 1, 1) * kCP + ci;
       H[o] = H[o] > T(0) ? acc : T(0);
     });
@@ -97,7 +109,7 @@ struct ConvAdapter {
     const Warps wn = both ? Warps{0, nw / 2} : Warps::all();
     const Warps wa = both ? Warps{nw / 2, nw - nw / 2} : Warps::all();
     if (jtv)
-      conv_bwd<T>(Bh, W1b, kCP, 64, wn, [&](int q, int ci, T acc) { jtv[q * 64 + ci] = acc; });
+      bwd(Bh, W1b, wn, [&](int q, int ci, T acc) { jtv[q * 64 + ci] = acc; });
     if (mu) conv_wgrad<T>(Bh, A, kCP, hs, mu + p.d.mwoff[0], mu + p.d.mboff[0], wa);
     __syncthreads();
   }
