@@ -340,7 +340,8 @@ void layout_smem(Plan& P) {
     s.x0 = take(18 * 18 * 68);
     for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
     s.hid[0] = take(18 * 18 * 68);
-    s.tA = s.tB = s.u = s.lam = s.lamn = s.w = s.jtv = s.aux = s.wts = s.ks = -1;
+    s.tA = s.tB = s.u = s.lam = s.lamn = s.w = s.jtv = s.aux = s.wts = s.ks = s.ring = -1;
+    s.ring_elems = 0;
     for (int i = 0; i < 8; ++i) s.vec[i] = -1;
     // double-buffered tap weights (2 x 64 x 68) for the staged conv GEMMs, when they fit
     if ((size_t)(o + 2 * 64 * 68) * P.esz <= smem_cap(P) && !getenv("OB_CONV_UNSTAGED")) s.tA = take(2 * 64 * 68);
@@ -382,6 +383,22 @@ void layout_smem(Plan& P) {
   if (ws_variant && (size_t)(o + d.n_packed) * P.esz <= smem_cap(P) && !getenv("OB_NO_SMEM_WEIGHTS")) {
     s.wts = take(d.n_packed);
     s.total = o;
+  }
+  // per-warp cp.async rings for weights streamed from L2 (weights not staged in smem)
+  s.ring = -1;
+  s.ring_elems = 0;
+  if (s.wts < 0 && !getenv("OB_NO_WRING")) {
+    const long long ctw = 4LL * (32 / P.LR);                  // widest column tile
+    const long long kd = P.esz == 4 ? 4 : 2;                  // RingDepth (gemm.cuh)
+    const long long want = (kThreads / 32) * kd * ctw * 4;
+    // leave 4 KB for the kernels' static shared memory (reductions, flags)
+    const long long avail = (long long)((smem_cap(P) - 4096) / P.esz) - o;
+    long long n = std::min(want, avail) / 64 * 64;
+    if (n >= (kThreads / 32) * kd * 64) {
+      s.ring = take(n);
+      s.ring_elems = (int)n;
+      s.total = o;
+    }
   }
   // explicit-RK stage scratch (k_i forward, Lambda_i reverse) in shared memory when it
   // fits beside everything else: the stage sums then read it without L2 latency
@@ -469,7 +486,8 @@ bool plan_tc(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   s = SmemLayout{};
   int o = 0;
   auto take = [&](long long n) { int r = o; o += (int)((n + 7) & ~7LL); return r; };
-  s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = s.ks = -1;
+  s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = s.ks = s.ring = -1;
+  s.ring_elems = 0;
   for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
   for (int i = 0; i < 8; ++i) s.vec[i] = -1;
   s.scr_elems = 0;

@@ -100,6 +100,19 @@ OB_DEV T warp_dot(const T* a, const T* b, int n) {
   return warp_sum(s);
 }
 
+// ---- per-warp cp.async rings for weights streamed from L2 (WS = false): each warp
+// copies the weight slice of k-step k + kRing - 1 into its private ring while it
+// consumes step k, so kRing - 1 steps of 16-byte loads are in flight per lane
+// without holding registers (one CTA per SM cannot hide L2 latency with 16 warps).
+template <typename T> struct RingDepth { static constexpr int value = sizeof(T) == 4 ? 4 : 2; };
+OB_DEV void ring_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+OB_DEV void ring_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> OB_DEV void ring_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // Warp range executing an op: warps [w0, w0 + nw) of the CTA.
 struct Warps {
   int w0, nw;
@@ -113,7 +126,7 @@ struct Warps {
 // `split` slices (multiples of 4) and calls epi(r, n, acc, slice).
 template <typename T, int TR, int TC, int LR, bool WS, class Epi>
 OB_DEV void gemm_nt(const T* X, int ldx, int Rt, const T* W, int ldw, int N, int Kp, Warps ws,
-                    int split, Epi epi) {
+                    int split, Epi epi, T* ring = nullptr, int ring_elems = 0) {
   constexpr int LC = 32 / LR, RT = TR * LR, CT = TC * LC;
   if (!ws.mine()) return;
   const int lr = lane_id() % LR, lc = lane_id() / LR;
@@ -121,6 +134,72 @@ OB_DEV void gemm_nt(const T* X, int ldx, int Rt, const T* W, int ldw, int N, int
   const int kq = Kp / 4, per = (kq + split - 1) / split;
   const uint32_t xs = smem_addr(X);
   const WOp<T, WS> wo(W);
+  if constexpr (!WS) {
+    // ring slot: the task's CT weight rows x 4 k (row-major [CT][4])
+    constexpr int kD = RingDepth<T>::value, kV = 16 / (int)sizeof(T), kPer = 4 / kV;
+    constexpr int kSlot = CT * 4;
+    if (ring && ring_elems / n_warps() >= kD * kSlot) {
+      T* wr = ring + (long long)warp_id() * (ring_elems / n_warps());
+      const int lane = lane_id();
+      for (int task = ws.me(); task < rtiles * ctiles * split; task += ws.nw) {
+        const int sl = task / (rtiles * ctiles), rc = task % (rtiles * ctiles);
+        const int r0 = (rc % rtiles) * RT + lr, cb = (rc / rtiles) * CT, c0 = cb + lc;
+        const int kb = sl * per * 4, ke = min(Kp, (sl + 1) * per * 4);
+        auto issue = [&](int kk, int slot) {
+          if (kk < ke)
+            for (int c = lane; c < CT * kPer; c += 32) {
+              const int r = c / kPer, hh = c % kPer;
+              ring_cp16(wr + slot * kSlot + r * 4 + hh * kV, W + (long long)(cb + r) * ldw + kk + hh * kV);
+            }
+          ring_commit();
+        };
+        __syncwarp();   // the previous task's reads of the ring are complete
+#pragma unroll
+        for (int dd = 0; dd < kD - 1; ++dd) issue(kb + 4 * dd, dd);
+        T acc[TR][TC];
+#pragma unroll
+        for (int i = 0; i < TR; ++i)
+#pragma unroll
+          for (int j = 0; j < TC; ++j) acc[i][j] = T(0);
+        int slot = 0;
+        for (int k = kb; k < ke; k += 4) {
+          __syncwarp();   // slot (slot - 1) mod kD was read last iteration; refill it
+          issue(k + 4 * (kD - 1), (slot + kD - 1) % kD);
+          ring_wait<kD - 1>();
+          __syncwarp();
+          T x[TR][4], w[TC][4];
+#pragma unroll
+          for (int j = 0; j < TC; ++j) {
+            const T* src = wr + slot * kSlot + (lc + j * LC) * 4;
+            if constexpr (sizeof(T) == 4) {
+              Ld<T>::s4(smem_addr(src), w[j]);
+            } else {
+              Ld<T>::s4(smem_addr(src), w[j]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < TR; ++i)
+            Ld<T>::s4(xs + (uint32_t)(((r0 + i * LR) * ldx + k) * sizeof(T)), x[i]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int i = 0; i < TR; ++i)
+#pragma unroll
+              for (int j = 0; j < TC; ++j) acc[i][j] = Num<T>::fma(x[i][q], w[j][q], acc[i][j]);
+          slot = slot + 1 == kD ? 0 : slot + 1;
+        }
+        ring_wait<0>();
+#pragma unroll
+        for (int i = 0; i < TR; ++i)
+#pragma unroll
+          for (int j = 0; j < TC; ++j) {
+            const int n = c0 + j * LC;
+            if (n < N) epi(r0 + i * LR, n, acc[i][j], sl);
+          }
+      }
+      return;
+    }
+  }
   for (int task = ws.me(); task < rtiles * ctiles * split; task += ws.nw) {
     const int sl = task / (rtiles * ctiles), rc = task % (rtiles * ctiles);
     const int r0 = (rc % rtiles) * RT + lr, c0 = (rc / rtiles) * CT + lc;
@@ -158,7 +237,7 @@ OB_DEV void gemm_nt(const T* X, int ldx, int Rt, const T* W, int ldw, int N, int
 // columns here are contiguous (k = c0 + TC*lc + j) so W rows load as vectors.
 template <typename T, int TR, int LR, bool WS, class Epi>
 OB_DEV void gemm_nn(const T* D, int ldd, int Rt, const T* W, int ldw, int Np, int K, Warps ws,
-                    Epi epi, int split = 1) {
+                    Epi epi, int split = 1, T* ring = nullptr, int ring_elems = 0) {
   constexpr int TC = 4, LC = 32 / LR, RT = TR * LR, CT = TC * LC;
   if (!ws.mine()) return;
   const int lr = lane_id() % LR, lc = lane_id() / LR;
@@ -166,6 +245,63 @@ OB_DEV void gemm_nn(const T* D, int ldd, int Rt, const T* W, int ldw, int Np, in
   const int nq = Np / 4, per = (nq + split - 1) / split;
   const uint32_t ds = smem_addr(D);
   const WOp<T, WS> wo(W);
+  if constexpr (!WS) {
+    // ring slot: 4 weight rows x the task's CT columns (row-major [4][CT])
+    constexpr int kD = RingDepth<T>::value, kV = 16 / (int)sizeof(T), kCh = CT / kV;
+    constexpr int kSlot = 4 * CT;
+    if (ring && ring_elems / n_warps() >= kD * kSlot) {
+      T* wr = ring + (long long)warp_id() * (ring_elems / n_warps());
+      const int lane = lane_id();
+      for (int task = ws.me(); task < rtiles * ctiles * split; task += ws.nw) {
+        const int sl = task / (rtiles * ctiles), rc = task % (rtiles * ctiles);
+        const int r0 = (rc % rtiles) * RT + lr, cb = (rc / rtiles) * CT, k0 = cb + TC * lc;
+        const int nb = sl * per * 4, ne = min(Np, (sl + 1) * per * 4);
+        auto issue = [&](int nn_, int slot) {
+          if (nn_ < ne)
+            for (int c = lane; c < 4 * kCh; c += 32) {
+              const int q = c / kCh, hh = c % kCh;
+              ring_cp16(wr + slot * kSlot + q * CT + hh * kV, W + (long long)(nn_ + q) * ldw + cb + hh * kV);
+            }
+          ring_commit();
+        };
+        __syncwarp();
+#pragma unroll
+        for (int dd = 0; dd < kD - 1; ++dd) issue(nb + 4 * dd, dd);
+        T acc[TR][TC];
+#pragma unroll
+        for (int i = 0; i < TR; ++i)
+#pragma unroll
+          for (int j = 0; j < TC; ++j) acc[i][j] = T(0);
+        int slot = 0;
+        for (int n = nb; n < ne; n += 4) {
+          __syncwarp();
+          issue(n + 4 * (kD - 1), (slot + kD - 1) % kD);
+          ring_wait<kD - 1>();
+          __syncwarp();
+          T d[TR][4], w[4][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) Ld<T>::s4(smem_addr(wr + slot * kSlot + q * CT + TC * lc), w[q]);
+#pragma unroll
+          for (int i = 0; i < TR; ++i)
+            Ld<T>::s4(ds + (uint32_t)(((r0 + i * LR) * ldd + n) * sizeof(T)), d[i]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int i = 0; i < TR; ++i)
+#pragma unroll
+              for (int j = 0; j < TC; ++j) acc[i][j] = Num<T>::fma(d[i][q], w[q][j], acc[i][j]);
+          slot = slot + 1 == kD ? 0 : slot + 1;
+        }
+        ring_wait<0>();
+#pragma unroll
+        for (int i = 0; i < TR; ++i)
+#pragma unroll
+          for (int j = 0; j < TC; ++j)
+            if (k0 + j < K) epi(r0 + i * LR, k0 + j, acc[i][j], sl);
+      }
+      return;
+    }
+  }
   for (int task = ws.me(); task < rtiles * ctiles * split; task += ws.nw) {
     const int sl = task / (rtiles * ctiles), rc = task % (rtiles * ctiles);
     const int r0 = (rc % rtiles) * RT + lr, k0 = (rc / rtiles) * CT + TC * lc;

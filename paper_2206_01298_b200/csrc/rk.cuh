@@ -20,6 +20,7 @@ struct SmemLayout {      // offsets in elements of T (-1: not allocated)
   int kry;                // theta: Krylov workspace in shared memory (or -1: global)
   int wts;                // packed weights staged in shared memory, or -1
   int ks;                 // per-tile stage scratch [2][s][Rt][ldn] in shared memory, or -1 (global)
+  int ring, ring_elems;   // per-warp cp.async rings for L2-streamed weights, or -1
   int total;
 };
 

@@ -38,6 +38,8 @@ OB_DEV void setup_tile(const RkParams<T>& p, T* sm, MlpSmem<T>& ms, Weights<T>& 
   }
   ms.tA = L.tA >= 0 ? sm + L.tA : nullptr;
   ms.tB = L.tB >= 0 ? sm + L.tB : nullptr;
+  ms.ring = L.ring >= 0 ? sm + L.ring : nullptr;
+  ms.ring_elems = L.ring >= 0 ? L.ring_elems : 0;
   const T* base = p.packed;
   if (L.wts >= 0) {
     T* dst = sm + L.wts;

@@ -159,6 +159,8 @@ struct MlpSmem {
   T* pre[OB_MAX_LAYERS];          // pre-activations (only when need_pre)
   T* tA;                          // tangent ping-pong (JVP only) [Rt][ldt]
   T* tB;
+  T* ring;                        // per-warp weight rings (streamed weights), or nullptr
+  int ring_elems;                 // total elements (split evenly over the CTA's warps)
 };
 
 template <typename T> OB_DEV T act_prime_from(T a, T z, int id) {
@@ -205,19 +207,21 @@ struct MlpTile {
   OB_DEV void nt(const T* X, int ldx, int l, int split, Warps ws, Epi epi) {
     const int N = d.w[l + 1], Kp = (d.w[l] + 3) & ~3;
     if (tasks_wide(N) * split >= ws.nw || 2 * LR > 32)
-      gemm_nt<T, 4, 4, LR, WS>(X, ldx, Rt, W.W[l], d.ldw[l], N, Kp, ws, split, epi);
+      gemm_nt<T, 4, 4, LR, WS>(X, ldx, Rt, W.W[l], d.ldw[l], N, Kp, ws, split, epi, s.ring,
+                               s.ring_elems);
     else
       gemm_nt<T, 2, 4, (2 * LR > 32 ? 32 : 2 * LR), WS>(X, ldx, Rt, W.W[l], d.ldw[l], N, Kp, ws,
-                                                         split, epi);
+                                                         split, epi, s.ring, s.ring_elems);
   }
   template <class Epi>
   OB_DEV void nn(const T* D, int ldD, int l, int K, Warps ws, Epi epi, int split = 1) {
     const int Np = (d.w[l + 1] + 3) & ~3;
     if (tasks_wide(K) * split >= ws.nw || 2 * LR > 32)
-      gemm_nn<T, 4, LR, WS>(D, ldD, Rt, W.W[l], d.ldw[l], Np, K, ws, epi, split);
+      gemm_nn<T, 4, LR, WS>(D, ldD, Rt, W.W[l], d.ldw[l], Np, K, ws, epi, split, s.ring,
+                            s.ring_elems);
     else
       gemm_nn<T, 2, (2 * LR > 32 ? 32 : 2 * LR), WS>(D, ldD, Rt, W.W[l], d.ldw[l], Np, K, ws, epi,
-                                                      split);
+                                                      split, s.ring, s.ring_elems);
   }
 
   // split-K factor for a narrow output product of n columns reducing over kred
