@@ -448,6 +448,7 @@ theta_reverse_kernel(const __grid_constant__ RkParams<T> p) {
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
+  ms.ring = nullptr;   // the transposed adjoint products run faster from L1/L2 (measured, C5)
   MlpTile<T, LR, WS> mt(p.d, W, ms, p.Rt);
   if (p.sm.scr >= 0) { mt.scratch = sm + p.sm.scr; mt.scratch_elems = p.sm.scr_elems; }
   ThetaCtx<T> c = theta_ctx(p, sm);
