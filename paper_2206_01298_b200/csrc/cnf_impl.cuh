@@ -29,7 +29,6 @@ struct CnfAdapter {
   static constexpr bool kHasJvp = false;
   static constexpr bool kScaledVjp = false;  // vjp returns J^T w; the caller scales by h
   static constexpr int kCombineBatch = 4;    // stage loads in flight per ordered sum (registers)
-  static constexpr int kCombineElems = 1;    // elements per thread combined together
   static constexpr bool kOwnsStep = false;   // the adapter runs whole RK steps itself
   OB_DEV void finish(T*) {}   // flush device-resident parameter cotangents (none here)
   OB_DEV void release() {}    // free per-CTA hardware resources (none here)

@@ -86,7 +86,6 @@ struct MlpAdapter {
   static constexpr bool kHasJvp = true;
   static constexpr bool kScaledVjp = false;  // vjp returns J^T w; the caller scales by h
   static constexpr int kCombineBatch = 4;    // stage loads in flight per ordered sum (registers)
-  static constexpr int kCombineElems = 1;    // elements per thread combined together
   static constexpr bool kOwnsStep = false;   // the adapter runs whole RK steps itself
   OB_DEV void finish(T*) {}   // flush device-resident parameter cotangents (none here)
   OB_DEV void release() {}    // free per-CTA hardware resources (none here)
@@ -156,40 +155,6 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
   const long long vec = (long long)p.B * N;
   PhaseTimer pt(p.prof ? p.phase : nullptr);
   for (int i = 0; i < s; ++i) {
-    if constexpr (F::kCombineElems > 1) {
-      // E elements per thread at once: every stage-derivative load of all of them in
-      // flight before the ordered sums (L2 latency paid once per stage)
-      constexpr int E = F::kCombineElems;
-      T ca[OB_MAX_STAGES];   // T(h a_iq) once per stage (uniform), exact zeros skipped
-      bool nz[OB_MAX_STAGES];
-#pragma unroll
-      for (int q = 0; q < OB_MAX_STAGES; ++q) {
-        const double aiq = q < i ? p.a[i * OB_MAX_STAGES + q] : 0.0;
-        nz[q] = aiq != 0.0;
-        ca[q] = T(h * aiq);
-      }
-      for (int b0 = threadIdx.x; b0 < Rt * N; b0 += E * blockDim.x) {
-        T kv[E][OB_MAX_STAGES];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int idx = b0 + e * blockDim.x, r = idx / N, j = idx % N;
-#pragma unroll
-          for (int q = 0; q < OB_MAX_STAGES; ++q)
-            kv[e][q] = (idx < Rt * N && q < i) ? ks[q * kst + r * ldn + j] : T(0);
-        }
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int idx = b0 + e * blockDim.x, r = idx / N, j = idx % N;
-          if (idx >= Rt * N) continue;
-          T v = u[r * ldn + j];
-#pragma unroll
-          for (int q = 0; q < OB_MAX_STAGES; ++q)
-            if (nz[q]) v = Num<T>::add(v, Num<T>::mul(ca[q], kv[e][q]));
-          if (j < nin) f.put(r, j, v);
-          if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * N + j] = v;
-        }
-      }
-    } else
     for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
       const int r = idx / N, j = idx % N;
       // issue every stage-derivative load (L2-resident scratch) before the dependent
@@ -222,42 +187,6 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
     pt.mark(9);   // field eval
   }
   int bad = 0;
-  if constexpr (F::kCombineElems > 1) {
-    constexpr int E = F::kCombineElems;
-    T cb[OB_MAX_STAGES];
-    bool nz[OB_MAX_STAGES];
-#pragma unroll
-    for (int q = 0; q < OB_MAX_STAGES; ++q) {
-      const double bq = q < s ? p.b[q] : 0.0;
-      nz[q] = bq != 0.0;
-      cb[q] = T(h * bq);
-    }
-    for (int b0 = threadIdx.x; b0 < Rt * N; b0 += E * blockDim.x) {
-      T kv[E][OB_MAX_STAGES];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int idx = b0 + e * blockDim.x, r = idx / N, j = idx % N;
-#pragma unroll
-        for (int q = 0; q < OB_MAX_STAGES; ++q)
-          kv[e][q] = (idx < Rt * N && q < s) ? ks[q * kst + r * ldn + j] : T(0);
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int idx = b0 + e * blockDim.x, r = idx / N, j = idx % N;
-        if (idx >= Rt * N) continue;
-        T v = u[r * ldn + j];
-#pragma unroll
-        for (int q = 0; q < OB_MAX_STAGES; ++q)
-          if (nz[q]) v = Num<T>::add(v, Num<T>::mul(cb[q], kv[e][q]));
-        u[r * ldn + j] = v;
-        if (r < Rv) {
-          if (!Num<T>::finite(v)) bad = 1;
-          if (rec) rec[s * vec + (long long)(row0 + r) * N + j] = v;
-        }
-      }
-    }
-    return __syncthreads_or(bad) == 0;
-  }
   for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
     T v = u[r * ldn + j];
@@ -650,99 +579,64 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
         return;
       }
       pt.mark(kPhVjp);
-      continue;
-    }
-    for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) lamn[idx] = lam[idx];
-    __syncthreads();
-    for (int i = s - 1; i >= 0; --i) {
-      if (p.skip_vjp & (1u << i)) {  // w_i == 0 exactly: Lam_i = 0 (still counted, B8)
-        for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) Lam[i * kst + idx] = T(0);
-        continue;
-      }
-      // w_i = b_i lam_{n+1} + sum_{j>i, a_ji != 0} a_ji Lam_j   (pad rows stay 0)
-      if constexpr (F::kCombineElems > 1) {
-        constexpr int E = F::kCombineElems;
-        T ca[OB_MAX_STAGES];
-        bool nz[OB_MAX_STAGES];
-#pragma unroll
-        for (int j = 0; j < OB_MAX_STAGES; ++j) {
-          const double aji = (j > i && j < s) ? p.a[j * OB_MAX_STAGES + i] : 0.0;
-          nz[j] = aji != 0.0;
-          ca[j] = T(aji);
-        }
-        const T bi = T(p.b[i]);
-        for (int b0 = threadIdx.x; b0 < Rt * N; b0 += E * blockDim.x) {
-          T lv[E][OB_MAX_STAGES];
-          T xs[E];
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int idx = b0 + e * blockDim.x, r = idx / N, jj = idx % N, o = r * ldn + jj;
-#pragma unroll
-            for (int j = 0; j < OB_MAX_STAGES; ++j)
-              lv[e][j] = (idx < Rt * N && j > i && j < s) ? Lam[j * kst + o] : T(0);
-            xs[e] = (idx < Rt * N && r < Rv && jj < nin) ? rec[i * vec + (long long)(row0 + r) * N + jj]
-                                                         : T(0);
-          }
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int idx = b0 + e * blockDim.x, r = idx / N, jj = idx % N, o = r * ldn + jj;
-            if (idx >= Rt * N) continue;
-            T v = Num<T>::mul(bi, lam[o]);
-#pragma unroll
-            for (int j = 0; j < OB_MAX_STAGES; ++j)
-              if (nz[j]) v = Num<T>::add(v, Num<T>::mul(ca[j], lv[e][j]));
-            w[o] = v;
-            if (r < Rv && jj < nin) f.put(r, jj, xs[e]);   // stage state U_i into the field input
-          }
-        }
-      } else {
-      for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
-        const int o = (idx / N) * ldn + idx % N;
-        T v = Num<T>::mul(T(p.b[i]), lam[o]);
-#pragma unroll
-        for (int j0 = 0; j0 < OB_MAX_STAGES; j0 += F::kCombineBatch) {   // loads in flight first
-          T lv[F::kCombineBatch];
-#pragma unroll
-          for (int t = 0; t < F::kCombineBatch; ++t)
-            lv[t] = (j0 + t > i && j0 + t < s) ? Lam[(j0 + t) * kst + o] : T(0);
-#pragma unroll
-          for (int t = 0; t < F::kCombineBatch; ++t) {
-            const double aji = (j0 + t > i && j0 + t < s) ? p.a[(j0 + t) * OB_MAX_STAGES + i] : 0.0;
-            if (aji != 0.0) v = Num<T>::add(v, Num<T>::mul(T(aji), lv[t]));
-          }
-        }
-        w[o] = v;
-      }
-      // stage state U_i into the field input (+ stage time)
-      for (int idx = threadIdx.x; idx < Rv * nin; idx += blockDim.x) {
-        const int r = idx / nin, j = idx % nin;
-        f.put(r, j, rec[i * vec + (long long)(row0 + r) * N + j]);
-      }
-      }
-      f.put_time(t + p.c[i] * h);
+    } else {
+      for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) lamn[idx] = lam[idx];
       __syncthreads();
-      pt.mark(kPhElem);
-      f.vjp(w, jtv, mu, h, Rv);
-      pt.mark(kPhVjp);
-      // Lam_i = h * jtv; lam_n += Lam_i  (scaled-VJP adapters return J^T (h w) directly)
-      for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
-        const int o = (idx / N) * ldn + idx % N;
-        const T li = F::kScaledVjp ? jtv[o] : Num<T>::mul(T(h), jtv[o]);
-        Lam[i * kst + o] = li;
-        lamn[o] = Num<T>::add(lamn[o], li);
+      for (int i = s - 1; i >= 0; --i) {
+        if (p.skip_vjp & (1u << i)) {  // w_i == 0 exactly: Lam_i = 0 (still counted, B8)
+          for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) Lam[i * kst + idx] = T(0);
+          continue;
+        }
+        // w_i = b_i lam_{n+1} + sum_{j>i, a_ji != 0} a_ji Lam_j   (pad rows stay 0)
+        {
+        for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
+          const int o = (idx / N) * ldn + idx % N;
+          T v = Num<T>::mul(T(p.b[i]), lam[o]);
+  #pragma unroll
+          for (int j0 = 0; j0 < OB_MAX_STAGES; j0 += F::kCombineBatch) {   // loads in flight first
+            T lv[F::kCombineBatch];
+  #pragma unroll
+            for (int t = 0; t < F::kCombineBatch; ++t)
+              lv[t] = (j0 + t > i && j0 + t < s) ? Lam[(j0 + t) * kst + o] : T(0);
+  #pragma unroll
+            for (int t = 0; t < F::kCombineBatch; ++t) {
+              const double aji = (j0 + t > i && j0 + t < s) ? p.a[(j0 + t) * OB_MAX_STAGES + i] : 0.0;
+              if (aji != 0.0) v = Num<T>::add(v, Num<T>::mul(T(aji), lv[t]));
+            }
+          }
+          w[o] = v;
+        }
+        // stage state U_i into the field input (+ stage time)
+        for (int idx = threadIdx.x; idx < Rv * nin; idx += blockDim.x) {
+          const int r = idx / nin, j = idx % nin;
+          f.put(r, j, rec[i * vec + (long long)(row0 + r) * N + j]);
+        }
+        }
+        f.put_time(t + p.c[i] * h);
+        __syncthreads();
+        pt.mark(kPhElem);
+        f.vjp(w, jtv, mu, h, Rv);
+        pt.mark(kPhVjp);
+        // Lam_i = h * jtv; lam_n += Lam_i  (scaled-VJP adapters return J^T (h w) directly)
+        for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
+          const int o = (idx / N) * ldn + idx % N;
+          const T li = F::kScaledVjp ? jtv[o] : Num<T>::mul(T(h), jtv[o]);
+          Lam[i * kst + o] = li;
+          lamn[o] = Num<T>::add(lamn[o], li);
+        }
+        __syncthreads();
+        pt.mark(kPhLam);
       }
-      __syncthreads();
-      pt.mark(kPhLam);
-    }
-    int bad = 0;
-    for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) {
-      lam[idx] = lamn[idx];
-      if (!Num<T>::finite(lamn[idx])) bad = 1;
-    }
-    if (__syncthreads_or(bad)) {  // AdjointState.check_finite (adjoint.py:42-44)
-      if (threadIdx.x == 0) set_status(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
-      f.release();
-      return;
+      int bad = 0;
+      for (int idx = threadIdx.x; idx < kst; idx += blockDim.x) {
+        lam[idx] = lamn[idx];
+        if (!Num<T>::finite(lamn[idx])) bad = 1;
+      }
+      if (__syncthreads_or(bad)) {  // AdjointState.check_finite (adjoint.py:42-44)
+        if (threadIdx.x == 0) set_status(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
+        f.release();
+        return;
+      }
     }
   }
   f.finish(mu);

@@ -22,9 +22,12 @@
 // mu += P^T (h w) need no per-stage rescale), biases and the time column in
 // fp32 shared-memory vectors; finish() adds them to the CTA's mu slot once.
 //
-// One thread issues the MMAs and commits them to an mbarrier; all threads
-// wait on it, read accumulators with tcgen05.ld (each warp its TMEM lane
-// quarter), apply the epilogue and write the next operand.
+// The tile runs whole RK steps (step(), reverse_step()): each stage's
+// derivative / cotangent stays in its TMEM slot and the stage sums read it
+// with tcgen05.ld.  One elected lane of warp 0 issues the MMAs and commits them
+// to an mbarrier; all threads wait on it, read accumulators with tcgen05.ld
+// (each warp its TMEM lane quarter), apply the epilogue and write the next
+// operand.
 #pragma once
 
 #include "rk_impl.cuh"
@@ -109,8 +112,6 @@ struct TcMlpAdapter {
   static_assert(sizeof(T) == 4, "tensor-core MLP tile is fp32");
   static constexpr bool kHasJvp = false;
   static constexpr bool kScaledVjp = true;   // vjp returns J^T (h w)
-  static constexpr int kCombineBatch = 8;    // all stage loads in flight (no register pressure)
-  static constexpr int kCombineElems = 4;    // ... for 4 elements per thread at once
   static constexpr bool kOwnsStep = true;    // step(): stage derivatives stay in TMEM
   static constexpr uint32_t kCols = 512;     // whole TMEM: one CTA per SM, base column 0
   static constexpr TcGeom G = tc_geom(D0, H, D2);
@@ -156,17 +157,8 @@ struct TcMlpAdapter {
       set_status(p.status, OB_ERR_UNSUPPORTED, -2);   // TMEM not at column 0: shared SM
   }
 
-  OB_DEV T* x0() { return nullptr; }
   OB_DEV int nin() const { return D0; }
   OB_DEV void set_scratch(T*, int) {}
-  // stage state element j of row r (rows >= Rv are padding: kept at zero)
-  OB_DEV void put(int r, int j, T v) {
-    uint16_t hi, lo;
-    tc::split_bf16(r < Rv ? v : 0.f, hi, lo);
-    const uint32_t off = tc::blk(j, r, G.SAx, 128);
-    *reinterpret_cast<uint16_t*>(ob_tc_smem + G.X0h + off) = hi;
-    *reinterpret_cast<uint16_t*>(ob_tc_smem + G.X0l + off) = lo;
-  }
   // samples s0..s0+7 of state component m (rows >= Rv zero): two 16-byte stores
   OB_DEV void put8(int m, int s0, const float* v) {
     uint32_t hw[4], lw[4];
@@ -234,13 +226,6 @@ struct TcMlpAdapter {
       tc_mma3<G.Hh + 16 * G.SAh, G.Hl + 16 * G.SAh, 128, G.SAh, 256, G.X0h,
               G.X0l, 128, G.SAx, 256, kTcNS / 16, id>(T_W1 + D0, acc);
   }
-  // dX[i][s] = sum_o W1[o][i] dZ[s][o]            (A = W1 MN-major, B = dZ^T MN-major, M = 64)
-  OB_DEV void issue_dx() {
-    constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, true, true);
-    tc_mma3<G.W1h, G.W1l, G.SA1, 128, 2 * G.SA1, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh,
-            H / 16, id>(T_ACC2, 0);
-  }
-
   // ---- epilogues (warp w: TMEM lane quarter q = w % 4, column group cg = w / 4)
   OB_DEV void ld_hidden(float v[16], int& o, int& c0, int& cg) const {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3;
@@ -279,42 +264,6 @@ struct TcMlpAdapter {
     }
     put_hid(c0, o, a);
   }
-  // M = 64 accumulator (rows m = 16 q + lane for lanes < 16) -> dst[s][m] (+ b2)
-  OB_DEV void epi_state(T* dst, int ldo, bool bias) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3, cg = w >> 2;
-    float v[8];
-    tc::ld8(T_ACC2 + ((uint32_t)(q * 32) << 16) + 8 * cg, v);
-    const int m = 16 * q + lane;
-    if (lane < 16 && m < D0) {
-      const float bm = bias ? b2()[m] : 0.f;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int s = 8 * cg + j;
-        if (s < p.Rt) dst[s * ldo + m] = v[j] + bm;
-      }
-    }
-  }
-
-  // f(x0) -> out [Rt][ldn] (global or shared), columns >= N untouched
-  OB_DEV void eval(T* out) {
-    PhaseTimer pt(p.prof ? p.phase : nullptr);   // 10: MMA issue + wait, 11: epilogues
-    sync_issue();
-    if (tc::uniform_warp() == 0) { issue_hidden(); tc::commit(bar()); }
-    wait();
-    pt.mark(10);
-    float ap[16];
-    epi_hidden<false>(ap);
-    sync_issue();
-    pt.mark(11);
-    if (tc::uniform_warp() == 0) { issue_out(); tc::commit(bar()); }
-    wait();
-    pt.mark(10);
-    epi_state(out, p.d.ldn, true);
-    tc::fence_before();
-    __syncthreads();
-    pt.mark(11);
-  }
-
   // f(x0) into stage slot k (TMEM, bias b2 not yet added); no epilogue
   OB_DEV void eval_slot(int k) {
     PhaseTimer pt(p.prof ? p.phase : nullptr);
@@ -582,83 +531,6 @@ struct TcMlpAdapter {
     }
     tc::fence_before();
     return __syncthreads_or(bad) == 0;
-  }
-
-  // jtv = J^T (h w); mu (nullable) += h P^T w, accumulated on chip until finish()
-  OB_DEV void vjp(const T* wv, T* jtv, T* mu, double h, int) {
-    const int ldn = p.d.ldn;
-    const float hf = float(h);
-    PhaseTimer pt(p.prof ? p.phase : nullptr);   // 14: operand prep, 10: MMA waits, 11: epilogues
-    // V = h w (rows >= Rv zero) as (hi, lo)
-    for (int i = threadIdx.x; i < kTcNS * D2; i += blockDim.x) {
-      const int s = i / D2, o2 = i % D2;
-      const float v = s < Rv ? hf * wv[s * ldn + o2] : 0.f;
-      uint16_t hi, lo;
-      tc::split_bf16(v, hi, lo);
-      const uint32_t off = tc::blk(o2, s, G.SAv, 128);
-      *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vh + off) = hi;
-      *reinterpret_cast<uint16_t*>(ob_tc_smem + G.Vl + off) = lo;
-    }
-    sync_issue();
-    pt.mark(14);
-    if (tc::uniform_warp() == 0) { issue_hidden(); tc::commit(bar()); }
-    if (mu && threadIdx.x < D2) {   // db2 += sum_s h w[s]
-      float acc = 0.f;
-      for (int s = 0; s < Rv; ++s) acc += hf * wv[s * ldn + threadIdx.x];
-      db2()[threadIdx.x] += acc;
-    }
-    wait();
-    pt.mark(10);
-    float ap[16];
-    epi_hidden<true>(ap);
-    sync_issue();
-    pt.mark(11);
-    const uint32_t acc = started ? 1u : 0u;
-    if (tc::uniform_warp() == 0) {
-      if (mu) issue_dw2(acc);
-      issue_dh();
-      tc::commit(bar());
-    }
-    wait();
-    pt.mark(10);
-    // dZ = dH * act'(z) overwrites H (its MMAs have completed); per-row partial sums
-    {
-      float v[16];
-      int o, c0, cg;
-      ld_hidden(v, o, c0, cg);
-      float ps = 0.f;
-#pragma unroll
-      for (int j = 0; j < CW; ++j) {
-        v[j] *= ap[j];
-        ps += v[j];
-      }
-      put_hid(c0, o, v);
-      // V is free now: partial sums part[k][o], k = column group within the row
-      float* part = reinterpret_cast<float*>(ob_tc_smem + G.Vh);
-      part[(cg % (4 / NMB)) * H + o] = ps;
-    }
-    sync_issue();
-    pt.mark(11);
-    if (tc::uniform_warp() == 0) {
-      if (mu) issue_dw1(acc);
-      issue_dx();
-      tc::commit(bar());
-    }
-    if (mu && threadIdx.x < H) {   // db1 += sum_s dZ, time column += t sum_s dZ
-      const float* part = reinterpret_cast<const float*>(ob_tc_smem + G.Vh);
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < 4 / NMB; ++k) s += part[k * H + threadIdx.x];
-      db1()[threadIdx.x] += s;
-      dwt()[threadIdx.x] += tcur * s;
-    }
-    wait();
-    pt.mark(10);
-    epi_state(jtv, ldn, false);
-    if (mu) started = true;
-    tc::fence_before();
-    __syncthreads();
-    pt.mark(11);
   }
 
   // add the sweep's parameter cotangent to the CTA's padded mu slot
