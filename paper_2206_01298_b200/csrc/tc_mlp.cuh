@@ -45,7 +45,7 @@ struct TcGeom {
   int D0, H, D2, nmb;
   uint32_t SA1, SA2, SAx, SAh, SAv;
   uint32_t W2h, W2l, W1h, W1l, fv, packed;
-  uint32_t X0h, X0l, Hh, Hl, Vh, Vl, vec, pw, bar, slot, total;
+  uint32_t X0h, X0l, Hh, Hl, Vh, Vl, vec, pw, bar, bar2, slot, total;
 };
 
 __host__ __device__ constexpr TcGeom tc_geom(int D0, int H, int D2) {
@@ -74,6 +74,7 @@ __host__ __device__ constexpr TcGeom tc_geom(int D0, int H, int D2) {
   g.pw = o;  o += (uint32_t)(4 * D2) * 4;           // db2 partials [4][D2] (reverse_step)
   o = (o + 15) & ~15u;
   g.bar = o; o += 8;
+  g.bar2 = o; o += 8;                               // parameter-cotangent MMAs (off the critical path)
   g.slot = o; o += 8;
   o = (o + 31) & ~31u;
   g.total = o;
@@ -126,12 +127,15 @@ struct TcMlpAdapter {
 
   const RkParams<T>& p;
   uint32_t phase;       // mbarrier parity
+  uint32_t phase2;      // parity of bar2 (dW MMAs)
+  bool pend2;           // a dW MMA group is still running (reads V / X0 / dZ)
   float tcur;           // stage time (CTA-wide, set by put_time)
   int Rv, act;
   bool started;         // parameter-cotangent accumulators hold data
 
   OB_DEV unsigned char* base() const { return ob_tc_smem; }
   OB_DEV uint64_t* bar() const { return reinterpret_cast<uint64_t*>(ob_tc_smem + G.bar); }
+  OB_DEV uint64_t* bar2() const { return reinterpret_cast<uint64_t*>(ob_tc_smem + G.bar2); }
   OB_DEV const float* w1t() const { return reinterpret_cast<const float*>(ob_tc_smem + G.fv); }
   OB_DEV const float* b1() const { return w1t() + H; }
   OB_DEV const float* b2() const { return w1t() + 2 * H; }
@@ -140,7 +144,7 @@ struct TcMlpAdapter {
   OB_DEV float* db2() const { return db1() + 2 * H; }
 
   OB_DEV TcMlpAdapter(const RkParams<T>& p_, const Weights<T>&, MlpSmem<T>&, T* sm, int, int Rv_)
-      : p(p_), phase(0), tcur(0.f), Rv(Rv_), act(p_.d.act), started(false) {
+      : p(p_), phase(0), phase2(0), pend2(false), tcur(0.f), Rv(Rv_), act(p_.d.act), started(false) {
     // operand tiles, accumulator vectors and the generic state buffers after the
     // region start at zero (padded samples stay 0)
     uint4* z = reinterpret_cast<uint4*>(ob_tc_smem + G.packed);
@@ -149,7 +153,10 @@ struct TcMlpAdapter {
       if (i < (int)((G.bar - G.packed) / 16) || i >= (int)((G.total - G.packed) / 16))
         z[i] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x < 32) tc::tmem_alloc(reinterpret_cast<uint32_t*>(ob_tc_smem + G.slot), kCols);
-    if (threadIdx.x == 0) tc::bar_init(bar(), 1);
+    if (threadIdx.x == 0) {
+      tc::bar_init(bar(), 1);
+      tc::bar_init(bar2(), 1);
+    }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -183,6 +190,14 @@ struct TcMlpAdapter {
     tc::bar_wait(bar(), phase);
     phase ^= 1u;
     tc::fence_after();
+  }
+  // wait for the outstanding parameter-cotangent MMAs before their operands are rewritten
+  OB_DEV void drain() {
+    if (!pend2) return;
+    tc::bar_wait(bar2(), phase2);
+    phase2 ^= 1u;
+    tc::fence_after();
+    pend2 = false;
   }
 
   // ---- products (issued by warp 0; one elected lane)
@@ -394,11 +409,13 @@ struct TcMlpAdapter {
     sync_issue();
     pt.mark(11);
     const uint32_t acc = started ? 1u : 0u;
+    // dH first (the critical path), dW2^T behind it on its own barrier
     if (tc::uniform_warp() == 0) {
-      if (mu) issue_dw2(acc);
       issue_dh();
       tc::commit(bar());
+      if (mu) { issue_dw2(acc); tc::commit(bar2()); }
     }
+    if (mu) pend2 = true;
     wait();
     pt.mark(10);
     {
@@ -411,18 +428,21 @@ struct TcMlpAdapter {
         v[j] *= ap[j];
         ps += v[j];
       }
+      drain();   // dW2^T reads H: dZ may overwrite it only now
       put_hid(c0, o, v);
       float* part = reinterpret_cast<float*>(ob_tc_smem + G.Vh);
       part[(cg % (4 / NMB)) * H + o] = ps;
     }
     sync_issue();
     pt.mark(11);
+    // dX first; dW1 keeps running into the next stage (drained before X0 / dZ change)
     if (tc::uniform_warp() == 0) {
-      if (mu) issue_dw1(acc);
       constexpr uint32_t id = tc::idesc_bf16(64, kTcNS, true, true);
       tc_mma3<G.W1h, G.W1l, G.SA1, 128, 2 * G.SA1, G.Hh, G.Hl, G.SAh, 128, 2 * G.SAh, H / 16, id>(dx, 0);
       tc::commit(bar());
+      if (mu) { issue_dw1(acc); tc::commit(bar2()); }
     }
+    if (mu) pend2 = true;
     if (mu && threadIdx.x < H) {
       const float* part = reinterpret_cast<const float*>(ob_tc_smem + G.Vh);
       float sm = 0.f;
@@ -487,6 +507,7 @@ struct TcMlpAdapter {
         for (int e = 0; e < 8; ++e) v[e] = Num<float>::add(v[e], Num<float>::mul(ca[j], k[e]));
       }
       // V = h w (padded samples zero), db2 partial, U_i into X0
+      drain();   // the previous stage's dW1 reads X0 and dZ
       float ps = 0.f;
       if (mine) {
         float hv[8];
@@ -509,6 +530,7 @@ struct TcMlpAdapter {
       vjp_core(mu, slot_col(i), true);
       live |= 1u << i;
     }
+    drain();
     // lam_n = lam_{n+1} + Lambda_{s-1} + ... + Lambda_0
     int bad = 0;
 #pragma unroll
