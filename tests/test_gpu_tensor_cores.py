@@ -215,3 +215,36 @@ def test_nonuniform_grid_on_tensor_cores():
                            len(times) - 1, "revolve:2", times=np.array(times))
     e = errs(res, ref)
     assert max(e.values()) <= TOL32, e
+
+
+def test_batch_shards_sum_to_full_batch_on_tensor_cores():
+    """Data-parallel contract on the tensor-core tile: shards with batch_global = B sum to
+    the full call (deterministic per-CTA slots, fixed-order reduction)."""
+    ci = make_config("C2", batch=700)
+    fld = field_from_config(ci)
+    full = run_config(ci, "revolve:8", field=fld)
+    a = run_config(ci, "revolve:8", field=fld, u0=ci.u0[:300], batch_global=ci.batch)
+    b = run_config(ci, "revolve:8", field=fld, u0=ci.u0[300:], batch_global=ci.batch)
+    assert full.device["tensor_cores"] == 1 and a.device["tensor_cores"] == 1
+    assert oc.rel_error(np_(a.dtheta) + np_(b.dtheta), np_(full.dtheta)) <= 1e-5
+    assert abs(a.loss + b.loss - full.loss) <= 1e-6 * abs(full.loss)
+    assert oc.rel_error(np.concatenate([np_(a.du0), np_(b.du0)]), np_(full.du0)) <= 1e-6
+
+
+def test_overflow_and_bad_input_on_tensor_cores():
+    from paper_2206_01298_b200 import IntegrationError
+    rng = np.random.default_rng(9)
+    widths, theta = make_mlp(rng, 64, 256, "identity", True)
+    model = MlpModel(MlpSpec(widths, "identity", time_input=True, dtype="f32"), theta * 40.0)
+    u0 = f32(rng.normal(size=(50, 64)))
+    with pytest.raises(IntegrationError):
+        grad(MlpField(model), tableau_catalog("rk4"), terminal_loss("half_sqnorm", 1.0),
+             torch.as_tensor(u0, dtype=torch.float32, device="cuda"), 0.0, 1.0, FixedController(30),
+             CheckpointPolicy.parse("store_all"))
+    bad = u0.copy()
+    bad[3, 5] = np.nan
+    model = MlpModel(MlpSpec(widths, "identity", time_input=True, dtype="f32"), theta)
+    with pytest.raises(ValueError):
+        grad(MlpField(model), tableau_catalog("rk4"), terminal_loss("half_sqnorm", 1.0),
+             torch.as_tensor(bad, dtype=torch.float32, device="cuda"), 0.0, 1.0, FixedController(3),
+             CheckpointPolicy.parse("store_all"))
