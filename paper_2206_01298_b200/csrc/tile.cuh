@@ -53,19 +53,47 @@ OB_DEV void load4(const double* p, double v[4]) {
 }
 
 // activations: kernels.py:45-77 (+ softplus for the CNF config)
-// fp32 tanh via one exp2 and one reciprocal: |rel err| ~ 1e-7 (vs ~20 instructions
-// for tanhf); fp64 keeps the libm tanh (fp64 parity is held to 1e-10)
+// fp32 transcendentals go through the SFU's ex2/lg2 (one op each) with the reciprocal
+// 1/(1 + e), e in (0, 1], refined by Newton steps on the FMA pipe: absolute error
+// ~1e-7, far inside the fp32 parity bar and several times cheaper than the libm
+// paths (exp2f / expf / log1pf / IEEE division); fp64 keeps libm (held to 1e-10).
+OB_DEV float ex2_fast(float x) {
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
+  return e;
+}
+OB_DEV float lg2_fast(float x) {
+  float l;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
+  return l;
+}
+OB_DEV float recip_1p(float e) {   // 1 / (1 + e) for e in [0, 1]
+  const float d = 1.0f + e;
+  float r = fmaf(-0.5f, d, 1.4571068f);
+  r = fmaf(r, fmaf(-d, r, 1.0f), r);
+  r = fmaf(r, fmaf(-d, r, 1.0f), r);
+  r = fmaf(r, fmaf(-d, r, 1.0f), r);
+  return r;
+}
 OB_DEV float fast_tanh(float x) {
-  const float ax = fabsf(x);
-  if (ax < 0.0625f) {                      // series near 0 avoids 1 - (1 - eps) cancellation
-    const float x2 = x * x;
-    return x * (1.0f + x2 * (-0.33333334f + x2 * (0.13333334f + x2 * -0.053968254f)));
-  }
-  const float e = exp2f(-2.8853900817779268f * ax);   // exp(-2|x|)
-  const float r = __fdividef(1.0f - e, 1.0f + e);
-  return copysignf(r, x);
+  const float e = ex2_fast(-2.8853900817779268f * fabsf(x));   // exp(-2|x|)
+  return copysignf((1.0f - e) * recip_1p(e), x);
 }
 OB_DEV double fast_tanh(double x) { return tanh(x); }
+OB_DEV float fast_sigmoid(float x) {       // 1 / (1 + exp(-x))
+  const float e = ex2_fast(-1.4426950408889634f * fabsf(x));   // exp(-|x|)
+  const float r = recip_1p(e);
+  return x >= 0.0f ? r : e * r;
+}
+OB_DEV double fast_sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+OB_DEV float fast_softplus(float x) {      // max(x, 0) + log1p(exp(-|x|))
+  const float e = ex2_fast(-1.4426950408889634f * fabsf(x));
+  return fmaxf(x, 0.0f) + 0.6931471805599453f * lg2_fast(1.0f + e);
+}
+OB_DEV double fast_softplus(double x) {
+  const double ax = x < 0.0 ? -x : x;
+  return (x > 0.0 ? x : 0.0) + log1p(exp(-ax));
+}
 
 template <typename T> OB_DEV T act_fn(T x, int id) {
   switch (id) {
@@ -73,10 +101,7 @@ template <typename T> OB_DEV T act_fn(T x, int id) {
     case OB_ACT_RELU: return x > T(0) ? x : T(0);
     case OB_ACT_TANH: return fast_tanh(x);
     case OB_ACT_GELU: return T(0.5) * x * (T(1) + erf(x * T(0.70710678118654752440)));
-    default: {  // softplus, overflow-safe: max(x,0) + log1p(exp(-|x|))
-      T ax = x < T(0) ? -x : x;
-      return (x > T(0) ? x : T(0)) + log1p(exp(-ax));
-    }
+    default: return fast_softplus(x);   // overflow-safe form
   }
 }
 template <typename T> OB_DEV T act_prime(T x, int id) {
@@ -87,13 +112,13 @@ template <typename T> OB_DEV T act_prime(T x, int id) {
     case OB_ACT_GELU:
       return T(0.5) * (T(1) + erf(x * T(0.70710678118654752440))) +
              x * T(0.39894228040143267794) * exp(T(-0.5) * x * x);
-    default: return T(1) / (T(1) + exp(-x));  // softplus' = sigmoid
+    default: return fast_sigmoid(x);  // softplus' = sigmoid
   }
 }
 template <typename T> OB_DEV T act_second(T x, int id) {
   switch (id) {
     case OB_ACT_TANH: { T t = tanh(x); return T(-2) * t * (T(1) - t * t); }
-    case OB_ACT_SOFTPLUS: { T s = T(1) / (T(1) + exp(-x)); return s * (T(1) - s); }
+    case OB_ACT_SOFTPLUS: { T s = fast_sigmoid(x); return s * (T(1) - s); }
     case OB_ACT_GELU: return T(0.39894228040143267794) * exp(T(-0.5) * x * x) * (T(2) - x * x);
     default: return T(0);
   }
