@@ -155,6 +155,15 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
   const long long vec = (long long)p.B * N;
   PhaseTimer pt(p.prof ? p.phase : nullptr);
   for (int i = 0; i < s; ++i) {
+    // stage coefficients T(h a_iq), formed once per stage (exact zeros skipped)
+    T cq[OB_MAX_STAGES];
+    unsigned nzq = 0;
+#pragma unroll
+    for (int q = 0; q < OB_MAX_STAGES; ++q) {
+      const double aiq = q < i ? p.a[i * OB_MAX_STAGES + q] : 0.0;
+      cq[q] = T(h * aiq);
+      if (aiq != 0.0) nzq |= 1u << q;
+    }
     for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
       const int r = idx / N, j = idx % N;
       // issue every stage-derivative load (L2-resident scratch) before the dependent
@@ -167,10 +176,8 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
         for (int t = 0; t < F::kCombineBatch; ++t)
           kv[t] = q0 + t < i ? ks[(q0 + t) * kst + r * ldn + j] : T(0);
 #pragma unroll
-        for (int t = 0; t < F::kCombineBatch; ++t) {
-          const double aiq = q0 + t < i ? p.a[i * OB_MAX_STAGES + q0 + t] : 0.0;
-          if (aiq != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * aiq), kv[t]));
-        }
+        for (int t = 0; t < F::kCombineBatch; ++t)
+          if ((nzq >> (q0 + t)) & 1u) v = Num<T>::add(v, Num<T>::mul(cq[q0 + t], kv[t]));
       }
       if (j < nin) f.put(r, j, v);
       if (rec && r < Rv) rec[i * vec + (long long)(row0 + r) * N + j] = v;
@@ -187,6 +194,14 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
     pt.mark(9);   // field eval
   }
   int bad = 0;
+  T cb[OB_MAX_STAGES];
+  unsigned nzb = 0;
+#pragma unroll
+  for (int q = 0; q < OB_MAX_STAGES; ++q) {
+    const double bq = q < s ? p.b[q] : 0.0;
+    cb[q] = T(h * bq);
+    if (bq != 0.0) nzb |= 1u << q;
+  }
   for (int idx = threadIdx.x; idx < Rt * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
     T v = u[r * ldn + j];
@@ -197,10 +212,8 @@ OB_DEV bool rk_step_tile(const RkParams<T>& p, F& f, T* u, T* ks, double t, doub
       for (int t = 0; t < F::kCombineBatch; ++t)
         kv[t] = i0 + t < s ? ks[(i0 + t) * kst + r * ldn + j] : T(0);
 #pragma unroll
-      for (int t = 0; t < F::kCombineBatch; ++t) {
-        const double bi = i0 + t < s ? p.b[i0 + t] : 0.0;
-        if (bi != 0.0) v = Num<T>::add(v, Num<T>::mul(T(h * bi), kv[t]));
-      }
+      for (int t = 0; t < F::kCombineBatch; ++t)
+        if ((nzb >> (i0 + t)) & 1u) v = Num<T>::add(v, Num<T>::mul(cb[i0 + t], kv[t]));
     }
     u[r * ldn + j] = v;
     if (r < Rv) {
