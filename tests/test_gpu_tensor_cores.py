@@ -248,3 +248,25 @@ def test_overflow_and_bad_input_on_tensor_cores():
         grad(MlpField(model), tableau_catalog("rk4"), terminal_loss("half_sqnorm", 1.0),
              torch.as_tensor(bad, dtype=torch.float32, device="cuda"), 0.0, 1.0, FixedController(3),
              CheckpointPolicy.parse("store_all"))
+
+
+def test_plan_cache_distinguishes_problems():
+    """The host plan is reused only for an identical problem (struct and host arrays):
+    alternating grids / batches / policies must reproduce fresh results exactly."""
+    from paper_2206_01298_b200 import FixedGridController
+    rng = np.random.default_rng(13)
+    widths, theta = make_mlp(rng, 64, 256, "tanh", True)
+    model = MlpModel(MlpSpec(widths, "tanh", time_input=True, dtype="f32"), theta)
+    fld = MlpField(model)
+    u0 = torch.as_tensor(f32(rng.normal(size=(64, 64))), dtype=torch.float32, device="cuda")
+
+    def run(times, pol, rows):
+        return grad(fld, tableau_catalog("dopri5"), terminal_loss("half_sqnorm", 1.0), u0[:rows],
+                    0.0, 1.0, FixedGridController(times), CheckpointPolicy.parse(pol))
+
+    ga, gb = (0.0, 0.25, 0.5, 1.0), (0.0, 0.5, 0.75, 1.0)   # same step count, other times
+    first = [run(ga, "store_all", 64), run(gb, "store_all", 64), run(ga, "revolve:1", 40)]
+    again = [run(ga, "revolve:1", 40), run(gb, "store_all", 64), run(ga, "store_all", 64)][::-1]
+    for x, y in zip(first, again):
+        assert torch.equal(x.dtheta, y.dtheta) and torch.equal(x.du0, y.du0) and x.loss == y.loss
+    assert not torch.equal(first[0].dtheta, first[1].dtheta)
