@@ -33,8 +33,14 @@ cudaError_t launch_field_ws(const RkParams<T>&, int, int, size_t, int, double, c
                             T*, cudaStream_t);
 template <typename T> cudaError_t launch_reduce(const Dims&, const T*, int, long long, T*,
                                                 const double*, double, double*, cudaStream_t);
+template <typename T, bool kFwd>
+cudaError_t launch_theta_dir(const RkParams<T>&, int, int, size_t, cudaStream_t);
 template <typename T>
-cudaError_t launch_theta(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
+cudaError_t launch_theta(const RkParams<T>& p, int lr, int tiles, size_t smem, cudaStream_t st,
+                         bool forward) {
+  return forward ? launch_theta_dir<T, true>(p, lr, tiles, smem, st)
+                 : launch_theta_dir<T, false>(p, lr, tiles, smem, st);
+}
 template <typename T>
 cudaError_t launch_cnf(const RkParams<T>&, int, int, size_t, cudaStream_t, bool);
 template <typename T>

@@ -542,21 +542,20 @@ theta_reverse_kernel(const __grid_constant__ RkParams<T> p) {
   flush_stats(p, c, row0, Rv);
 }
 
-template <typename T, int LR>
-static cudaError_t launch_theta_lr(const RkParams<T>& p, int tiles, size_t smem, cudaStream_t st,
-                                   bool forward) {
-  return forward ? launch_smem(theta_forward_kernel<T, LR, false>, tiles, smem, st, p)
-                 : launch_smem(theta_reverse_kernel<T, LR, false>, tiles, smem, st, p);
+// one sweep direction per translation unit (theta_*_fwd.cu / theta_*_rev.cu compile in parallel)
+template <typename T, bool kFwd, int LR>
+static cudaError_t launch_theta_lr(const RkParams<T>& p, int tiles, size_t smem, cudaStream_t st) {
+  if constexpr (kFwd) return launch_smem(theta_forward_kernel<T, LR, false>, tiles, smem, st, p);
+  else return launch_smem(theta_reverse_kernel<T, LR, false>, tiles, smem, st, p);
 }
 
-template <typename T>
-cudaError_t launch_theta(const RkParams<T>& p, int lr, int tiles, size_t smem, cudaStream_t st,
-                         bool forward) {
+template <typename T, bool kFwd>
+cudaError_t launch_theta_dir(const RkParams<T>& p, int lr, int tiles, size_t smem, cudaStream_t st) {
   switch (lr) {
-    case 1: return launch_theta_lr<T, 1>(p, tiles, smem, st, forward);
-    case 2: return launch_theta_lr<T, 2>(p, tiles, smem, st, forward);
+    case 1: return launch_theta_lr<T, kFwd, 1>(p, tiles, smem, st);
+    case 2: return launch_theta_lr<T, kFwd, 2>(p, tiles, smem, st);
     default:
-      if constexpr (sizeof(T) == 4) return launch_theta_lr<T, 8>(p, tiles, smem, st, forward);
+      if constexpr (sizeof(T) == 4) return launch_theta_lr<T, kFwd, 8>(p, tiles, smem, st);
       return cudaErrorInvalidConfiguration;
   }
 }
