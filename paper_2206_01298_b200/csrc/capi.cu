@@ -346,8 +346,8 @@ void layout_smem(Plan& P) {
     s.x0 = take(18 * 18 * 68);
     for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
     s.hid[0] = take(18 * 18 * 68);
-    s.tA = s.tB = s.u = s.lam = s.lamn = s.w = s.jtv = s.aux = s.wts = s.ks = s.ring = -1;
-    s.ring_elems = 0;
+    s.tA = s.tB = s.u = s.lam = s.lamn = s.w = s.jtv = s.aux = s.wts = s.ks = s.ring = s.hscr = -1;
+    s.ring_elems = s.hscr_elems = 0;
     for (int i = 0; i < 8; ++i) s.vec[i] = -1;
     // double-buffered tap weights (2 x 64 x 68) for the staged conv GEMMs, when they fit
     if ((size_t)(o + 2 * 64 * 68) * P.esz <= smem_cap(P) && !getenv("OB_CONV_UNSTAGED")) s.tA = take(2 * 64 * 68);
@@ -389,6 +389,17 @@ void layout_smem(Plan& P) {
   if (ws_variant && (size_t)(o + d.n_packed) * P.esz <= smem_cap(P) && !getenv("OB_NO_SMEM_WEIGHTS")) {
     s.wts = take(d.n_packed);
     s.total = o;
+  }
+  // hidden-layer split-K partials for tiny explicit-RK MLP tiles (4 slices of the widest layer)
+  s.hscr = -1;
+  s.hscr_elems = 0;
+  if (!P.theta && !d.cnf && !getenv("OB_NO_HSPLIT")) {
+    const long long n = 4LL * P.Rt * d.maxw;
+    if ((size_t)(o + n) * P.esz + 4096 <= smem_cap(P)) {
+      s.hscr = take(n);
+      s.hscr_elems = (int)n;
+      s.total = o;
+    }
   }
   // per-warp cp.async rings for weights streamed from L2 (weights not staged in smem)
   s.ring = -1;
@@ -492,8 +503,8 @@ bool plan_tc(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   s = SmemLayout{};
   int o = 0;
   auto take = [&](long long n) { int r = o; o += (int)((n + 7) & ~7LL); return r; };
-  s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = s.ks = s.ring = -1;
-  s.ring_elems = 0;
+  s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = s.ks = s.ring = s.hscr = -1;
+  s.ring_elems = s.hscr_elems = 0;
   for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
   for (int i = 0; i < 8; ++i) s.vec[i] = -1;
   s.scr_elems = 0;

@@ -21,6 +21,7 @@ struct SmemLayout {      // offsets in elements of T (-1: not allocated)
   int wts;                // packed weights staged in shared memory, or -1
   int ks;                 // per-tile stage scratch [2][s][Rt][ldn] in shared memory, or -1 (global)
   int ring, ring_elems;   // per-warp cp.async rings for L2-streamed weights, or -1
+  int hscr, hscr_elems;   // hidden-layer split-K partials (MLP explicit-RK tiles), or -1
   int total;
 };
 

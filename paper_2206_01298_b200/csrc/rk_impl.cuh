@@ -66,9 +66,10 @@ template <typename T, int LR, bool WS>
 struct MlpAdapter {
   const RkParams<T>& p;
   MlpTile<T, LR, WS> mt;
-  OB_DEV MlpAdapter(const RkParams<T>& p_, const Weights<T>& W, MlpSmem<T>& ms, T*, int, int)
+  OB_DEV MlpAdapter(const RkParams<T>& p_, const Weights<T>& W, MlpSmem<T>& ms, T* sm, int, int)
       : p(p_), mt(p_.d, W, ms, p_.Rt) {
     mt.prof_acc = p.prof ? p.phase : nullptr;
+    if (p.sm.hscr >= 0) { mt.hscratch = sm + p.sm.hscr; mt.hscratch_elems = p.sm.hscr_elems; }
   }
   OB_DEV MlpAdapter(const RkParams<T>& p_, const MlpTile<T, LR, WS>& m) : p(p_), mt(m) {}
   OB_DEV T* x0() { return mt.s.x0; }

@@ -217,9 +217,12 @@ struct MlpTile {
   int Rt;
   T* scratch;          // split-K partials for narrow output layers (nullable)
   int scratch_elems;
+  T* hscratch;         // split-K partials for hidden layers (dedicated region, nullable)
+  int hscratch_elems;
 
   OB_DEV MlpTile(const Dims& d_, const Weights<T>& W_, MlpSmem<T>& s_, int Rt_)
-      : d(d_), W(W_), s(s_), Rt(Rt_), scratch(nullptr), scratch_elems(0) {}
+      : d(d_), W(W_), s(s_), Rt(Rt_), scratch(nullptr), scratch_elems(0), hscratch(nullptr),
+        hscratch_elems(0) {}
 
   OB_DEV const T* in(int l) const { return l == 0 ? s.x0 : s.hid[l - 1]; }
 
@@ -309,11 +312,34 @@ struct MlpTile {
         T* hid = s.hid[l];
         T* pre = d.need_pre ? s.pre[l] : nullptr;
         const int act = d.act;
-        nt(in(l), d.lda[l], l, 1, Warps::all(), [&](int r, int n, T acc, int) {
-          const T z = Num<T>::add(acc, b[n]);
-          hid[r * ldh + n] = act_fn(z, act);
-          if (pre) pre[r * ldh + n] = z;
-        });
+        // too few column tasks for the CTA (tiny tiles): deterministic split-K through
+        // the dedicated partials region, summed in slice order
+        int hsplit = 1;
+        if (hscratch && tasks_narrow(N) * 2 <= n_warps()) {
+          hsplit = min(n_warps() / max(tasks_narrow(N), 1), hscratch_elems / (Rt * N));
+          hsplit = max(1, min(hsplit, (d.w[l] + 3) / 16));
+        }
+        if (hsplit > 1) {
+          T* part = hscratch;
+          const int pst = Rt * N;
+          nt(in(l), d.lda[l], l, hsplit, Warps::all(),
+             [&](int r, int n, T acc, int sl) { part[sl * pst + r * N + n] = acc; });
+          __syncthreads();
+          for (int i = threadIdx.x; i < Rt * N; i += blockDim.x) {
+            T acc = part[i];
+            for (int sl = 1; sl < hsplit; ++sl) acc = Num<T>::add(acc, part[sl * pst + i]);
+            const int r = i / N, n = i % N;
+            const T z = Num<T>::add(acc, b[n]);
+            hid[r * ldh + n] = act_fn(z, act);
+            if (pre) pre[r * ldh + n] = z;
+          }
+        } else {
+          nt(in(l), d.lda[l], l, 1, Warps::all(), [&](int r, int n, T acc, int) {
+            const T z = Num<T>::add(acc, b[n]);
+            hid[r * ldh + n] = act_fn(z, act);
+            if (pre) pre[r * ldh + n] = z;
+          });
+        }
         __syncthreads();
         pt.mark(10);
       }
