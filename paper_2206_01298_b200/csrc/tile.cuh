@@ -363,11 +363,31 @@ struct MlpTile {
         }
         T* h = s.hid[l - 1];
         const T* z = d.need_pre ? s.pre[l - 1] : nullptr;
-        const int ldh = d.lda[l], act = d.act;
-        nn(D, ldD, l, d.w[l], Warps::all(), [&](int r, int k, T acc, int) {
-          const T a = h[r * ldh + k];
-          h[r * ldh + k] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + k] : a, act));
-        });
+        const int ldh = d.lda[l], act = d.act, K = d.w[l];
+        int hsplit = 1;   // tiny tiles: deterministic split-K as in forward()
+        if (hscratch && tasks_narrow(K) * 2 <= n_warps()) {
+          hsplit = min(n_warps() / max(tasks_narrow(K), 1), hscratch_elems / (Rt * K));
+          hsplit = max(1, min(hsplit, (d.w[l + 1] + 3) / 16));
+        }
+        if (hsplit > 1) {
+          T* part = hscratch;
+          const int pst = Rt * K;
+          nn(D, ldD, l, K, Warps::all(),
+             [&](int r, int k, T acc, int sl) { part[sl * pst + r * K + k] = acc; }, hsplit);
+          __syncthreads();
+          for (int i = threadIdx.x; i < Rt * K; i += blockDim.x) {
+            T acc = part[i];
+            for (int sl = 1; sl < hsplit; ++sl) acc = Num<T>::add(acc, part[sl * pst + i]);
+            const int r = i / K, k = i % K;
+            const T a = h[r * ldh + k];
+            h[r * ldh + k] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + k] : a, act));
+          }
+        } else {
+          nn(D, ldD, l, K, Warps::all(), [&](int r, int k, T acc, int) {
+            const T a = h[r * ldh + k];
+            h[r * ldh + k] = Num<T>::mul(acc, act_prime_from(a, z ? z[r * ldh + k] : a, act));
+          });
+        }
         __syncthreads();
       } else {
         // first layer: the input product (narrow, N columns) and the dW0
