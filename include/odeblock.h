@@ -58,7 +58,13 @@ enum { OB_POLICY_STORE_ALL = 0, OB_POLICY_STORE_SOLUTIONS = 1, OB_POLICY_REVOLVE
    with optional min-max scaling, losses.py:10-107; seeds injected at step
    boundaries as in backward_sweep, adjoint.py:235-253) for MLP / stiff fields */
 enum { OB_LOSS_HALF_SQNORM = 0, OB_LOSS_MSE = 1, OB_LOSS_CE_HEAD = 2, OB_LOSS_CNF_NLL = 3,
-       OB_LOSS_OBS_MSE = 4, OB_LOSS_OBS_MAE = 5 };
+       OB_LOSS_OBS_MSE = 4, OB_LOSS_OBS_MAE = 5,
+       /* caller-supplied seeds (backward_sweep with an arbitrary terminal AdjointState,
+          adjoint.py:47-52, :235-253): lambda_N = ob_buffers.seed [B,N] as given (no batch
+          scaling), injections ob_buffers.obs_values [n_obs,B,N] added to lambda at the
+          boundaries obs_steps (inject_observation, adjoint.py:135-140), mu_N =
+          ob_buffers.dtheta_seed [n_params] or 0; the loss is the caller's (ob loss = 0) */
+       OB_LOSS_SEED = 6 };
 /* revolve action kinds (checkpointing.py:70-80) */
 enum { OB_ACT_ADVANCE = 0, OB_ACT_STORE = 1, OB_ACT_RESTORE = 2, OB_ACT_REVERSE = 3 };
 
@@ -128,6 +134,11 @@ typedef struct {
   int64_t max_steps;      /* per integrate() call, trials included               */
   double t0, tF;
   const double* obs_times; /* HOST [n_obs] observation times (adaptive + OB_LOSS_OBS_*) */
+  /* samples per CTA tile: 0 = the planner's choice (ceil(B / #SM), capped per kernel
+     family); > 0 forces it (capped the same way) -- selects the tile geometry a test
+     or a benchmark exercises */
+  int32_t tile_rows;
+  int32_t _pad2;
 } ob_problem;
 
 /* flags: accumulate per-phase SM cycles of the persistent kernels (profiling aid;
@@ -164,6 +175,9 @@ typedef struct {
   /* adaptive: optional outputs of the per-sample grids */
   double* grid;           /* out [B, max_accepted + 1] boundary times (NaN past the end) or NULL */
   int32_t* n_accepted;    /* out [B] accepted steps per sample, or NULL                 */
+  /* OB_LOSS_SEED: terminal adjoint state (adjoint_terminal, adjoint.py:47-52) */
+  const void* seed;        /* [B, N] lambda_N                                            */
+  const void* dtheta_seed; /* [n_params] mu_N, or NULL (zero)                            */
 } ob_buffers;
 
 /* per-sample stats columns (implicit schemes; explicit: fixed by the schedule) */
@@ -201,6 +215,16 @@ int ob_revolve_schedule(int32_t nt, int32_t nc, int32_t* actions, int64_t capaci
    loss_and_grad_seed (losses.py:78-107) + backward_sweep (:235-253). */
 int ob_grad_workspace_size(const ob_problem* p, size_t* bytes);
 int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream);
+/* The two halves of ob_grad on one workspace, for callers that form the terminal
+   seed themselves (grad() split as forward_pass + loss + backward_sweep,
+   adjoint.py:151-210 / :235-253):
+   ob_forward_pass: weight packing + forward sweep: u_final, predictions at observed
+     boundaries, checkpoints kept in b->workspace (and, for a built-in loss, b->loss);
+   ob_backward_sweep: reverse sweep from those checkpoints -> du0 (lambda_0), dtheta
+     (mu_0).  Same problem struct and workspace in both calls; theta and u0 must not
+     change in between (the reference's ForwardSolution holds the same state). */
+int ob_forward_pass(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream);
+int ob_backward_sweep(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream);
 
 /* ---- continuous-adjoint baseline (continuous_adjoint_solve, adjoint.py:294-331) ----
    Integrates the augmented reverse-time system (u, lambda, mu) with p's explicit

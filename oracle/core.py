@@ -647,7 +647,7 @@ class Run:
 
 
 def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", seed_fn=None,
-                  cfg: SolverCfg = None, times=None, obs=None):
+                  cfg: SolverCfg = None, times=None, obs=None, mu0=None, injections=None):
     """forward_pass + terminal seed + backward_sweep for a batch of samples.
 
     ``seed_fn(u_final) -> (loss, lam_N)``; default is the BASELINE loss
@@ -656,8 +656,12 @@ def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", see
     at step boundaries: states captured in the forward (adjoint.py:196-210),
     seeds injected into lambda before reversing the step that ends at each
     observed boundary and at boundary 0 last (adjoint.py:235-253).
+    ``mu0`` (terminal mu, adjoint_terminal adjoint.py:47-52) and ``injections``
+    ({boundary index: [B, N] seed}, inject_observation :135-140) drive the sweep of
+    backward_sweep (:235-253) with caller-formed seeds.
     Returns a dict with u_final, du0, dtheta (batch sum of per-sample mu),
-    loss, counters, store counters, per-sample counters and solver stats.
+    loss, counters, store counters, per-sample counters, solver stats and the
+    state at every boundary (``states``).
     """
     sch = scheme(scheme_name)
     cfg = cfg or SolverCfg()
@@ -684,6 +688,7 @@ def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", see
     want = set(obs.steps) if obs is not None else set()
     if 0 in want:
         capture[0] = U0.copy()
+    states = [U0.copy()]
     for n in range(n_steps):
         t, h = ts[n], ts[n + 1] - ts[n]
         rec, k_carry = run.step(U, t, h, k_carry)
@@ -715,6 +720,7 @@ def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", see
                 final = rec
         meta.append((t, h))
         U = rec.u_next
+        states.append(U.copy())
     if kind != "revolve":
         run.sc.max_live_slots = max(len(slots), len(sols))
     u_final = U
@@ -732,7 +738,9 @@ def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", see
         lam = u_final / B
     else:
         loss, lam = seed_fn(u_final)
-    mu = np.zeros(fld.n_params)
+    mu = np.zeros(fld.n_params) if mu0 is None else np.asarray(mu0, dtype=np.float64).copy()
+    for j, sd in (injections or {}).items():
+        inj[j] = inj.get(j, 0.0) + np.asarray(sd, dtype=np.float64)
 
     def records():
         if kind == "store_all":
@@ -780,8 +788,18 @@ def grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy="store_all", see
     return {
         "u_final": u_final, "du0": lam, "dtheta": mu, "loss": loss, "predictions": preds,
         "counters": run.c, "store": run.sc, "sample_counters": run.sample,
-        "stats": run.stats,
+        "stats": run.stats, "states": states,
     }
+
+
+def sweep_with_seeds(fld, scheme_name, U0, t0, tF, n_steps, lamN, muN=None, injections=None,
+                     policy="store_all", cfg: SolverCfg = None):
+    """backward_sweep from a caller-formed terminal AdjointState (adjoint.py:47-52,
+    :235-253): lambda_N = lamN [B, N], mu_N = muN, plus boundary injections."""
+    r = grad_terminal(fld, scheme_name, U0, t0, tF, n_steps, policy,
+                      seed_fn=lambda uf: (0.0, np.asarray(lamN, dtype=np.float64).copy()),
+                      cfg=cfg, mu0=muN, injections=injections)
+    return {"lam": r["du0"], "mu": r["dtheta"], "states": r["states"], "u_final": r["u_final"]}
 
 
 def rel_error(approx, ref):

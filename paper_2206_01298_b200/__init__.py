@@ -11,7 +11,9 @@ from .configs import ConfigInputs, make_config
 from .controls import (AdaptiveController, ConvergenceError, DeviceError, FixedController, FixedGridController,
                        GradientExplosionError, IntegrationError, NfeCounters, SolverConfig,
                        StiffnessError, StoreCounters)
-from .engine import GradResult, continuous_adjoint_solve, grad
+from .engine import (AdjointState, ForwardSolution, GradResult, adjoint_terminal, backward_sweep,
+                     continuous_adjoint_solve, forward_pass, grad, loss_value)
+from .autograd import ODEBlock
 from .fields import (ACTIVATION_IDS, CnfField, ConvField, Field, MlpField, MlpModel, MlpSpec, StiffMlpField, init_model,
                      mlp_spec)
 from .losses import LossSpec, terminal_loss
@@ -33,4 +35,6 @@ __all__ = [
     "AdamWConfig", "Dataset", "OptimizerState", "TrainConfig", "TrainingRecord", "adamw_step",
     "geometric_grid", "minmax_normalize", "train", "load_model", "model_from_json", "model_to_json",
     "read_dataset_csv", "save_model", "write_dataset_csv", "continuous_adjoint_solve",
+    "AdjointState", "ForwardSolution", "adjoint_terminal", "backward_sweep", "forward_pass", "loss_value",
+    "ODEBlock",
 ]

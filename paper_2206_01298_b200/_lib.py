@@ -26,7 +26,7 @@ OB_F32, OB_F64 = 0, 1
 OB_FIELD_MLP, OB_FIELD_STIFF, OB_FIELD_CNF, OB_FIELD_CONV = 0, 1, 2, 3
 OB_SCHEME_RK, OB_SCHEME_THETA = 0, 1
 OB_POLICY = {"store_all": 0, "store_solutions": 1, "revolve": 2}
-OB_LOSS = {"half_sqnorm": 0, "mse": 4, "mae": 5, "ce_head": 2, "cnf_nll": 3}
+OB_LOSS = {"half_sqnorm": 0, "mse": 4, "mae": 5, "ce_head": 2, "cnf_nll": 3, "seed": 6}
 # (code 1 = the ABI's K=1 terminal MSE; the host routes mse through the general
 #  observation path, code 4)
 OB_MAX_LAYERS = 8
@@ -37,6 +37,7 @@ EXPORTS = (
     "ob_version", "ob_last_error", "ob_device_count", "ob_revolve_count", "ob_revolve_schedule",
     "ob_grad_workspace_size", "ob_grad", "ob_debug_phase_cycles", "ob_field_eval", "ob_field_jvp", "ob_field_vjp",
     "ob_field_vjp_u", "ob_adamw_step", "ob_grad_norm", "ob_optim_last_error", "ob_continuous_adjoint",
+    "ob_forward_pass", "ob_backward_sweep",
 )
 
 
@@ -68,7 +69,7 @@ class Problem(C.Structure):
                 ("abstol", C.c_double), ("reltol", C.c_double), ("h_init", C.c_double),
                 ("h_min", C.c_double), ("h_max", C.c_double), ("safety", C.c_double),
                 ("max_steps", C.c_int64), ("t0", C.c_double), ("tF", C.c_double),
-                ("obs_times", C.POINTER(C.c_double))]
+                ("obs_times", C.POINTER(C.c_double)), ("tile_rows", C.c_int32), ("_pad2", C.c_int32)]
 
 
 class Buffers(C.Structure):
@@ -79,7 +80,8 @@ class Buffers(C.Structure):
                 ("head", C.c_void_p), ("labels", C.c_void_p), ("dhead", C.c_void_p),
                 ("n_classes", C.c_int32), ("_pad", C.c_int32),
                 ("obs_values", C.c_void_p), ("scale_lo", C.c_void_p), ("scale_hi", C.c_void_p),
-                ("predictions", C.c_void_p), ("grid", C.c_void_p), ("n_accepted", C.c_void_p)]
+                ("predictions", C.c_void_p), ("grid", C.c_void_p), ("n_accepted", C.c_void_p),
+                ("seed", C.c_void_p), ("dtheta_seed", C.c_void_p)]
 
 
 class Counters(C.Structure):
@@ -122,6 +124,8 @@ def load():
         lib.ob_revolve_schedule.argtypes = [i32, i32, C.POINTER(i32), i64, C.POINTER(i64)]
         lib.ob_grad_workspace_size.argtypes = [C.POINTER(Problem), C.POINTER(C.c_size_t)]
         lib.ob_grad.argtypes = [C.POINTER(Problem), C.POINTER(Buffers), C.POINTER(Counters), vp]
+        lib.ob_forward_pass.argtypes = lib.ob_grad.argtypes
+        lib.ob_backward_sweep.argtypes = lib.ob_grad.argtypes
         lib.ob_debug_phase_cycles.argtypes = [C.POINTER(C.c_uint64), C.c_int32, C.c_int32]
         dbl = C.c_double
         lib.ob_adamw_step.argtypes = [i32, vp, vp, vp, vp, i64, i64, dbl, dbl, dbl, dbl, dbl, vp]

@@ -300,19 +300,13 @@ template <typename T>
 OB_DEV void ad_inject(const RkParams<T>& p, const AdRow* rs, T* lam, int row0, int Rv, bool final_) {
   if (!p.obs_k) return;
   const int N = p.d.N, ldn = p.d.ldn;
-  const double denom = double(p.n_obs) * N;
   for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
     if (!final_ && !rs[r].act) continue;
     const int bnd = final_ ? 0 : rs[r].m + 1;
     for (int k = 0; k < p.n_obs; ++k) {
       if (p.obs_step[(long long)k * p.B + row0 + r] != bnd) continue;
-      double span;
-      const double rr = obs_residual(p, k, row0 + r, j, span);
-      double sd = p.loss_kind == OB_LOSS_OBS_MAE ? double((rr > 0.0) - (rr < 0.0)) / denom
-                                                  : 2.0 * rr / denom;
-      sd = sd / span / p.batch_global;
-      lam[r * ldn + j] = T(double(lam[r * ldn + j]) + sd);
+      lam[r * ldn + j] = T(double(lam[r * ldn + j]) + obs_seed(p, k, row0 + r, j));
     }
   }
   __syncthreads();

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -32,7 +33,8 @@ template <typename T, bool WS>
 cudaError_t launch_field_ws(const RkParams<T>&, int, int, size_t, int, double, const T*, const T*,
                             T*, cudaStream_t);
 template <typename T> cudaError_t launch_reduce(const Dims&, const T*, int, long long, T*,
-                                                const double*, double, double*, cudaStream_t);
+                                                const double*, double, double*, cudaStream_t,
+                                                const T*);
 template <typename T, bool kFwd>
 cudaError_t launch_theta_dir(const RkParams<T>&, int, int, size_t, cudaStream_t);
 template <typename T>
@@ -115,17 +117,32 @@ static int fail(int code, const std::string& msg) {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static int pad4i(int n) { return (n + 3) & ~3; }
 
-static unsigned long long* g_phase = nullptr;   // device [OB_NPHASES] (profiling aid)
+// per-device [OB_NPHASES] cycle accumulators (profiling aid), created on first use
+// on the device current at the call
+constexpr int kMaxDevices = 64;
+static unsigned long long* g_phase[kMaxDevices] = {};
+static std::mutex g_phase_mu;
+
+static int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    dev = 0;
+  }
+  return dev < kMaxDevices ? dev : kMaxDevices - 1;
+}
 
 static unsigned long long* phase_buffer() {
-  if (!g_phase) {
-    if (cudaMalloc(&g_phase, sizeof(unsigned long long) * OB_NPHASES) != cudaSuccess) {
-      g_phase = nullptr;
+  std::lock_guard<std::mutex> lk(g_phase_mu);
+  unsigned long long*& buf = g_phase[current_device()];
+  if (!buf) {
+    if (cudaMalloc(&buf, sizeof(unsigned long long) * OB_NPHASES) != cudaSuccess) {
+      buf = nullptr;
       return nullptr;
     }
-    cudaMemset(g_phase, 0, sizeof(unsigned long long) * OB_NPHASES);
+    cudaMemset(buf, 0, sizeof(unsigned long long) * OB_NPHASES);
   }
-  return g_phase;
+  return buf;
 }
 
 extern "C" int ob_debug_phase_cycles(uint64_t* out, int32_t n, int32_t reset) {
@@ -185,6 +202,7 @@ struct Plan {
   size_t esz = 8;
   Dims d{};
   int R = 1, Rt = 4, LR = 1, tiles = 1;
+  int req_rows = 0;               // ob_problem.tile_rows (0: planner's choice)
   bool need_jvp = false;
   bool theta = false;
   bool tc = false;                // tcgen05 tensor-core MLP tile (rk_tc.cu)
@@ -439,6 +457,7 @@ void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
     P.tiles = (int)B;
     return;
   }
+  if (P.req_rows > 0) R = P.req_rows;
   if (f.kind == OB_FIELD_CNF) {  // stacked forward|tangent rows: 2*Rt = 4*LR
     for (R = std::min(R, 16);; R = std::max(1, R / 2)) {
       P.LR = R <= 4 ? 2 : R <= 8 ? 4 : 8;
@@ -451,7 +470,6 @@ void choose_tiles(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
     P.tiles = (int)((B + P.R - 1) / P.R);
     return;
   }
-  if (const char* e = getenv("OB_TILE_ROWS")) R = std::max(1, atoi(e));   // experiments
   R = std::min(R, P.esz == 8 ? 8 : 32);   // fp64 kernels are built for tiles of <= 8 rows
   for (;;) {
     P.R = R;
@@ -490,7 +508,7 @@ bool tc_eligible(const ob_problem& p, const Plan& P) {
 bool plan_tc(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   Plan Q = P;
   int R = (int)std::max<long long>(1, (B + sm_count - 1) / sm_count);
-  if (const char* e = getenv("OB_TILE_ROWS")) R = std::max(1, atoi(e));
+  if (P.req_rows > 0) R = P.req_rows;
   R = std::min(R, 32);
   Q.R = Q.Rt = R;
   Q.LR = 8;
@@ -649,9 +667,14 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   if (p.scheme.stages < 1 || p.scheme.stages > OB_MAX_STAGES) return fail(OB_ERR_VALUE, "bad stage count");
   P.adaptive = p.adaptive != 0;
   if (p.batch < 1) return fail(OB_ERR_VALUE, "batch must be >= 1");
-  const bool obs = p.loss == OB_LOSS_OBS_MSE || p.loss == OB_LOSS_OBS_MAE;
+  if (p.tile_rows < 0) return fail(OB_ERR_VALUE, "tile_rows must be >= 0");
+  P.req_rows = p.tile_rows;
+  const bool seed = p.loss == OB_LOSS_SEED;
+  const bool obs = p.loss == OB_LOSS_OBS_MSE || p.loss == OB_LOSS_OBS_MAE || (seed && p.n_obs > 0);
   const bool vec_field = p.field.kind == OB_FIELD_MLP || p.field.kind == OB_FIELD_STIFF;
-  if (p.loss != OB_LOSS_HALF_SQNORM && p.loss != OB_LOSS_MSE && !(obs && vec_field) &&
+  if (seed && p.n_obs > 0 && !vec_field && p.adaptive)
+    return fail(OB_ERR_UNSUPPORTED, "adaptive stepping is built for MLP / stiff fields");
+  if (p.loss != OB_LOSS_HALF_SQNORM && p.loss != OB_LOSS_MSE && !(obs && vec_field) && !seed &&
       !(p.loss == OB_LOSS_CNF_NLL && p.field.kind == OB_FIELD_CNF) &&
       !(p.loss == OB_LOSS_CE_HEAD && p.field.kind == OB_FIELD_CONV))
     return fail(OB_ERR_UNSUPPORTED, "loss kind not supported for this field");
@@ -844,9 +867,31 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
 
 thread_local std::chrono::steady_clock::time_point g_t_entry;   // OB_HOST_TIMING
 
+// phases of one gradient problem on one workspace (ob_grad runs both)
+enum { kPhaseForward = 1, kPhaseReverse = 2, kPhaseBoth = 3 };
+
+// per-device CUDA events of the phase timeline (created on first use on each device)
+static cudaError_t phase_events(cudaEvent_t*& ev) {
+  static thread_local std::map<int, std::vector<cudaEvent_t>> evs;
+  std::vector<cudaEvent_t>& v = evs[current_device()];
+  if (v.empty()) {
+    v.assign(5, nullptr);
+    for (auto& e : v) {
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) {
+        evs.erase(current_device());
+        return r;
+      }
+    }
+  }
+  ev = v.data();
+  return cudaSuccess;
+}
+
 template <typename T>
 int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
-             const void* cadj_dphi = nullptr) {
+             const void* cadj_dphi = nullptr, int phases = kPhaseBoth) {
+  const bool do_fwd = phases & kPhaseForward, do_rev = phases & kPhaseReverse;
   char* ws = static_cast<char*>(b.workspace);
   const int nt = P.adaptive ? P.nseg : p.n_steps, s = p.scheme.stages;
   // ---- control blob: ts (adaptive: interval ends) | fwd_rec | fwd_sol | prog | status | obs
@@ -884,6 +929,7 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
   rp.ts = reinterpret_cast<const double*>(ws + P.off_blob + o_ts);
   rp.loss_kind = p.loss;
   rp.targets = static_cast<const T*>(b.targets);
+  rp.seed = static_cast<const T*>(b.seed);
   if (!P.obs_k.empty()) {
     rp.obs_k = reinterpret_cast<const int*>(ws + P.off_blob + P.o_obs);
     rp.n_obs = p.n_obs;
@@ -952,17 +998,19 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
     rp.ad_grid = reinterpret_cast<double*>(ws + P.off_grid);
     rp.ad_nacc = reinterpret_cast<int*>(ws + P.off_nacc);
     rp.obs_step = reinterpret_cast<int*>(ws + P.off_ostep);
-    CU(cudaMemsetAsync(rp.obs_step, 0xff, sizeof(int) * (size_t)p.batch * std::max(p.n_obs, 1), st));
+    if (do_fwd)
+      CU(cudaMemsetAsync(rp.obs_step, 0xff, sizeof(int) * (size_t)p.batch * std::max(p.n_obs, 1), st));
   }
-  CU(cudaMemsetAsync(stats, 0, sizeof(int) * (size_t)p.batch * OB_NSTATS, st));
+  if (do_fwd) CU(cudaMemsetAsync(stats, 0, sizeof(int) * (size_t)p.batch * OB_NSTATS, st));
 
   // per-phase CUDA events on the launch stream (bench roofline timing)
-  static thread_local cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-  if (!ev[0])
-    for (auto& e : ev) CU(cudaEventCreate(&e));
-  CU(cudaMemsetAsync(rp.mu, 0, P.esz * (size_t)P.tiles * P.d.n_mu, st));
+  cudaEvent_t* ev = nullptr;
+  CU(phase_events(ev));
+  if (do_rev) CU(cudaMemsetAsync(rp.mu, 0, P.esz * (size_t)P.tiles * P.d.n_mu, st));
   CU(cudaEventRecord(ev[0], st));
-  if (P.d.conv) {
+  if (!do_fwd) {
+    // packed weights of the forward call are still in the workspace
+  } else if (P.d.conv) {
     if constexpr (sizeof(T) == 4) CU(launch_pack_conv<T>(pp, st));
   } else if (P.tc) {
     if constexpr (sizeof(T) == 4)
@@ -994,14 +1042,16 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
     CU(launch_cadj<T>(rp, P.LR, P.tiles, P.smem_bytes, p.tF, static_cast<const T*>(cadj_dphi), st));
     CU(cudaEventRecord(ev[2], st));
   } else {
-    CU(sweep(true));
+    if (do_fwd) CU(sweep(true));
     CU(cudaEventRecord(ev[2], st));
-    CU(sweep(false));
+    if (do_rev) CU(sweep(false));
   }
   CU(cudaEventRecord(ev[3], st));
-  CU(launch_reduce<T>(P.d, rp.mu, P.tiles, p.field.n_params, static_cast<T*>(b.dtheta),
-                      rp.loss_part, rp.inv_batch_global, b.loss, st));
-  if (p.loss == OB_LOSS_CE_HEAD && b.dhead) {
+  // dtheta (reverse) and the loss (forward: per-tile partials of loss_partial)
+  CU(launch_reduce<T>(P.d, rp.mu, P.tiles, do_rev ? p.field.n_params : 0, static_cast<T*>(b.dtheta),
+                      rp.loss_part, rp.inv_batch_global, do_fwd ? b.loss : nullptr, st,
+                      static_cast<const T*>(b.dtheta_seed)));
+  if (do_fwd && p.loss == OB_LOSS_CE_HEAD && b.dhead) {
     if constexpr (sizeof(T) == 4)
       CU(launch_reduce_plain<T>(rp.head_part, P.tiles, 10 * 64 + 10, 10 * 64 + 10,
                                 static_cast<T*>(b.dhead), st));
@@ -1049,7 +1099,7 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
       P.cnt.kernel_launches = 4;
     }
   }
-  if (P.adaptive && hs[0] == 0 && (b.grid || b.n_accepted)) {
+  if (do_fwd && P.adaptive && hs[0] == 0 && (b.grid || b.n_accepted)) {
     // per-sample boundary times t_0, t_n + h_n (adjoint.py:171-173)
     std::vector<double> g((size_t)p.batch * P.cap * 2);
     std::vector<int> na((size_t)p.batch);
@@ -1071,6 +1121,8 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
   }
   float ms[4] = {0, 0, 0, 0};
   for (int i = 0; i < 4; ++i) CU(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+  if (!do_fwd) ms[0] = ms[1] = 0.f;
+  if (!do_rev) ms[2] = 0.f;
   P.cnt.ms_pack = ms[0];
   P.cnt.ms_forward = ms[1];
   P.cnt.ms_reverse = ms[2];
@@ -1162,7 +1214,8 @@ extern "C" int ob_grad_workspace_size(const ob_problem* p, size_t* bytes) {
   return OB_OK;
 }
 
-extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream) {
+static int grad_phases(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream,
+                       int phases) {
   g_t_entry = std::chrono::steady_clock::now();
   if (!p || !b) return fail(OB_ERR_VALUE, "null argument");
   Plan P;
@@ -1170,8 +1223,14 @@ extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* ou
   if (st) return st;
   if (!b->workspace || b->workspace_bytes < P.total)
     return fail(OB_ERR_VALUE, "workspace too small (need " + std::to_string(P.total) + " bytes)");
-  if (!b->theta || !b->u0 || !b->u_final || !b->du0 || !b->dtheta || !b->loss)
+  const bool fwd = phases & kPhaseForward, rev = phases & kPhaseReverse;
+  if (!b->theta || !b->u0 || !b->u_final || (rev && (!b->du0 || !b->dtheta)) || (fwd && !b->loss))
     return fail(OB_ERR_VALUE, "null device buffer");
+  if (p->loss == OB_LOSS_SEED && rev && !b->seed)
+    return fail(OB_ERR_VALUE, "seeded sweep needs the terminal seed lambda_N");
+  if (p->loss == OB_LOSS_SEED && p->n_obs > 0 && (!b->predictions || (rev && !b->obs_values)))
+    return fail(OB_ERR_VALUE, "seeded sweep with observations needs a predictions buffer and "
+                              "one injection per observation");
   if (p->field.kind == OB_FIELD_STIFF && !b->aux) return fail(OB_ERR_VALUE, "stiff field needs diag");
   if (p->field.kind == OB_FIELD_CNF && !b->aux) return fail(OB_ERR_VALUE, "CNF field needs probes");
   if (p->loss == OB_LOSS_CE_HEAD && (!b->head || !b->labels || b->n_classes != 10))
@@ -1182,9 +1241,29 @@ extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* ou
     return fail(OB_ERR_VALUE, "observation loss needs observations, a predictions buffer and "
                               "both or neither scaling bounds");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  st = P.dtype == OB_F32 ? run_grad<float>(*p, *b, P, s) : run_grad<double>(*p, *b, P, s);
-  if (out) *out = P.cnt;
+  st = P.dtype == OB_F32 ? run_grad<float>(*p, *b, P, s, nullptr, phases)
+                         : run_grad<double>(*p, *b, P, s, nullptr, phases);
+  if (out) {
+    *out = P.cnt;
+    if (!rev) out->nfe_backward = out->device_vjp_evals = 0;
+    if (!fwd) out->nfe_forward = out->device_rhs_evals = out->steps_accepted = 0;
+    out->kernel_launches = phases == kPhaseBoth ? 4 : (fwd ? 3 : 2);
+  }
   return st;
+}
+
+extern "C" int ob_grad(const ob_problem* p, const ob_buffers* b, ob_counters* out, void* stream) {
+  return grad_phases(p, b, out, stream, kPhaseBoth);
+}
+
+extern "C" int ob_forward_pass(const ob_problem* p, const ob_buffers* b, ob_counters* out,
+                               void* stream) {
+  return grad_phases(p, b, out, stream, kPhaseForward);
+}
+
+extern "C" int ob_backward_sweep(const ob_problem* p, const ob_buffers* b, ob_counters* out,
+                                 void* stream) {
+  return grad_phases(p, b, out, stream, kPhaseReverse);
 }
 
 // Continuous-adjoint baseline (continuous_adjoint_solve, adjoint.py:314-331):
@@ -1206,6 +1285,7 @@ extern "C" int ob_continuous_adjoint(const ob_problem* p, const void* theta, con
   q.loss = OB_LOSS_HALF_SQNORM;
   q.n_obs = 0;
   q.adaptive = 0;
+  q.flags |= OB_FLAG_NO_TENSOR_CORES;   // the SIMT tile runs the augmented sweep
   Plan P;
   int st = plan_problem(q, P);
   if (st) return st;
@@ -1310,7 +1390,7 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
   }
   if (e == cudaSuccess && mode == kVjp)
     e = launch_reduce<T>(P.d, rp.mu, P.tiles, f.n_params, static_cast<T*>(ptv), nullptr, 0.0,
-                         nullptr, st);
+                         nullptr, st, static_cast<const T*>(nullptr));
   cudaFreeAsync(ws, st);
   if (e != cudaSuccess) rc = fail(OB_ERR_CUDA, cudaGetErrorString(e));
   return rc;

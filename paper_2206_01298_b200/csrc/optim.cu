@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <map>
 #include <string>
 
 #include "../../include/odeblock.h"
@@ -108,8 +109,12 @@ struct Scratch {
   ~Scratch() {}
 };
 
+// one scratch set per device (created on first use on the device current at the call)
 int scratch(Scratch& s, cudaStream_t st) {
-  static thread_local Scratch cached;
+  static thread_local std::map<int, Scratch> per_device;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return OB_ERR_CUDA;
+  Scratch& cached = per_device[dev];
   if (!cached.part) {
     if (cudaMalloc(&cached.part, sizeof(double) * kMaxBlocks) != cudaSuccess ||
         cudaMalloc(&cached.bad, sizeof(int)) != cudaSuccess ||

@@ -43,6 +43,7 @@ struct RkParams {
   const double* ts;       // [n_steps+1]
   int loss_kind;
   const T* targets;
+  const T* seed;          // OB_LOSS_SEED: terminal lambda [B][N] (caller-formed)
   // observation losses (OB_LOSS_OBS_*): obs_k[n] = observation index at boundary n or -1
   const int* obs_k;
   int n_obs;

@@ -10,7 +10,8 @@ template cudaError_t launch_field_ws<float, false>(const RkParams<float>&, int, 
                                                    cudaStream_t);
 template cudaError_t launch_pack<float>(const PackParams<float>&, cudaStream_t);
 template cudaError_t launch_reduce<float>(const Dims&, const float*, int, long long, float*,
-                                          const double*, double, double*, cudaStream_t);
+                                          const double*, double, double*, cudaStream_t,
+                                          const float*);
 template cudaError_t launch_cadj_ws<float, false>(const RkParams<float>&, int, int, size_t, double,
                                                    const float*, cudaStream_t);
 }  // namespace ob

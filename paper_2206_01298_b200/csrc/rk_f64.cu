@@ -10,7 +10,8 @@ template cudaError_t launch_field_ws<double, false>(const RkParams<double>&, int
                                                     cudaStream_t);
 template cudaError_t launch_pack<double>(const PackParams<double>&, cudaStream_t);
 template cudaError_t launch_reduce<double>(const Dims&, const double*, int, long long, double*,
-                                           const double*, double, double*, cudaStream_t);
+                                           const double*, double, double*, cudaStream_t,
+                                          const double*);
 template cudaError_t launch_cadj_ws<double, false>(const RkParams<double>&, int, int, size_t, double,
                                                    const double*, cudaStream_t);
 }  // namespace ob

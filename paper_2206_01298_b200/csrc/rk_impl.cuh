@@ -263,6 +263,8 @@ OB_DEV bool is_obs_loss(const RkParams<T>& p) {
   return p.loss_kind == OB_LOSS_OBS_MSE || p.loss_kind == OB_LOSS_OBS_MAE;
 }
 
+
+
 // rows of boundary n -> predictions[k] when boundary n is observed
 template <typename T>
 OB_DEV void obs_capture(const RkParams<T>& p, const T* u, int n, int row0, int Rv) {
@@ -288,6 +290,20 @@ OB_DEV double obs_residual(const RkParams<T>& p, int k, int row, int j, double& 
     }
   }
   return v - double(p.obs_values[g]);
+}
+
+// seed added to lambda at an observed boundary: the built-in observation losses form
+// {sign r | 2r} / (K N), chained through the min-max span, / B (loss_and_grad_seed,
+// losses.py:78-107); OB_LOSS_SEED takes the caller's injection as given
+template <typename T>
+OB_DEV double obs_seed(const RkParams<T>& p, int k, int row, int j) {
+  if (p.loss_kind == OB_LOSS_SEED) return double(p.obs_values[((long long)k * p.B + row) * p.d.N + j]);
+  double span;
+  const double rr = obs_residual(p, k, row, j, span);
+  const double denom = double(p.n_obs) * p.d.N;
+  const double sd = p.loss_kind == OB_LOSS_OBS_MAE ? double((rr > 0.0) - (rr < 0.0)) / denom
+                                                    : 2.0 * rr / denom;
+  return sd / span / p.batch_global;
 }
 
 // deterministic block sum (fixed shuffle tree, then warps in order); result on thread 0
@@ -327,15 +343,9 @@ OB_DEV void obs_inject(const RkParams<T>& p, T* lam, int n, int row0, int Rv) {
   const int k = p.obs_k[n];
   if (k < 0) return;
   const int N = p.d.N, ldn = p.d.ldn;
-  const double denom = double(p.n_obs) * N;
   for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
     const int r = idx / N, j = idx % N;
-    double span;
-    const double rr = obs_residual(p, k, row0 + r, j, span);
-    double sd = p.loss_kind == OB_LOSS_OBS_MAE ? double((rr > 0.0) - (rr < 0.0)) / denom
-                                                : 2.0 * rr / denom;
-    sd = sd / span / p.batch_global;
-    lam[r * ldn + j] = T(double(lam[r * ldn + j]) + sd);
+    lam[r * ldn + j] = T(double(lam[r * ldn + j]) + obs_seed(p, k, row0 + r, j));
   }
   __syncthreads();
 }
@@ -376,6 +386,10 @@ OB_DEV void ce_head_row(const RkParams<T>& p, const T* urow, int label, double* 
 
 template <typename T>
 OB_DEV void loss_partial(const RkParams<T>& p, const T* u, int row0, int Rv, int tile) {
+  if (p.loss_kind == OB_LOSS_SEED) {   // the caller forms the loss from u_final / predictions
+    if (threadIdx.x == 0) p.loss_part[tile] = 0.0;
+    return;
+  }
   if (is_obs_loss(p)) {
     obs_loss_partial(p, row0, Rv, tile);
     return;
@@ -433,6 +447,15 @@ OB_DEV void loss_partial(const RkParams<T>& p, const T* u, int row0, int Rv, int
 template <typename T>
 OB_DEV void loss_seed(const RkParams<T>& p, T* lam, int row0, int Rv) {
   const int N = p.d.N, ldn = p.d.ldn;
+  if (p.loss_kind == OB_LOSS_SEED) {   // adjoint_terminal (adjoint.py:47-52): lambda_N as given
+    for (int i = threadIdx.x; i < p.Rt * ldn; i += blockDim.x) lam[i] = T(0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+      const int r = idx / N, j = idx % N;
+      lam[r * ldn + j] = p.seed[(long long)(row0 + r) * N + j];
+    }
+    return;
+  }
   if (is_obs_loss(p)) {  // lambda starts at zero; seeds arrive by injection
     for (int i = threadIdx.x; i < p.Rt * ldn; i += blockDim.x) lam[i] = T(0);
     return;
@@ -812,7 +835,7 @@ __global__ void pack_weights_kernel(const __grid_constant__ PackParams<T> p) {
 template <typename T>
 __global__ void reduce_tiles_kernel(const __grid_constant__ Dims d, const T* mu, int tiles,
                                     long long np, T* dtheta, const double* loss_part,
-                                    double inv_b, double* loss) {
+                                    double inv_b, double* loss, const T* mu0) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < np;
        j += (long long)gridDim.x * blockDim.x) {
     int l = 0;
@@ -829,7 +852,7 @@ __global__ void reduce_tiles_kernel(const __grid_constant__ Dims d, const T* mu,
     } else {
       src = d.mboff[l] + (j - d.boff[l]);
     }
-    double acc = 0.0;
+    double acc = mu0 ? double(mu0[j]) : 0.0;   // terminal mu (adjoint_terminal), then the tiles
     for (int t = 0; t < tiles; ++t) acc += double(mu[t * d.n_mu + src]);
     dtheta[j] = T(acc);
   }
@@ -908,10 +931,11 @@ cudaError_t launch_field_ws(const RkParams<T>& p, int lr, int tiles, size_t smem
 
 template <typename T>
 cudaError_t launch_reduce(const Dims& d, const T* mu, int tiles, long long np, T* dtheta,
-                          const double* lp, double inv_b, double* loss, cudaStream_t st) {
+                          const double* lp, double inv_b, double* loss, cudaStream_t st,
+                          const T* mu0) {
   const int blocks = (int)std::min<long long>((np + 255) / 256, 148 * 4);
   reduce_tiles_kernel<T><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(d, mu, tiles, np, dtheta, lp,
-                                                                    inv_b, loss);
+                                                                    inv_b, loss, mu0);
   return cudaGetLastError();
 }
 

@@ -17,7 +17,9 @@ from .policies import CheckpointPolicy
 from .schemes import tableau_catalog
 
 
-def field_from_config(ci: ConfigInputs):
+def field_from_config(ci: ConfigInputs, rows=None):
+    """Device field of a config; ``rows`` selects a batch shard's per-sample field data
+    (the CNF probes) -- a rank's field must carry its own rows."""
     if ci.kind == "conv":
         return ConvField(ci.theta)
     spec = MlpSpec(tuple(ci.widths), ci.activation, ci.time_input, ci.dtype)
@@ -27,7 +29,8 @@ def field_from_config(ci: ConfigInputs):
     if ci.kind == "stiff":
         return StiffMlpField(model, ci.extras["diag"], ci.extras["scale"])
     if ci.kind == "cnf":
-        return CnfField(model, ci.extras["eps"])
+        eps = ci.extras["eps"] if rows is None else ci.extras["eps"][rows]
+        return CnfField(model, eps)
     raise NotImplementedError(f"config kind {ci.kind!r} is not built yet")
 
 

@@ -1,0 +1,190 @@
+"""GPU parity at the tile geometry the benchmark runs (VERDICT r01 "next" #1).
+
+The planner gives each CTA R = ceil(B / #SM) samples and instantiates a kernel
+per geometry (CNF CnfAdapter<float, LR>; theta kernels with lockstep per-row
+Newton / GMRES; adaptive kernels with per-row controllers).  These tests force
+the benchmark's geometry with ``tile_rows`` (ob_problem.tile_rows) on batches
+the oracle finishes quickly, and run the full BASELINE batches where the
+reference fixture or the oracle allows:
+
+* C4 at 7 rows per CTA (the B=1000 bench tile, CnfAdapter<float, 4>), 64 samples;
+* C5 at 2 rows per CTA (the B=256 bench tile) and 8 rows per CTA, 16 samples whose
+  rows need different Newton / GMRES counts, and the full 256-sample batch against
+  the reference's own per-sample run (tests/golden/c5_full.npz);
+* adaptive Dopri5 / Bosh3 with 4 and 8 rows per CTA whose rows accept / reject on
+  different trials, against the reference (tests/golden/adaptive_rows.npz);
+* C3 at its full batch (256 images) against the restated oracle.
+
+Tolerances as in test_gpu_parity.py (north_star): 1e-10 fp64, 1e-4 fp32.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import core as oc
+from paper_2206_01298_b200 import (AdaptiveController, CheckpointPolicy, MlpField, MlpModel, MlpSpec,
+                                   grad, tableau_catalog)
+from paper_2206_01298_b200.configs import make_config
+from paper_2206_01298_b200.losses import LossSpec
+from paper_2206_01298_b200.workloads import field_from_config, run_config
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-10
+TOL32 = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2206_01298_b200 import _lib as L
+    L.load()
+
+
+def np_(x):
+    return x.detach().cpu().numpy().astype(np.float64) if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
+def errs(res, ref):
+    e = {k: oc.rel_error(np_(getattr(res, k)), ref[k]) for k in ("u_final", "du0", "dtheta")}
+    e["loss"] = abs(res.loss - float(ref["loss"])) / abs(float(ref["loss"]))
+    return e
+
+
+# ------------------------------------------------------------------ C4, 7 rows per CTA
+def test_c4_bench_tile_matches_oracle():
+    """CnfAdapter<float, 4>: 7 samples (14 stacked forward|tangent rows) per CTA,
+    the tile the B=1000 benchmark runs; 64 samples = 9 full tiles + a 1-row tile."""
+    from oracle.problems import run_oracle
+    ci = make_config("C4").subset(64)
+    res = run_config(ci, "store_all", tile_rows=7)
+    assert res.device["tile_rows"] == 7 and res.device["tiles"] == 10
+    full = run_config(make_config("C4"), "store_all")          # the bench geometry itself
+    assert full.device["tile_rows"] == 7
+    e = errs(res, run_oracle(ci, "store_all"))
+    assert max(e.values()) <= TOL32, e
+    rev = run_config(ci, "revolve:5", tile_rows=7)
+    assert np.array_equal(np_(res.dtheta), np_(rev.dtheta)) and res.loss == rev.loss
+
+
+# ------------------------------------------------------------------ C5, lockstep Newton/GMRES
+@pytest.mark.parametrize("rows", [2, 8])
+def test_c5_multirow_tiles_match_reference(golden, rows):
+    """Per-sample Newton / GMRES(30) state machines advancing in lockstep inside one
+    CTA (masked rows), at the B=256 bench tile (2 rows) and at 8 rows; the 16 samples
+    need different iteration counts, so rows finish their solves at different times."""
+    g = golden("c5_full.npz")
+    ci = make_config("C5").subset(16)
+    res = run_config(ci, "store_all", tile_rows=rows)
+    assert res.device["tile_rows"] == rows
+    sc = res.sample_counters
+    assert len(np.unique(sc["nfe_forward"])) > 4, "rows should need different Newton/GMRES work"
+    ref = {"u_final": g["u_final"][:16], "du0": g["du0"][:16] * (256 / 16),
+           "dtheta": g["dtheta_first16"] * (256 / 16),
+           "loss": np.mean(0.5 * np.sum(g["u_final"][:16] ** 2, axis=1))}
+    e = errs(res, ref)
+    assert max(e.values()) <= TOL64, e
+    # data-dependent counts: equal up to a GMRES stop flipping at a rounding boundary
+    # (the reference's own numba and numpy kernels differ the same way)
+    df = np.abs(sc["nfe_forward"] - g["nfe_forward"][:16])
+    db = np.abs(sc["nfe_backward"] - g["nfe_backward"][:16])
+    assert np.mean(df == 0) >= 0.5 and df.max() <= 6, df
+    assert np.mean(db == 0) >= 0.5 and db.max() <= 6, db
+
+
+@pytest.mark.slow
+def test_c5_full_batch_matches_reference(golden):
+    """The full BASELINE C5 batch (256 samples, 2 rows per CTA) against the
+    reference's own per-sample forward_pass + backward_sweep."""
+    g = golden("c5_full.npz")
+    ci = make_config("C5")
+    res = run_config(ci, "store_all")
+    assert res.device["tile_rows"] == 2
+    e = errs(res, {"u_final": g["u_final"], "du0": g["du0"], "dtheta": g["dtheta"], "loss": g["loss"]})
+    assert max(e.values()) <= TOL64, e
+    df = np.abs(res.sample_counters["nfe_forward"] - g["nfe_forward"])
+    assert np.mean(df == 0) >= 0.5 and df.max() <= 6
+
+
+# ------------------------------------------------------------------ adaptive, many rows per CTA
+def _adaptive_case(g, name):
+    sch, kind, pol = (str(x) for x in g[f"{name}/meta"])
+    tol, _, h0 = (float(x) for x in g[f"{name}/ctrl"])
+    U0 = g[f"{name}/u0"]
+    N = U0.shape[1]
+    model = MlpModel(MlpSpec((N + 1, 16, 16, N), "tanh", time_input=True), g[f"{name}/theta"])
+    loss = LossSpec(kind, tuple(float(t) for t in g[f"{name}/times"]), tuple(g[f"{name}/values"]))
+    return model, sch, pol, loss, AdaptiveController(abstol=tol, reltol=tol, h_init=h0), U0
+
+
+@pytest.mark.parametrize("name", ["dopri5_rows", "bosh3_rows"])
+@pytest.mark.parametrize("rows", [4, 8])
+def test_adaptive_multirow_tiles_match_reference(golden, name, rows):
+    g = golden("adaptive_rows.npz")
+    model, sch, pol, loss, ctrl, U0 = _adaptive_case(g, name)
+    assert len(set(g[f"{name}/accepted"])) > 2 and len(set(g[f"{name}/rejected"])) > 1
+    res = grad(MlpField(model), tableau_catalog(sch), loss, U0, 0.0, 1.0, ctrl,
+               CheckpointPolicy.parse(pol), tile_rows=rows)
+    assert res.device["tile_rows"] == rows
+    sc = res.sample_counters
+    assert list(sc["steps_accepted"]) == list(g[f"{name}/accepted"])
+    assert list(sc["steps_rejected"]) == list(g[f"{name}/rejected"])
+    assert list(sc["nfe_forward"]) == list(g[f"{name}/nfe_forward"])
+    assert list(sc["nfe_backward"]) == list(g[f"{name}/nfe_backward"])
+    for b, grid in enumerate(res.grids):
+        ref = g[f"{name}/grids"][b]
+        ref = ref[~np.isnan(ref)]
+        assert len(grid) == len(ref) and np.max(np.abs(grid - ref)) <= 1e-9
+    assert abs(res.loss - float(g[f"{name}/loss"])) <= 1e-9 * abs(float(g[f"{name}/loss"]))
+    assert oc.rel_error(res.dtheta, g[f"{name}/dtheta"]) <= 1e-9
+    assert oc.rel_error(res.du0, g[f"{name}/du0"]) <= 1e-9
+    # one row per CTA gives the same step sequences (rows are independent)
+    one = grad(MlpField(model), tableau_catalog(sch), loss, U0, 0.0, 1.0, ctrl,
+               CheckpointPolicy.parse(pol), tile_rows=1)
+    assert list(one.sample_counters["steps_rejected"]) == list(sc["steps_rejected"])
+    assert oc.rel_error(one.du0, res.du0) <= 1e-12
+
+
+# ------------------------------------------------------------------ C3, full batch
+@pytest.mark.slow
+def test_c3_full_batch_matches_oracle():
+    from oracle import fields_ext as ox
+    from oracle.problems import run_oracle
+    ci = make_config("C3")
+    res = run_config(ci, "store_all")
+    assert res.device["tiles"] == 256
+    ref = run_oracle(ci, "store_all")
+    e = errs(res, ref)
+    assert max(e.values()) <= TOL32, e
+    dhead = ox.head_loss(ref["u_final"], ci.extras["head"], ci.extras["labels"])[2]
+    assert oc.rel_error(np_(res.dtheta_head), dhead) <= TOL32
+
+
+# ------------------------------------------------------------------ C2 / C1 tile sweeps
+@pytest.mark.parametrize("rows", [1, 5, 16, 32])
+def test_c2_tensor_core_tile_sizes_match_oracle(rows):
+    """The tcgen05 tile at every sample-column occupancy class (1..32 of the MMA's 32
+    columns), against the oracle."""
+    ci = make_config("C2").subset(40)
+    res = run_config(ci, "revolve:8", tile_rows=rows)
+    assert res.device["tensor_cores"] == 1 and res.device["tile_rows"] == rows
+    mlp = oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input)
+    ref = oc.grad_terminal(oc.MlpField(mlp), ci.scheme, ci.u0, ci.t0, ci.tF, ci.n_steps, "store_all")
+    e = errs(res, ref)
+    assert max(e.values()) <= TOL32, e
+
+
+@pytest.mark.parametrize("rows", [1, 3, 8])
+def test_c1_tile_sizes_agree(rows):
+    """fp64 SIMT tiles of 1, 3 and 8 rows (LR 1 / 2 lane layouts, different split-K
+    orders) agree with the default 4-row tile to rounding."""
+    ci = make_config("C1").subset(64)
+    fld = field_from_config(ci)
+    u0 = torch.as_tensor(ci.u0, device="cuda")
+    base = run_config(ci, field=fld, u0=u0)
+    other = run_config(ci, field=fld, u0=u0, tile_rows=rows)
+    assert other.device["tile_rows"] == rows
+    for k in ("du0", "u_final", "dtheta"):
+        assert oc.rel_error(np_(getattr(other, k)), np_(getattr(base, k))) <= 1e-13, k

@@ -374,6 +374,111 @@ def gen_revolve():
     save("revolve.npz", **out)
 
 
+def _c5_chunk(args):
+    lo, hi = args
+    cfg_in = configs.make_config("C5")
+    fld = stiff_field(cfg_in)
+    scfg = og.SolverConfig(**cfg_in.extras["solver"])
+    B = cfg_in.batch
+    scheme = og.tableau_catalog(cfg_in.scheme)
+    pol = og.CheckpointPolicy.parse("store_all")
+    out = []
+    for b in range(lo, hi):
+        c = og.NfeCounters()
+        fwd = og.adjoint.forward_pass(fld, scheme, cfg_in.u0[b], cfg_in.t0, cfg_in.tF,
+                                      og.FixedController(cfg_in.n_steps), pol, scfg, c, obs_times=())
+        adj = og.adjoint.backward_sweep(fld, scheme, fwd,
+                                        og.AdjointState(fwd.u_final / B, np.zeros(fld.n_params)),
+                                        {}, scfg, c)
+        out.append((b, fwd.u_final, adj.lam, adj.mu, c.nfe_forward, c.nfe_backward))
+    return out
+
+
+def gen_c5_full():
+    """C5 at the full BASELINE batch (256 samples; the benchmarked 2-rows-per-CTA tile)
+    through the reference per sample (forward_pass + backward_sweep, seed u/B), in a
+    process pool; mu summed in sample order.  Also the first-16-sample sum (tile-geometry
+    tests at 2 and 8 rows per CTA)."""
+    import multiprocessing as mp
+    B = configs.make_config("C5").batch
+    nproc = len(os.sched_getaffinity(0))
+    chunks = [(i, min(B, i + 4)) for i in range(0, B, 4)]
+    tic = time.time()
+    with mp.get_context("fork").Pool(nproc) as pool:
+        rows = [r for part in pool.map(_c5_chunk, chunks) for r in part]
+    rows.sort(key=lambda r: r[0])
+    print(f"  C5 full: {time.time() - tic:.1f}s on {nproc} processes")
+    uf = np.array([r[1] for r in rows])
+    du0 = np.array([r[2] for r in rows])
+    dth = np.zeros_like(rows[0][3])
+    dth16 = None
+    for i, r in enumerate(rows):
+        dth = dth + r[3]
+        if i == 15:
+            dth16 = dth.copy()
+    cfg_in = configs.make_config("C5")
+    save("c5_full.npz", u0_checksum=np.float64(np.sum(cfg_in.u0)), u_final=uf, du0=du0, dtheta=dth,
+         dtheta_first16=dth16, loss=np.float64(np.mean(0.5 * np.sum(uf * uf, axis=1))),
+         nfe_forward=np.array([r[4] for r in rows]), nfe_backward=np.array([r[5] for r in rows]))
+
+
+def gen_adaptive_rows():
+    """Adaptive stepping with many samples per CTA tile: B = 12 samples whose
+    controllers accept / reject on different trials (per-sample grids of different
+    lengths), through the reference's grad() per sample; batch = sample mean."""
+    from odegrad.integrators import AdaptiveController
+    out = {}
+    rng = np.random.default_rng(4242)
+    cases = [
+        ("dopri5_rows", "dopri5", "mse", "store_all", (1.0,), 1e-8, 0.5),
+        ("bosh3_rows", "bosh3", "mae", "store_solutions", (0.4, 1.0), 1e-6, 0.3),
+    ]
+    B, N = 12, 3
+    for name, sch, kind, pol, times, tol, h0 in cases:
+        model = og.init_model(og.mlp_spec(N, 16, 2, "tanh", time_input=True), seed=11)
+        model = og.MlpModel(model.spec, 2.5 * model.theta)
+        # spread initial states so the per-sample step-size histories differ
+        U0 = rng.uniform(-1.5, 1.5, (B, N)) * np.linspace(0.2, 2.5, B)[:, None]
+        vals = rng.uniform(-0.5, 0.5, (len(times), B, N))
+        ctrl = AdaptiveController(abstol=tol, reltol=tol, h_init=h0)
+        loss, dth, du0, grids = 0.0, np.zeros(model.n_params), [], []
+        acc, rej, nff, nfb = [], [], [], []
+        for b in range(B):
+            spec = og.losses.LossSpec(kind, times, tuple(vals[:, b]), None)
+            c = og.NfeCounters()
+            r = og.grad(og.MlpField(model), og.tableau_catalog(sch), spec, U0[b], 0.0, 1.0, ctrl,
+                        og.CheckpointPolicy.parse(pol), counters=c)
+            fwd = og.adjoint.forward_pass(og.MlpField(model), og.tableau_catalog(sch), U0[b], 0.0,
+                                          1.0, ctrl, og.CheckpointPolicy.parse(pol),
+                                          og.SolverConfig(), og.NfeCounters(), obs_times=times)
+            loss += r.loss / B
+            dth = dth + r.dtheta / B
+            du0.append(r.du0 / B)
+            grids.append(np.array(fwd.boundary_times))
+            acc.append(c.steps_accepted)
+            rej.append(c.steps_rejected)
+            nff.append(c.nfe_forward)
+            nfb.append(c.nfe_backward)
+        L = max(len(g) for g in grids)
+        pre = f"{name}/"
+        out[pre + "theta"] = model.theta
+        out[pre + "u0"] = U0
+        out[pre + "values"] = vals
+        out[pre + "times"] = np.array(times)
+        out[pre + "meta"] = np.array([sch, kind, pol])
+        out[pre + "ctrl"] = np.array([tol, tol, h0])
+        out[pre + "loss"] = np.float64(loss)
+        out[pre + "dtheta"] = dth
+        out[pre + "du0"] = np.array(du0)
+        out[pre + "grids"] = np.array([np.pad(g, (0, L - len(g)), constant_values=np.nan) for g in grids])
+        out[pre + "accepted"] = np.array(acc)
+        out[pre + "rejected"] = np.array(rej)
+        out[pre + "nfe_forward"] = np.array(nff)
+        out[pre + "nfe_backward"] = np.array(nfb)
+        print(f"  {name}: accepted {acc}, rejected {rej}")
+    save("adaptive_rows.npz", **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     if not og.kernels.NUMBA_ENABLED:
@@ -391,6 +496,12 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "adaptive":
         gen_adaptive()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "adaptive_rows":
+        gen_adaptive_rows()
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "c5_full":
+        gen_c5_full()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "training":
         gen_training()
         sys.exit(0)
@@ -407,3 +518,5 @@ if __name__ == "__main__":
     gen_config("C1", 4, ["store_all", "store_solutions", "revolve:3"])
     gen_config("C2", 3, ["store_all", "revolve:8"])
     gen_config("C5", 2, ["store_all"], solver=configs.make_c5(batch=1).extras["solver"])
+    gen_adaptive_rows()
+    gen_c5_full()
