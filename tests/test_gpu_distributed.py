@@ -104,7 +104,7 @@ def test_two_rank_grad_sharded_through_engine(name):
         assert np.array_equal(hdth, dth) and hloss == loss   # host-memory inputs: same bits
         assert np.array_equal(rdu0, du0[rank])
     full = run_config(ci)
-    tol = 1e-13 if ci.dtype == "f64" else 1e-5
+    tol = 1e-13 if ci.dtype == "f64" else 1e-4   # fp32: a different tile geometry per shard
     assert oc.rel_error(outs[0][1], full.dtheta.cpu().numpy() if isinstance(full.dtheta, torch.Tensor)
                         else full.dtheta) <= tol
     assert abs(outs[0][2] - full.loss) <= tol * abs(full.loss)

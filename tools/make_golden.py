@@ -479,6 +479,20 @@ def gen_adaptive_rows():
     save("adaptive_rows.npz", **out)
 
 
+def gen_c5_rows_numpy():
+    """Per-sample NFE counts of the first 16 C5 samples on the reference's numpy
+    kernel path (ODEGRAD_NO_NUMBA=1): how far the reference's own two kernel paths
+    disagree on data-dependent Newton / GMRES counts (rounding-boundary stops), the
+    yardstick for the GPU's counts against c5_full.npz (numba path)."""
+    import multiprocessing as mp
+    with mp.get_context("fork").Pool(len(os.sched_getaffinity(0))) as pool:
+        rows = [r for part in pool.map(_c5_chunk, [(i, i + 1) for i in range(16)]) for r in part]
+    rows.sort(key=lambda r: r[0])
+    save("c5_rows_numpy.npz", nfe_forward=np.array([r[4] for r in rows]),
+         nfe_backward=np.array([r[5] for r in rows]),
+         du0=np.array([r[2] for r in rows]))
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     if not og.kernels.NUMBA_ENABLED:
@@ -486,8 +500,12 @@ if __name__ == "__main__":
         # ulp-level differences from the numba path flip GMRES stopping
         # decisions at rounding boundaries, so C5 iteration counts are pinned
         # against both paths ("iteration-count parity").
+        if len(sys.argv) > 1 and sys.argv[1] == "c5_rows":
+            gen_c5_rows_numpy()
+            sys.exit(0)
         gen_config("C5", 2, ["store_all"], solver=configs.make_c5(batch=1).extras["solver"],
                    suffix="_numpy")
+        gen_c5_rows_numpy()
         sys.exit(0)
     og.kernels.warmup()
     if len(sys.argv) > 1 and sys.argv[1] == "obs":
