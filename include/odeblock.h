@@ -247,6 +247,15 @@ int ob_adamw_step(int32_t dtype, void* theta, const void* g, void* m, void* v, i
                   int64_t step, double lr, double beta1, double beta2, double eps,
                   double weight_decay, void* stream);
 int ob_grad_norm(int32_t dtype, const void* g, int64_t n, double* norm, void* stream);
+/* The training loop's per-epoch optimizer step with no host round trip (train,
+   training.py:276-283): ||g|| into the device slot *norm_out, then a sticky device
+   status (*status = 1: gradient explosion -- g non-finite or ||g|| > threshold, the
+   reference's GradientExplosionError / explosion_threshold stop), then the AdamW
+   update unless the status is set.  The host reads norms and status when it logs. */
+int ob_adamw_step_gated(int32_t dtype, void* theta, const void* g, void* m, void* v, int64_t n,
+                        int64_t step, double lr, double beta1, double beta2, double eps,
+                        double weight_decay, double threshold, double* norm_out, int32_t* status,
+                        void* stream);
 const char* ob_optim_last_error(void);
 
 /* ---- profiling aid: per-phase cycle totals summed over CTAs (reset: zero them) */

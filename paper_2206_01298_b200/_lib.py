@@ -37,7 +37,7 @@ EXPORTS = (
     "ob_version", "ob_last_error", "ob_device_count", "ob_revolve_count", "ob_revolve_schedule",
     "ob_grad_workspace_size", "ob_grad", "ob_debug_phase_cycles", "ob_field_eval", "ob_field_jvp", "ob_field_vjp",
     "ob_field_vjp_u", "ob_adamw_step", "ob_grad_norm", "ob_optim_last_error", "ob_continuous_adjoint",
-    "ob_forward_pass", "ob_backward_sweep",
+    "ob_forward_pass", "ob_backward_sweep", "ob_adamw_step_gated",
 )
 
 
@@ -130,6 +130,8 @@ def load():
         dbl = C.c_double
         lib.ob_adamw_step.argtypes = [i32, vp, vp, vp, vp, i64, i64, dbl, dbl, dbl, dbl, dbl, vp]
         lib.ob_grad_norm.argtypes = [i32, vp, i64, C.POINTER(dbl), vp]
+        lib.ob_adamw_step_gated.argtypes = [i32, vp, vp, vp, vp, i64, i64, dbl, dbl, dbl, dbl, dbl, dbl,
+                                            vp, vp, vp]
         lib.ob_continuous_adjoint.argtypes = [C.POINTER(Problem), vp, vp, vp, vp, vp, vp, vp,
                                               C.c_size_t, C.POINTER(Counters), vp]
         fd = C.POINTER(FieldDesc)

@@ -72,6 +72,17 @@ __global__ void finish_norm_kernel(const double* part, int nb, double* out) {
   *out = __dsqrt_rn(acc);
 }
 
+// training-loop gate (training.py:276-283): record ||g|| into the caller's history slot and
+// raise the sticky status (1: gradient explosion) when g is non-finite or ||g|| exceeds the
+// threshold; the update that follows is skipped once the status is set
+__global__ void gate_kernel(const double* norm, int* bad, double threshold, double* norm_out,
+                            int* status) {
+  const double nv = *norm;
+  if (norm_out) *norm_out = nv;
+  if (*status == 0 && (*bad || !(nv <= threshold))) *status = 1;
+  if (*status != 0) *bad = 1;
+}
+
 // theta = theta * decay; m = b1 m + (1-b1) g; v = b2 v + ((1-b2) g) g;
 // theta = theta - (lr * (m / bc1)) / (sqrt(v / bc2) + eps)   (training.py:184-189)
 template <typename T>
@@ -153,6 +164,42 @@ extern "C" int ob_grad_norm(int32_t dtype, const void* g, int64_t n, double* nor
       cudaStreamSynchronize(st) != cudaSuccess)
     return set_err(OB_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
   return OB_OK;
+}
+
+// One training-loop step without a host round trip: ||g|| -> norm_out (device), the
+// explosion gate -> *status (device, sticky), then AdamW unless the gate tripped.
+extern "C" int ob_adamw_step_gated(int32_t dtype, void* theta, const void* g, void* m, void* v,
+                                   int64_t n, int64_t step, double lr, double beta1, double beta2,
+                                   double eps, double weight_decay, double threshold,
+                                   double* norm_out, int32_t* status, void* stream) {
+  if (!theta || !g || !m || !v || !status || n < 0) return set_err(OB_ERR_VALUE, "null argument");
+  if (step < 1) return set_err(OB_ERR_VALUE, "step counts from 1");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Scratch sc;
+  if (scratch(sc, st)) return set_err(OB_ERR_CUDA, "cudaMalloc failed");
+  AdamScalars s;
+  s.decay = 1.0 - lr * weight_decay;
+  s.b1 = beta1;
+  s.omb1 = 1.0 - beta1;
+  s.b2 = beta2;
+  s.omb2 = 1.0 - beta2;
+  s.bc1 = 1.0 - std::pow(beta1, (double)step);
+  s.bc2 = 1.0 - std::pow(beta2, (double)step);
+  s.lr = lr;
+  s.eps = eps;
+  int nb = 0;
+  int rc = dtype == OB_F64 ? run_norm(static_cast<const double*>(g), n, sc, st, nb)
+                           : run_norm(static_cast<const float*>(g), n, sc, st, nb);
+  if (rc) return set_err(rc, "norm kernel failed");
+  gate_kernel<<<1, 1, 0, st>>>(sc.norm, sc.bad, threshold, norm_out, status);
+  const int blocks = (int)std::min<long long>(148 * 8, std::max<long long>(1, (n + kBlock - 1) / kBlock));
+  if (dtype == OB_F64)
+    adamw_kernel<double><<<blocks, kBlock, 0, st>>>(static_cast<double*>(theta), static_cast<const double*>(g),
+                                                    static_cast<double*>(m), static_cast<double*>(v), n, s, sc.bad);
+  else
+    adamw_kernel<float><<<blocks, kBlock, 0, st>>>(static_cast<float*>(theta), static_cast<const float*>(g),
+                                                   static_cast<float*>(m), static_cast<float*>(v), n, s, sc.bad);
+  return cudaGetLastError() == cudaSuccess ? OB_OK : set_err(OB_ERR_CUDA, "launch failed");
 }
 
 // One AdamW step on device vectors of n parameters; step = the new step count t.
