@@ -12,6 +12,9 @@ import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libodeblock.so")
+# experiments only: load another in-tree build of the same ABI (e.g. a variant under tools/)
+if os.environ.get("OB_LIB_VARIANT"):
+    LIB_PATH = os.path.join(os.path.dirname(PKG), os.environ["OB_LIB_VARIANT"])
 
 OB_OK = 0
 OB_ERR_VALUE = 1
