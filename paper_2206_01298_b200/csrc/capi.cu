@@ -66,6 +66,13 @@ bool tc_shape_supported(int D0, int H, int D2);
 cudaError_t launch_pack_tc(const Dims& d, const float* theta, float* packed, cudaStream_t st);
 cudaError_t launch_rk_tc(const RkParams<float>& p, int tiles, size_t smem, cudaStream_t st,
                          bool forward);
+// tcgen05 CNF tile (cnf_tc.cu)
+bool tc_cnf_shape(int D, int H);
+void tc_cnf_sizes(unsigned* packed_bytes, unsigned* smem_bytes, unsigned* log_record_bytes);
+cudaError_t launch_pack_tc_cnf(const Dims& d, const float* theta, void* img, cudaStream_t st);
+cudaError_t launch_cnf_tc(const RkParams<float>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
+cudaError_t launch_cnf_tc_field(const RkParams<float>& p, int tiles, size_t smem, int mode, double t,
+                                const float* u, const float* w, float* out, cudaStream_t st);
 
 // dispatch on where the weights live (fp32 only stages them in shared memory)
 template <typename T>
@@ -206,6 +213,8 @@ struct Plan {
   bool need_jvp = false;
   bool theta = false;
   bool tc = false;                // tcgen05 tensor-core MLP tile (rk_tc.cu)
+  bool tc_cnf = false;            // tcgen05 CNF tile (cnf_tc.cu)
+  long long cnf_log_rec = 0;      // tcgen05 CNF tile: bytes of one VJP record of the dW log
   int s_stages = 0;               // scheme stages (stage scratch sizing)
   int gmres_m = 0;
   size_t off_kry = 0, off_stats = 0, off_cnf = 0, off_state = 0, off_head = 0;
@@ -541,6 +550,54 @@ bool plan_tc(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   return true;
 }
 
+// Tensor-core CNF tile: fp32 softplus CNF field of the C4 shape on an explicit scheme.
+bool tc_cnf_eligible(const ob_field_desc& f, int flags) {
+  if (f.kind != OB_FIELD_CNF || f.dtype != OB_F32 || f.n_layers != 3 || f.activation != OB_ACT_SOFTPLUS)
+    return false;
+  if ((flags & OB_FLAG_NO_TENSOR_CORES) || getenv("OB_NO_TC")) return false;
+  const int D = f.widths[3], H = f.widths[1];
+  return f.widths[0] == D + 1 && f.widths[2] == H && tc_cnf_shape(D, H);
+}
+
+// <= 8 samples per CTA (the tile's N = 16 stacks forward and tangent rows); generic
+// state buffers after the tcgen05 region, stage scratch in global memory
+bool plan_tc_cnf(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
+  Plan Q = P;
+  int R = (int)std::max<long long>(1, (B + sm_count - 1) / sm_count);
+  if (P.req_rows > 0) R = P.req_rows;
+  R = std::min(R, 8);
+  Q.R = R;
+  Q.Rt = 8;
+  Q.LR = 2;
+  make_dims(f, Q.LR, Q.d);
+  unsigned packed = 0, total = 0, rec = 0;
+  tc_cnf_sizes(&packed, &total, &rec);
+  Q.d.n_packed = packed / 4;
+  for (int l = 0; l < OB_MAX_LAYERS; ++l) Q.d.pwoff[l] = 0;
+  SmemLayout& s = Q.sm;
+  s = SmemLayout{};
+  int o = 0;
+  auto take = [&](long long n) { int r = o; o += (int)((n + 7) & ~7LL); return r; };
+  s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = s.ks = s.ring = s.hscr = s.wts = -1;
+  s.ring_elems = s.hscr_elems = s.scr_elems = 0;
+  for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
+  for (int i = 0; i < 8; ++i) s.vec[i] = -1;
+  take(total / 4);   // the tcgen05 region first (offset 0)
+  s.u = take((long long)Q.Rt * Q.d.ldn);
+  s.lam = take((long long)Q.Rt * Q.d.ldn);
+  s.lamn = take((long long)Q.Rt * Q.d.ldn);
+  s.w = take((long long)Q.Rt * Q.d.ldn);
+  s.jtv = take((long long)Q.Rt * Q.d.ldn);
+  s.total = o;
+  Q.smem_bytes = (size_t)o * 4;
+  if (Q.smem_bytes > smem_cap(Q)) return false;
+  Q.tiles = (int)((B + R - 1) / R);
+  Q.tc_cnf = true;
+  Q.cnf_log_rec = rec;
+  P = Q;
+  return true;
+}
+
 // compile the checkpoint policy into forward store directives + a reverse
 // program (checkpointing.py:242-340), with reference-semantics counters.
 int compile_policy(const ob_problem& p, Plan& P) {
@@ -760,6 +817,7 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   P.s_stages = (P.adaptive || P.theta) ? 0 : p.scheme.stages;   // fixed explicit: smem stage scratch
   choose_tiles(P, p.field, p.batch, sms);
   if (allow_tc && tc_eligible(p, P)) plan_tc(P, p.field, p.batch, sms);
+  if (allow_tc && !P.adaptive && tc_cnf_eligible(p.field, p.flags)) plan_tc_cnf(P, p.field, p.batch, sms);
   if (P.smem_bytes > smem_cap(P)) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   if (P.adaptive) {
     P.prog.clear();
@@ -808,7 +866,7 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   if (P.adaptive) c = ob_counters{};   // per-sample grids: filled after the run
   c.tile_rows = P.R;
   c.tiles = P.tiles;
-  c.tensor_cores = P.tc ? 1 : 0;
+  c.tensor_cores = (P.tc || P.tc_cnf) ? 1 : 0;
   c.kernel_launches = 4;
   // workspace
   const long long B = p.batch, N = P.d.N;
@@ -839,7 +897,9 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   o = align_up(o + sizeof(int) * (size_t)p.batch * OB_NSTATS, 256);
   P.off_cnf = o;
   P.cnf_stride = 0;
-  if (P.d.cnf) {
+  if (P.tc_cnf) {   // per-tile log of the deferred parameter cotangents: one record per VJP
+    P.cnf_stride = std::max<long long>(1, c.device_vjp_evals) * P.cnf_log_rec / 4;
+  } else if (P.d.cnf) {
     for (int l = 0; l < P.d.L - 1; ++l) P.cnf_stride += 2LL * P.Rt * P.d.lda[l + 1];
   } else if (P.d.conv) {
     P.cnf_stride = 18LL * 18 * 68;   // parked input tile
@@ -1016,6 +1076,9 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
     if constexpr (sizeof(T) == 4)
       CU(launch_pack_tc(P.d, reinterpret_cast<const float*>(pp.theta),
                         reinterpret_cast<float*>(pp.packed), st));
+  } else if (P.tc_cnf) {
+    if constexpr (sizeof(T) == 4)
+      CU(launch_pack_tc_cnf(P.d, reinterpret_cast<const float*>(pp.theta), pp.packed, st));
   } else {
     CU(launch_pack<T>(pp, st));
   }
@@ -1027,6 +1090,11 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
       if constexpr (sizeof(T) == 4)
         return launch_rk_tc(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.smem_bytes, st,
                             fwd);
+      return cudaErrorNotSupported;
+    }
+    if (P.tc_cnf) {
+      if constexpr (sizeof(T) == 4)
+        return launch_cnf_tc(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.smem_bytes, st, fwd);
       return cudaErrorNotSupported;
     }
     if (P.d.cnf || P.d.conv) {
@@ -1331,11 +1399,13 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   choose_tiles(P, f, batch, sms);
+  if (mode != kJvp && tc_cnf_eligible(f, 0)) plan_tc_cnf(P, f, batch, sms);
   if (P.smem_bytes > kSmemLimit) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   const size_t pk_bytes = align_up(P.esz * (size_t)P.d.n_packed, 256);
   const size_t mu_bytes = mode == kVjp ? P.esz * (size_t)P.tiles * P.d.n_mu : 0;
   long long cnf_stride = 0;
-  for (int l = 0; P.d.cnf && l < P.d.L - 1; ++l) cnf_stride += 2LL * P.Rt * P.d.lda[l + 1];
+  for (int l = 0; P.d.cnf && !P.tc_cnf && l < P.d.L - 1; ++l) cnf_stride += 2LL * P.Rt * P.d.lda[l + 1];
+  if (P.tc_cnf) cnf_stride = P.cnf_log_rec / 4;   // one VJP record per tile
   if (P.d.conv) cnf_stride = 18LL * 18 * 68;
   const size_t cnf_bytes = align_up(P.esz * (size_t)P.tiles * cnf_stride, 256);
   const size_t st_bytes = P.sm.u < 0 ? align_up(P.esz * (size_t)P.tiles * 5 * P.Rt * P.d.ldn, 256) : 0;
@@ -1370,6 +1440,8 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
   if (e == cudaSuccess) {
     if (P.d.conv) {
       if constexpr (sizeof(T) == 4) e = launch_pack_conv<T>(pp, st);
+    } else if (P.tc_cnf) {
+      if constexpr (sizeof(T) == 4) e = launch_pack_tc_cnf(P.d, reinterpret_cast<const float*>(theta), ws, st);
     } else {
       e = launch_pack<T>(pp, st);
     }
@@ -1379,6 +1451,11 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
       if constexpr (sizeof(T) == 4)
         e = launch_conv_field<T>(rp, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
                                  static_cast<const T*>(w), static_cast<T*>(out), st);
+    } else if (P.tc_cnf) {
+      if constexpr (sizeof(T) == 4)
+        e = launch_cnf_tc_field(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.smem_bytes, mode,
+                                t, reinterpret_cast<const float*>(u), reinterpret_cast<const float*>(w),
+                                reinterpret_cast<float*>(out), st);
     } else if (P.d.cnf) {
       if constexpr (sizeof(T) == 4)
         e = launch_cnf_field<T>(rp, P.LR, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),

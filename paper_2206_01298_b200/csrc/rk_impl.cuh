@@ -713,8 +713,11 @@ field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const
   } else if (mode == 1) {
     if constexpr (F::kHasJvp) f.jvp(wb, res);
   } else {
-    f.vjp(wb, res, mode == 2 ? p.mu + tile * p.d.n_mu : nullptr, 1.0, Rv);
+    T* mu = mode == 2 ? p.mu + tile * p.d.n_mu : nullptr;
+    f.vjp(wb, res, mu, 1.0, Rv);
+    f.finish(mu);   // adapters with device-resident / deferred parameter cotangents
   }
+  f.release();
   store_rows(out, N, res, ldn, row0, Rv);
 }
 
