@@ -70,9 +70,10 @@ cudaError_t launch_rk_tc(const RkParams<float>& p, int tiles, size_t smem, cudaS
 bool tc_cnf_shape(int D, int H);
 void tc_cnf_sizes(unsigned* packed_bytes, unsigned* smem_bytes, unsigned* log_record_bytes);
 cudaError_t launch_pack_tc_cnf(const Dims& d, const float* theta, void* img, cudaStream_t st);
-cudaError_t launch_cnf_tc(const RkParams<float>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
-cudaError_t launch_cnf_tc_field(const RkParams<float>& p, int tiles, size_t smem, int mode, double t,
-                                const float* u, const float* w, float* out, cudaStream_t st);
+cudaError_t launch_cnf_tc(const RkParams<float>& p, int tiles, int cl, size_t smem, cudaStream_t st,
+                          bool forward);
+cudaError_t launch_cnf_tc_field(const RkParams<float>& p, int tiles, int cl, size_t smem, int mode,
+                                double t, const float* u, const float* w, float* out, cudaStream_t st);
 
 // dispatch on where the weights live (fp32 only stages them in shared memory)
 template <typename T>
@@ -215,6 +216,7 @@ struct Plan {
   bool tc = false;                // tcgen05 tensor-core MLP tile (rk_tc.cu)
   bool tc_cnf = false;            // tcgen05 CNF tile (cnf_tc.cu)
   long long cnf_log_rec = 0;      // tcgen05 CNF tile: bytes of one VJP record of the dW log
+  int cnf_cluster = 1;            // tcgen05 CNF tile: CTAs per cluster sharing the weight stream
   int s_stages = 0;               // scheme stages (stage scratch sizing)
   int gmres_m = 0;
   size_t off_kry = 0, off_stats = 0, off_cnf = 0, off_state = 0, off_head = 0;
@@ -591,7 +593,12 @@ bool plan_tc_cnf(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   s.total = o;
   Q.smem_bytes = (size_t)o * 4;
   if (Q.smem_bytes > smem_cap(Q)) return false;
-  Q.tiles = (int)((B + R - 1) / R);
+  // clusters of CTAs share the weight stream (TMA multicast); pad to whole clusters
+  int cl = 2;
+  if (const char* e = getenv("OB_CNF_CLUSTER")) cl = atoi(e);   // experiments: 1, 2, 4
+  if (cl != 1 && cl != 2 && cl != 4) cl = 2;
+  Q.cnf_cluster = cl;
+  Q.tiles = (int)(((B + R - 1) / R + cl - 1) / cl * cl);
   Q.tc_cnf = true;
   Q.cnf_log_rec = rec;
   P = Q;
@@ -1094,7 +1101,8 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
     }
     if (P.tc_cnf) {
       if constexpr (sizeof(T) == 4)
-        return launch_cnf_tc(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.smem_bytes, st, fwd);
+        return launch_cnf_tc(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.cnf_cluster,
+                             P.smem_bytes, st, fwd);
       return cudaErrorNotSupported;
     }
     if (P.d.cnf || P.d.conv) {
@@ -1453,7 +1461,8 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
                                  static_cast<const T*>(w), static_cast<T*>(out), st);
     } else if (P.tc_cnf) {
       if constexpr (sizeof(T) == 4)
-        e = launch_cnf_tc_field(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.smem_bytes, mode,
+        e = launch_cnf_tc_field(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.cnf_cluster,
+                                P.smem_bytes, mode,
                                 t, reinterpret_cast<const float*>(u), reinterpret_cast<const float*>(w),
                                 reinterpret_cast<float*>(out), st);
     } else if (P.d.cnf) {

@@ -11,6 +11,7 @@
 // contraction), reproducing the reference combination bit-for-bit in fp64.
 #pragma once
 #include <algorithm>
+#include <type_traits>
 
 #include "rk.cuh"
 
@@ -19,6 +20,13 @@ namespace ob {
 OB_DEV void set_status(int* status, int code, int info) {
   if (atomicCAS(status, 0, code) == 0) status[1] = info;
 }
+
+// Adapters whose CTAs cooperate across a thread-block cluster (multicast weight
+// streams) must not leave the sweep early: a CTA that hits an error records it and
+// keeps stepping with its cluster (its results are discarded by the host).
+template <class F, class = void> struct NoEarlyExit { static constexpr bool value = false; };
+template <class F>
+struct NoEarlyExit<F, std::void_t<decltype(F::kNoEarlyExit)>> { static constexpr bool value = F::kNoEarlyExit; };
 
 template <typename T>
 OB_DEV void zero_smem(T* sm, int n) {
@@ -502,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
   zero_smem(sm, p.sm.wts >= 0 ? p.sm.wts : p.sm.total);
   const int tile = blockIdx.x;
   const int row0 = tile * p.R;
-  const int Rv = min(p.R, p.B - row0);
+  const int Rv = max(0, min(p.R, p.B - row0));   // 0 on cluster-padding tiles
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
@@ -522,8 +530,10 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
     if (!Num<T>::finite(u[(idx / N) * ldn + idx % N])) bad = 1;
   if (__syncthreads_or(bad)) {
     if (threadIdx.x == 0) set_status(p.status, OB_ERR_VALUE, -1);
-    f.release();
-    return;
+    if constexpr (!NoEarlyExit<F>::value) {
+      f.release();
+      return;
+    }
   }
   for (int n = 0; n < p.n_steps; ++n) {
     const double t = p.ts[n], h = p.ts[n + 1] - p.ts[n];
@@ -543,8 +553,10 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
     pt.mark(kPhFwdStep);
     if (!ok) {  // integrators.py:219-220
       if (threadIdx.x == 0) set_status(p.status, OB_ERR_INTEGRATION, n);
-      f.release();
-      return;
+      if constexpr (!NoEarlyExit<F>::value) {
+        f.release();
+        return;
+      }
     }
   }
   f.release();
@@ -562,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
   zero_smem(sm, p.sm.wts >= 0 ? p.sm.wts : p.sm.total);
   const int tile = blockIdx.x;
   const int row0 = tile * p.R;
-  const int Rv = min(p.R, p.B - row0);
+  const int Rv = max(0, min(p.R, p.B - row0));   // 0 on cluster-padding tiles
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
@@ -612,8 +624,10 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
     if constexpr (F::kOwnsStep) {
       if (!f.reverse_step(lam, t, h, rec, row0, mu)) {
         if (threadIdx.x == 0) set_status(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
-        f.release();
-        return;
+        if constexpr (!NoEarlyExit<F>::value) {
+          f.release();
+          return;
+        }
       }
       pt.mark(kPhVjp);
     } else {
@@ -671,8 +685,10 @@ __global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_co
       }
       if (__syncthreads_or(bad)) {  // AdjointState.check_finite (adjoint.py:42-44)
         if (threadIdx.x == 0) set_status(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
-        f.release();
-        return;
+        if constexpr (!NoEarlyExit<F>::value) {
+          f.release();
+          return;
+        }
       }
     }
   }
@@ -693,7 +709,7 @@ field_op_kernel(const __grid_constant__ RkParams<T> p, int mode, double t, const
   zero_smem(sm, p.sm.wts >= 0 ? p.sm.wts : p.sm.total);
   const int tile = blockIdx.x;
   const int row0 = tile * p.R;
-  const int Rv = min(p.R, p.B - row0);
+  const int Rv = max(0, min(p.R, p.B - row0));   // 0 on cluster-padding tiles
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);
@@ -737,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) cadj_kernel(const __grid_constant
   zero_smem(sm, p.sm.wts >= 0 ? p.sm.wts : p.sm.total);
   const int tile = blockIdx.x;
   const int row0 = tile * p.R;
-  const int Rv = min(p.R, p.B - row0);
+  const int Rv = max(0, min(p.R, p.B - row0));   // 0 on cluster-padding tiles
   MlpSmem<T> ms;
   Weights<T> W;
   setup_tile(p, sm, ms, W);

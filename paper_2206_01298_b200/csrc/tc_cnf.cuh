@@ -34,9 +34,14 @@ namespace ob {
 namespace cnf_tc {
 constexpr int kRows = 16;         // MMA N: forward rows 0..7 | tangent rows 8..15
 constexpr int kHalf = 8;          // samples per tile (max)
-constexpr int kKc = 32;           // K per weight chunk (two 16-wide K slices)
-constexpr int kNS = 6;            // weight ring slots
-constexpr uint32_t kSlot = 16384; // bytes per slot (M = 128 chunk, hi | lo)
+// Weight chunks are large: a bulk copy costs ~600 cycles of TMA service per SM almost
+// independently of its size up to ~64 KB (tools/tma_probe: 16 KB copies stream at
+// 17-27 B/cycle/SM, 64 KB copies at 73 B/cycle/SM with one copy in flight behind the
+// one being consumed), so the ring holds three 48 KB chunks (128 rows x 96 K, hi | lo):
+// two copies stay in flight behind the chunk the MMAs consume.
+constexpr int kKc = 96;           // K per weight chunk (six 16-wide K slices; 864 = 9 x 96)
+constexpr int kNS = 3;            // weight ring slots
+constexpr uint32_t kSlot = 49152; // bytes per slot (M = 128 chunk, hi | lo)
 constexpr int kNW = 224;          // N per dW GEMM output tile (<= 256)
 
 // stacked activation tile [kRows][K] (bf16) in core blocks: byte(row, k) =
@@ -48,9 +53,10 @@ __host__ __device__ constexpr uint32_t act_off(int row, int k) {
   return (uint32_t)(row >> 3) * 128u + (uint32_t)(k >> 3) * 256u + (uint32_t)(row & 7) * 16u +
          (uint32_t)(k & 7) * 2u;
 }
-// weight chunk [M][kKc] K-major: byte(m, k) = (m/8)*512 + (k/8)*128 + (m%8)*16 + (k%8)*2
+// weight chunk [M][kKc] K-major: byte(m, k) = (m/8)*kWSA + (k/8)*128 + (m%8)*16 + (k%8)*2
+constexpr uint32_t kWSA = (uint32_t)(kKc / 8) * 128u;   // row-group stride (descriptor SBO)
 __host__ __device__ constexpr uint32_t w_off(int m, int k) {
-  return (uint32_t)(m >> 3) * 512u + (uint32_t)(k >> 3) * 128u + (uint32_t)(m & 7) * 16u +
+  return (uint32_t)(m >> 3) * kWSA + (uint32_t)(k >> 3) * 128u + (uint32_t)(m & 7) * 16u +
          (uint32_t)(k & 7) * 2u;
 }
 }  // namespace cnf_tc
@@ -65,8 +71,8 @@ struct CnfProd {
 
 template <int D, int H>
 struct CnfGeom {
-  static constexpr int K0 = 64;                      // [z, t] padded (D + 1 <= 64)
-  static constexpr int KH = (H + 31) / 32 * 32;      // hidden padded to whole chunks
+  static constexpr int K0 = cnf_tc::kKc;             // [z, t] padded to one chunk (D + 1 <= 64)
+  static constexpr int KH = (H + cnf_tc::kKc - 1) / cnf_tc::kKc * cnf_tc::kKc;   // whole chunks
   static constexpr int MB = (H + 127) / 128;         // M blocks of a hidden layer
   static constexpr uint32_t C128 = 2 * 128 * cnf_tc::kKc * 2;   // 16 KB chunk (hi | lo)
   static constexpr uint32_t C64 = 2 * 64 * cnf_tc::kKc * 2;     // 8 KB
@@ -79,25 +85,33 @@ struct CnfGeom {
   static constexpr uint32_t P0b = P1b + MB * (KH / cnf_tc::kKc) * C128;
   static constexpr uint32_t Packed = P0b + (KH / cnf_tc::kKc) * C64;
   // shared memory (bytes from the start of dynamic shared memory)
-  static constexpr uint32_t TX = cnf_tc::tile_bytes(K0);     // X0 / Z3 tiles (K = 64)
+  static constexpr uint32_t TX = cnf_tc::tile_bytes(K0);     // X0 / Z3 tiles (K = K0)
   static constexpr uint32_t TA = cnf_tc::tile_bytes(KH);     // hidden tiles
   static constexpr uint32_t X0h = 0, X0l = X0h + TX;
   static constexpr uint32_t Z3h = X0l + TX, Z3l = Z3h + TX;
-  static constexpr uint32_t A1h = Z3l + TX, A1l = A1h + TA;
-  static constexpr uint32_t A2h = A1l + TA, A2l = A2h + TA;
-  static constexpr uint32_t Ring = A2l + TA;                  // kNS slots (contiguous after A2)
+  // one stacked hidden tile serves every hidden-width operand in turn ([a1; u1], [a2; u2],
+  // [zbar2; sbar2], [zbar1; sbar1]): each is logged and consumed by its product before the
+  // next epilogue overwrites it, which leaves room for a deeper weight ring
+  static constexpr uint32_t ABh = Z3l + TX, ABl = ABh + TA;
+  static constexpr uint32_t Ring = ABl + TA;                  // kNS slots (contiguous after AB)
   static constexpr uint32_t Jeps = Ring + cnf_tc::kNS * cnf_tc::kSlot;   // fp32 [8][64]
   static constexpr uint32_t Bars = Jeps + 8 * 64 * 4;         // full[kNS] empty[kNS] done gemm[4]
   static constexpr uint32_t Slot = Bars + 8 * (2 * cnf_tc::kNS + 8);
   static constexpr uint32_t Total = (Slot + 8 + 127) / 128 * 128;
-  // per-VJP log record (bytes): Z3 | A2 | Zb2 | A1 | Zb1 | X0, each hi | lo
-  static constexpr uint32_t LZ3 = 0, LA2 = LZ3 + 2 * TX, LZ2 = LA2 + 2 * TA, LA1 = LZ2 + 2 * TA,
-                            LZ1 = LA1 + 2 * TA, LX0 = LZ1 + 2 * TA, Log = LX0 + 2 * TX;
+  // dW log, panel layout: for every operand tile a VJP logs, its blocks (the dW GEMMs'
+  // M blocks / N chunks: 128 or 224 features x 16 rows) are stored [block][vjp][hi | lo],
+  // so a dW output tile streams many VJPs of one block in a single bulk copy
+  static constexpr int NC = (KH + cnf_tc::kNW - 1) / cnf_tc::kNW;       // N chunks of a hidden input
+  static constexpr uint32_t BZ = 16 * 256;                             // 128-feature block (per copy)
+  static constexpr uint32_t BA = (uint32_t)cnf_tc::kNW / 8 * 256;      // 224-feature chunk
+  static constexpr uint32_t BZ3 = 8 * 256;                             // 64 features (M = 64)
+  static constexpr uint32_t BX0 = TX;                                  // the whole X0 tile
+  static constexpr uint32_t Log = 2 * (2 * MB * BZ + 2 * NC * BA + BZ3 + BX0);   // bytes per VJP
   // TMEM columns (fp32, N = 16 per M block)
   static constexpr uint32_t T_Z1 = 0, T_Z2 = T_Z1 + 16 * MB, T_OUT = T_Z2 + 16 * MB,
                             T_G2 = T_OUT + 16, T_G1 = T_G2 + 16 * MB, T_G0 = T_G1 + 16 * MB,
                             T_END = T_G0 + 16;
-  static_assert(D + 1 <= K0, "state dim");
+  static_assert(D + 1 <= 64, "state dim (M = 64 blocks for the D-row layers)");
   static_assert(T_END <= 512, "TMEM");
 };
 
@@ -124,6 +138,11 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t 
                "r"(tc::smem_u32(src)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -151,7 +170,7 @@ __device__ __forceinline__ float sigmoid_from_e(float z, float e) {   // e = exp
 }
 }  // namespace cnf_tc
 
-template <typename T, int D, int H>
+template <typename T, int D, int H, int CL>
 struct TcCnfAdapter {
   static_assert(sizeof(T) == 4, "tensor-core CNF tile is fp32");
   using G = CnfGeom<D, H>;
@@ -159,7 +178,9 @@ struct TcCnfAdapter {
   static constexpr bool kScaledVjp = true;    // vjp returns J^T (h w), mu += P^T (h w)
   static constexpr int kCombineBatch = 4;
   static constexpr bool kOwnsStep = false;
+  static constexpr bool kNoEarlyExit = CL > 1;   // the cluster streams weights together
   static constexpr uint32_t kCols = 512;
+  static constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
 
   const RkParams<T>& p;
   int Rv, row0;
@@ -168,6 +189,7 @@ struct TcCnfAdapter {
   uint32_t head, tail, done_phase;
   int nlog;              // VJPs logged so far
   unsigned char* logp;   // this tile's log
+  uint32_t crank;        // rank in the thread-block cluster (chunk c is loaded by rank c % CL)
 
   OB_DEV unsigned char* sm() const { return ob_tc_smem; }
   OB_DEV uint64_t* full(int s) const { return reinterpret_cast<uint64_t*>(ob_tc_smem + G::Bars) + s; }
@@ -178,7 +200,8 @@ struct TcCnfAdapter {
   OB_DEV const unsigned char* packed() const { return reinterpret_cast<const unsigned char*>(p.packed); }
 
   OB_DEV TcCnfAdapter(const RkParams<T>& p_, const Weights<T>&, MlpSmem<T>&, T*, int row0_, int Rv_)
-      : p(p_), Rv(Rv_), row0(row0_), tcur(0.f), head(0), tail(0), done_phase(0), nlog(0) {
+      : p(p_), Rv(Rv_ > 0 ? Rv_ : 0), row0(row0_), tcur(0.f), head(0), tail(0), done_phase(0), nlog(0), crank(0) {
+    if constexpr (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
     logp = reinterpret_cast<unsigned char*>(p.cnf_pre) + (long long)blockIdx.x * p.cnf_pre_stride * sizeof(T);
     // zero the operand tiles (padded rows / features stay exactly zero)
     uint4* z = reinterpret_cast<uint4*>(ob_tc_smem);
@@ -187,13 +210,14 @@ struct TcCnfAdapter {
     if (threadIdx.x == 0) {
       for (int s = 0; s < cnf_tc::kNS; ++s) {
         tc::bar_init(full(s), 1);
-        tc::bar_init(empty(s), 1);
+        tc::bar_init(empty(s), CL);   // every CTA of the cluster releases the slot
       }
       tc::bar_init(done(), 1);
     }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
+    if constexpr (CL > 1) cluster_sync();   // barriers initialised cluster-wide before any multicast
     if (threadIdx.x == 0 && p.status && *reinterpret_cast<volatile uint32_t*>(ob_tc_smem + G::Slot) != 0u)
       set_status(p.status, OB_ERR_UNSUPPORTED, -2);   // TMEM not at column 0: shared SM
     // Hutchinson probes: the tangent rows of X0 (time tangent 0)
@@ -226,12 +250,37 @@ struct TcCnfAdapter {
     tc::fence_after();
   }
 
-  // ---- weight stream (warp 0)
+  OB_DEV static void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+  // MMA completion of this CTA -> the slot's empty barrier in every CTA of the cluster
+  OB_DEV void commit_empty(int s) {
+    if constexpr (CL == 1) {
+      tc::commit(empty(s));
+    } else {
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+              tc::smem_u32(empty(s))),
+          "h"(kMask)
+          : "memory");
+    }
+  }
+  // ---- weight stream (warp 0): chunk idx lands in slot idx % kNS of every CTA of the
+  // cluster; rank idx % CL issues it (multicast), every CTA expects its bytes
   OB_DEV void load_chunk(uint32_t idx, uint32_t src, uint32_t bytes) {
     const int s = (int)(idx % cnf_tc::kNS);
     if (cnf_tc::elect_one()) {
       cnf_tc::bar_expect_tx(full(s), bytes);
-      cnf_tc::bulk_load(sm() + G::Ring + s * cnf_tc::kSlot, packed() + src, bytes, full(s));
+      if constexpr (CL == 1) {
+        cnf_tc::bulk_load(sm() + G::Ring + s * cnf_tc::kSlot, packed() + src, bytes, full(s));
+      } else if (idx % CL == crank) {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+            " [%0], [%1], %2, [%3], %4;" ::"r"(tc::smem_u32(sm() + G::Ring + s * cnf_tc::kSlot)),
+            "l"(packed() + src), "r"(bytes), "r"(tc::smem_u32(full(s))), "h"(kMask)
+            : "memory");
+      }
     }
     __syncwarp();
   }
@@ -242,34 +291,37 @@ struct TcCnfAdapter {
     const uint32_t cbytes = (uint32_t)M * cnf_tc::kKc * 2 * 2, half = cbytes / 2;
     const uint32_t n = (uint32_t)(pr.nmb * pr.nkc);
     const uint32_t sb = tc::smem_u32(ob_tc_smem);
+    constexpr int KS = cnf_tc::kKc / 16;   // K slices per chunk
     // prefetch kNS - 1 chunks (the ring is empty between products)
     for (; head < tail + cnf_tc::kNS - 1 && head < tail + n; ++head)
       load_chunk(head, pr.src + (head - tail) * cbytes, cbytes);
     for (uint32_t c = 0; c < n; ++c) {
       const uint32_t idx = tail + c;
       const int s = (int)(idx % cnf_tc::kNS);
-      tc::bar_wait(full(s), (idx / cnf_tc::kNS) & 1u);
-      tc::fence_after();
-      const int mb = (int)(c / pr.nkc), kc = (int)(c % pr.nkc);
-      const uint32_t a = sb + G::Ring + s * cnf_tc::kSlot;
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const uint64_t Ah = tc::sdesc(a + ks * 256, 128, 512), Al = tc::sdesc(a + half + ks * 256, 128, 512);
-        const uint32_t bo = (uint32_t)(2 * kc + ks) * 512u;
-        const uint64_t Bh = tc::sdesc(sb + bh + bo, 256, 128), Bl = tc::sdesc(sb + bl + bo, 256, 128);
-        const uint32_t dt = dcol + 16u * mb;
-        tc::mma_bf16_keep_a(dt, Ah, Bh, id, (kc > 0 || ks > 0) ? 1u : 0u);
-        tc::mma_bf16_reuse_a(dt, Ah, Bl, id, 1u);
-        tc::mma_bf16(dt, Al, Bh, id, 1u);
-      }
-      tc::commit(empty(s));
-      // refill the previous chunk's slot (its MMAs were issued one chunk earlier)
+      // keep kNS - 1 copies in flight: refill the slot of chunk idx - 1 (its MMAs were
+      // issued an iteration ago) before consuming chunk idx
       if (head < tail + n) {
         const uint32_t prev = head - cnf_tc::kNS;   // the chunk that last used head's slot
         if (head >= (uint32_t)cnf_tc::kNS) tc::bar_wait(empty((int)(prev % cnf_tc::kNS)), (prev / cnf_tc::kNS) & 1u);
         load_chunk(head, pr.src + (head - tail) * cbytes, cbytes);
         ++head;
       }
+      tc::bar_wait(full(s), (idx / cnf_tc::kNS) & 1u);
+      tc::fence_after();
+      const int mb = (int)(c / pr.nkc), kc = (int)(c % pr.nkc);
+      const uint32_t a = sb + G::Ring + s * cnf_tc::kSlot;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const uint64_t Ah = tc::sdesc(a + ks * 256, 128, cnf_tc::kWSA),
+                       Al = tc::sdesc(a + half + ks * 256, 128, cnf_tc::kWSA);
+        const uint32_t bo = (uint32_t)(KS * kc + ks) * 512u;
+        const uint64_t Bh = tc::sdesc(sb + bh + bo, 256, 128), Bl = tc::sdesc(sb + bl + bo, 256, 128);
+        const uint32_t dt = dcol + 16u * mb;
+        tc::mma_bf16_keep_a(dt, Ah, Bh, id, (kc > 0 || ks > 0) ? 1u : 0u);
+        tc::mma_bf16_reuse_a(dt, Ah, Bl, id, 1u);
+        tc::mma_bf16(dt, Al, Bh, id, 1u);
+      }
+      commit_empty(s);
     }
     tail += n;
     tc::commit(done());
@@ -330,20 +382,22 @@ struct TcCnfAdapter {
   }
 
   // forward through the two hidden layers (pre-activations stay in TMEM Z1 / Z2)
-  OB_DEV void hidden_forward() {
+  // (log: the VJP's layer inputs are logged as they are produced)
+  OB_DEV void hidden_forward(bool log) {
     sync_issue();
     issue(0, G::T_Z1, G::X0h, G::X0l);
-    epi_hidden(G::T_Z1, p.W.bias[0], G::A1h, G::A1l);
+    epi_hidden(G::T_Z1, p.W.bias[0], G::ABh, G::ABl);         // [a1; u1]
     sync_issue();
-    issue(1, G::T_Z2, G::A1h, G::A1l);
-    epi_hidden(G::T_Z2, p.W.bias[1], G::A2h, G::A2l);
+    if (log) log_panel(G::ABh, G::ABl, kSecA1, G::NC, G::BA);
+    issue(1, G::T_Z2, G::ABh, G::ABl);
+    epi_hidden(G::T_Z2, p.W.bias[1], G::ABh, G::ABl);         // [a2; u2] over [a1; u1]
   }
 
   // f_aug(x0) -> out [Rt][ldn]: columns [0, D) = f, column D = -eps^T J eps
   OB_DEV void eval(T* out) {
-    hidden_forward();
+    hidden_forward(false);
     sync_issue();
-    issue(2, G::T_OUT, G::A2h, G::A2l);
+    issue(2, G::T_OUT, G::ABh, G::ABl);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* je = reinterpret_cast<float*>(sm() + G::Jeps);
     if (w < 4) {   // M = 64 accumulator: row n -> lane 32 (n / 16) + n % 16 (lanes < 16)
@@ -401,19 +455,35 @@ struct TcCnfAdapter {
     }
   }
 
-  // log the stacked tile at smem offsets (hi, lo) -> this VJP's record at byte offset lo_
-  OB_DEV void log_tile(uint32_t h, uint32_t l, uint32_t bytes, uint32_t rec_off) {
-    if (threadIdx.x == 0) {
-      unsigned char* dst = logp + (long long)nlog * G::Log + rec_off;
-      cnf_tc::bulk_store(dst, sm() + h, bytes);
-      cnf_tc::bulk_store(dst + bytes, sm() + l, bytes);
-      cnf_tc::bulk_commit();
+  // ---- dW log (panel layout, see CnfGeom): section offsets for this tile's capacity
+  enum { kSecZ2 = 0, kSecZ1, kSecA1, kSecA2, kSecZ3, kSecX0 };
+  OB_DEV long long cap() const { return p.cnf_pre_stride * (long long)sizeof(T) / G::Log; }
+  OB_DEV long long sec_off(int sec) const {
+    const long long c = cap();
+    const long long z = (long long)G::MB * c * 2 * G::BZ, a = (long long)G::NC * c * 2 * G::BA;
+    switch (sec) {
+      case kSecZ2: return 0;
+      case kSecZ1: return z;
+      case kSecA1: return 2 * z;
+      case kSecA2: return 2 * z + a;
+      case kSecZ3: return 2 * z + 2 * a;
+      default: return 2 * z + 2 * a + c * 2 * G::BZ3;
     }
   }
-  // the logged shared-memory tiles have been read: they may be overwritten now
-  OB_DEV void log_read_done() {
-    if (threadIdx.x == 0) cnf_tc::bulk_wait_read();
-    __syncthreads();
+  // append the blocks of the stacked tile (hi, lo) to section sec for VJP nlog (all
+  // threads, 16-byte copies; the tile may be overwritten after the next barrier)
+  OB_DEV void log_panel(uint32_t h, uint32_t l, int sec, int nblk, uint32_t bb) {
+#ifdef OB_EXP_NO_LOG
+    return;
+#endif
+    uint4* dst0 = reinterpret_cast<uint4*>(logp + sec_off(sec));
+    const int units = (int)(bb / 16);
+    const long long c = cap();
+    for (int i = threadIdx.x; i < nblk * 2 * units; i += blockDim.x) {
+      const int blk = i / (2 * units), r = i % (2 * units), hl = r / units, u = r % units;
+      const uint4 v = *reinterpret_cast<const uint4*>(sm() + (hl ? l : h) + blk * bb + u * 16);
+      dst0[((blk * c + nlog) * 2 * bb + hl * bb) / 16 + u] = v;
+    }
   }
 
   // (J_aug^T (h w), mu += P_aug^T (h w)) at x0; w: [Rt][ldn], columns [0, D) the cotangent
@@ -426,7 +496,7 @@ struct TcCnfAdapter {
       if (threadIdx.x == 0 && p.status) set_status(p.status, OB_ERR_UNSUPPORTED, -3);   // log capacity
       mu = nullptr;
     }
-    hidden_forward();
+    hidden_forward(mu != nullptr);
     // output-layer cotangent Z3 = h [v_z ; -v_Delta eps]; db2 += h sum_rows v_z
     for (int i = threadIdx.x; i < cnf_tc::kHalf * D; i += blockDim.x) {
       const int c = i / D, n = i % D;
@@ -444,23 +514,20 @@ struct TcCnfAdapter {
       mu[d.mboff[2] + threadIdx.x] += T(s);
     }
     sync_issue();
-    if (mu) {   // layer inputs of this VJP (final now): X0, A1, A2
-      log_tile(G::X0h, G::X0l, G::TX, G::LX0);
-      log_tile(G::A1h, G::A1l, G::TA, G::LA1);
-      log_tile(G::A2h, G::A2l, G::TA, G::LA2);
-      log_tile(G::Z3h, G::Z3l, G::TX, G::LZ3);
+    if (mu) {   // the rest of this VJP's layer inputs and the output cotangent
+      log_panel(G::X0h, G::X0l, kSecX0, 1, G::BX0);
+      log_panel(G::ABh, G::ABl, kSecA2, G::NC, G::BA);
+      log_panel(G::Z3h, G::Z3l, kSecZ3, 1, G::BZ3);
     }
     issue(3, G::T_G2, G::Z3h, G::Z3l);                   // [abar2; ubar2] = W2^T Z3
-    if (mu) log_read_done();                             // A2 may be overwritten
-    epi_back(G::T_G2, G::T_Z2, p.W.bias[1], G::A2h, G::A2l, mu ? mu + d.mboff[1] : nullptr);
+    epi_back(G::T_G2, G::T_Z2, p.W.bias[1], G::ABh, G::ABl, mu ? mu + d.mboff[1] : nullptr);
     sync_issue();
-    if (mu) log_tile(G::A2h, G::A2l, G::TA, G::LZ2);     // Zb2
-    issue(4, G::T_G1, G::A2h, G::A2l);                   // [abar1; ubar1] = W1^T Zb2
-    if (mu) log_read_done();
-    epi_back(G::T_G1, G::T_Z1, p.W.bias[0], G::A1h, G::A1l, mu ? mu + d.mboff[0] : nullptr);
+    if (mu) log_panel(G::ABh, G::ABl, kSecZ2, G::MB, G::BZ);   // Zb2
+    issue(4, G::T_G1, G::ABh, G::ABl);                   // [abar1; ubar1] = W1^T Zb2
+    epi_back(G::T_G1, G::T_Z1, p.W.bias[0], G::ABh, G::ABl, mu ? mu + d.mboff[0] : nullptr);
     sync_issue();
-    if (mu) log_tile(G::A1h, G::A1l, G::TA, G::LZ1);     // Zb1
-    issue(5, G::T_G0, G::A1h, G::A1l);                   // W0^T Zb1: rows 0..D-1 = J^T (h w)
+    if (mu) log_panel(G::ABh, G::ABl, kSecZ1, G::MB, G::BZ);   // Zb1
+    issue(5, G::T_G0, G::ABh, G::ABl);                   // W0^T Zb1: rows 0..D-1 = J^T (h w)
     const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (wp < 4) {
       float v[16];
@@ -471,121 +538,147 @@ struct TcCnfAdapter {
     }
     if (jtv)
       for (int c = threadIdx.x; c < p.Rt; c += blockDim.x) jtv[c * ldn + D] = T(0);
-    if (mu) {
-      log_read_done();
-      ++nlog;
-    }
+    if (mu) ++nlog;
     tc::fence_before();
     __syncthreads();
   }
 
   // ---- deferred parameter cotangents: dW_l = sum over logged VJPs of [zbar; sbar]^T [a; u]
-  // D[M block of outputs][N chunk of inputs] accumulated in TMEM over K = 16 rows per VJP,
-  // operand sub-blocks streamed from the log through the ring (A: outputs, B: inputs)
-  OB_DEV void gemm_log(uint32_t zoff, uint32_t ztile, int mb_count, int mdim, uint32_t aoff,
-                       uint32_t atile, int kin, T* dst, int ldm, int mrows) {
+  // One output tile D[M block][N chunk] at a time, accumulated in TMEM over K = 16 rows per
+  // VJP; the operands stream from the panel log kVB VJPs per stage (two bulk copies),
+  // through three stages in the AB + ring region.
+  static constexpr int kVB = 3;
+  OB_DEV void gemm_panel(int secA, int nblkA, int mdim, uint32_t bbA, int secB, int nblkB,
+                         uint32_t bbB, int kin, T* dst, int ldm, int mrows) {
     const uint32_t sb = tc::smem_u32(ob_tc_smem);
-    const int nch = (kin + cnf_tc::kNW - 1) / cnf_tc::kNW;
-    // staging: two buffers of [A hi | A lo | B hi | B lo] in the A1 / A2 / ring region
-    const uint32_t abytes = (uint32_t)mdim / 8 * 256;                 // M features x 16 rows
-    for (int mb = 0; mb < mb_count; ++mb) {
-      for (int c0 = 0; c0 < nch; c0 += 2) {
-        reinit();   // fresh staging barriers per output tile (phases restart at v = 0)
-        const int ncur = min(2, nch - c0);
-        int nw[2] = {0, 0};
-        for (int j = 0; j < ncur; ++j) nw[j] = min(cnf_tc::kNW, kin - (c0 + j) * cnf_tc::kNW);
-        uint32_t bbytes[2] = {(uint32_t)nw[0] / 8 * 256, (uint32_t)nw[1] / 8 * 256};
-        const uint32_t stage = 2 * abytes + 2 * (bbytes[0] + bbytes[1]);
-        if (tc::uniform_warp() == 0) {
-          for (int v = 0; v < nlog; ++v) {
-            const int s = v & 1;
-            const uint32_t base = G::A1h + s * 2 * 40960;   // two 80 KB stages
-            const unsigned char* rec = logp + (long long)v * G::Log;
-            if (v >= 2) tc::bar_wait(empty(s), ((v - 2) >> 1) & 1u);
-            if (cnf_tc::elect_one()) {
-              cnf_tc::bar_expect_tx(full(s), stage);
-              const uint32_t ab = (uint32_t)(mb * mdim) / 8 * 256;
-              cnf_tc::bulk_load(sm() + base, rec + zoff + ab, abytes, full(s));
-              cnf_tc::bulk_load(sm() + base + abytes, rec + zoff + ztile + ab, abytes, full(s));
-              uint32_t o = base + 2 * abytes;
-              for (int j = 0; j < ncur; ++j) {
-                const uint32_t bb = (uint32_t)((c0 + j) * cnf_tc::kNW) / 8 * 256;
-                cnf_tc::bulk_load(sm() + o, rec + aoff + bb, bbytes[j], full(s));
-                cnf_tc::bulk_load(sm() + o + bbytes[j], rec + aoff + atile + bb, bbytes[j], full(s));
-                o += 2 * bbytes[j];
-              }
+    const long long c = cap();
+    const int nst = (nlog + kVB - 1) / kVB;
+    const uint32_t stage = (uint32_t)kVB * 2 * (bbA + bbB);
+    const unsigned char* pa = logp + sec_off(secA);
+    const unsigned char* pb = logp + sec_off(secB);
+    PhaseTimer pt(p.prof ? p.phase : nullptr);
+    for (int mb = 0; mb < nblkA; ++mb) {
+      for (int nc = 0; nc < nblkB; ++nc) {
+        reinit();
+        pt.mark(12);
+        const int nw = min(cnf_tc::kNW, kin - nc * cnf_tc::kNW);
+        const uint32_t id = mdim == 128 ? tc::idesc_bf16(128, nw, true, true) : tc::idesc_bf16(64, nw, true, true);
+        // staging by every thread with 16-byte cp.async (the log lives in HBM: many
+        // small requests in flight beat a few serialized bulk copies here)
+        auto load = [&](int st) {
+          const int v0 = st * kVB, nvb = min(kVB, nlog - v0), sl = st % 3;
+          const uint32_t bytesA = (uint32_t)nvb * 2 * bbA, bytesB = (uint32_t)nvb * 2 * bbB;
+          unsigned char* base = sm() + G::ABh + sl * stage;
+          const unsigned char* ga = pa + ((long long)mb * c + v0) * 2 * bbA;
+          const unsigned char* gb = pb + ((long long)nc * c + v0) * 2 * bbB;
+          for (uint32_t o = threadIdx.x * 16u; o < bytesA; o += blockDim.x * 16u) cnf_tc::cp16(base + o, ga + o);
+          for (uint32_t o = threadIdx.x * 16u; o < bytesB; o += blockDim.x * 16u)
+            cnf_tc::cp16(base + kVB * 2 * bbA + o, gb + o);
+          cnf_tc::cp_commit();
+        };
+        load(0);
+        if (nst > 1) load(1); else cnf_tc::cp_commit();
+        for (int st = 0; st < nst; ++st) {
+          if (st + 2 < nst) {   // refill the slot of stage st - 1 once its MMAs completed
+            if (st >= 1) {
+              tc::bar_wait(empty((st - 1) % 3), ((st - 1) / 3) & 1u);
+              tc::fence_after();
             }
-            __syncwarp();
-            tc::bar_wait(full(s), (v >> 1) & 1u);
-            tc::fence_after();
-            const uint32_t a = sb + base;
-            const uint64_t Ah = tc::sdesc(a, 128, 256), Al = tc::sdesc(a + abytes, 128, 256);
-            uint32_t o = a + 2 * abytes;
-            for (int j = 0; j < ncur; ++j) {
-              const uint64_t Bh = tc::sdesc(o, 128, 256), Bl = tc::sdesc(o + bbytes[j], 128, 256);
-              const uint32_t dt = (uint32_t)j * cnf_tc::kNW;
-              const uint32_t id = mdim == 128 ? tc::idesc_bf16(128, nw[j], true, true)
-                                              : tc::idesc_bf16(64, nw[j], true, true);
-              tc::mma_bf16_keep_a(dt, Ah, Bh, id, v > 0 ? 1u : 0u);
-              tc::mma_bf16_reuse_a(dt, Ah, Bl, id, 1u);
-              tc::mma_bf16(dt, Al, Bh, id, 1u);
-              o += 2 * bbytes[j];
-            }
-            tc::commit(empty(s));
+            load(st + 2);
+          } else {
+            cnf_tc::cp_commit();   // keep one group per iteration
           }
-          for (int v = max(0, nlog - 2); v < nlog; ++v) tc::bar_wait(empty(v & 1), (v >> 1) & 1u);
-          tc::commit(done());
+          cnf_tc::cp_wait<2>();    // this thread's copies of stage st landed
+          tc::fence_async_smem();
+          __syncthreads();
+          if (tc::uniform_warp() == 0) {
+            tc::fence_after();
+            const int sl = st % 3, v0 = st * kVB, nvb = min(kVB, nlog - v0);
+            const uint32_t base = sb + G::ABh + sl * stage;
+            for (int jv = 0; jv < nvb; ++jv) {
+              const uint32_t a = base + jv * 2 * bbA, b = base + kVB * 2 * bbA + jv * 2 * bbB;
+              const uint64_t Ah = tc::sdesc(a, 128, 256), Al = tc::sdesc(a + bbA, 128, 256);
+              const uint64_t Bh = tc::sdesc(b, 128, 256), Bl = tc::sdesc(b + bbB, 128, 256);
+              tc::mma_bf16_keep_a(0u, Ah, Bh, id, (v0 + jv) > 0 ? 1u : 0u);
+              tc::mma_bf16_reuse_a(0u, Ah, Bl, id, 1u);
+              tc::mma_bf16(0u, Al, Bh, id, 1u);
+            }
+            tc::commit(empty(sl));
+            if (st == nst - 1) tc::commit(done());
+          }
         }
         tc::bar_wait(done(), done_phase);
         done_phase ^= 1u;
         tc::fence_after();
-        // flush: rows (outputs) -> TMEM lanes (M = 128: lane = row; M = 64: 32 (r/16) + r%16)
-        const int wq = threadIdx.x >> 5, lane = threadIdx.x & 31, q = wq & 3, cg = wq >> 2;
-        int r;
-        bool ok;
-        if (mdim == 128) { r = 32 * q + lane; ok = true; }
-        else { r = 16 * q + lane; ok = lane < 16; }
-        const int orow = mb * mdim + r;
-        for (int j = 0; j < ncur; ++j) {
-          for (int cc = cg * 16; cc < nw[j]; cc += 64) {   // 16-column groups per warp group
+        pt.mark(10);
+        // flush: TMEM rows (M = 128: lane = row; M = 64: lane 32 (r/16) + r%16) -> a shared
+        // fp32 tile -> coalesced 16-byte stores.  Every dW entry is produced by exactly one
+        // output tile of one finish(), so it is stored, not accumulated (mu starts at zero).
+        {
+          constexpr int kLd = cnf_tc::kNW + 4;   // padded row stride (floats)
+          float* tile = reinterpret_cast<float*>(sm() + G::ABh);
+          const int wq = threadIdx.x >> 5, lane = threadIdx.x & 31, q = wq & 3, cg = wq >> 2;
+          const int r = mdim == 128 ? 32 * q + lane : 16 * q + lane;
+          const bool ok = mdim == 128 || lane < 16;
+          for (int cc = cg * 16; cc < nw; cc += 64) {
             float v16[16];
-            tc::ld16(((uint32_t)(32 * q) << 16) + (uint32_t)j * cnf_tc::kNW + cc, v16);
-            if (ok && orow < mrows) {
-              T* drow = dst + (long long)orow * ldm;
-              const int k0 = (c0 + j) * cnf_tc::kNW + cc;
-              for (int e = 0; e < 16; ++e)
-                if (k0 + e < ldm) drow[k0 + e] += T(v16[e]);
+            tc::ld16(((uint32_t)(32 * q) << 16) + (uint32_t)cc, v16);
+            if (ok)
+              for (int e = 0; e < 16; e += 4)
+                *reinterpret_cast<float4*>(tile + r * kLd + cc + e) =
+                    make_float4(v16[e], v16[e + 1], v16[e + 2], v16[e + 3]);
+          }
+          tc::fence_before();
+          __syncthreads();
+          const int rows = min(mdim, mrows - mb * mdim), k0 = nc * cnf_tc::kNW;
+          const int ncol = min(nw, ldm - k0), n4 = (ncol + 3) / 4;
+          for (int i = threadIdx.x; i < rows * n4; i += blockDim.x) {
+            const int rr = i / n4, c4 = i % n4;
+            const float4 v = *reinterpret_cast<const float4*>(tile + rr * kLd + 4 * c4);
+            T* drow = dst + (long long)(mb * mdim + rr) * ldm + k0 + 4 * c4;
+            if (4 * c4 + 3 < ncol) {
+              *reinterpret_cast<float4*>(drow) = v;
+            } else {
+              const float e4[4] = {v.x, v.y, v.z, v.w};
+              for (int e = 0; 4 * c4 + e < ncol; ++e) drow[e] = T(e4[e]);
             }
           }
         }
         tc::fence_before();
         __syncthreads();
-        tc::fence_after();
+        pt.mark(11);
       }
     }
   }
 
   OB_DEV void finish(T* mu) {
-    if (!mu || nlog == 0) return;
-    const Dims& d = p.d;
-    if (threadIdx.x == 0) {
-      cnf_tc::bulk_wait_all();
-      cnf_tc::fence_async_global();
+    // the cluster's weight multicasts into this CTA's ring are over before the ring
+    // region is reused for the log GEMM staging
+    if constexpr (CL > 1) {
+      tc::fence_before();
+      cluster_sync();
     }
+    if (!mu || nlog == 0) return;
+#ifdef OB_EXP_NO_FINISH
+    return;
+#endif
+    const Dims& d = p.d;
+    // the log was written by generic stores: visible to the bulk (async-proxy) loads
+    cnf_tc::fence_async_global();
     __syncthreads();
-    // dW1 [H][H] (mu row stride ldm[1]): zbar2 outputs x [a1; u1] inputs
-    gemm_log(G::LZ2, G::TA, G::MB, 128, G::LA1, G::TA, G::KH, mu + d.mwoff[1], d.ldm[1], H);
-    // dW0 [H][D + 1]: zbar1 x X0
-    gemm_log(G::LZ1, G::TA, G::MB, 128, G::LX0, G::TX, G::K0, mu + d.mwoff[0], d.ldm[0], H);
+    // dW1 [H][H] (mu row stride ldm[1]): [zbar2; sbar2] outputs x [a1; u1] inputs
+    gemm_panel(kSecZ2, G::MB, 128, G::BZ, kSecA1, G::NC, G::BA, G::KH, mu + d.mwoff[1], d.ldm[1], H);
+    // dW0 [H][D + 1]: [zbar1; sbar1] x [x; e]
+    gemm_panel(kSecZ1, G::MB, 128, G::BZ, kSecX0, 1, G::BX0, G::K0, mu + d.mwoff[0], d.ldm[0], H);
     // dW2 [D][H]: Z3 x [a2; u2]
-    gemm_log(G::LZ3, G::TX, 1, 64, G::LA2, G::TA, G::KH, mu + d.mwoff[2], d.ldm[2], D);
+    gemm_panel(kSecZ3, 1, 64, G::BZ3, kSecA2, G::NC, G::BA, G::KH, mu + d.mwoff[2], d.ldm[2], D);
     __syncthreads();
   }
   OB_DEV void reinit() {
     tc::fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < 3; ++s) {
         asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(full(s))) : "memory");
         asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(empty(s))) : "memory");
         tc::bar_init(full(s), 1);
@@ -598,6 +691,7 @@ struct TcCnfAdapter {
   OB_DEV void release() {
     tc::fence_before();
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync();   // no CTA leaves while a partner may still multicast to it
     if (threadIdx.x < 32) tc::tmem_free(0u, kCols);
   }
 };

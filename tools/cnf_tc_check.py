@@ -35,7 +35,7 @@ for n, rows in ((24, None), (64, 7)):
 ci = make_config("C4")
 fl = field_from_config(ci)
 u0 = torch.as_tensor(initial_state(ci), dtype=torch.float32, device="cuda")
-for tcf in (True, False):
+for tcf in ((True,) if os.environ.get("OB_CNF_CLUSTER") else (True, False)):
     for _ in range(2):
         r = run_config(ci, "store_all", field=fl, u0=u0, tensor_cores=tcf)
     torch.cuda.synchronize(); t0 = time.perf_counter()
