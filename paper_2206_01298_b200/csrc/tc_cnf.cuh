@@ -284,28 +284,30 @@ struct TcCnfAdapter {
     }
     __syncwarp();
   }
+  // ---- products, warp-specialised: warp 1 streams the weight chunks (TMA) as ring slots
+  // free up, warp 0 issues the MMAs of each chunk as it lands; chunk ordinals run on
+  // across products (slot = ordinal % kNS), so warp 1 may load the next product's first
+  // chunks while the epilogue of this one runs.
+  OB_DEV static uint32_t chunk_bytes(int m) { return (uint32_t)m * cnf_tc::kKc * 2 * 2; }
+  OB_DEV void produce(uint32_t idx, uint32_t src, uint32_t bytes) {
+    const int s = (int)(idx % cnf_tc::kNS);
+    if (idx >= (uint32_t)cnf_tc::kNS) {   // every CTA of the cluster consumed the slot's last chunk
+      const uint32_t prev = idx - cnf_tc::kNS;
+      tc::bar_wait(empty(s), (prev / cnf_tc::kNS) & 1u);
+    }
+    load_chunk(idx, src, bytes);
+  }
   // D[mb] (+)= W x B over the product's K: chunk c = (mb, kc); B = tile at smem offset bh / bl
   template <int M>
-  OB_DEV void product(const CnfProd& pr, uint32_t dcol, uint32_t bh, uint32_t bl) {
+  OB_DEV void consume(const CnfProd& pr, uint32_t dcol, uint32_t bh, uint32_t bl) {
     constexpr uint32_t id = tc::idesc_bf16(M, cnf_tc::kRows, false, false);
-    const uint32_t cbytes = (uint32_t)M * cnf_tc::kKc * 2 * 2, half = cbytes / 2;
+    const uint32_t half = chunk_bytes(M) / 2;
     const uint32_t n = (uint32_t)(pr.nmb * pr.nkc);
     const uint32_t sb = tc::smem_u32(ob_tc_smem);
     constexpr int KS = cnf_tc::kKc / 16;   // K slices per chunk
-    // prefetch kNS - 1 chunks (the ring is empty between products)
-    for (; head < tail + cnf_tc::kNS - 1 && head < tail + n; ++head)
-      load_chunk(head, pr.src + (head - tail) * cbytes, cbytes);
     for (uint32_t c = 0; c < n; ++c) {
       const uint32_t idx = tail + c;
       const int s = (int)(idx % cnf_tc::kNS);
-      // keep kNS - 1 copies in flight: refill the slot of chunk idx - 1 (its MMAs were
-      // issued an iteration ago) before consuming chunk idx
-      if (head < tail + n) {
-        const uint32_t prev = head - cnf_tc::kNS;   // the chunk that last used head's slot
-        if (head >= (uint32_t)cnf_tc::kNS) tc::bar_wait(empty((int)(prev % cnf_tc::kNS)), (prev / cnf_tc::kNS) & 1u);
-        load_chunk(head, pr.src + (head - tail) * cbytes, cbytes);
-        ++head;
-      }
       tc::bar_wait(full(s), (idx / cnf_tc::kNS) & 1u);
       tc::fence_after();
       const int mb = (int)(c / pr.nkc), kc = (int)(c % pr.nkc);
@@ -323,7 +325,6 @@ struct TcCnfAdapter {
       }
       commit_empty(s);
     }
-    tail += n;
     tc::commit(done());
   }
   // every thread: wait for the product issued by warp 0
@@ -332,17 +333,28 @@ struct TcCnfAdapter {
     done_phase ^= 1u;
     tc::fence_after();
   }
-  // the ring slots are refilled only after their MMAs completed; drain the last
-  // empties of a product so the next product's prefetch can reuse every slot
-  OB_DEV void issue(int which, uint32_t dcol, uint32_t bh, uint32_t bl) {
-    if (tc::uniform_warp() == 0) {
-      const CnfProd pr = prod(which);
-      if (pr.m == 128) product<128>(pr, dcol, bh, bl);
-      else product<64>(pr, dcol, bh, bl);
-      // wait for the product's remaining chunks' MMAs (slots free for the next prefetch)
-      for (uint32_t j = (tail >= (uint32_t)cnf_tc::kNS ? tail - cnf_tc::kNS : 0); j < tail; ++j)
-        tc::bar_wait(empty((int)(j % cnf_tc::kNS)), (j / cnf_tc::kNS) & 1u);
+  // product `which` into TMEM columns dcol from the B tile (bh, bl); `next`: the product
+  // that follows within the same field call (its first chunks are prefetched), or -1
+  OB_DEV void issue(int which, int next, uint32_t dcol, uint32_t bh, uint32_t bl) {
+    const CnfProd pr = prod(which);
+    const uint32_t n = (uint32_t)(pr.nmb * pr.nkc);
+    const int w = tc::uniform_warp();
+    if (w == 1) {
+      const uint32_t cb = chunk_bytes(pr.m);
+      for (uint32_t idx = head > tail ? head : tail; idx < tail + n; ++idx)
+        produce(idx, pr.src + (idx - tail) * cb, cb);
+      head = tail + n;
+      if (next >= 0) {
+        const CnfProd nx = prod(next);
+        const uint32_t nn = (uint32_t)(nx.nmb * nx.nkc), ncb = chunk_bytes(nx.m);
+        for (uint32_t k = 0; k + 1 < (uint32_t)cnf_tc::kNS && k < nn; ++k, ++head)
+          produce(head, nx.src + k * ncb, ncb);
+      }
+    } else if (w == 0) {
+      if (pr.m == 128) consume<128>(pr, dcol, bh, bl);
+      else consume<64>(pr, dcol, bh, bl);
     }
+    tail += n;
     wait_done();
   }
   OB_DEV static CnfProd prod(int which) {
@@ -383,21 +395,21 @@ struct TcCnfAdapter {
 
   // forward through the two hidden layers (pre-activations stay in TMEM Z1 / Z2)
   // (log: the VJP's layer inputs are logged as they are produced)
-  OB_DEV void hidden_forward(bool log) {
+  OB_DEV void hidden_forward(bool log, int next) {
     sync_issue();
-    issue(0, G::T_Z1, G::X0h, G::X0l);
+    issue(0, 1, G::T_Z1, G::X0h, G::X0l);
     epi_hidden(G::T_Z1, p.W.bias[0], G::ABh, G::ABl);         // [a1; u1]
     sync_issue();
     if (log) log_panel(G::ABh, G::ABl, kSecA1, G::NC, G::BA);
-    issue(1, G::T_Z2, G::ABh, G::ABl);
+    issue(1, next, G::T_Z2, G::ABh, G::ABl);
     epi_hidden(G::T_Z2, p.W.bias[1], G::ABh, G::ABl);         // [a2; u2] over [a1; u1]
   }
 
   // f_aug(x0) -> out [Rt][ldn]: columns [0, D) = f, column D = -eps^T J eps
   OB_DEV void eval(T* out) {
-    hidden_forward(false);
+    hidden_forward(false, 2);
     sync_issue();
-    issue(2, G::T_OUT, G::ABh, G::ABl);
+    issue(2, -1, G::T_OUT, G::ABh, G::ABl);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* je = reinterpret_cast<float*>(sm() + G::Jeps);
     if (w < 4) {   // M = 64 accumulator: row n -> lane 32 (n / 16) + n % 16 (lanes < 16)
@@ -496,7 +508,7 @@ struct TcCnfAdapter {
       if (threadIdx.x == 0 && p.status) set_status(p.status, OB_ERR_UNSUPPORTED, -3);   // log capacity
       mu = nullptr;
     }
-    hidden_forward(mu != nullptr);
+    hidden_forward(mu != nullptr, 3);
     // output-layer cotangent Z3 = h [v_z ; -v_Delta eps]; db2 += h sum_rows v_z
     for (int i = threadIdx.x; i < cnf_tc::kHalf * D; i += blockDim.x) {
       const int c = i / D, n = i % D;
@@ -519,15 +531,15 @@ struct TcCnfAdapter {
       log_panel(G::ABh, G::ABl, kSecA2, G::NC, G::BA);
       log_panel(G::Z3h, G::Z3l, kSecZ3, 1, G::BZ3);
     }
-    issue(3, G::T_G2, G::Z3h, G::Z3l);                   // [abar2; ubar2] = W2^T Z3
+    issue(3, 4, G::T_G2, G::Z3h, G::Z3l);                // [abar2; ubar2] = W2^T Z3
     epi_back(G::T_G2, G::T_Z2, p.W.bias[1], G::ABh, G::ABl, mu ? mu + d.mboff[1] : nullptr);
     sync_issue();
     if (mu) log_panel(G::ABh, G::ABl, kSecZ2, G::MB, G::BZ);   // Zb2
-    issue(4, G::T_G1, G::ABh, G::ABl);                   // [abar1; ubar1] = W1^T Zb2
+    issue(4, 5, G::T_G1, G::ABh, G::ABl);                // [abar1; ubar1] = W1^T Zb2
     epi_back(G::T_G1, G::T_Z1, p.W.bias[0], G::ABh, G::ABl, mu ? mu + d.mboff[0] : nullptr);
     sync_issue();
     if (mu) log_panel(G::ABh, G::ABl, kSecZ1, G::MB, G::BZ);   // Zb1
-    issue(5, G::T_G0, G::ABh, G::ABl);                   // W0^T Zb1: rows 0..D-1 = J^T (h w)
+    issue(5, -1, G::T_G0, G::ABh, G::ABl);               // W0^T Zb1: rows 0..D-1 = J^T (h w)
     const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (wp < 4) {
       float v[16];
