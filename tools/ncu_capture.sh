@@ -5,6 +5,7 @@
 # bring back).
 name=$1; shift; regex=$1; shift; [ "$1" = "--" ] && shift
 rep=/tmp/${name}.ncu-rep
+mkdir -p $(dirname $rep) $(dirname gpurun_out/${name})
 ncu $(cat tools/ncu_sections.txt) --clock-control none --import-source on -k regex:${regex} -s 1 -c 1 -f -o ${rep%.ncu-rep} "$@" > gpurun_out/${name}_ncu.log 2>&1
 ncu -i $rep --page raw --csv > gpurun_out/${name}_raw.csv 2>/dev/null
 ncu -i $rep --page details --csv > gpurun_out/${name}_details.csv 2>/dev/null
