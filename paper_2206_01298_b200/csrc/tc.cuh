@@ -191,6 +191,46 @@ __device__ __forceinline__ float tanh_1sfu(float x) {
   return copysignf((1.0f - e) * r, x);
 }
 
+// ---- paired fp32 arithmetic (Blackwell FFMA2 / FADD2 / FMUL2: two lanes of work per
+// instruction; each lane is the IEEE round-to-nearest operation of its scalar form)
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// tanh_1sfu of two values with the FMA-pipe work paired: bit-identical to two scalar
+// calls (-(1 + e) and 1 - e are formed exactly as fma(e, -1, -/+1); -0.5 d = 0.5 (-d))
+__device__ __forceinline__ void tanh2_1sfu(float x0, float x1, float& y0, float& y1) {
+  float e0, e1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(-2.8853900817779268f * fabsf(x0)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(-2.8853900817779268f * fabsf(x1)));
+  const uint64_t e = pk2(e0, e1), m1 = pk2(-1.f, -1.f), p1 = pk2(1.f, 1.f);
+  const uint64_t nd = fma2(e, m1, m1);                                // -(1 + e)
+  uint64_t r = fma2(pk2(0.5f, 0.5f), nd, pk2(1.4571068f, 1.4571068f));
+  r = fma2(r, fma2(nd, r, p1), r);
+  r = fma2(r, fma2(nd, r, p1), r);
+  r = fma2(r, fma2(nd, r, p1), r);
+  const uint64_t y = mul2(fma2(e, m1, p1), r);                        // (1 - e) r
+  float a, b;
+  upk2(y, a, b);
+  y0 = copysignf(a, x0);
+  y1 = copysignf(b, x1);
+}
+
 // byte offset of element (a, b) in a core-blocked operand (see the header comment)
 __host__ __device__ __forceinline__ uint32_t blk(int a, int b, uint32_t SA, uint32_t SB) {
   return (uint32_t)(a >> 3) * SA + (uint32_t)(b >> 3) * SB + (uint32_t)(a & 7) * 16u +

@@ -271,11 +271,22 @@ struct TcMlpAdapter {
     ld_hidden(v, o, c0, cg);
     const float bo = b1()[o], wt = w1t()[o];
     float a[16];
+    if (act == OB_ACT_TANH) {
 #pragma unroll
-    for (int j = 0; j < CW; ++j) {
-      const float z = v[j] + bo + tcur * wt;
-      a[j] = act == OB_ACT_TANH ? tc::tanh_1sfu(z) : z;
-      if (kVjp) ap[j] = act == OB_ACT_TANH ? 1.f - a[j] * a[j] : 1.f;
+      for (int j = 0; j < CW; j += 2) {
+        const float z0 = v[j] + bo + tcur * wt, z1 = v[j + 1] + bo + tcur * wt;
+        tc::tanh2_1sfu(z0, z1, a[j], a[j + 1]);
+        if (kVjp) {
+          ap[j] = 1.f - a[j] * a[j];
+          ap[j + 1] = 1.f - a[j + 1] * a[j + 1];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        a[j] = v[j] + bo + tcur * wt;
+        if (kVjp) ap[j] = 1.f;
+      }
     }
     put_hid(c0, o, a);
   }
