@@ -21,6 +21,7 @@ namespace ob {
 
 enum { kPhTop = 0, kPhCycle = 1, kPhFinal = 2, kPhDone = 3, kPhFail = 4 };
 constexpr int kMaxTileRows = 32;
+constexpr int kMgsV = 4;   // state elements per lane in the register MGS path (N <= 128)
 
 struct SampleState {
   int phase, total, k, used, breakdown;
@@ -159,13 +160,47 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
       } else if (S.phase == kPhCycle) {
         const int k = S.k;
         S.total += 1;
-        // modified Gram-Schmidt (linalg.py:73-75)
-        for (int i = 0; i <= k; ++i) {
-          const T* qi = Q + (long long)i * ldn;
-          const T hik = warp_dot(vo, qi, N);
-          for (int j = lane; j < N; j += 32) vo[j] = Num<T>::add(vo[j], -Num<T>::mul(hik, qi[j]));
+        // modified Gram-Schmidt (linalg.py:73-75).  The operator output stays in registers
+        // (kMgsV elements per lane) and the next basis vector is loaded while the current
+        // projection reduces (the basis lives in L2); same operation order as warp_dot.
+        if (N <= 32 * kMgsV) {
+          T v[kMgsV], q[kMgsV], qn[kMgsV];
+#pragma unroll
+          for (int e = 0; e < kMgsV; ++e) {
+            const int j = lane + 32 * e;
+            v[e] = j < N ? vo[j] : T(0);
+            q[e] = j < N ? Q[j] : T(0);
+          }
+          for (int i = 0; i <= k; ++i) {
+            if (i < k) {
+              const T* qx = Q + (long long)(i + 1) * ldn;
+#pragma unroll
+              for (int e = 0; e < kMgsV; ++e) qn[e] = lane + 32 * e < N ? qx[lane + 32 * e] : T(0);
+            }
+            T sdot = T(0);
+#pragma unroll
+            for (int e = 0; e < kMgsV; ++e)
+              if (lane + 32 * e < N) sdot = Num<T>::fma(v[e], q[e], sdot);
+            const T hik = warp_sum(sdot);
+#pragma unroll
+            for (int e = 0; e < kMgsV; ++e)
+              if (lane + 32 * e < N) v[e] = Num<T>::add(v[e], -Num<T>::mul(hik, q[e]));
+            if (lane == 0) H[i * m + k] = hik;
+#pragma unroll
+            for (int e = 0; e < kMgsV; ++e) q[e] = qn[e];
+          }
+#pragma unroll
+          for (int e = 0; e < kMgsV; ++e)
+            if (lane + 32 * e < N) vo[lane + 32 * e] = v[e];
           __syncwarp();
-          if (lane == 0) H[i * m + k] = hik;
+        } else {
+          for (int i = 0; i <= k; ++i) {
+            const T* qi = Q + (long long)i * ldn;
+            const T hik = warp_dot(vo, qi, N);
+            for (int j = lane; j < N; j += 32) vo[j] = Num<T>::add(vo[j], -Num<T>::mul(hik, qi[j]));
+            __syncwarp();
+            if (lane == 0) H[i * m + k] = hik;
+          }
         }
         const T hn = sqrt(warp_dot(vo, vo, N));
         if (lane == 0) H[(k + 1) * m + k] = hn;
