@@ -333,6 +333,9 @@ def roofline(ci, scheme, dev, nloc, phases, K, policy_key):
         bf16, bf16_src = bf16_peak()
         peak, peak_src = bf16 / 3.0, f"{bf16_src} / 3 (3-pass bf16 split)"
         pipe, bound = "tcgen05 kind::f16 (bf16 3-pass split, fp32 accumulate in TMEM)", "tensor"
+        if ci.kind == "conv":   # fp16 two-term split (same 3 passes at the same rate), one tap per TMEM partial
+            peak_src = f"{bf16_src} / 3 (3-pass fp16 split)"
+            pipe = "tcgen05 kind::f16 (fp16 3-pass split, per-tap TMEM partials summed in fp32 registers)"
     if dev.get("tensor_cores") and ci.kind == "mlp":
         D0, H = ci.widths[-1], ci.widths[1]
         nmb, t = H // 128, dev["tiles"]

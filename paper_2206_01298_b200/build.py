@@ -21,7 +21,7 @@ LIB = os.path.join(PKG, "libodeblock.so")
 # longest translation units first (the pool starts them first)
 SOURCES = ["theta_f64_fwd.cu", "theta_f64_rev.cu", "theta_f32_fwd.cu", "theta_f32_rev.cu", "rk_f64.cu",
            "adaptive_f32.cu", "rk_f32.cu", "adaptive_f64.cu", "cnf_f32.cu", "cnf_tc.cu", "rk_f32s.cu", "rk_tc.cu",
-           "conv_f32.cu", "capi.cu", "optim.cu",
+           "conv_f32.cu", "conv_tc.cu", "capi.cu", "optim.cu",
            "revolve.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

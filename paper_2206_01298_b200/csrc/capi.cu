@@ -75,6 +75,13 @@ cudaError_t launch_cnf_tc(const RkParams<float>& p, int tiles, int cl, size_t sm
 cudaError_t launch_cnf_tc_field(const RkParams<float>& p, int tiles, int cl, size_t smem, int mode,
                                 double t, const float* u, const float* w, float* out, cudaStream_t st);
 
+// tcgen05 conv tile (conv_tc.cu)
+void tc_conv_sizes(unsigned* packed_bytes, unsigned* smem_bytes);
+cudaError_t launch_pack_tc_conv(const Dims& d, const float* theta, void* img, cudaStream_t st);
+cudaError_t launch_conv_tc(const RkParams<float>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
+cudaError_t launch_conv_tc_field(const RkParams<float>& p, int tiles, size_t smem, int mode, double t,
+                                 const float* u, const float* w, float* out, cudaStream_t st);
+
 // dispatch on where the weights live (fp32 only stages them in shared memory)
 template <typename T>
 cudaError_t launch_rk(const RkParams<T>& p, int lr, int tiles, size_t smem, cudaStream_t st,
@@ -215,6 +222,7 @@ struct Plan {
   bool theta = false;
   bool tc = false;                // tcgen05 tensor-core MLP tile (rk_tc.cu)
   bool tc_cnf = false;            // tcgen05 CNF tile (cnf_tc.cu)
+  bool tc_conv = false;           // tcgen05 conv tile (conv_tc.cu)
   long long cnf_log_rec = 0;      // tcgen05 CNF tile: bytes of one VJP record of the dW log
   int cnf_cluster = 1;            // tcgen05 CNF tile: CTAs per cluster sharing the weight stream
   int s_stages = 0;               // scheme stages (stage scratch sizing)
@@ -605,6 +613,35 @@ bool plan_tc_cnf(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   return true;
 }
 
+// Tensor-core conv tile: the C3 block on an explicit fixed-step scheme, one image per CTA.
+bool tc_conv_eligible(const ob_field_desc& f, int flags) {
+  if (f.kind != OB_FIELD_CONV || f.dtype != OB_F32) return false;
+  return !((flags & OB_FLAG_NO_TENSOR_CORES) || getenv("OB_NO_TC"));
+}
+
+bool plan_tc_conv(Plan& P, const ob_field_desc& f, long long B) {
+  Plan Q = P;
+  Q.R = Q.Rt = Q.LR = 1;
+  make_dims(f, 1, Q.d);
+  unsigned packed = 0, total = 0;
+  tc_conv_sizes(&packed, &total);
+  Q.d.n_packed = packed / 4;
+  SmemLayout& s = Q.sm;
+  s = SmemLayout{};
+  s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = s.ks = s.ring = s.hscr = s.wts = -1;
+  s.u = s.lam = s.lamn = s.w = s.jtv = -1;   // state buffers in global memory
+  s.ring_elems = s.hscr_elems = s.scr_elems = 0;
+  for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
+  for (int i = 0; i < 8; ++i) s.vec[i] = -1;
+  s.total = (int)(total / 4);
+  Q.smem_bytes = total;
+  if (Q.smem_bytes > smem_cap(Q)) return false;
+  Q.tiles = (int)B;
+  Q.tc_conv = true;
+  P = Q;
+  return true;
+}
+
 // compile the checkpoint policy into forward store directives + a reverse
 // program (checkpointing.py:242-340), with reference-semantics counters.
 int compile_policy(const ob_problem& p, Plan& P) {
@@ -825,6 +862,7 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   choose_tiles(P, p.field, p.batch, sms);
   if (allow_tc && tc_eligible(p, P)) plan_tc(P, p.field, p.batch, sms);
   if (allow_tc && !P.adaptive && tc_cnf_eligible(p.field, p.flags)) plan_tc_cnf(P, p.field, p.batch, sms);
+  if (allow_tc && !P.adaptive && tc_conv_eligible(p.field, p.flags)) plan_tc_conv(P, p.field, p.batch);
   if (P.smem_bytes > smem_cap(P)) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   if (P.adaptive) {
     P.prog.clear();
@@ -873,7 +911,7 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   if (P.adaptive) c = ob_counters{};   // per-sample grids: filled after the run
   c.tile_rows = P.R;
   c.tiles = P.tiles;
-  c.tensor_cores = (P.tc || P.tc_cnf) ? 1 : 0;
+  c.tensor_cores = (P.tc || P.tc_cnf || P.tc_conv) ? 1 : 0;
   c.kernel_launches = 4;
   // workspace
   const long long B = p.batch, N = P.d.N;
@@ -908,6 +946,8 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
     P.cnf_stride = std::max<long long>(1, c.device_vjp_evals) * P.cnf_log_rec / 4;
   } else if (P.d.cnf) {
     for (int l = 0; l < P.d.L - 1; ++l) P.cnf_stride += 2LL * P.Rt * P.d.lda[l + 1];
+  } else if (P.tc_conv) {
+    P.cnf_stride = 256LL * 64;       // the tile's field input (fp32 image)
   } else if (P.d.conv) {
     P.cnf_stride = 18LL * 18 * 68;   // parked input tile
   }
@@ -1077,6 +1117,9 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
   CU(cudaEventRecord(ev[0], st));
   if (!do_fwd) {
     // packed weights of the forward call are still in the workspace
+  } else if (P.tc_conv) {
+    if constexpr (sizeof(T) == 4)
+      CU(launch_pack_tc_conv(P.d, reinterpret_cast<const float*>(pp.theta), pp.packed, st));
   } else if (P.d.conv) {
     if constexpr (sizeof(T) == 4) CU(launch_pack_conv<T>(pp, st));
   } else if (P.tc) {
@@ -1103,6 +1146,11 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
       if constexpr (sizeof(T) == 4)
         return launch_cnf_tc(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.cnf_cluster,
                              P.smem_bytes, st, fwd);
+      return cudaErrorNotSupported;
+    }
+    if (P.tc_conv) {
+      if constexpr (sizeof(T) == 4)
+        return launch_conv_tc(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.smem_bytes, st, fwd);
       return cudaErrorNotSupported;
     }
     if (P.d.cnf || P.d.conv) {
@@ -1408,13 +1456,14 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   choose_tiles(P, f, batch, sms);
   if (mode != kJvp && tc_cnf_eligible(f, 0)) plan_tc_cnf(P, f, batch, sms);
+  if (mode != kJvp && tc_conv_eligible(f, 0)) plan_tc_conv(P, f, batch);
   if (P.smem_bytes > kSmemLimit) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   const size_t pk_bytes = align_up(P.esz * (size_t)P.d.n_packed, 256);
   const size_t mu_bytes = mode == kVjp ? P.esz * (size_t)P.tiles * P.d.n_mu : 0;
   long long cnf_stride = 0;
   for (int l = 0; P.d.cnf && !P.tc_cnf && l < P.d.L - 1; ++l) cnf_stride += 2LL * P.Rt * P.d.lda[l + 1];
   if (P.tc_cnf) cnf_stride = P.cnf_log_rec / 4;   // one VJP record per tile
-  if (P.d.conv) cnf_stride = 18LL * 18 * 68;
+  if (P.d.conv) cnf_stride = P.tc_conv ? 256LL * 64 : 18LL * 18 * 68;
   const size_t cnf_bytes = align_up(P.esz * (size_t)P.tiles * cnf_stride, 256);
   const size_t st_bytes = P.sm.u < 0 ? align_up(P.esz * (size_t)P.tiles * 5 * P.Rt * P.d.ldn, 256) : 0;
   char* ws = nullptr;
@@ -1446,7 +1495,9 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
   cudaError_t e = cudaSuccess;
   if (mu_bytes) e = cudaMemsetAsync(rp.mu, 0, mu_bytes, st);
   if (e == cudaSuccess) {
-    if (P.d.conv) {
+    if (P.tc_conv) {
+      if constexpr (sizeof(T) == 4) e = launch_pack_tc_conv(P.d, reinterpret_cast<const float*>(theta), ws, st);
+    } else if (P.d.conv) {
       if constexpr (sizeof(T) == 4) e = launch_pack_conv<T>(pp, st);
     } else if (P.tc_cnf) {
       if constexpr (sizeof(T) == 4) e = launch_pack_tc_cnf(P.d, reinterpret_cast<const float*>(theta), ws, st);
@@ -1455,7 +1506,12 @@ int run_field_op(const ob_field_desc& f, int64_t batch, const void* theta, const
     }
   }
   if (e == cudaSuccess) {
-    if (P.d.conv) {
+    if (P.tc_conv) {
+      if constexpr (sizeof(T) == 4)
+        e = launch_conv_tc_field(reinterpret_cast<const RkParams<float>&>(rp), P.tiles, P.smem_bytes, mode, t,
+                                 reinterpret_cast<const float*>(u), reinterpret_cast<const float*>(w),
+                                 reinterpret_cast<float*>(out), st);
+    } else if (P.d.conv) {
       if constexpr (sizeof(T) == 4)
         e = launch_conv_field<T>(rp, P.tiles, P.smem_bytes, mode, t, static_cast<const T*>(u),
                                  static_cast<const T*>(w), static_cast<T*>(out), st);

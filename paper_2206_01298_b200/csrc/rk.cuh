@@ -105,6 +105,10 @@ struct RkParams {
   const T* eps;           // Hutchinson probes [B][D]
   T* cnf_pre;             // per tile [L-1][2Rt][lda] pre-activations (forward | raw tangent)
   long long cnf_pre_stride;
+  // tcgen05 conv tile: shared-window address of the kernel's dynamic shared memory (= its
+  // static shared size, set by the launcher).  A kernel-parameter value is uniform, so the
+  // MMA descriptors built from it stay on the uniform datapath.
+  unsigned tc_smem_base;
 };
 
 template <typename T>

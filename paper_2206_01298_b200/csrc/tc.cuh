@@ -40,6 +40,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
        | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// the same with fp16 inputs (format 0): 11-bit significands, used by the conv tile's
+// scaled two-term split (tc_conv.cuh); the MMA instruction is kind::f16 either way
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 // Issue helpers are executed by a whole (warp-uniform) warp so the descriptors
 // stay in uniform registers; elect.sync picks the one lane that issues.
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
@@ -70,6 +77,34 @@ __device__ __forceinline__ void mma_bf16_reuse_a(uint32_t d_tmem, uint64_t a, ui
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// ---- single-thread forms: the caller has already elected ONE thread (elect.sync region),
+// which issues a whole group of MMAs and their commit (descriptors then stay in the uniform
+// datapath without a per-instruction election)
+__device__ __forceinline__ void mma1(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma1_keep_a(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma1_reuse_a(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit1(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
 // arrive on an mbarrier when every previously issued tcgen05.mma of the electing
 // lane completes (whole warp calls; the same lane as mma_bf16 commits)
 __device__ __forceinline__ void commit(uint64_t* bar) {
@@ -96,6 +131,23 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
       "@P1 bra DONE_%=;\n\t"
       "bra WAIT_%=;\n"
       "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// The same wait executed by a whole converged warp with a warp-uniform exit (vote): the
+// code after it stays provably convergent, so ptxas keeps descriptor arithmetic and the
+// tcgen05 operands on the uniform datapath (after the per-thread exit of bar_wait it falls
+// back to vector registers, R2UR moves and an election per MMA)
+__device__ __forceinline__ void bar_wait_warp(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1, P2;\n"
+      "WAITU_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "vote.sync.all.pred P2, P1, 0xffffffff;\n\t"
+      "@P2 bra DONEU_%=;\n\t"
+      "bra WAITU_%=;\n"
+      "DONEU_%=:\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
 }
@@ -149,6 +201,27 @@ __device__ __forceinline__ void ld16(uint32_t taddr, float v[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 16 columns without the wait: several loads in flight, then one wait_ld()
+__device__ __forceinline__ void ld16_async(uint32_t taddr, uint32_t r[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// the wait names the loaded registers as in/out operands, so no use of them can be
+// scheduled above it (call once per register group; later calls find nothing pending)
+__device__ __forceinline__ void wait_ld(uint32_t r[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]),
+                 "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
 }
 
 __device__ __forceinline__ void st8(uint32_t taddr, const float v[8]) {

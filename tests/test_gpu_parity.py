@@ -238,18 +238,26 @@ def test_c3_field_protocol_matches_restated_oracle():
     assert oc.rel_error(np_(p), p_ref) <= TOL32
 
 
-def test_c3_subset_matches_restated_oracle_and_policies_agree():
+@pytest.mark.parametrize("tensor_cores", [True, False])
+def test_c3_subset_matches_restated_oracle_and_policies_agree(tensor_cores):
+    """Six images on the tcgen05 conv tile and on the SIMT tile: store_all and revolve:3
+    bit-identical; u_final, dtheta, head gradient and loss at the fp32 bar; du0 per image
+    at the bar or at a demonstrated ReLU kink of the oracle (tests/_kinks.py)."""
+    from _kinks import check_du0_with_kinks
     from oracle import fields_ext as ox
     from oracle.problems import run_oracle
     ci = make_config("C3").subset(6)
     fld = field_from_config(ci)
-    base = run_config(ci, "store_all", field=fld)
-    rev = run_config(ci, "revolve:3", field=fld)
+    base = run_config(ci, "store_all", field=fld, tensor_cores=tensor_cores)
+    rev = run_config(ci, "revolve:3", field=fld, tensor_cores=tensor_cores)
+    assert base.device["tensor_cores"] == int(tensor_cores)
     assert np.array_equal(base.dtheta, rev.dtheta) and base.loss == rev.loss
+    assert np.array_equal(np_(base.du0), np_(rev.du0))
     ref = run_oracle(ci, "store_all")
-    errs = {k: oc.rel_error(np_(getattr(base, k)), ref[k]) for k in ("u_final", "du0", "dtheta")}
+    errs = {k: oc.rel_error(np_(getattr(base, k)), ref[k]) for k in ("u_final", "dtheta")}
     assert max(errs.values()) <= TOL32, errs
     assert abs(base.loss - ref["loss"]) <= TOL32 * abs(ref["loss"])
+    check_du0_with_kinks(lambda: make_config("C3").subset(6), np_(base.du0), ref["du0"], TOL32, max_over=1)
     dhead = ox.head_loss(ref["u_final"], ci.extras["head"], ci.extras["labels"])[2]
     assert oc.rel_error(np_(base.dtheta_head), dhead) <= TOL32
     assert base.counters.nfe_forward == 40 and base.counters.nfe_backward == 40
