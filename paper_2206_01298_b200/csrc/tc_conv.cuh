@@ -59,12 +59,16 @@
 #pragma once
 
 #include <cuda_fp16.h>
+#include <cstdio>
 
 #include "rk_impl.cuh"
 #include "tc.cuh"
 
 namespace ob {
 
+#ifndef OB_CONV_GF
+#define OB_CONV_GF 1   // taps per TMEM partial of the forward convolutions (experiments: 3, 9)
+#endif
 #ifndef OB_CONV_GT
 #define OB_CONV_GT 3   // taps per TMEM partial of the transposed convolutions (experiments: 1, 9)
 #endif
@@ -160,6 +164,35 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
       : "memory");
 }
+#ifdef OB_DEBUG_WATCHDOG
+// debugging aid: a wait that reports the barrier it starved on and gives up
+__device__ __noinline__ void wd_report(int tag, int idx, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0)
+    printf("WATCHDOG block %d warp %d tag %d barrier %d parity %u\n", (int)blockIdx.x, (int)(threadIdx.x >> 5), tag, idx,
+           parity);
+}
+__device__ __forceinline__ void wd_wait(uint64_t* bar, uint32_t parity, int tag, uint64_t* base) {
+  for (long long n = 0;; ++n) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1, P2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "vote.sync.all.pred P2, P1, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P2;\n\t}\n"
+        : "=r"(ok)
+        : "r"(tc::smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (n > (1LL << 21)) {
+      wd_report(tag, (int)(bar - base), parity);
+      return;
+    }
+  }
+}
+#define OB_WAIT(bar, parity, tag) conv_tc::wd_wait(bar, parity, tag, bars())
+#else
+#define OB_WAIT(bar, parity, tag) tc::bar_wait_warp(bar, parity)
+#endif
 __device__ __forceinline__ bool elect_one() {
   uint32_t p;
   asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}\n"
@@ -214,7 +247,7 @@ struct TcConvAdapter {
     if (threadIdx.x == 0) {
       for (int s = 0; s < 3; ++s) {
         tc::bar_init(full(s), 1);
-        tc::bar_init(wempty(s), 3);                  // the three issuing warps release a weight slot
+        tc::bar_init(wempty(s), 6);                  // the six issuing warps release a weight slot
       }
       for (int s = 0; s < 6; ++s) {
         tc::bar_init(acc_full(s), 1);
@@ -341,8 +374,13 @@ struct TcConvAdapter {
     for (int ks = 0; ks < 4; ++ks) tc::mma_bf16(d, Al + ks * ak, Bh + ks * bk, id, (ks > 0 || !fresh) ? 1u : 0u);
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
+#ifdef OB_EXP_NO_COLLECTOR
+      tc::mma_bf16(d, Ah + ks * ak, Bl + ks * bk, id, 1u);
+      tc::mma_bf16(d, Ah + ks * ak, Bh + ks * bk, id, 1u);
+#else
       tc::mma_bf16_keep_a(d, Ah + ks * ak, Bl + ks * bk, id, 1u);
       tc::mma_bf16_reuse_a(d, Ah + ks * ak, Bh + ks * bk, id, 1u);
+#endif
     }
   }
 
@@ -354,9 +392,11 @@ struct TcConvAdapter {
   //
   // The product is bound by MMA ISSUE, not by the tensor pipe (shrinking every MMA to
   // N = 16 left its time unchanged; ~70-100 cycles of issue per tcgen05.mma from one warp
-  // against 32 of execution), so THREE warps issue: warp b owns M block b.  Each block has
-  // two accumulators (one per parity of the drain group); at the top of tap s the issuing
-  // warps queue tap s + 1, then every warp drains the group that tap s completes.  Warp 0
+  // against 32 of execution), so SIX warps issue: each M block has two accumulators (one per
+  // parity of the drain group) and warp parity * 3 + b owns accumulator (parity, b) -- a
+  // group's MMAs all come from one thread, so its fresh MMA is ordered before the
+  // accumulating ones.  At the top of tap s the issuing warps queue tap s + 1, then every
+  // warp drains the group that tap s completes.  Warp 0
   // also streams the weights: tap s + 2 into the ring slot tap s - 1 released.  `next`: the
   // conv whose first taps are prefetched behind this product (-1: none).  Tap ordinals
   // advance by 9 per convolution: tap s sits in ring slot s % 3.
@@ -374,34 +414,43 @@ struct TcConvAdapter {
       for (int e = 0; e < 16; ++e) v[b][e] = 0.f;
     // (warp b < 3) tap s2 of block b: wait for the weights and, for a fresh accumulator, for
     // every warp's drain of its previous partial (two groups ago)
+    // Every issuing warp observes EVERY phase of the weight barriers, and a slot is refilled
+    // only when all six have released it: a warp that skipped a tap could otherwise test a
+    // parity one phase ahead of the barrier, which reads as "complete" (measured: a hang).
     auto issue = [&](int s2) {
       const uint32_t gg = G0 + (uint32_t)(s2 / G);
-      const int slot = (int)(gg & 1u) * 3 + w;
+      OB_WAIT(full(s2 % 3), ((W0 + s2) / 3u) & 1u, 2);
+      if ((int)(gg & 1u) != w / 3) {   // the other warp of this block issues this group
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(wempty(s2 % 3))) : "memory");
+        __syncwarp();
+        return;
+      }
+      tc::fence_after();
+      const int slot = w;              // = parity * 3 + block
       const bool fresh = s2 % G == 0;
       if (fresh && gg >= 2) {
-        tc::bar_wait_warp(acc_empty(slot), ((gg >> 1) - 1) & 1u);
+        OB_WAIT(acc_empty(slot), ((gg >> 1) - 1) & 1u, 1);
         tc::fence_after();
       }
-      tc::bar_wait_warp(full(s2 % 3), ((W0 + s2) / 3u) & 1u);
-      tc::fence_after();
-      issue_unit<TR, TILE>(s2, w, slot, fresh);
+      issue_unit<TR, TILE>(s2, w % 3, slot, fresh);
       if (s2 % G == G - 1) tc::commit(acc_full(slot));
       tc::commit(wempty(s2 % 3));
     };
-    if (w < 3) issue(0);
+    if (w < 6) issue(0);
 #pragma unroll 1
     for (int s = 0; s < 9; ++s) {
       if (w == 0 && s >= 1 && s + 2 < 9) {   // tap s - 1 completed: its ring slot takes tap s + 2
-        tc::bar_wait_warp(wempty((s - 1) % 3), ((W0 + s - 1) / 3u) & 1u);
+        OB_WAIT(wempty((s - 1) % 3), ((W0 + s - 1) / 3u) & 1u, 3);
         load_tap(W0 + s + 2, layer, s + 2);
       }
-      if (w < 3 && s + 1 < 9) issue(s + 1);
+      if (w < 6 && s + 1 < 9) issue(s + 1);
       if (s % G != G - 1) continue;
       const uint32_t gg = G0 + (uint32_t)(s / G);
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
         const int slot = (int)(gg & 1u) * 3 + b;
-        tc::bar_wait_warp(acc_full(slot), (gg >> 1) & 1u);
+        OB_WAIT(acc_full(slot), (gg >> 1) & 1u, 4);
         tc::fence_after();
         if (b < 2 || q == 0) {   // block 2: only rows 0..15 (positions 274..289) are pixels
           float r[16];
@@ -419,7 +468,7 @@ struct TcConvAdapter {
     // every tap's MMAs completed (the last drain saw them); the last three release barriers
     // are consumed here so the phases stay aligned with the tap ordinals
     if (w == 0)
-      for (int j = 6; j < 9; ++j) tc::bar_wait_warp(wempty(j % 3), ((W0 + j) / 3u) & 1u);
+      for (int j = 6; j < 9; ++j) OB_WAIT(wempty(j % 3), ((W0 + j) / 3u) & 1u, 5);
     wuse = W0 + 9;
     pref_layer = next;
     if (w == 0 && next >= 0)
@@ -483,7 +532,7 @@ struct TcConvAdapter {
       }
     };
     auto flush = [&](int j) {   // column group j: taps 2 j (lanes 0..15 of a quarter) and 2 j + 1
-      tc::bar_wait_warp(dw_full(j), par);
+      OB_WAIT(dw_full(j), par, 6);
       tc::fence_after();
       float v[16];
       tc::ld16(((uint32_t)(32 * q) << 16) + conv_tc::kDw + 64u * (uint32_t)j + 16u * cg, v);
@@ -527,7 +576,11 @@ struct TcConvAdapter {
       }
     }
     if (w == 0) flush(4);
+    // the next convolution's accumulators (columns 0..383) overlap these tiles: every
+    // warp's flush must have read them before any warp issues into them
     tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
   }
 
   // ---- convolution epilogues.  Thread rows: position 18 + 128 b + 32 quarter + lane of M
@@ -558,7 +611,7 @@ struct TcConvAdapter {
   // the relu mask is kept for the VJP
   OB_DEV void hidden_tile() {
     float v[3][16];
-    conv<false, 1, conv_tc::kT0>(0, 1, v);
+    conv<false, OB_CONV_GF, conv_tc::kT0>(0, 1, v);
     pt.mark(10);
     const int lane = threadIdx.x & 31, q = (threadIdx.x >> 5) & 3, cg = threadIdx.x >> 7;
     const float sc = inv0 * invw[0];
@@ -587,7 +640,7 @@ struct TcConvAdapter {
     hidden_tile();
     sync_issue();
     float v[3][16];
-    conv<false, 1, conv_tc::kT1>(1, 0, v);
+    conv<false, OB_CONV_GF, conv_tc::kT1>(1, 0, v);
     pt.mark(10);
     const int lane = threadIdx.x & 31, q = (threadIdx.x >> 5) & 3, cg = threadIdx.x >> 7;
     const float sc = inv1 * invw[1];

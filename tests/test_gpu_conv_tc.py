@@ -144,6 +144,22 @@ def test_other_schemes_and_policies(scheme, policy):
     check_du0_with_kinks(make, np_(res.du0), ref["du0"], TOL32, max_over=1)
 
 
+@pytest.mark.timeout(300)
+def test_full_batch_repeated_runs_identical():
+    """Two waves of CTAs (256 images on 148 SMs), eight gradients in a row: identical bits
+    every time.  The tile's six issuing warps, accumulator ring and weight ring synchronise
+    through ~20 mbarriers; a protocol slip shows up here as differing bits or a hang (one
+    did: a warp that skipped a weight phase read the next parity as complete)."""
+    ci = make_config("C3")
+    fld = field_from_config(ci)
+    u0 = torch.as_tensor(ci.u0.reshape(ci.batch, -1), dtype=torch.float32, device="cuda")
+    first = run_config(ci, "store_all", field=fld, u0=u0)
+    for _ in range(7):
+        r = run_config(ci, "store_all", field=fld, u0=u0)
+        assert r.loss == first.loss
+        assert torch.equal(r.dtheta, first.dtheta) and torch.equal(r.du0, first.du0)
+
+
 def test_non_finite_input_raises():
     ci = make_config("C3").subset(2)
     fld = field_from_config(ci)
