@@ -561,21 +561,27 @@ struct TcConvAdapter {
         }
       }
     };
-    // warp 0 issues group j before it flushes group j - 1, so its share of the flush does
-    // not trail the whole product (five warps issuing one group each measured slower: the
-    // groups then finish together and no flush overlaps the MMAs)
+    // Issue-bound like the convolutions: warps 0 and 1 issue alternate column groups (0, 2, 4
+    // and 1, 3), each before it flushes the group two back, so the flushes of a pair overlap
+    // the MMAs of the next pair (five warps issuing one group each measured slower: the
+    // groups then finish together and no flush overlaps the MMAs).
 #pragma unroll 1
     for (int j = 0; j < 5; ++j) {
-      if (w == 0) {
-        issue(2 * j);
-        issue(2 * j + 1);
-        tc::commit(dw_full(j));
-        if (j >= 1) flush(j - 1);
+      if (w < 2) {
+        if ((j & 1) == w) {
+          issue(2 * j);
+          issue(2 * j + 1);
+          tc::commit(dw_full(j));
+        }
+        if (j >= 2) flush(j - 2);
       } else {
         flush(j);
       }
     }
-    if (w == 0) flush(4);
+    if (w < 2) {
+      flush(3);
+      flush(4);
+    }
     // the next convolution's accumulators (columns 0..383) overlap these tiles: every
     // warp's flush must have read them before any warp issues into them
     tc::fence_before();
