@@ -144,7 +144,8 @@ typedef struct {
 /* flags: accumulate per-phase SM cycles of the persistent kernels (profiling aid;
    read with ob_debug_phase_cycles) */
 enum { OB_FLAG_PHASE_TIMING = 1,
-       /* force the SIMT (FMA) MLP tile even where the tcgen05 tensor-core tile applies */
+       /* force the baseline single-CTA SIMT kernels: no tcgen05 tensor-core tiles (MLP, CNF,
+          conv) and no cluster-resident weights for the theta methods */
        OB_FLAG_NO_TENSOR_CORES = 2 };
 #define OB_NPHASES 16
 

@@ -75,6 +75,10 @@ cudaError_t launch_cnf_tc(const RkParams<float>& p, int tiles, int cl, size_t sm
 cudaError_t launch_cnf_tc_field(const RkParams<float>& p, int tiles, int cl, size_t smem, int mode,
                                 double t, const float* u, const float* w, float* out, cudaStream_t st);
 
+// cluster-resident-weights theta kernels (theta_cl_f64.cu)
+void theta_cluster_geom(int N, int H, int R, int RC, int* region_doubles, int* cluster);
+int theta_cluster_max_active(size_t smem);
+cudaError_t launch_theta_cluster(const RkParams<double>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
 // tcgen05 conv tile (conv_tc.cu)
 void tc_conv_sizes(unsigned* packed_bytes, unsigned* smem_bytes);
 cudaError_t launch_pack_tc_conv(const Dims& d, const float* theta, void* img, cudaStream_t st);
@@ -223,6 +227,8 @@ struct Plan {
   bool tc = false;                // tcgen05 tensor-core MLP tile (rk_tc.cu)
   bool tc_cnf = false;            // tcgen05 CNF tile (cnf_tc.cu)
   bool tc_conv = false;           // tcgen05 conv tile (conv_tc.cu)
+  bool theta_cluster = false;     // theta kernels with the weights resident across a cluster
+  int cluster_rows = 0;           // ... rows per cluster the shared-memory layout is sized for
   long long cnf_log_rec = 0;      // tcgen05 CNF tile: bytes of one VJP record of the dW log
   int cnf_cluster = 1;            // tcgen05 CNF tile: CTAs per cluster sharing the weight stream
   int s_stages = 0;               // scheme stages (stage scratch sizing)
@@ -613,6 +619,80 @@ bool plan_tc_cnf(Plan& P, const ob_field_desc& f, long long B, int sm_count) {
   return true;
 }
 
+// Theta methods on fp64 two-layer MLP / stiff fields: clusters of 8 CTAs keep the weights
+// in shared memory (hidden units split across the cluster) instead of streaming them from
+// L2 for every Krylov operator product.  2 rows per CTA (16 per cluster).
+bool theta_cluster_eligible(const ob_problem& p, const Plan& P) {
+  const ob_field_desc& f = p.field;
+  if (!P.theta || P.adaptive || P.esz != 8) return false;
+  if (f.kind != OB_FIELD_MLP && f.kind != OB_FIELD_STIFF) return false;
+  if (f.n_layers != 2 || f.time_input) return false;
+  // act' from the activation value (tanh, identity, relu)
+  if (f.activation != OB_ACT_TANH && f.activation != OB_ACT_IDENTITY && f.activation != OB_ACT_RELU) return false;
+  const int N = f.widths[2], H = f.widths[1];
+  if (N % 4 || N > 128 || H % 64 || H / 8 < 8) return false;
+  if (p.tile_rows != 0 && p.tile_rows != 2) return false;
+  if (p.batch < 16) return false;   // a cluster holds 16 rows: tiny batches keep the single-CTA kernels
+  if ((p.flags & OB_FLAG_NO_TENSOR_CORES) || getenv("OB_NO_THETA_CLUSTER")) return false;
+  return true;
+}
+
+// Geometry: the batch is dealt evenly to ncl clusters and a cluster's rows evenly to its 8
+// CTAs.  16 rows per cluster (2 per CTA) when that many clusters are resident at once;
+// otherwise as many clusters as fit with up to 18 rows each (3 per CTA at most: the
+// shared-memory budget), so the sweep still runs as ONE wave (C5: 256 rows on 15 clusters
+// of 17-18); beyond that, waves of 16-row clusters.
+bool plan_theta_cluster(Plan& P, const ob_field_desc& f, long long B) {
+  auto layout = [&](Plan& Q, int R, int RC) {
+    Q.R = Q.Rt = R;
+    Q.LR = 1;
+    make_dims(f, 1, Q.d);
+    int region = 0, cl = 0;
+    theta_cluster_geom(Q.d.N, f.widths[1], R, RC, &region, &cl);
+    const long long m = Q.gmres_m;
+    Q.krylov_stride = (long long)R * ((m + 1) * Q.d.ldn + (m + 1) * m + 2 * m + (m + 1) + m);
+    SmemLayout& s = Q.sm;
+    s = SmemLayout{};
+    int o = 0;
+    auto take = [&](long long n) { int r = o; o += (int)((n + 1) & ~1LL); return r; };
+    s.x0 = s.tA = s.tB = s.aux = s.scr = s.kry = s.ks = s.ring = s.hscr = -1;
+    s.lamn = s.w = -1;
+    s.ring_elems = s.hscr_elems = s.scr_elems = 0;
+    for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
+    const long long v = (long long)Q.Rt * Q.d.ldn;
+    s.u = take(v);
+    s.lam = take(v);
+    for (int i = 0; i < 8; ++i) s.vec[i] = take(v);
+    s.jtv = s.vec[6];       // the adjoint sweep's product buffer shares the forward's f buffer
+    s.wts = take(region);   // the cluster region (weight slices, exchange buffers)
+    s.total = o;
+    Q.smem_bytes = (size_t)o * 8;
+    Q.smem_reserve = 3072;  // static shared memory of the theta context
+    return Q.smem_bytes <= smem_cap(Q);
+  };
+  Plan Q = P;
+  if (!layout(Q, 2, 16)) return false;
+  const int max_active = theta_cluster_max_active(Q.smem_bytes);
+  if (max_active < 1) return false;
+  long long ncl = (B + 15) / 16;
+  int rc = 16;
+  if (ncl > max_active) {
+    const long long per = (B + max_active - 1) / max_active;   // rows per cluster in one wave
+    Plan Q2 = P;
+    if (per <= 24 && layout(Q2, (int)((per + 7) / 8), (int)per) &&
+        theta_cluster_max_active(Q2.smem_bytes) >= max_active) {
+      Q = Q2;
+      ncl = max_active;
+      rc = (int)per;
+    }
+  }
+  Q.tiles = (int)ncl * 8;
+  Q.cluster_rows = rc;
+  Q.theta_cluster = true;
+  P = Q;
+  return true;
+}
+
 // Tensor-core conv tile: the C3 block on an explicit fixed-step scheme, one image per CTA.
 bool tc_conv_eligible(const ob_field_desc& f, int flags) {
   if (f.kind != OB_FIELD_CONV || f.dtype != OB_F32) return false;
@@ -863,6 +943,7 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   if (allow_tc && tc_eligible(p, P)) plan_tc(P, p.field, p.batch, sms);
   if (allow_tc && !P.adaptive && tc_cnf_eligible(p.field, p.flags)) plan_tc_cnf(P, p.field, p.batch, sms);
   if (allow_tc && !P.adaptive && tc_conv_eligible(p.field, p.flags)) plan_tc_conv(P, p.field, p.batch);
+  if (allow_tc && theta_cluster_eligible(p, P)) plan_theta_cluster(P, p.field, p.batch);
   if (P.smem_bytes > smem_cap(P)) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   if (P.adaptive) {
     P.prog.clear();
@@ -1135,6 +1216,14 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
   CU(cudaEventRecord(ev[1], st));
   auto sweep = [&](bool fwd) -> cudaError_t {
     if (P.adaptive) return launch_adaptive<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
+    if (P.theta_cluster) {
+      if constexpr (sizeof(T) == 8) {
+        RkParams<double> q = reinterpret_cast<const RkParams<double>&>(rp);
+        q.tile_aux = (unsigned)P.cluster_rows;
+        return launch_theta_cluster(q, P.tiles, P.smem_bytes, st, fwd);
+      }
+      return cudaErrorNotSupported;
+    }
     if (P.theta) return launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);
     if (P.tc) {
       if constexpr (sizeof(T) == 4)

@@ -23,7 +23,7 @@ static cudaError_t with_smem_base(K kf, const RkParams<float>& p, RkParams<float
   cudaError_t e = cudaFuncGetAttributes(&at, kf);
   if (e != cudaSuccess) return e;
   q = p;
-  q.tc_smem_base = 1024u + (unsigned)((at.sharedSizeBytes + 127) / 128 * 128);
+  q.tile_aux = 1024u + (unsigned)((at.sharedSizeBytes + 127) / 128 * 128);
   return cudaSuccess;
 }
 

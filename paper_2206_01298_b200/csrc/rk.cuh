@@ -105,10 +105,11 @@ struct RkParams {
   const T* eps;           // Hutchinson probes [B][D]
   T* cnf_pre;             // per tile [L-1][2Rt][lda] pre-activations (forward | raw tangent)
   long long cnf_pre_stride;
-  // tcgen05 conv tile: shared-window address of the kernel's dynamic shared memory (= its
-  // static shared size, set by the launcher).  A kernel-parameter value is uniform, so the
-  // MMA descriptors built from it stay on the uniform datapath.
-  unsigned tc_smem_base;
+  // one launcher-set word for the specialised tiles.  tcgen05 conv tile: the shared-window
+  // address of the kernel's dynamic shared memory (1 KB reserved + its static shared size; a
+  // kernel-parameter value is uniform, so MMA descriptors built from it can stay on the
+  // uniform datapath).  Cluster theta kernels: rows per cluster the layout is sized for.
+  unsigned tile_aux;
 };
 
 template <typename T>

@@ -269,7 +269,7 @@ struct TcConvAdapter {
     tc::fence_after();
     if (threadIdx.x == 0 && p.status && *reinterpret_cast<volatile uint32_t*>(ob_tc_smem + conv_tc::kSlot) != 0u)
       set_status(p.status, OB_ERR_UNSUPPORTED, -2);   // TMEM not at column 0: shared SM
-    if (threadIdx.x == 0 && p.status && tc::smem_u32(ob_tc_smem) != p.tc_smem_base)
+    if (threadIdx.x == 0 && p.status && tc::smem_u32(ob_tc_smem) != p.tile_aux)
       set_status(p.status, OB_ERR_UNSUPPORTED, -(int)tc::smem_u32(ob_tc_smem));   // the launcher's base is wrong: -(actual)
   }
 
@@ -532,19 +532,24 @@ struct TcConvAdapter {
       }
     };
     auto flush = [&](int j) {   // column group j: taps 2 j (lanes 0..15 of a quarter) and 2 j + 1
+      const int s = 2 * j + (lane >> 4);
+      // the mu values are loaded BEFORE the wait: their L2 round trip hides behind the MMAs
+      float4* dst = reinterpret_cast<float4*>(row + (s < 9 ? s : 0) * 68 + 16 * cg);
+      float4 m4[4];
+#ifndef OB_EXP_NO_WFLUSH
+      if (s < 9) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m4[e] = dst[e];
+      }
+#endif
       OB_WAIT(dw_full(j), par, 6);
       tc::fence_after();
       float v[16];
       tc::ld16(((uint32_t)(32 * q) << 16) + conv_tc::kDw + 64u * (uint32_t)j + 16u * cg, v);
-      const int s = 2 * j + (lane >> 4);
 #ifdef OB_EXP_NO_WFLUSH
       return;
 #endif
       if (s < 9) {
-        float4* dst = reinterpret_cast<float4*>(row + s * 68 + 16 * cg);
-        float4 m4[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) m4[e] = dst[e];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           m4[e].x = fmaf(sc, v[4 * e], m4[e].x);

@@ -1,0 +1,685 @@
+// theta_cluster.cuh -- theta-method (Crank-Nicolson / backward Euler) forward and
+// discrete-adjoint kernels for fp64 two-layer MLP / stiff fields with the WEIGHTS RESIDENT
+// ON CHIP across a thread-block cluster (config C5: a*u + s*MLP(u), 128 -> 512 -> 128).
+//
+// The single-CTA theta kernels (theta_impl.cuh) stream the 1 MB of fp64 weights from L2
+// for every Krylov operator product of a 2-row tile: 65 % of the C5 sweep, at 53k cycles
+// per product.  Here a cluster of CL = 8 CTAs splits the HIDDEN units: CTA c keeps rows
+// [c H/8, (c+1) H/8) of W1 and the matching columns of W2 in shared memory (2 x 64 KB)
+// and evaluates its slice for ALL 8 x R rows of the cluster, so a product needs no weight
+// traffic at all:
+//   1. all-gather: every CTA writes its R input rows into every CTA's X (distributed
+//      shared memory stores), cluster barrier;
+//   2. slice products: Z = X W1_c^T, T = act'(.) o Z, partial O = T W2_c^T;
+//   3. reduce-scatter: the partial rows go straight into the owning CTA's receive buffer
+//      [source rank][row], cluster barrier, and the owner sums the eight partials in rank
+//      order (deterministic).
+// Everything per sample -- Newton iterates, GMRES(m) state machines, Arnoldi, Givens --
+// stays with the CTA that owns the row, exactly as in theta_impl.cuh (gmres_tile is shared);
+// the lockstep loops vote across the cluster so that all eight CTAs apply the operator the
+// same number of times.  Parameter cotangents need no exchange: CTA c accumulates dW for its
+// own hidden slice over all 16 rows.
+// Reference: theta_step / newton_solve / gmres (integrators.py:225-244, linalg.py:37-142),
+// theta_adjoint_step (adjoint.py:97-126); same per-sample semantics as theta_impl.cuh.
+#pragma once
+
+#include "theta_impl.cuh"
+
+namespace ob {
+
+namespace thcl {
+constexpr int kCL = 8;   // CTAs per cluster (the portable maximum)
+
+OB_DEV uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+OB_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// address of the same shared-memory location in CTA `rank` of the cluster
+OB_DEV uint32_t remote(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+  return r;
+}
+OB_DEV void st_remote(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+OB_DEV void st_remote(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+}  // namespace thcl
+
+// Geometry of one cluster tile (host and device)
+struct ThclGeom {
+  int N, H, HS, R, RC;      // state dim, hidden, hidden slice, max rows per CTA, max rows per cluster (even)
+  int ld1, ld2;             // leading dims of the W1 slice [HS][ld1] and the W2 slice [N][ld2]
+  // offsets in doubles from the start of the cluster region
+  int w1, w2, b1, b2, x, hs, ts, recv, flags, total;
+};
+__host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC) {
+  ThclGeom g{};
+  g.N = N; g.H = H; g.HS = H / thcl::kCL; g.R = R; g.RC = (RC + 1) & ~1;
+  g.ld1 = N + 2;            // 16-byte loads of 8 consecutive rows tile all 32 banks
+  g.ld2 = g.HS + 2;
+  int o = 0;
+  auto take = [&](int n) { int r = o; o += (n + 1) & ~1; return r; };
+  g.w1 = take(g.HS * g.ld1);
+  g.w2 = take(N * g.ld2);
+  g.b1 = take(g.HS);
+  g.b2 = take(N);
+  g.x = take(g.RC * N);
+  g.hs = take(g.RC * g.HS);
+  g.ts = take(g.RC * g.HS);
+  g.recv = take(thcl::kCL * R * N);
+  g.flags = take(2 * thcl::kCL);   // int pairs inside doubles: 2 x kCL ints fit
+  g.total = o;
+  return g;
+}
+
+// The MLP of the field on the cluster (two affine layers, no time input).
+struct ClusterNet {
+  const RkParams<double>& p;
+  ThclGeom g;
+  double *w1, *w2, *b1, *b2, *X, *Hs, *Ts, *recv;
+  int* flags;
+  uint32_t rank, vpar;
+  // rows of the batch are dealt evenly to the clusters, and a cluster's rows evenly
+  // (contiguous ranges) to its CTAs: nk rows in this cluster, q or q + 1 per CTA
+  int nk, q, e;
+  int row0, Rv;   // this CTA's global rows [row0, row0 + Rv)
+  int off;        // its first row within the cluster
+
+  OB_DEV ClusterNet(const RkParams<double>& p_, double* region)
+      : p(p_), g(thcl_geom(p_.d.N, p_.d.w[1], p_.R, p_.tile_aux)), vpar(0) {
+    w1 = region + g.w1; w2 = region + g.w2; b1 = region + g.b1; b2 = region + g.b2;
+    X = region + g.x; Hs = region + g.hs; Ts = region + g.ts; recv = region + g.recv;
+    flags = reinterpret_cast<int*>(region + g.flags);
+    rank = thcl::cta_rank();
+    {
+      const int ncl = (int)gridDim.x / thcl::kCL, k = (int)blockIdx.x / thcl::kCL;
+      nk = p.B / ncl + (k < p.B % ncl ? 1 : 0);
+      const int base = k * (p.B / ncl) + min(k, p.B % ncl);
+      q = nk / thcl::kCL;
+      e = nk % thcl::kCL;
+      Rv = q + ((int)rank < e ? 1 : 0);
+      off = (int)rank * q + min((int)rank, e);
+      row0 = base + off;
+    }
+    // weight slices from the packed (zero padded) copies: W1 [H][ldw0], W2 [N][ldw1]
+    const double* W1 = p.packed + p.d.pwoff[0];
+    const double* W2 = p.packed + p.d.pwoff[1];
+    const int N = g.N, HS = g.HS, k0 = (int)rank * HS;
+    for (int i = threadIdx.x; i < HS * N; i += blockDim.x) {
+      const int k = i / N, c = i % N;
+      w1[k * g.ld1 + c] = W1[(long long)(k0 + k) * p.d.ldw[0] + c];
+    }
+    for (int i = threadIdx.x; i < N * HS; i += blockDim.x) {
+      const int j = i / HS, k = i % HS;
+      w2[j * g.ld2 + k] = W2[(long long)j * p.d.ldw[1] + k0 + k];
+    }
+    for (int i = threadIdx.x; i < HS; i += blockDim.x) b1[i] = p.W.bias[0][k0 + i];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) b2[i] = p.W.bias[1][i];
+    for (int i = threadIdx.x; i < 2 * thcl::kCL; i += blockDim.x) flags[i] = 0;
+    __syncthreads();
+    thcl::cluster_sync();   // every CTA's buffers exist before anyone writes into them
+  }
+
+  // ---- cluster-wide votes (double-buffered flags: one cluster barrier per vote)
+  OB_DEV int vote_any(int v) {
+    const int loc = __syncthreads_or(v);
+    int* f = flags + thcl::kCL * vpar;
+    if (threadIdx.x < thcl::kCL) thcl::st_remote(thcl::remote(f + rank, threadIdx.x), loc);
+    thcl::cluster_sync();
+    int r = 0;
+#pragma unroll
+    for (int c = 0; c < thcl::kCL; ++c) r |= f[c];
+    vpar ^= 1u;
+    return r;
+  }
+  OB_DEV int vote_all(int v) { return !vote_any(!v); }
+
+  // ---- step 1: this CTA's rows (src [Rv][ld]) -> every CTA's X at the cluster row index.
+  // any_io (nullable): a cluster-wide "any" vote carried on the same barrier.
+  OB_DEV void gather(const double* src, int ld, int, int* any_io = nullptr) {
+    const int N = g.N;
+    int* f = flags + thcl::kCL * vpar;
+    if (any_io) {
+      const int loc = __syncthreads_or(*any_io);
+      if (threadIdx.x < thcl::kCL) thcl::st_remote(thcl::remote(f + rank, threadIdx.x), loc);
+    }
+    for (int i = threadIdx.x; i < Rv * N * thcl::kCL; i += blockDim.x) {
+      const int c = i / (Rv * N), el = i % (Rv * N), r = el / N, j = el % N;
+      thcl::st_remote(thcl::remote(X + (off + r) * N + j, c), src[r * ld + j]);
+    }
+    thcl::cluster_sync();
+    if (any_io) {
+      int r = 0;
+#pragma unroll
+      for (int c = 0; c < thcl::kCL; ++c) r |= f[c];
+      vpar ^= 1u;
+      *any_io = r;
+    }
+  }
+  // ---- step 3: owner side of the reduce-scatter: out[r][j] = sum over ranks (+ bias)
+  OB_DEV void reduce(double* out, int ldo, const double* bias) {
+    thcl::cluster_sync();
+    const int N = g.N, R = g.R;
+    for (int i = threadIdx.x; i < Rv * N; i += blockDim.x) {
+      const int r = i / N, j = i % N;
+      double acc = recv[(0 * R + r) * N + j];
+#pragma unroll
+      for (int c = 1; c < thcl::kCL; ++c) acc = Num<double>::add(acc, recv[(c * R + r) * N + j]);
+      out[r * ldo + j] = bias ? Num<double>::add(acc, bias[j]) : acc;
+    }
+    __syncthreads();
+  }
+  // partial output row r (cluster row index < nk), column j -> the owner's receive buffer
+  OB_DEV void scatter(int r, int j, double v) {
+    if (r >= nk) return;
+    const int big = e * (q + 1);   // rows held by the CTAs with q + 1 rows
+    const int c = r < big ? r / (q + 1) : e + (r - big) / max(q, 1);
+    const int loc = r < big ? r % (q + 1) : (r - big) % max(q, 1);
+    thcl::st_remote(thcl::remote(recv + ((int)rank * g.R + loc) * g.N + j, (uint32_t)c), v);
+  }
+
+  // ---- slice products.  A thread owns 6 rows x 2 columns (24 FMAs per 2 weight + 6 row
+  // loads).  Lanes 0..15 of a warp take 16 column pairs over the first half of the reduction
+  // index, lanes 16..31 the same pairs over the second half; one shuffle joins them
+  // (lo + hi: fixed order).  Measured on C5 (cycles per product, 18 rows): one thread per
+  // 2 outputs 14k; this tile 11k; a 4-way reduction split on all 16 warps 13-20k.
+  // acc[q][c]: row r0 + q, column cp + c * (columns / 2)
+  template <int KH, class Load, class Out>
+  OB_DEV void tile_6x2(int ntask_cols, int RC, Load load_w, const double* In, int ldin, Out out) {
+    const int lane = lane_id(), wq = warp_id();
+    const int groups = (RC + 5) / 6;
+    for (int task = wq; task < groups * ntask_cols; task += n_warps()) {
+      const int cp = 16 * (task % ntask_cols) + (lane & 15), r0 = 6 * (task / ntask_cols);
+      const int h0 = (lane >> 4) * KH;             // this half of the reduction index
+      const double* x = In + r0 * ldin + h0;       // (rows past RC: finite shared memory, discarded)
+      double a[6][2];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) a[q][0] = a[q][1] = 0.0;
+      for (int i = 0; i < KH; i += 2) {
+        const double2 w0 = load_w(cp, 0, h0 + i), w1v = load_w(cp, 1, h0 + i);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const double2 u = *reinterpret_cast<const double2*>(x + q * ldin + i);
+          a[q][0] = Num<double>::fma(w0.x, u.x, a[q][0]);
+          a[q][0] = Num<double>::fma(w0.y, u.y, a[q][0]);
+          a[q][1] = Num<double>::fma(w1v.x, u.x, a[q][1]);
+          a[q][1] = Num<double>::fma(w1v.y, u.y, a[q][1]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double o = __shfl_xor_sync(0xffffffffu, a[q][c], 16);
+          const double sum = (lane >> 4) ? Num<double>::add(o, a[q][c]) : Num<double>::add(a[q][c], o);
+          if (lane < 16 && r0 + q < RC) out(r0 + q, cp, c, sum);
+        }
+    }
+  }
+  // A: Z[r][k] = sum_i In[r][i] W1s[k][i]; columns k = cp, cp + HS / 2
+  template <class Epi>
+  OB_DEV void prod_a(const double* In, Epi epi) {   // In: [RC][N]
+    const int HS = g.HS, ld1 = g.ld1;
+    const double* W = w1;
+    if (g.N == 128)
+      tile_6x2<64>(HS / 32, g.RC,
+                   [&](int cp, int c, int i) { return *reinterpret_cast<const double2*>(W + (cp + c * (HS / 2)) * ld1 + i); },
+                   In, g.N, [&](int r, int cp, int c, double v) { epi(r, cp + c * (HS / 2), v); });
+    else
+      prod_a_generic(In, epi);
+  }
+  template <class Epi>
+  OB_DEV void prod_a_generic(const double* In, Epi epi) {
+    const int N = g.N, HS = g.HS, RC = g.RC;
+    for (int t = threadIdx.x; t < HS * RC; t += blockDim.x) {
+      const int k = t % HS, r = t / HS;
+      double acc = 0.0;
+      for (int i = 0; i < N; ++i) acc = Num<double>::fma(w1[k * g.ld1 + i], In[r * N + i], acc);
+      epi(r, k, acc);
+    }
+  }
+  // B: O[r][j] = sum_k Tin[r][k] W2s[j][k]  (partial over this slice) -> scatter; columns
+  // j = cp, cp + N / 2
+  OB_DEV void prod_b(const double* Tin) {   // Tin: [RC][HS]
+    const int N = g.N, HS = g.HS, RC = g.RC, ld2 = g.ld2;
+    const double* W = w2;
+    if (HS == 64 && N % 32 == 0) {
+      tile_6x2<32>(N / 32, RC,
+                   [&](int cp, int c, int k) { return *reinterpret_cast<const double2*>(W + (cp + c * (N / 2)) * ld2 + k); },
+                   Tin, HS, [&](int r, int cp, int c, double v) { scatter(r, cp + c * (N / 2), v); });
+    } else {
+      for (int t = threadIdx.x; t < N * RC; t += blockDim.x) {
+        const int j = t % N, r = t / N;
+        double acc = 0.0;
+        for (int k = 0; k < HS; ++k) acc = Num<double>::fma(W[j * ld2 + k], Tin[r * HS + k], acc);
+        scatter(r, j, acc);
+      }
+    }
+  }
+  // C: G[r][k] = sum_j V[r][j] W2s[j][k]
+  template <class Epi>
+  OB_DEV void prod_c(const double* V, Epi epi) {   // V: [RC][N]
+    const int N = g.N, HS = g.HS, RC = g.RC;
+    for (int t = threadIdx.x; t < HS * (RC / 2); t += blockDim.x) {
+      const int k = t % HS, r = 2 * (t / HS);
+      const double *v0 = V + r * N, *v1 = v0 + N;
+      double a0 = 0.0, a1 = 0.0;
+      for (int j = 0; j < N; ++j) {
+        const double w = w2[j * g.ld2 + k];
+        a0 = Num<double>::fma(w, v0[j], a0);
+        a1 = Num<double>::fma(w, v1[j], a1);
+      }
+      epi(r, k, a0);
+      epi(r + 1, k, a1);
+    }
+  }
+  // D: O[r][i] = sum_k Tin[r][k] W1s[k][i]  (partial over this slice) -> scatter
+  OB_DEV void prod_d(const double* Tin) {
+    const int N = g.N, HS = g.HS, RC = g.RC;
+    for (int t = threadIdx.x; t < N * ((RC + 3) / 4); t += blockDim.x) {
+      const int i = t % N, r = 4 * (t / N);
+      const double* tr = Tin + r * HS;
+      double a[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < HS; ++k) {
+        const double w = w1[k * g.ld1 + i];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[q] = Num<double>::fma(w, tr[q * HS + k], a[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) scatter(r + q, i, a[q]);
+    }
+  }
+
+  // hidden activations of the rows in `src` (cached for the tangent / cotangent passes);
+  // with out: the MLP value W2 act(W1 x + b1) + b2 for this CTA's rows
+  OB_DEV void forward(const double* src, int ld, int Rv, double* out, int ldo) {
+    gather(src, ld, Rv);
+    const int HS = g.HS, act = p.d.act;
+    double* H = Hs;
+    const double* bb = b1;
+    prod_a(X, [&](int r, int k, double z) { H[r * HS + k] = act_fn(Num<double>::add(z, bb[k]), act); });
+    __syncthreads();
+    if (out) {
+      prod_b(Hs);
+      reduce(out, ldo, b2);
+    } else {
+      thcl::cluster_sync();   // X is rewritten by the next gather of any CTA
+    }
+  }
+  // (dMLP/du) v at the cached linearisation (tanh / identity / relu: act' from the value)
+  OB_DEV void jvp(const double* v, int ld, int Rv, double* out, int ldo, int* any_io = nullptr) {
+    PhaseTimer pt(p.prof ? p.phase : nullptr);
+    gather(v, ld, Rv, any_io);
+    if (any_io && !*any_io) return;   // (cluster-uniform) nobody iterates: no product
+    pt.mark(0);   // all-gather (remote stores + cluster barrier)
+    const int HS = g.HS, act = p.d.act;
+    const double* H = Hs;
+    double* Tt = Ts;
+    prod_a(X, [&](int r, int k, double z) {
+      const double a = H[r * HS + k];
+      Tt[r * HS + k] = Num<double>::mul(z, act_prime_from(a, a, act));
+    });
+    __syncthreads();
+    pt.mark(1);   // first slice product
+    prod_b(Ts);
+    __syncthreads();
+    pt.mark(2);   // second slice product + scatter stores
+    reduce(out, ldo, nullptr);
+    pt.mark(3);   // cluster barrier + owner sum
+  }
+  // (dMLP/du)^T v -> jtv; with mu: mu += scale (dMLP/dtheta)^T v over the valid rows.  xin:
+  // the rows the linearisation was taken at (for dW1), gathered again when mu is given.
+  OB_DEV void vjp(const double* v, int ld, int Rv, double* jtv, int ldo, double* mu, double scale,
+                  const double* xin, int ldx, int* any_io = nullptr) {
+    const int N = g.N, HS = g.HS, act = p.d.act;
+    const double* H = Hs;
+    double* Tt = Ts;
+    gather(v, ld, Rv, any_io);   // X = V (all rows of the cluster)
+    if (any_io && !*any_io) return;
+    prod_c(X, [&](int r, int k, double gk) {
+      const double a = H[r * HS + k];
+      Tt[r * HS + k] = Num<double>::mul(gk, act_prime_from(a, a, act));
+    });
+    __syncthreads();
+    if (mu) {   // dW2 slice, db2 (own rows), db1 slice
+      const int k0 = (int)rank * HS;
+      for (int t = threadIdx.x; t < N * HS; t += blockDim.x) {
+        const int j = t / HS, k = t % HS;
+        double acc = 0.0;
+        for (int r = 0; r < nk; ++r) acc = Num<double>::fma(X[r * N + j], H[r * HS + k], acc);
+        double* m = mu + p.d.mwoff[1] + (long long)j * p.d.ldm[1] + k0 + k;
+        *m = Num<double>::fma(scale, acc, *m);
+      }
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        double acc = 0.0;
+        for (int r = 0; r < Rv; ++r) acc = Num<double>::add(acc, X[(off + r) * N + j]);
+        double* m = mu + p.d.mboff[1] + j;
+        *m = Num<double>::fma(scale, acc, *m);
+      }
+      for (int k = threadIdx.x; k < HS; k += blockDim.x) {
+        double acc = 0.0;
+        for (int r = 0; r < nk; ++r) acc = Num<double>::add(acc, Tt[r * HS + k]);
+        double* m = mu + p.d.mboff[0] + k0 + k;
+        *m = Num<double>::fma(scale, acc, *m);
+      }
+    }
+    prod_d(Ts);
+    reduce(jtv, ldo, nullptr);   // (cluster barrier: X may be overwritten below)
+    if (mu) {   // dW1 slice needs the layer input of every row
+      gather(xin, ldx, Rv);
+      const int k0 = (int)rank * HS;
+      for (int t = threadIdx.x; t < HS * N; t += blockDim.x) {
+        const int k = t / N, i = t % N;
+        double acc = 0.0;
+        for (int r = 0; r < nk; ++r) acc = Num<double>::fma(Tt[r * HS + k], X[r * N + i], acc);
+        double* m = mu + p.d.mwoff[0] + (long long)(k0 + k) * p.d.ldm[0] + i;
+        *m = Num<double>::fma(scale, acc, *m);
+      }
+      __syncthreads();
+      thcl::cluster_sync();   // X is rewritten by the next gather of any CTA
+    }
+  }
+};
+
+struct ClVote {
+  ClusterNet* net;
+  OB_DEV int any(int v) const { return net->vote_any(v); }
+  OB_DEV int all(int v) const { return net->vote_all(v); }
+};
+
+// Operator A v = v - (h theta) J v / J^T v on the cluster (see ThetaOp)
+struct ThclOp {
+  const RkParams<double>& p;
+  ClusterNet& net;
+  double hth;
+  bool transpose;
+  double* tmp;
+  int Rv;
+  template <class Vote>
+  OB_DEV bool apply_any(int any, const double* vin, double* vout, Vote&) {
+    const int N = p.d.N, ldn = p.d.ldn;
+    if (transpose) net.vjp(vin, ldn, Rv, tmp, ldn, nullptr, 0.0, nullptr, 0, &any);
+    else net.jvp(vin, ldn, Rv, tmp, ldn, &any);
+    if (!any) return false;
+    for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
+      const int o = (i / N) * ldn + i % N, j = i % N;
+      double jv = tmp[o];
+      if (p.field_kind == OB_FIELD_STIFF)
+        jv = Num<double>::add(Num<double>::mul(p.diag[j], vin[o]), Num<double>::mul(p.out_scale, jv));
+      vout[o] = Num<double>::add(vin[o], -Num<double>::mul(hth, jv));
+    }
+    __syncthreads();
+    return true;
+  }
+};
+
+// f(x) for this CTA's rows into c.fb (MlpAdapter::eval semantics), linearisation cached
+OB_DEV void thcl_eval(const RkParams<double>& p, ClusterNet& net, ThetaCtx<double>& c, const double* x, int Rv,
+                      bool count_all) {
+  const int N = p.d.N, ldn = p.d.ldn;
+  net.forward(x, ldn, Rv, c.fb, ldn);
+  if (p.field_kind == OB_FIELD_STIFF) {
+    for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
+      const int o = (i / N) * ldn + i % N, j = i % N;
+      c.fb[o] = Num<double>::add(Num<double>::mul(p.diag[j], x[o]), Num<double>::mul(p.out_scale, c.fb[o]));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < Rv && (count_all || c.active[threadIdx.x])) c.cnt[threadIdx.x * OB_NSTATS + OB_STAT_NFE_F] += 1;
+}
+
+OB_DEV void thcl_residual(const RkParams<double>& p, ClusterNet& net, ThetaCtx<double>& c, int Rv, double hth) {
+  const int N = p.d.N, ldn = p.d.ldn;
+  thcl_eval(p, net, c, c.xk, Rv, false);
+  for (int i = threadIdx.x; i < p.Rt * N; i += blockDim.x) {
+    const int o = (i / N) * ldn + i % N;
+    c.rv[o] = Num<double>::add(Num<double>::add(c.xk[o], -c.base[o]), -Num<double>::mul(hth, c.fb[o]));
+  }
+  __syncthreads();
+  if (warp_id() < Rv) {
+    const double nr = sqrt(warp_dot(c.rv + warp_id() * ldn, c.rv + warp_id() * ldn, N));
+    int fin = 1;
+    for (int j = lane_id(); j < N; j += 32) fin &= Num<double>::finite(c.rv[warp_id() * ldn + j]) ? 1 : 0;
+    fin = __all_sync(0xffffffffu, fin);
+    if (lane_id() == 0) c.rn[warp_id()] = fin ? nr : __longlong_as_double(0x7ff8000000000000LL);
+  }
+  __syncthreads();
+}
+
+// theta_step_tile on the cluster: identical per-sample logic, cluster-wide loop votes
+OB_DEV int thcl_step(const RkParams<double>& p, ClusterNet& net, ThetaCtx<double>& c, double* u, double t,
+                     double h, double* rec, int row0, int Rv, double* kry) {
+  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt;
+  const long long vec = (long long)p.B * N;
+  const double th = p.theta;
+  const double hth = h * th, h1 = h * (1.0 - th);
+  for (int r = threadIdx.x; r < Rv; r += blockDim.x) c.active[r] = 1;
+  __syncthreads();
+  thcl_eval(p, net, c, u, Rv, true);
+  for (int i = threadIdx.x; i < Rt * N; i += blockDim.x) {
+    const int o = (i / N) * ldn + i % N;
+    c.base[o] = Num<double>::add(u[o], Num<double>::mul(h1, c.fb[o]));
+    c.xk[o] = u[o];
+    if (rec && i / N < Rv) rec[(long long)(row0 + i / N) * N + i % N] = u[o];
+  }
+  __syncthreads();
+  thcl_residual(p, net, c, Rv, hth);
+  ThclOp op{p, net, hth, false, c.fb, Rv};
+  ClVote vote{&net};
+  for (int it = 0; it < p.newton_maxit; ++it) {
+    int any = 0, bad = 0;
+    if (threadIdx.x < Rv) {
+      const double rn = c.rn[threadIdx.x];
+      const bool act = c.active[threadIdx.x] && !(rn <= p.newton_tol);
+      if (act && !isfinite(rn)) bad = 1;
+      c.active[threadIdx.x] = act ? 1 : 0;
+      any = act ? 1 : 0;
+    }
+    if (net.vote_any(bad)) return OB_ERR_CONVERGENCE;
+    if (!net.vote_any(any)) break;
+    for (int i = threadIdx.x; i < Rt * N; i += blockDim.x) {
+      const int o = (i / N) * ldn + i % N;
+      c.rhs[o] = -c.rv[o];
+    }
+    __syncthreads();
+    if (!gmres_tile<double>(p, op, c, c.rhs, c.gx, Rv, kry, OB_STAT_GMRES_F, OB_STAT_NFE_F, vote))
+      return OB_ERR_CONVERGENCE;
+    for (int i = threadIdx.x; i < Rt * N; i += blockDim.x) {
+      const int r = i / N, o = r * ldn + i % N;
+      if (r < Rv && c.active[r]) c.xk[o] = Num<double>::add(c.xk[o], c.gx[o]);
+    }
+    if (threadIdx.x < Rv && c.active[threadIdx.x]) c.cnt[threadIdx.x * OB_NSTATS + OB_STAT_NEWTON] += 1;
+    __syncthreads();
+    thcl_residual(p, net, c, Rv, hth);
+  }
+  int bad = 0;
+  if (threadIdx.x < Rv && !(c.rn[threadIdx.x] <= p.newton_tol)) bad = 1;
+  if (net.vote_any(bad)) return OB_ERR_CONVERGENCE;
+  for (int i = threadIdx.x; i < Rt * N; i += blockDim.x) {
+    const int r = i / N, o = r * ldn + i % N;
+    u[o] = c.xk[o];
+    if (rec && r < Rv) {
+      const long long gi = (long long)(row0 + r) * N + i % N;
+      rec[vec + gi] = u[o];
+      rec[2 * vec + gi] = u[o];
+    }
+  }
+  __syncthreads();
+  return OB_OK;
+}
+
+// --------------------------------------------------------------- forward
+__global__ void __launch_bounds__(kThreads, 1) thcl_forward_kernel(const __grid_constant__ RkParams<double> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  zero_smem(sm, p.sm.total);
+  const int tile = blockIdx.x;
+  ClusterNet net(p, sm + p.sm.wts);
+  const int row0 = net.row0, Rv = net.Rv;
+  ThetaCtx<double> c = theta_ctx(p, sm);
+  double* u = sm + p.sm.u;
+  double* kry = p.krylov + tile * p.krylov_stride;
+  const int N = p.d.N, ldn = p.d.ldn;
+  const long long vec = (long long)p.B * N;
+  load_rows(u, ldn, p.u0, N, row0, Rv);
+  __syncthreads();
+  int bad = 0;  // as_state (nn.py:31-32)
+  for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x)
+    if (!Num<double>::finite(u[(idx / N) * ldn + idx % N])) bad = 1;
+  if (net.vote_any(bad)) {
+    if (threadIdx.x == 0 && bad) set_status(p.status, OB_ERR_VALUE, -1);
+    thcl::cluster_sync();
+    return;
+  }
+  for (int n = 0; n < p.n_steps; ++n) {
+    const double t = p.ts[n], h = p.ts[n + 1] - p.ts[n];
+    obs_capture(p, u, n, row0, Rv);
+    if (p.fwd_sol[n] >= 0) {
+      store_rows(p.sol + p.fwd_sol[n] * vec, N, u, ldn, row0, Rv);
+      __syncthreads();
+    }
+    double* rec = p.fwd_rec[n] >= 0 ? p.rec + (long long)p.fwd_rec[n] * 3 * vec : nullptr;
+    const int st = thcl_step(p, net, c, u, t, h, rec, row0, Rv, kry);
+    if (st != OB_OK) {   // cluster-uniform (voted)
+      if (threadIdx.x == 0) set_status(p.status, st, n);
+      flush_stats(p, c, row0, Rv);
+      thcl::cluster_sync();
+      return;
+    }
+  }
+  store_rows(p.u_final, N, u, ldn, row0, Rv);
+  obs_capture(p, u, p.n_steps, row0, Rv);
+  flush_stats(p, c, row0, Rv);
+  loss_partial(p, u, row0, Rv, tile);
+  thcl::cluster_sync();   // no CTA leaves while a partner may still write into it
+}
+
+// --------------------------------------------------------------- reverse
+__global__ void __launch_bounds__(kThreads, 1) thcl_reverse_kernel(const __grid_constant__ RkParams<double> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  if (*(volatile int*)p.status != 0) return;   // grid-uniform: the forward finished before
+  zero_smem(sm, p.sm.total);
+  const int tile = blockIdx.x;
+  ClusterNet net(p, sm + p.sm.wts);
+  const int row0 = net.row0, Rv = net.Rv;
+  ThetaCtx<double> c = theta_ctx(p, sm);
+  const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt;
+  const long long vec = (long long)p.B * N;
+  double* u = sm + p.sm.u;
+  double* lam = sm + p.sm.lam;
+  double* jtv = sm + p.sm.jtv;
+  double* kry = p.krylov + tile * p.krylov_stride;
+  double* mu = p.mu + tile * p.d.n_mu;
+  const double th = p.theta;
+  ClVote vote{&net};
+  loss_seed(p, lam, row0, Rv);
+  __syncthreads();
+  for (int pc = 0; pc < p.prog_len; ++pc) {
+    const int4 op = p.prog[pc];
+    const int n = op.y;
+    const double t = p.ts[n], h = p.ts[n + 1] - p.ts[n];
+    if (op.x == kOpReplay) {
+      const int src_kind = op.z >> 24, src = op.z & 0xffffff;
+      const double* srcp = src_kind == kSrcU0 ? p.u0
+                         : src_kind == kSrcSol ? p.sol + src * vec
+                         : p.rec + ((long long)src * 3 + 2) * vec;
+      load_rows(u, ldn, srcp, N, row0, Rv);
+      __syncthreads();
+      double* rec = p.rec + (long long)op.w * 3 * vec;
+      const int st = thcl_step(p, net, c, u, t, h, rec, row0, Rv, kry);
+      if (st != OB_OK) {
+        if (threadIdx.x == 0) set_status(p.status, st, n);
+        flush_stats(p, c, row0, Rv);
+        thcl::cluster_sync();
+        return;
+      }
+      continue;
+    }
+    // theta_adjoint_step (adjoint.py:97-126)
+    obs_inject(p, lam, n + 1, row0, Rv);
+    const double* rec = p.rec + (long long)op.w * 3 * vec;
+    const double hth = h * th, h1 = h * (1.0 - th);
+    for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+      const int r = idx / N, j = idx % N;
+      u[r * ldn + j] = rec[vec + (long long)(row0 + r) * N + j];
+    }
+    __syncthreads();
+    net.forward(u, ldn, Rv, nullptr, 0);   // linearisation at u1
+    for (int r = threadIdx.x; r < Rv; r += blockDim.x) c.active[r] = 1;
+    for (int i = threadIdx.x; i < Rt * ldn; i += blockDim.x) c.rhs[i] = lam[i];
+    __syncthreads();
+    ThclOp aop{p, net, hth, true, jtv, Rv};
+    if (!gmres_tile<double>(p, aop, c, c.rhs, c.gx, Rv, kry, OB_STAT_GMRES_B, OB_STAT_NFE_B, vote)) {
+      if (threadIdx.x == 0) set_status(p.status, OB_ERR_CONVERGENCE, n);
+      flush_stats(p, c, row0, Rv);
+      thcl::cluster_sync();
+      return;
+    }
+    // mu += h theta P(u1)^T lam_s  (one VJP pair at u1)
+    const double sc = p.field_kind == OB_FIELD_STIFF ? p.out_scale : 1.0;
+    net.vjp(c.gx, ldn, Rv, jtv, ldn, mu, hth * sc, u, ldn);
+    if (threadIdx.x < Rv) c.cnt[threadIdx.x * OB_NSTATS + OB_STAT_NFE_B] += 1;
+    if (th < 1.0) {
+      for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x) {
+        const int r = idx / N, j = idx % N;
+        u[r * ldn + j] = rec[(long long)(row0 + r) * N + j];
+      }
+      __syncthreads();
+      net.forward(u, ldn, Rv, nullptr, 0);
+      net.vjp(c.gx, ldn, Rv, jtv, ldn, mu, h1 * sc, u, ldn);
+      if (threadIdx.x < Rv) c.cnt[threadIdx.x * OB_NSTATS + OB_STAT_NFE_B] += 1;
+      for (int i = threadIdx.x; i < Rt * N; i += blockDim.x) {
+        const int o = (i / N) * ldn + i % N, j = i % N;
+        double jv = jtv[o];
+        if (p.field_kind == OB_FIELD_STIFF)
+          jv = Num<double>::add(Num<double>::mul(p.diag[j], c.gx[o]), Num<double>::mul(p.out_scale, jv));
+        lam[o] = Num<double>::add(c.gx[o], Num<double>::mul(h1, jv));
+      }
+    } else {
+      for (int i = threadIdx.x; i < Rt * ldn; i += blockDim.x) lam[i] = c.gx[i];
+    }
+    int bad = 0;
+    for (int i = threadIdx.x; i < Rt * N; i += blockDim.x)
+      if (!Num<double>::finite(lam[(i / N) * ldn + i % N])) bad = 1;
+    if (net.vote_any(bad)) {
+      if (threadIdx.x == 0 && bad) set_status(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
+      flush_stats(p, c, row0, Rv);
+      thcl::cluster_sync();
+      return;
+    }
+  }
+  obs_inject(p, lam, 0, row0, Rv);
+  store_rows(p.du0, N, lam, ldn, row0, Rv);
+  flush_stats(p, c, row0, Rv);
+  thcl::cluster_sync();
+}
+
+// ------------------------------------------------------------ launchers
+template <typename K>
+static cudaError_t thcl_launch(K kf, int grid, size_t smem, cudaStream_t st, const RkParams<double>& p) {
+  cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = thcl::kCL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kf, p);
+}
+
+}  // namespace ob

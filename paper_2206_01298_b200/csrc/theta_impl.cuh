@@ -62,15 +62,27 @@ struct ThetaOp {
     }
     __syncthreads();
   }
+  template <class Vote>
+  OB_DEV bool apply_any(int any, const T* vin, T* vout, Vote& vote) {
+    if (!vote.any(any)) return false;
+    apply(vin, vout);
+    return true;
+  }
+};
+
+// block-wide votes of the lockstep loops (the cluster kernels vote across their CTAs)
+struct CtaVote {
+  OB_DEV int any(int v) const { return __syncthreads_or(v); }
+  OB_DEV int all(int v) const { return __syncthreads_and(v); }
 };
 
 // Batched restarted GMRES(m) on the tile: solves A x_r = rhs_r for every row r
 // with active[r]; inactive rows are left untouched.  cnt_col: stats column to
 // add the Arnoldi steps to; nfe_col: stats column counting operator calls.
 // Returns false if some active sample failed (ConvergenceError).
-template <typename T, class Op>
+template <typename T, class Op, class Vote = CtaVote>
 OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rhs, T* x,
-                       int Rv, T* kry, int cnt_col, int nfe_col) {
+                       int Rv, T* kry, int cnt_col, int nfe_col, Vote vote = Vote()) {
   const int N = p.d.N, ldn = p.d.ldn, Rt = p.Rt;
   const int m = min(p.gmres_restart, N);
   const long long qs = (long long)(m + 1) * ldn, hs = (long long)(m + 1) * m;
@@ -119,9 +131,10 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
       if (ph <= kPhFinal) any = 1;
       c.vin[r * ldn + j] = v;
     }
-    if (!__syncthreads_or(any)) break;
     pt.mark(14);   // operator-input assembly
-    op.apply(c.vin, c.vout);
+    // "is any sample of the (cluster) tile still iterating?" and the operator product: the
+    // cluster operator carries the vote on its all-gather barrier
+    if (!op.apply_any(any, c.vin, c.vout, vote)) break;
     pt.mark(kPhGmres);   // operator products (JVP / transposed VJP)
     if (w < Rv) {
       SampleState S = c.st[w];           // warp-uniform copy, written back by lane 0
@@ -270,7 +283,7 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
     pt.mark(kPhOther);   // per-sample Arnoldi / Givens / update work
   }
   if (w < Rv && lane_id() == 0 && c.active[w]) c.cnt[w * OB_NSTATS + cnt_col] += c.st[w].total;
-  return __syncthreads_and(ok) != 0;
+  return vote.all(ok) != 0;
 }
 
 // field eval at x0 (already loaded) into c.fb, counting one forward evaluation

@@ -107,7 +107,8 @@ def test_c5_full_batch_matches_reference(golden):
     g = golden("c5_full.npz")
     ci = make_config("C5")
     res = run_config(ci, "store_all")
-    assert res.device["tile_rows"] == 2
+    # cluster-resident weights: 15 clusters of 8 CTAs hold 17-18 rows each (up to 3 per CTA)
+    assert res.device["tile_rows"] == 3 and res.device["tiles"] == 120
     e = errs(res, {"u_final": g["u_final"], "du0": g["du0"], "dtheta": g["dtheta"], "loss": g["loss"]})
     assert max(e.values()) <= TOL64, e
     gn = golden("c5_rows_numpy.npz")
