@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1) thcl_forward_kernel(const __grid_
   int bad = 0;  // as_state (nn.py:31-32)
   for (int idx = threadIdx.x; idx < Rv * N; idx += blockDim.x)
     if (!Num<double>::finite(u[(idx / N) * ldn + idx % N])) bad = 1;
+  bad = __syncthreads_or(bad);   // this CTA's rows
   if (net.vote_any(bad)) {
     if (threadIdx.x == 0 && bad) set_status(p.status, OB_ERR_VALUE, -1);
     thcl::cluster_sync();
@@ -649,6 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) thcl_reverse_kernel(const __grid_
     int bad = 0;
     for (int i = threadIdx.x; i < Rt * N; i += blockDim.x)
       if (!Num<double>::finite(lam[(i / N) * ldn + i % N])) bad = 1;
+    bad = __syncthreads_or(bad);
     if (net.vote_any(bad)) {
       if (threadIdx.x == 0 && bad) set_status(p.status, OB_ERR_GRADIENT_EXPLOSION, n);
       flush_stats(p, c, row0, Rv);

@@ -1,0 +1,136 @@
+"""GPU tests of the cluster-resident-weights theta kernels (csrc/theta_cluster.cuh): the
+fp64 weights of a two-layer MLP / stiff field split over the 8 CTAs of a thread-block
+cluster (hidden-unit slices in shared memory, all-gather / reduce-scatter through
+distributed shared memory) against the single-CTA theta kernels (theta_impl.cuh, selected
+with tensor_cores=False, which keeps every specialised tile off) and the oracle.
+
+Same per-sample algorithm (Newton, GMRES(30) with modified Gram-Schmidt, transposed adjoint
+solve); only the operator products are summed in a different order (eight hidden-slice
+partials added in rank order), so values agree to fp64 rounding and iteration counts within
+a few operator calls.
+"""
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import core as oc
+from paper_2206_01298_b200 import IntegrationError
+from paper_2206_01298_b200.configs import make_config
+from paper_2206_01298_b200.workloads import field_from_config, run_config
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2206_01298_b200 import _lib as L
+    L.load()
+
+
+def np_(x):
+    return x.detach().cpu().numpy().astype(np.float64) if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
+@pytest.mark.parametrize("n,tiles,rows", [(16, 8, 2), (37, 24, 2), (250, 120, 3)])
+def test_cluster_kernels_match_single_cta_kernels(n, tiles, rows):
+    """16 rows = one full cluster; 37 = three clusters of 13 / 12 / 12 rows (CTAs with 2 and 1
+    rows); 250 = the one-wave geometry of the C5 bench (15 resident clusters, 16-17 rows
+    each, up to 3 per CTA).  Against the single-CTA kernels on the same inputs."""
+    ci = make_config("C5").subset(n)
+    fld = field_from_config(ci)
+    cl = run_config(ci, "store_all", field=fld)
+    base = run_config(ci, "store_all", field=fld, tensor_cores=False)
+    assert cl.device["tiles"] == tiles and cl.device["tile_rows"] == rows
+    assert base.device["tiles"] * base.device["tile_rows"] >= n and base.device["tiles"] != tiles
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(np_(getattr(cl, k)), np_(getattr(base, k))) <= TOL64, k
+    assert abs(cl.loss - base.loss) <= TOL64 * abs(base.loss)
+    a, b = cl.sample_counters, base.sample_counters
+    for key in ("newton_iters", "steps_accepted"):
+        if key in a:
+            assert list(a[key]) == list(b[key]), key
+    assert np.max(np.abs(np.asarray(a["nfe_forward"]) - np.asarray(b["nfe_forward"]))) <= 8
+    assert np.max(np.abs(np.asarray(a["nfe_backward"]) - np.asarray(b["nfe_backward"]))) <= 8
+
+
+def test_cluster_kernels_match_oracle_and_policies_agree():
+    from oracle.problems import run_oracle
+    ci = make_config("C5").subset(24)
+    fld = field_from_config(ci)
+    res = run_config(ci, "store_all", field=fld)
+    assert res.device["tiles"] == 16
+    ref = run_oracle(ci, "store_all")
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(np_(getattr(res, k)), ref[k]) <= TOL64, k
+    for pol in ("store_solutions", "revolve:4"):
+        other = run_config(ci, pol, field=fld)
+        assert other.device["tiles"] == 16
+        for k in ("u_final", "du0", "dtheta"):
+            assert np.array_equal(np_(getattr(other, k)), np_(getattr(res, k))), (pol, k)
+
+
+def test_backward_euler_and_plain_mlp_field():
+    """theta = 1 (no explicit half step in the adjoint) and a plain MlpField (no stiff
+    diagonal) go through the same cluster kernels."""
+    from paper_2206_01298_b200 import MlpField, MlpModel, MlpSpec
+    from paper_2206_01298_b200.workloads import loss_for
+    from paper_2206_01298_b200 import grad, tableau_catalog, FixedController, CheckpointPolicy, SolverConfig
+    ci = dataclasses.replace(make_config("C5").subset(20), scheme="beuler", n_steps=5)
+    fld = field_from_config(ci)
+    cl = run_config(ci, "store_all", field=fld)
+    base = run_config(ci, "store_all", field=fld, tensor_cores=False)
+    assert cl.device["tiles"] == 16
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(np_(getattr(cl, k)), np_(getattr(base, k))) <= TOL64, k
+    rng = np.random.default_rng(3)
+    spec = MlpSpec((32, 128, 32), "tanh", False, "f64")
+    model = MlpModel(spec, 0.3 * rng.standard_normal(32 * 128 + 128 + 128 * 32 + 32))
+    mf = MlpField(model)
+    u0 = rng.standard_normal((19, 32))
+    from paper_2206_01298_b200.losses import terminal_loss
+    args = (mf, tableau_catalog("cn"), terminal_loss("half_sqnorm", 0.5), u0, 0.0, 0.5, FixedController(4),
+            CheckpointPolicy.parse("store_all"), SolverConfig())
+    a = grad(*args)
+    b = grad(*args, tensor_cores=False)
+    assert a.device["tiles"] == 16 and b.device["tiles"] != 16
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(np_(getattr(a, k)), np_(getattr(b, k))) <= TOL64, k
+
+
+@pytest.mark.timeout(120)
+def test_errors_leave_the_cluster_together():
+    """A non-finite input row and a Newton solve that cannot converge are voted across the
+    cluster: every CTA returns (no CTA is left waiting on a cluster barrier) and the host
+    raises the reference's exceptions."""
+    from paper_2206_01298_b200 import SolverConfig
+    ci = make_config("C5").subset(32)
+    fld = field_from_config(ci)
+    u0 = ci.u0.copy()
+    u0[21, 5] = np.inf
+    with pytest.raises(ValueError):
+        run_config(ci, "store_all", field=fld, u0=u0)
+    ci2 = make_config("C5").subset(32)
+    ci2.extras["solver"] = dict(ci2.extras.get("solver") or {}, newton_maxit=1, gmres_maxit=2, gmres_restart=2)
+    with pytest.raises(IntegrationError):
+        run_config(ci2, "store_all", field=field_from_config(ci2))
+    ok = run_config(ci, "store_all", field=fld)     # the device is fine afterwards
+    assert np.isfinite(ok.loss)
+
+
+@pytest.mark.timeout(300)
+def test_full_batch_repeated_runs_identical():
+    ci = make_config("C5")
+    fld = field_from_config(ci)
+    first = run_config(ci, "store_all", field=fld)
+    assert first.device["tiles"] == 120 and first.device["tile_rows"] == 3
+    again = run_config(ci, "store_all", field=fld)
+    assert again.loss == first.loss
+    for k in ("u_final", "du0", "dtheta"):
+        assert np.array_equal(np_(getattr(again, k)), np_(getattr(first, k))), k
