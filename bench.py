@@ -428,7 +428,11 @@ def measure(name, args, steps, warmup, world, rank, local, flush, policy_arg=Non
     clocks = sampler.stop()
     ms_step = statistics.mean(ms)
     # ---- end-to-end through the public API from pinned host memory (H2D in, results D2H)
-    for _ in range(2):
+    # warm-up: the results come back in pinned staging buffers from torch's caching host
+    # allocator, and two generations of them are alive at once (the previous result is
+    # released after the next call returns); four calls populate the cache, otherwise
+    # cudaHostAlloc (milliseconds per 16 MB) lands in the timed steps
+    for _ in range(4):
         step(u0_host)
     e2e_s = []
     for _ in range(steps):
