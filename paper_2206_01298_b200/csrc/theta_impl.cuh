@@ -173,6 +173,13 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
       } else if (S.phase == kPhCycle) {
         const int k = S.k;
         S.total += 1;
+        // Column k of H, the rotations and (at a cycle end) y are worked on in this row's
+        // slice of the operator-input buffer, which is dead until the next lockstep
+        // iteration: the Krylov workspace lives in global memory (L2: ~800 cycles per
+        // dependent access, and stores do not allocate in L1), and lane 0's serial Givens
+        // chain read its own fresh stores back from there.  Needs 96 doubles per row.
+        const bool fast = ldn >= 96 && m <= 31;
+        T* scr = c.vin + w * ldn;
         // modified Gram-Schmidt (linalg.py:73-75).  The operator output stays in registers
         // (kMgsV elements per lane) and the next basis vector is loaded while the current
         // projection reduces (the basis lives in L2); same operation order as warp_dot.
@@ -198,7 +205,10 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
 #pragma unroll
             for (int e = 0; e < kMgsV; ++e)
               if (lane + 32 * e < N) v[e] = Num<T>::add(v[e], -Num<T>::mul(hik, q[e]));
-            if (lane == 0) H[i * m + k] = hik;
+            if (lane == 0) {
+              if (fast) scr[i] = hik;
+              else H[i * m + k] = hik;
+            }
 #pragma unroll
             for (int e = 0; e < kMgsV; ++e) q[e] = qn[e];
           }
@@ -212,37 +222,80 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
             const T hik = warp_dot(vo, qi, N);
             for (int j = lane; j < N; j += 32) vo[j] = Num<T>::add(vo[j], -Num<T>::mul(hik, qi[j]));
             __syncwarp();
-            if (lane == 0) H[i * m + k] = hik;
+            if (lane == 0) {
+              if (fast) scr[i] = hik;
+              else H[i * m + k] = hik;
+            }
           }
         }
         const T hn = sqrt(warp_dot(vo, vo, N));
-        if (lane == 0) H[(k + 1) * m + k] = hn;
+        if (lane == 0) {
+          if (fast) scr[k + 1] = hn;
+          else H[(k + 1) * m + k] = hn;
+        }
         if (double(hn) > 1e-300) {
           T* qn = Q + (long long)(k + 1) * ldn;
           for (int j = lane; j < N; j += 32) qn[j] = vo[j] / hn;
         } else {
           S.breakdown = 1;                              // linalg.py:79-80
         }
-        if (lane == 0) {
-          // Givens rotations on the fly (linalg.py:81-93)
-          for (int i = 0; i < k; ++i) {
-            const T a = H[i * m + k], bb = H[(i + 1) * m + k];
-            const T top = Num<T>::add(Num<T>::mul(cs[i], a), Num<T>::mul(sn[i], bb));
-            H[(i + 1) * m + k] = Num<T>::add(Num<T>::mul(-sn[i], a), Num<T>::mul(cs[i], bb));
-            H[i * m + k] = top;
+        T gk1;   // g[k + 1] after this step's rotation (every lane)
+        if (fast) {
+          // Givens rotations on the fly (linalg.py:81-93): the k earlier rotations are
+          // fetched by k lanes at once, the chain itself runs on lane 0 out of the scratch
+          if (lane < k) {
+            scr[32 + lane] = cs[lane];
+            scr[64 + lane] = sn[lane];
           }
-          const T hkk = H[k * m + k], hk1 = H[(k + 1) * m + k];
-          const T den = hypot(hkk, hk1);
-          if (den == T(0)) { cs[k] = T(1); sn[k] = T(0); }
-          else { cs[k] = hkk / den; sn[k] = hk1 / den; }
-          H[k * m + k] = Num<T>::add(Num<T>::mul(cs[k], hkk), Num<T>::mul(sn[k], hk1));
-          H[(k + 1) * m + k] = T(0);
-          g[k + 1] = Num<T>::mul(-sn[k], g[k]);
-          g[k] = Num<T>::mul(cs[k], g[k]);
+          T gk = lane == 0 ? g[k] : T(0);
+          __syncwarp();
+          T gn = T(0);
+          if (lane == 0) {
+            for (int i = 0; i < k; ++i) {
+              const T a = scr[i], bb = scr[i + 1], ci = scr[32 + i], si = scr[64 + i];
+              const T top = Num<T>::add(Num<T>::mul(ci, a), Num<T>::mul(si, bb));
+              scr[i + 1] = Num<T>::add(Num<T>::mul(-si, a), Num<T>::mul(ci, bb));
+              scr[i] = top;
+            }
+            const T hkk = scr[k], hk1 = scr[k + 1];
+            const T den = hypot(hkk, hk1);
+            T ck, sk;
+            if (den == T(0)) { ck = T(1); sk = T(0); }
+            else { ck = hkk / den; sk = hk1 / den; }
+            cs[k] = ck;
+            sn[k] = sk;
+            scr[k] = Num<T>::add(Num<T>::mul(ck, hkk), Num<T>::mul(sk, hk1));
+            scr[k + 1] = T(0);
+            gn = Num<T>::mul(-sk, gk);
+            g[k + 1] = gn;
+            g[k] = Num<T>::mul(ck, gk);
+          }
+          gk1 = __shfl_sync(0xffffffffu, gn, 0);
+          __syncwarp();
+          if (lane <= k + 1) H[lane * m + k] = scr[lane];   // column k goes to the workspace once
+        } else {
+          if (lane == 0) {
+            // Givens rotations on the fly (linalg.py:81-93)
+            for (int i = 0; i < k; ++i) {
+              const T a = H[i * m + k], bb = H[(i + 1) * m + k];
+              const T top = Num<T>::add(Num<T>::mul(cs[i], a), Num<T>::mul(sn[i], bb));
+              H[(i + 1) * m + k] = Num<T>::add(Num<T>::mul(-sn[i], a), Num<T>::mul(cs[i], bb));
+              H[i * m + k] = top;
+            }
+            const T hkk = H[k * m + k], hk1 = H[(k + 1) * m + k];
+            const T den = hypot(hkk, hk1);
+            if (den == T(0)) { cs[k] = T(1); sn[k] = T(0); }
+            else { cs[k] = hkk / den; sn[k] = hk1 / den; }
+            H[k * m + k] = Num<T>::add(Num<T>::mul(cs[k], hkk), Num<T>::mul(sn[k], hk1));
+            H[(k + 1) * m + k] = T(0);
+            g[k + 1] = Num<T>::mul(-sn[k], g[k]);
+            g[k] = Num<T>::mul(cs[k], g[k]);
+          }
+          __syncwarp();
+          gk1 = g[k + 1];
         }
-        __syncwarp();
         S.used = k + 1;
-        bool stop = double(fabs(g[k + 1])) <= S.tol || S.breakdown;   // linalg.py:95-96
+        bool stop = double(fabs(gk1)) <= S.tol || S.breakdown;   // linalg.py:95-96
         if (!stop) {
           S.k = k + 1;
           if (S.k == m || S.total >= p.gmres_maxit) stop = true;      // loop end / :69-70
@@ -252,23 +305,44 @@ OB_DEV bool gmres_tile(const RkParams<T>& p, Op& op, ThetaCtx<T>& c, const T* rh
           // LAPACK trsm) and x += Q[:u]^T y (linalg.py:99-106)
           const int u = S.used;
           int singular = 0;
-          if (lane == 0) {
-            for (int i = 0; i < u; ++i) y[i] = g[i];
+          if (fast) {
+            // the same column-oriented substitution with lane i holding y[i]: after y[j] is
+            // formed every y[i], i < j, takes its update at once (the serial loop spent
+            // O(u^2) dependent accesses on the workspace); identical operations per element
+            __syncwarp();   // column k of H written above
+            T yi = lane < u ? g[lane] : T(0);
+            T hnext = (u >= 1 && lane <= u - 1) ? H[lane * m + (u - 1)] : T(0);
             for (int j = u - 1; j >= 0; --j) {
-              const T d = H[j * m + j];
+              const T hcol = hnext;                       // H[lane][j] (lane <= j)
+              if (j >= 1 && lane <= j - 1) hnext = H[lane * m + (j - 1)];
+              const T d = __shfl_sync(0xffffffffu, hcol, j);
               if (d == T(0)) { singular = 1; break; }
-              y[j] = y[j] / d;
-              for (int i = 0; i < j; ++i) y[i] = Num<T>::add(y[i], -Num<T>::mul(y[j], H[i * m + j]));
+              if (lane == j) yi = yi / d;
+              const T yj = __shfl_sync(0xffffffffu, yi, j);
+              if (lane < j) yi = Num<T>::add(yi, -Num<T>::mul(yj, hcol));
             }
+            if (lane < u) scr[lane] = yi;
+            __syncwarp();
+          } else {
+            if (lane == 0) {
+              for (int i = 0; i < u; ++i) y[i] = g[i];
+              for (int j = u - 1; j >= 0; --j) {
+                const T d = H[j * m + j];
+                if (d == T(0)) { singular = 1; break; }
+                y[j] = y[j] / d;
+                for (int i = 0; i < j; ++i) y[i] = Num<T>::add(y[i], -Num<T>::mul(y[j], H[i * m + j]));
+              }
+            }
+            singular = __shfl_sync(0xffffffffu, singular, 0);
+            __syncwarp();
           }
-          singular = __shfl_sync(0xffffffffu, singular, 0);
-          __syncwarp();
           if (singular) {
             S.phase = kPhFail;
           } else {
+            const T* yv = fast ? scr : y;
             for (int j = lane; j < N; j += 32) {
               T acc = T(0);
-              for (int i = 0; i < u; ++i) acc = Num<T>::fma(Q[(long long)i * ldn + j], y[i], acc);
+              for (int i = 0; i < u; ++i) acc = Num<T>::fma(Q[(long long)i * ldn + j], yv[i], acc);
               x[w * ldn + j] = Num<T>::add(x[w * ldn + j], acc);
             }
             S.phase = kPhTop;
