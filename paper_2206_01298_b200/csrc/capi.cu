@@ -79,6 +79,9 @@ cudaError_t launch_cnf_tc_field(const RkParams<float>& p, int tiles, int cl, siz
 void theta_cluster_geom(int N, int H, int R, int RC, int* region_doubles, int* cluster);
 int theta_cluster_max_active(size_t smem);
 cudaError_t launch_theta_cluster(const RkParams<double>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
+// explicit-RK kernels on the cluster MLP (rk_cl_f64.cu)
+int rk_cluster_max_active(size_t smem);
+cudaError_t launch_rk_cluster(const RkParams<double>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
 // tcgen05 conv tile (conv_tc.cu)
 void tc_conv_sizes(unsigned* packed_bytes, unsigned* smem_bytes);
 cudaError_t launch_pack_tc_conv(const Dims& d, const float* theta, void* img, cudaStream_t st);
@@ -228,6 +231,7 @@ struct Plan {
   bool tc_cnf = false;            // tcgen05 CNF tile (cnf_tc.cu)
   bool tc_conv = false;           // tcgen05 conv tile (conv_tc.cu)
   bool theta_cluster = false;     // theta kernels with the weights resident across a cluster
+  bool rk_cluster = false;        // explicit-RK kernels on the cluster MLP (fp64 two-layer MLP fields)
   int cluster_rows = 0;           // ... rows per cluster the shared-memory layout is sized for
   long long cnf_log_rec = 0;      // tcgen05 CNF tile: bytes of one VJP record of the dW log
   int cnf_cluster = 1;            // tcgen05 CNF tile: CTAs per cluster sharing the weight stream
@@ -693,6 +697,66 @@ bool plan_theta_cluster(Plan& P, const ob_field_desc& f, long long B) {
   return true;
 }
 
+// Explicit fixed-step schemes on fp64 two-layer MLP fields without a time input (C1): the
+// generic RK kernels with the cluster MLP adapter -- the weights stay in the shared memory
+// of 8 CTAs (hidden units split), and the batch is sized to ONE wave of resident clusters.
+bool rk_cluster_eligible(const ob_problem& p, const Plan& P) {
+  const ob_field_desc& f = p.field;
+  if (P.theta || P.adaptive || P.esz != 8 || f.kind != OB_FIELD_MLP) return false;
+  if (f.n_layers != 2 || f.time_input) return false;
+  if (f.activation != OB_ACT_TANH && f.activation != OB_ACT_IDENTITY && f.activation != OB_ACT_RELU) return false;
+  const int N = f.widths[2], H = f.widths[1];
+  if (N % 4 || N > 128 || H % 64 || H / 8 < 8) return false;
+  if (p.tile_rows != 0) return false;
+  if (p.batch < 32) return false;
+  if (p.n_obs > 0) return false;   // (observation losses keep the single-CTA tiles)
+  if ((p.flags & OB_FLAG_NO_TENSOR_CORES) || getenv("OB_NO_RK_CLUSTER")) return false;
+  return true;
+}
+
+bool plan_rk_cluster(Plan& P, const ob_field_desc& f, long long B) {
+  auto layout = [&](Plan& Q, int R) {
+    Q.R = Q.Rt = R;
+    Q.LR = 1;
+    make_dims(f, 1, Q.d);
+    int region = 0, cl = 0;
+    theta_cluster_geom(Q.d.N, f.widths[1], R, 8 * R, &region, &cl);
+    SmemLayout& s = Q.sm;
+    s = SmemLayout{};
+    int o = 0;
+    auto take = [&](long long n) { int r = o; o += (int)((n + 1) & ~1LL); return r; };
+    s.tA = s.tB = s.scr = s.kry = s.ring = s.hscr = s.wts = -1;
+    s.ring_elems = s.hscr_elems = s.scr_elems = 0;
+    for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
+    for (int i = 0; i < 8; ++i) s.vec[i] = -1;
+    const long long v = (long long)Q.Rt * Q.d.ldn;
+    s.x0 = take((long long)Q.Rt * Q.d.lda[0]);
+    s.u = take(v);
+    s.lam = take(v);
+    s.lamn = take(v);
+    s.w = take(v);
+    s.jtv = take(v);
+    s.ks = take(2LL * Q.s_stages * v);
+    s.aux = take(region);   // the cluster region (weight slices, exchange buffers)
+    s.total = o;
+    Q.smem_bytes = (size_t)o * 8;
+    return Q.smem_bytes + 1024 <= smem_cap(Q);
+  };
+  Plan Q = P;
+  if (!layout(Q, 2)) return false;
+  const int max_active = rk_cluster_max_active(Q.smem_bytes);
+  if (max_active < 1) return false;
+  // rows per CTA so that the batch is one wave of resident clusters (<= 6: the tiles' row groups)
+  int R = (int)((B + 8LL * max_active - 1) / (8LL * max_active));
+  R = std::max(2, std::min(R, 6));
+  Plan Q2 = P;
+  if (!layout(Q2, R) || rk_cluster_max_active(Q2.smem_bytes) < 1) return false;
+  Q2.tiles = (int)(((B + R - 1) / R + 7) / 8 * 8);
+  Q2.rk_cluster = true;
+  P = Q2;
+  return true;
+}
+
 // Tensor-core conv tile: the C3 block on an explicit fixed-step scheme, one image per CTA.
 bool tc_conv_eligible(const ob_field_desc& f, int flags) {
   if (f.kind != OB_FIELD_CONV || f.dtype != OB_F32) return false;
@@ -944,6 +1008,7 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   if (allow_tc && !P.adaptive && tc_cnf_eligible(p.field, p.flags)) plan_tc_cnf(P, p.field, p.batch, sms);
   if (allow_tc && !P.adaptive && tc_conv_eligible(p.field, p.flags)) plan_tc_conv(P, p.field, p.batch);
   if (allow_tc && theta_cluster_eligible(p, P)) plan_theta_cluster(P, p.field, p.batch);
+  if (allow_tc && rk_cluster_eligible(p, P)) plan_rk_cluster(P, p.field, p.batch);
   if (P.smem_bytes > smem_cap(P)) return fail(OB_ERR_UNSUPPORTED, "layer widths exceed shared memory");
   if (P.adaptive) {
     P.prog.clear();
@@ -1222,6 +1287,11 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
         q.tile_aux = (unsigned)P.cluster_rows;
         return launch_theta_cluster(q, P.tiles, P.smem_bytes, st, fwd);
       }
+      return cudaErrorNotSupported;
+    }
+    if (P.rk_cluster) {
+      if constexpr (sizeof(T) == 8)
+        return launch_rk_cluster(reinterpret_cast<const RkParams<double>&>(rp), P.tiles, P.smem_bytes, st, fwd);
       return cudaErrorNotSupported;
     }
     if (P.theta) return launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);

@@ -1,4 +1,5 @@
 // theta_cl_f64.cu -- cluster-resident-weights theta kernels (theta_cluster.cuh), fp64.
+#define OB_THCL_KERNELS
 #include "theta_cluster.cuh"
 
 namespace ob {

@@ -92,13 +92,21 @@ struct ClusterNet {
   int row0, Rv;   // this CTA's global rows [row0, row0 + Rv)
   int off;        // its first row within the cluster
 
-  OB_DEV ClusterNet(const RkParams<double>& p_, double* region)
-      : p(p_), g(thcl_geom(p_.d.N, p_.d.w[1], p_.R, p_.tile_aux)), vpar(0) {
+  OB_DEV ClusterNet(const RkParams<double>& p_, double* region, bool fixed_rows = false)
+      : p(p_), g(thcl_geom(p_.d.N, p_.d.w[1], p_.R, fixed_rows ? thcl::kCL * p_.R : (int)p_.tile_aux)), vpar(0) {
     w1 = region + g.w1; w2 = region + g.w2; b1 = region + g.b1; b2 = region + g.b2;
     X = region + g.x; Hs = region + g.hs; Ts = region + g.ts; recv = region + g.recv;
     flags = reinterpret_cast<int*>(region + g.flags);
     rank = thcl::cta_rank();
-    {
+    if (fixed_rows) {   // the generic RK kernels' mapping: tile t holds rows [t R, t R + R)
+      const int base = (int)(blockIdx.x - rank) * p.R;
+      nk = max(0, min(thcl::kCL * p.R, p.B - base));
+      q = p.R;
+      e = 0;
+      off = (int)rank * p.R;
+      row0 = base + off;
+      Rv = max(0, min(p.R, p.B - row0));
+    } else {
       const int ncl = (int)gridDim.x / thcl::kCL, k = (int)blockIdx.x / thcl::kCL;
       nk = p.B / ncl + (k < p.B % ncl ? 1 : 0);
       const int base = k * (p.B / ncl) + min(k, p.B % ncl);
@@ -228,12 +236,11 @@ struct ClusterNet {
   OB_DEV void prod_a(const double* In, Epi epi) {   // In: [RC][N]
     const int HS = g.HS, ld1 = g.ld1;
     const double* W = w1;
-    if (g.N == 128)
-      tile_6x2<64>(HS / 32, g.RC,
-                   [&](int cp, int c, int i) { return *reinterpret_cast<const double2*>(W + (cp + c * (HS / 2)) * ld1 + i); },
-                   In, g.N, [&](int r, int cp, int c, double v) { epi(r, cp + c * (HS / 2), v); });
-    else
-      prod_a_generic(In, epi);
+    auto lw = [&](int cp, int c, int i) { return *reinterpret_cast<const double2*>(W + (cp + c * (HS / 2)) * ld1 + i); };
+    auto ow = [&](int r, int cp, int c, double v) { epi(r, cp + c * (HS / 2), v); };
+    if (g.N == 128 && HS % 32 == 0) tile_6x2<64>(HS / 32, g.RC, lw, In, g.N, ow);
+    else if (g.N == 64 && HS % 32 == 0) tile_6x2<32>(HS / 32, g.RC, lw, In, g.N, ow);
+    else prod_a_generic(In, epi);
   }
   template <class Epi>
   OB_DEV void prod_a_generic(const double* In, Epi epi) {
@@ -250,10 +257,12 @@ struct ClusterNet {
   OB_DEV void prod_b(const double* Tin) {   // Tin: [RC][HS]
     const int N = g.N, HS = g.HS, RC = g.RC, ld2 = g.ld2;
     const double* W = w2;
+    auto lw = [&](int cp, int c, int k) { return *reinterpret_cast<const double2*>(W + (cp + c * (N / 2)) * ld2 + k); };
+    auto ow = [&](int r, int cp, int c, double v) { scatter(r, cp + c * (N / 2), v); };
     if (HS == 64 && N % 32 == 0) {
-      tile_6x2<32>(N / 32, RC,
-                   [&](int cp, int c, int k) { return *reinterpret_cast<const double2*>(W + (cp + c * (N / 2)) * ld2 + k); },
-                   Tin, HS, [&](int r, int cp, int c, double v) { scatter(r, cp + c * (N / 2), v); });
+      tile_6x2<32>(N / 32, RC, lw, Tin, HS, ow);
+    } else if (HS == 32 && N % 32 == 0) {
+      tile_6x2<16>(N / 32, RC, lw, Tin, HS, ow);
     } else {
       for (int t = threadIdx.x; t < N * RC; t += blockDim.x) {
         const int j = t % N, r = t / N;
@@ -263,37 +272,66 @@ struct ClusterNet {
       }
     }
   }
+  // the same 6 x 2 tile for the transposed products: the reduction index runs over the ROWS
+  // of the weight slice (columns contiguous: 8-byte loads, lanes on consecutive columns)
+  template <int KH, class Out>
+  OB_DEV void tile_6x2t(int ntask_cols, int RC, const double* Wm, int ldw, int cstride, const double* In, int ldin,
+                        Out out) {
+    const int lane = lane_id(), wq = warp_id();
+    const int groups = (RC + 5) / 6;
+    for (int task = wq; task < groups * ntask_cols; task += n_warps()) {
+      const int cp = 16 * (task % ntask_cols) + (lane & 15), r0 = 6 * (task / ntask_cols);
+      const int h0 = (lane >> 4) * KH;
+      const double* wc = Wm + h0 * ldw + cp;
+      const double* x = In + r0 * ldin + h0;
+      double a[6][2];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) a[q][0] = a[q][1] = 0.0;
+#pragma unroll 4
+      for (int i = 0; i < KH; ++i) {
+        const double w0 = wc[i * ldw], w1v = wc[i * ldw + cstride];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const double u = x[q * ldin + i];
+          a[q][0] = Num<double>::fma(w0, u, a[q][0]);
+          a[q][1] = Num<double>::fma(w1v, u, a[q][1]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double o = __shfl_xor_sync(0xffffffffu, a[q][c], 16);
+          const double sum = (lane >> 4) ? Num<double>::add(o, a[q][c]) : Num<double>::add(a[q][c], o);
+          if (lane < 16 && r0 + q < RC) out(r0 + q, cp, c, sum);
+        }
+    }
+  }
   // C: G[r][k] = sum_j V[r][j] W2s[j][k]
   template <class Epi>
   OB_DEV void prod_c(const double* V, Epi epi) {   // V: [RC][N]
     const int N = g.N, HS = g.HS, RC = g.RC;
-    for (int t = threadIdx.x; t < HS * (RC / 2); t += blockDim.x) {
-      const int k = t % HS, r = 2 * (t / HS);
-      const double *v0 = V + r * N, *v1 = v0 + N;
-      double a0 = 0.0, a1 = 0.0;
-      for (int j = 0; j < N; ++j) {
-        const double w = w2[j * g.ld2 + k];
-        a0 = Num<double>::fma(w, v0[j], a0);
-        a1 = Num<double>::fma(w, v1[j], a1);
-      }
-      epi(r, k, a0);
-      epi(r + 1, k, a1);
+    auto ow = [&](int r, int cp, int c, double v) { epi(r, cp + c * (HS / 2), v); };
+    if (N == 128 && HS % 32 == 0) { tile_6x2t<64>(HS / 32, RC, w2, g.ld2, HS / 2, V, N, ow); return; }
+    if (N == 64 && HS % 32 == 0) { tile_6x2t<32>(HS / 32, RC, w2, g.ld2, HS / 2, V, N, ow); return; }
+    for (int t = threadIdx.x; t < HS * RC; t += blockDim.x) {
+      const int k = t % HS, r = t / HS;
+      double acc = 0.0;
+      for (int j = 0; j < N; ++j) acc = Num<double>::fma(w2[j * g.ld2 + k], V[r * N + j], acc);
+      epi(r, k, acc);
     }
   }
   // D: O[r][i] = sum_k Tin[r][k] W1s[k][i]  (partial over this slice) -> scatter
   OB_DEV void prod_d(const double* Tin) {
     const int N = g.N, HS = g.HS, RC = g.RC;
-    for (int t = threadIdx.x; t < N * ((RC + 3) / 4); t += blockDim.x) {
-      const int i = t % N, r = 4 * (t / N);
-      const double* tr = Tin + r * HS;
-      double a[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int k = 0; k < HS; ++k) {
-        const double w = w1[k * g.ld1 + i];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) a[q] = Num<double>::fma(w, tr[q * HS + k], a[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) scatter(r + q, i, a[q]);
+    auto ow = [&](int r, int cp, int c, double v) { scatter(r, cp + c * (N / 2), v); };
+    if (HS == 64 && N % 32 == 0) { tile_6x2t<32>(N / 32, RC, w1, g.ld1, N / 2, Tin, HS, ow); return; }
+    if (HS == 32 && N % 32 == 0) { tile_6x2t<16>(N / 32, RC, w1, g.ld1, N / 2, Tin, HS, ow); return; }
+    for (int t = threadIdx.x; t < N * RC; t += blockDim.x) {
+      const int i = t % N, r = t / N;
+      double acc = 0.0;
+      for (int k = 0; k < HS; ++k) acc = Num<double>::fma(w1[k * g.ld1 + i], Tin[r * HS + k], acc);
+      scatter(r, i, acc);
     }
   }
 
@@ -385,6 +423,35 @@ struct ClusterNet {
       __syncthreads();
       thcl::cluster_sync();   // X is rewritten by the next gather of any CTA
     }
+  }
+};
+
+// Field adapter of the generic explicit-RK kernels (rk_impl.cuh) over the cluster MLP:
+// fp64 two-layer MlpField without a time input (config C1).  Tiles keep the generic row
+// mapping (tile t = rows [t R, t R + R)); eval / vjp are the cluster products.
+struct ClusterMlpAdapter {
+  static constexpr bool kHasJvp = false;
+  static constexpr bool kScaledVjp = false;   // vjp returns J^T w; mu += h P^T w
+  static constexpr int kCombineBatch = 4;
+  static constexpr bool kOwnsStep = false;
+  static constexpr bool kNoEarlyExit = true;  // the cluster applies its products together
+  const RkParams<double>& p;
+  ClusterNet net;
+  double* xin;   // field input rows [Rt][lda0]
+  OB_DEV ClusterMlpAdapter(const RkParams<double>& p_, const Weights<double>&, MlpSmem<double>& ms, double* sm, int, int)
+      : p(p_), net(p_, sm + p_.sm.aux, true), xin(ms.x0) {}
+  OB_DEV double* x0() { return xin; }
+  OB_DEV int nin() const { return p.d.N; }
+  OB_DEV void put(int r, int j, double v) { xin[r * p.d.lda[0] + j] = v; }
+  OB_DEV void put_time(double) {}
+  OB_DEV void set_scratch(double*, int) {}
+  OB_DEV void jvp(const double*, double*) {}
+  OB_DEV void finish(double*) {}
+  OB_DEV void release() { thcl::cluster_sync(); }   // no CTA leaves while a partner may still write into it
+  OB_DEV void eval(double* out) { net.forward(xin, p.d.lda[0], net.Rv, out, p.d.ldn); }
+  OB_DEV void vjp(const double* w, double* jtv, double* mu, double h, int) {
+    net.forward(xin, p.d.lda[0], net.Rv, nullptr, 0);   // hidden activations at the stage state
+    net.vjp(w, p.d.ldn, net.Rv, jtv, p.d.ldn, mu, h, xin, p.d.lda[0]);
   }
 };
 
@@ -515,6 +582,7 @@ OB_DEV int thcl_step(const RkParams<double>& p, ClusterNet& net, ThetaCtx<double
   return OB_OK;
 }
 
+#ifdef OB_THCL_KERNELS   // the theta kernels are emitted by theta_cl_f64.cu only
 // --------------------------------------------------------------- forward
 __global__ void __launch_bounds__(kThreads, 1) thcl_forward_kernel(const __grid_constant__ RkParams<double> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -663,6 +731,8 @@ __global__ void __launch_bounds__(kThreads, 1) thcl_reverse_kernel(const __grid_
   flush_stats(p, c, row0, Rv);
   thcl::cluster_sync();
 }
+
+#endif  // OB_THCL_KERNELS
 
 // ------------------------------------------------------------ launchers
 template <typename K>

@@ -134,3 +134,39 @@ def test_full_batch_repeated_runs_identical():
     assert again.loss == first.loss
     for k in ("u_final", "du0", "dtheta"):
         assert np.array_equal(np_(getattr(again, k)), np_(getattr(first, k))), k
+
+
+# ------------------------------------------------------------------ explicit RK on the cluster MLP
+@pytest.mark.parametrize("scheme,policy", [("rk4", "store_all"), ("dopri5", "revolve:3"), ("midpoint", "store_solutions")])
+def test_explicit_rk_on_cluster_matches_single_cta_kernels(scheme, policy):
+    """C1's field (fp64 64-256-64 tanh MLP, no time input) on explicit schemes: the generic RK
+    kernels with the cluster MLP adapter (weights resident across 8 CTAs, rows per CTA sized
+    to one wave of resident clusters) against the single-CTA SIMT tile and the oracle."""
+    ci = dataclasses.replace(make_config("C1"), scheme=scheme, n_steps=6)
+    fld = field_from_config(ci)
+    cl = run_config(ci, policy, field=fld)
+    base = run_config(ci, policy, field=fld, tensor_cores=False)
+    assert cl.device["tiles"] == 104 and cl.device["tile_rows"] == 5     # 13 clusters x 8 CTAs x 5 rows
+    assert base.device["tile_rows"] == 4 and base.device["tiles"] == 128
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(np_(getattr(cl, k)), np_(getattr(base, k))) <= 1e-12, k
+    assert abs(cl.loss - base.loss) <= 1e-12 * abs(base.loss)
+    assert cl.counters.nfe_forward == base.counters.nfe_forward
+    mlp = oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input)
+    ref = oc.grad_terminal(oc.MlpField(mlp), ci.scheme, ci.u0, ci.t0, ci.tF, ci.n_steps, "store_all")
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(np_(getattr(cl, k)), ref[k]) <= TOL64, k
+
+
+def test_explicit_rk_cluster_ragged_batch_and_bits():
+    """A batch that leaves the last cluster partly empty (padding tiles), twice: identical bits."""
+    ci = make_config("C1").subset(77)
+    fld = field_from_config(ci)
+    a = run_config(ci, "store_all", field=fld)
+    b = run_config(ci, "store_all", field=fld)
+    base = run_config(ci, "store_all", field=fld, tensor_cores=False)
+    assert a.device["tiles"] % 8 == 0 and a.device["tiles"] * a.device["tile_rows"] >= 77
+    assert a.loss == b.loss
+    for k in ("u_final", "du0", "dtheta"):
+        assert np.array_equal(np_(getattr(a, k)), np_(getattr(b, k))), k
+        assert oc.rel_error(np_(getattr(a, k)), np_(getattr(base, k))) <= 1e-12, k
