@@ -634,7 +634,8 @@ bool theta_cluster_eligible(const ob_problem& p, const Plan& P) {
   // act' from the activation value (tanh, identity, relu)
   if (f.activation != OB_ACT_TANH && f.activation != OB_ACT_IDENTITY && f.activation != OB_ACT_RELU) return false;
   const int N = f.widths[2], H = f.widths[1];
-  if (N % 4 || N > 128 || H % 64 || H / 8 < 8) return false;
+  // fp64 MMA tiles over swizzled rows: state dim and hidden slice multiples of 16, >= 32
+  if (N % 16 || N < 32 || N > 128 || H % 128 || H < 256) return false;
   if (p.tile_rows != 0 && p.tile_rows != 2) return false;
   if (p.batch < 16) return false;   // a cluster holds 16 rows: tiny batches keep the single-CTA kernels
   if ((p.flags & OB_FLAG_NO_TENSOR_CORES) || getenv("OB_NO_THETA_CLUSTER")) return false;
@@ -706,7 +707,8 @@ bool rk_cluster_eligible(const ob_problem& p, const Plan& P) {
   if (f.n_layers != 2 || f.time_input) return false;
   if (f.activation != OB_ACT_TANH && f.activation != OB_ACT_IDENTITY && f.activation != OB_ACT_RELU) return false;
   const int N = f.widths[2], H = f.widths[1];
-  if (N % 4 || N > 128 || H % 64 || H / 8 < 8) return false;
+  // fp64 MMA tiles over swizzled rows: state dim and hidden slice multiples of 16, >= 32
+  if (N % 16 || N < 32 || N > 128 || H % 128 || H < 256) return false;
   if (p.tile_rows != 0) return false;
   if (p.batch < 32) return false;
   if (p.n_obs > 0) return false;   // (observation losses keep the single-CTA tiles)

@@ -50,6 +50,17 @@ OB_DEV void st_remote(uint32_t addr, double v) {
 OB_DEV void st_remote(uint32_t addr, int v) {
   asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+// Element (row, col) of a row-major [rows][ld] fp64 array whose 32-byte chunks are XOR-swizzled
+// with the row (ld / 4 >= 8 chunks): the 8 x 4 and 4 x 8 operand fragments of the fp64 MMA then
+// touch every bank once, with no padding.
+OB_DEV int sw(int row, int col, int ld) { return row * ld + ((((col >> 2) ^ (row & 7)) << 2) | (col & 3)); }
+// fp64 tensor-core MMA, D (8 x 8) += A (8 x 4, row) B (4 x 8, col): lane l holds A[l/4][l%4],
+// B[l%4][l/4] and D[l/4][2 (l%4) .. + 1]
+OB_DEV void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 }  // namespace thcl
 
 // Geometry of one cluster tile (host and device)
@@ -62,8 +73,8 @@ struct ThclGeom {
 __host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC) {
   ThclGeom g{};
   g.N = N; g.H = H; g.HS = H / thcl::kCL; g.R = R; g.RC = (RC + 1) & ~1;
-  g.ld1 = N + 2;            // 16-byte loads of 8 consecutive rows tile all 32 banks
-  g.ld2 = g.HS + 2;
+  g.ld1 = N;                // rows are XOR-swizzled in 32-byte chunks (thcl::sw), not padded
+  g.ld2 = g.HS;
   int o = 0;
   auto take = [&](int n) { int r = o; o += (n + 1) & ~1; return r; };
   g.w1 = take(g.HS * g.ld1);
@@ -122,11 +133,11 @@ struct ClusterNet {
     const int N = g.N, HS = g.HS, k0 = (int)rank * HS;
     for (int i = threadIdx.x; i < HS * N; i += blockDim.x) {
       const int k = i / N, c = i % N;
-      w1[k * g.ld1 + c] = W1[(long long)(k0 + k) * p.d.ldw[0] + c];
+      w1[thcl::sw(k, c, N)] = W1[(long long)(k0 + k) * p.d.ldw[0] + c];
     }
     for (int i = threadIdx.x; i < N * HS; i += blockDim.x) {
       const int j = i / HS, k = i % HS;
-      w2[j * g.ld2 + k] = W2[(long long)j * p.d.ldw[1] + k0 + k];
+      w2[thcl::sw(j, k, HS)] = W2[(long long)j * p.d.ldw[1] + k0 + k];
     }
     for (int i = threadIdx.x; i < HS; i += blockDim.x) b1[i] = p.W.bias[0][k0 + i];
     for (int i = threadIdx.x; i < N; i += blockDim.x) b2[i] = p.W.bias[1][i];
@@ -160,7 +171,7 @@ struct ClusterNet {
     }
     for (int i = threadIdx.x; i < Rv * N * thcl::kCL; i += blockDim.x) {
       const int c = i / (Rv * N), el = i % (Rv * N), r = el / N, j = el % N;
-      thcl::st_remote(thcl::remote(X + (off + r) * N + j, c), src[r * ld + j]);
+      thcl::st_remote(thcl::remote(X + thcl::sw(off + r, j, N), c), src[r * ld + j]);
     }
     thcl::cluster_sync();
     if (any_io) {
@@ -193,146 +204,99 @@ struct ClusterNet {
     thcl::st_remote(thcl::remote(recv + ((int)rank * g.R + loc) * g.N + j, (uint32_t)c), v);
   }
 
-  // ---- slice products.  A thread owns 6 rows x 2 columns (24 FMAs per 2 weight + 6 row
-  // loads).  Lanes 0..15 of a warp take 16 column pairs over the first half of the reduction
-  // index, lanes 16..31 the same pairs over the second half; one shuffle joins them
-  // (lo + hi: fixed order).  Measured on C5 (cycles per product, 18 rows): one thread per
-  // 2 outputs 14k; this tile 11k; a 4-way reduction split on all 16 warps 13-20k.
-  // acc[q][c]: row r0 + q, column cp + c * (columns / 2)
-  template <int KH, class Load, class Out>
-  OB_DEV void tile_6x2(int ntask_cols, int RC, Load load_w, const double* In, int ldin, Out out) {
-    const int lane = lane_id(), wq = warp_id();
-    const int groups = (RC + 5) / 6;
-    for (int task = wq; task < groups * ntask_cols; task += n_warps()) {
-      const int cp = 16 * (task % ntask_cols) + (lane & 15), r0 = 6 * (task / ntask_cols);
-      const int h0 = (lane >> 4) * KH;             // this half of the reduction index
-      const double* x = In + r0 * ldin + h0;       // (rows past RC: finite shared memory, discarded)
-      double a[6][2];
+  // ---- slice products on the fp64 tensor cores (mma.sync m8n8k4).  With FMAs on the vector
+  // pipe the products ran at a fifth of its rate (10.7k cycles for 147 k FMAs): every FMA
+  // needs a shared-memory operand, and a warp-wide broadcast operand costs as many wavefronts
+  // as a distinct one.  An MMA takes 32 + 32 distinct operand values for 256 FMAs, and the A
+  // fragment is reused across the N tiles of a task.  (The pipes' rates are equal: 64
+  // FMA/clk/SM for DMMA, tools/dmma_probe.cu.)
+  // D[r][n] = sum_k A[r][k] Bm[n][k]   (A: [rows][KD], Bm: [ncols][KD], both swizzled).
+  // Task = (group of MTG row tiles, pair of column tiles), one per warp.
+  template <int MTG, class Out>
+  OB_DEV void mma_nt(const double* A, int RC, const double* Bm, int ncols, int KD, Out out) {
+    const int lane = lane_id(), lr = lane >> 2, lc = lane & 3;
+    const int MT = (RC + 7) / 8, mgroups = (MT + MTG - 1) / MTG, npairs = ncols / 16;
+    for (int task = warp_id(); task < mgroups * npairs; task += n_warps()) {
+      const int np = task % npairs, mg = task / npairs;
+      double c[MTG][2][2];
 #pragma unroll
-      for (int q = 0; q < 6; ++q) a[q][0] = a[q][1] = 0.0;
-      for (int i = 0; i < KH; i += 2) {
-        const double2 w0 = load_w(cp, 0, h0 + i), w1v = load_w(cp, 1, h0 + i);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const double2 u = *reinterpret_cast<const double2*>(x + q * ldin + i);
-          a[q][0] = Num<double>::fma(w0.x, u.x, a[q][0]);
-          a[q][0] = Num<double>::fma(w0.y, u.y, a[q][0]);
-          a[q][1] = Num<double>::fma(w1v.x, u.x, a[q][1]);
-          a[q][1] = Num<double>::fma(w1v.y, u.y, a[q][1]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 6; ++q)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const double o = __shfl_xor_sync(0xffffffffu, a[q][c], 16);
-          const double sum = (lane >> 4) ? Num<double>::add(o, a[q][c]) : Num<double>::add(a[q][c], o);
-          if (lane < 16 && r0 + q < RC) out(r0 + q, cp, c, sum);
-        }
-    }
-  }
-  // A: Z[r][k] = sum_i In[r][i] W1s[k][i]; columns k = cp, cp + HS / 2
-  template <class Epi>
-  OB_DEV void prod_a(const double* In, Epi epi) {   // In: [RC][N]
-    const int HS = g.HS, ld1 = g.ld1;
-    const double* W = w1;
-    auto lw = [&](int cp, int c, int i) { return *reinterpret_cast<const double2*>(W + (cp + c * (HS / 2)) * ld1 + i); };
-    auto ow = [&](int r, int cp, int c, double v) { epi(r, cp + c * (HS / 2), v); };
-    if (g.N == 128 && HS % 32 == 0) tile_6x2<64>(HS / 32, g.RC, lw, In, g.N, ow);
-    else if (g.N == 64 && HS % 32 == 0) tile_6x2<32>(HS / 32, g.RC, lw, In, g.N, ow);
-    else prod_a_generic(In, epi);
-  }
-  template <class Epi>
-  OB_DEV void prod_a_generic(const double* In, Epi epi) {
-    const int N = g.N, HS = g.HS, RC = g.RC;
-    for (int t = threadIdx.x; t < HS * RC; t += blockDim.x) {
-      const int k = t % HS, r = t / HS;
-      double acc = 0.0;
-      for (int i = 0; i < N; ++i) acc = Num<double>::fma(w1[k * g.ld1 + i], In[r * N + i], acc);
-      epi(r, k, acc);
-    }
-  }
-  // B: O[r][j] = sum_k Tin[r][k] W2s[j][k]  (partial over this slice) -> scatter; columns
-  // j = cp, cp + N / 2
-  OB_DEV void prod_b(const double* Tin) {   // Tin: [RC][HS]
-    const int N = g.N, HS = g.HS, RC = g.RC, ld2 = g.ld2;
-    const double* W = w2;
-    auto lw = [&](int cp, int c, int k) { return *reinterpret_cast<const double2*>(W + (cp + c * (N / 2)) * ld2 + k); };
-    auto ow = [&](int r, int cp, int c, double v) { scatter(r, cp + c * (N / 2), v); };
-    if (HS == 64 && N % 32 == 0) {
-      tile_6x2<32>(N / 32, RC, lw, Tin, HS, ow);
-    } else if (HS == 32 && N % 32 == 0) {
-      tile_6x2<16>(N / 32, RC, lw, Tin, HS, ow);
-    } else {
-      for (int t = threadIdx.x; t < N * RC; t += blockDim.x) {
-        const int j = t % N, r = t / N;
-        double acc = 0.0;
-        for (int k = 0; k < HS; ++k) acc = Num<double>::fma(W[j * ld2 + k], Tin[r * HS + k], acc);
-        scatter(r, j, acc);
-      }
-    }
-  }
-  // the same 6 x 2 tile for the transposed products: the reduction index runs over the ROWS
-  // of the weight slice (columns contiguous: 8-byte loads, lanes on consecutive columns)
-  template <int KH, class Out>
-  OB_DEV void tile_6x2t(int ntask_cols, int RC, const double* Wm, int ldw, int cstride, const double* In, int ldin,
-                        Out out) {
-    const int lane = lane_id(), wq = warp_id();
-    const int groups = (RC + 5) / 6;
-    for (int task = wq; task < groups * ntask_cols; task += n_warps()) {
-      const int cp = 16 * (task % ntask_cols) + (lane & 15), r0 = 6 * (task / ntask_cols);
-      const int h0 = (lane >> 4) * KH;
-      const double* wc = Wm + h0 * ldw + cp;
-      const double* x = In + r0 * ldin + h0;
-      double a[6][2];
-#pragma unroll
-      for (int q = 0; q < 6; ++q) a[q][0] = a[q][1] = 0.0;
+      for (int m = 0; m < MTG; ++m) c[m][0][0] = c[m][0][1] = c[m][1][0] = c[m][1][1] = 0.0;
+      const int n0 = 16 * np + lr, n1 = n0 + 8;
 #pragma unroll 4
-      for (int i = 0; i < KH; ++i) {
-        const double w0 = wc[i * ldw], w1v = wc[i * ldw + cstride];
+      for (int ks = 0; ks < KD / 4; ++ks) {
+        const double b0 = Bm[n0 * KD + (((ks ^ (n0 & 7)) << 2) | lc)];
+        const double b1 = Bm[n1 * KD + (((ks ^ (n1 & 7)) << 2) | lc)];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const double u = x[q * ldin + i];
-          a[q][0] = Num<double>::fma(w0, u, a[q][0]);
-          a[q][1] = Num<double>::fma(w1v, u, a[q][1]);
+        for (int m = 0; m < MTG; ++m) {
+          const int r = 8 * (mg * MTG + m) + lr;   // (rows past RC: finite shared memory, discarded)
+          const double a = A[r * KD + (((ks ^ (r & 7)) << 2) | lc)];
+          thcl::dmma(c[m][0][0], c[m][0][1], a, b0);
+          thcl::dmma(c[m][1][0], c[m][1][1], a, b1);
         }
       }
 #pragma unroll
-      for (int q = 0; q < 6; ++q)
+      for (int m = 0; m < MTG; ++m) {
+        const int r = 8 * (mg * MTG + m) + lr;
+        if (r < RC) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const double o = __shfl_xor_sync(0xffffffffu, a[q][c], 16);
-          const double sum = (lane >> 4) ? Num<double>::add(o, a[q][c]) : Num<double>::add(a[q][c], o);
-          if (lane < 16 && r0 + q < RC) out(r0 + q, cp, c, sum);
+          for (int t = 0; t < 2; ++t) {
+            out(r, 16 * np + 8 * t + 2 * lc, c[m][t][0]);
+            out(r, 16 * np + 8 * t + 2 * lc + 1, c[m][t][1]);
+          }
         }
+      }
     }
+  }
+  // D[r][n] = sum_k A[r][k] Bt[k][n]   (Bt: [KD][ncols], swizzled by its rows k)
+  template <int MTG, class Out>
+  OB_DEV void mma_tn(const double* A, int RC, const double* Bt, int ncols, int KD, Out out) {
+    const int lane = lane_id(), lr = lane >> 2, lc = lane & 3;
+    const int MT = (RC + 7) / 8, mgroups = (MT + MTG - 1) / MTG, npairs = ncols / 16;
+    for (int task = warp_id(); task < mgroups * npairs; task += n_warps()) {
+      const int np = task % npairs, mg = task / npairs;
+      double c[MTG][2][2];
+#pragma unroll
+      for (int m = 0; m < MTG; ++m) c[m][0][0] = c[m][0][1] = c[m][1][0] = c[m][1][1] = 0.0;
+      const int n0 = 16 * np + lr, n1 = n0 + 8;
+#pragma unroll 4
+      for (int ks = 0; ks < KD / 4; ++ks) {
+        const int kr = 4 * ks + lc;   // B fragment: row k = 4 ks + l % 4, column n = l / 4
+        const double b0 = Bt[thcl::sw(kr, n0, ncols)];
+        const double b1 = Bt[thcl::sw(kr, n1, ncols)];
+#pragma unroll
+        for (int m = 0; m < MTG; ++m) {
+          const int r = 8 * (mg * MTG + m) + lr;
+          const double a = A[r * KD + (((ks ^ (r & 7)) << 2) | lc)];
+          thcl::dmma(c[m][0][0], c[m][0][1], a, b0);
+          thcl::dmma(c[m][1][0], c[m][1][1], a, b1);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < MTG; ++m) {
+        const int r = 8 * (mg * MTG + m) + lr;
+        if (r < RC) {
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            out(r, 16 * np + 8 * t + 2 * lc, c[m][t][0]);
+            out(r, 16 * np + 8 * t + 2 * lc + 1, c[m][t][1]);
+          }
+        }
+      }
+    }
+  }
+  // A: Z[r][k] = sum_i In[r][i] W1s[k][i]
+  template <class Epi>
+  OB_DEV void prod_a(const double* In, Epi epi) { mma_nt<1>(In, nk, w1, g.HS, g.N, epi); }
+  // B: O[r][j] = sum_k Tin[r][k] W2s[j][k]  (partial over this slice) -> scatter
+  OB_DEV void prod_b(const double* Tin) {
+    mma_nt<3>(Tin, nk, w2, g.N, g.HS, [&](int r, int j, double v) { scatter(r, j, v); });
   }
   // C: G[r][k] = sum_j V[r][j] W2s[j][k]
   template <class Epi>
-  OB_DEV void prod_c(const double* V, Epi epi) {   // V: [RC][N]
-    const int N = g.N, HS = g.HS, RC = g.RC;
-    auto ow = [&](int r, int cp, int c, double v) { epi(r, cp + c * (HS / 2), v); };
-    if (N == 128 && HS % 32 == 0) { tile_6x2t<64>(HS / 32, RC, w2, g.ld2, HS / 2, V, N, ow); return; }
-    if (N == 64 && HS % 32 == 0) { tile_6x2t<32>(HS / 32, RC, w2, g.ld2, HS / 2, V, N, ow); return; }
-    for (int t = threadIdx.x; t < HS * RC; t += blockDim.x) {
-      const int k = t % HS, r = t / HS;
-      double acc = 0.0;
-      for (int j = 0; j < N; ++j) acc = Num<double>::fma(w2[j * g.ld2 + k], V[r * N + j], acc);
-      epi(r, k, acc);
-    }
-  }
+  OB_DEV void prod_c(const double* V, Epi epi) { mma_tn<1>(V, nk, w2, g.HS, g.N, epi); }
   // D: O[r][i] = sum_k Tin[r][k] W1s[k][i]  (partial over this slice) -> scatter
   OB_DEV void prod_d(const double* Tin) {
-    const int N = g.N, HS = g.HS, RC = g.RC;
-    auto ow = [&](int r, int cp, int c, double v) { scatter(r, cp + c * (N / 2), v); };
-    if (HS == 64 && N % 32 == 0) { tile_6x2t<32>(N / 32, RC, w1, g.ld1, N / 2, Tin, HS, ow); return; }
-    if (HS == 32 && N % 32 == 0) { tile_6x2t<16>(N / 32, RC, w1, g.ld1, N / 2, Tin, HS, ow); return; }
-    for (int t = threadIdx.x; t < N * RC; t += blockDim.x) {
-      const int i = t % N, r = t / N;
-      double acc = 0.0;
-      for (int k = 0; k < HS; ++k) acc = Num<double>::fma(w1[k * g.ld1 + i], Tin[r * HS + k], acc);
-      scatter(r, i, acc);
-    }
+    mma_tn<3>(Tin, nk, w1, g.N, g.HS, [&](int r, int i, double v) { scatter(r, i, v); });
   }
 
   // hidden activations of the rows in `src` (cached for the tangent / cotangent passes);
@@ -342,7 +306,7 @@ struct ClusterNet {
     const int HS = g.HS, act = p.d.act;
     double* H = Hs;
     const double* bb = b1;
-    prod_a(X, [&](int r, int k, double z) { H[r * HS + k] = act_fn(Num<double>::add(z, bb[k]), act); });
+    prod_a(X, [&](int r, int k, double z) { H[thcl::sw(r, k, HS)] = act_fn(Num<double>::add(z, bb[k]), act); });
     __syncthreads();
     if (out) {
       prod_b(Hs);
@@ -361,8 +325,8 @@ struct ClusterNet {
     const double* H = Hs;
     double* Tt = Ts;
     prod_a(X, [&](int r, int k, double z) {
-      const double a = H[r * HS + k];
-      Tt[r * HS + k] = Num<double>::mul(z, act_prime_from(a, a, act));
+      const double a = H[thcl::sw(r, k, HS)];
+      Tt[thcl::sw(r, k, HS)] = Num<double>::mul(z, act_prime_from(a, a, act));
     });
     __syncthreads();
     pt.mark(1);   // first slice product
@@ -382,8 +346,8 @@ struct ClusterNet {
     gather(v, ld, Rv, any_io);   // X = V (all rows of the cluster)
     if (any_io && !*any_io) return;
     prod_c(X, [&](int r, int k, double gk) {
-      const double a = H[r * HS + k];
-      Tt[r * HS + k] = Num<double>::mul(gk, act_prime_from(a, a, act));
+      const double a = H[thcl::sw(r, k, HS)];
+      Tt[thcl::sw(r, k, HS)] = Num<double>::mul(gk, act_prime_from(a, a, act));
     });
     __syncthreads();
     if (mu) {   // dW2 slice, db2 (own rows), db1 slice
@@ -391,19 +355,19 @@ struct ClusterNet {
       for (int t = threadIdx.x; t < N * HS; t += blockDim.x) {
         const int j = t / HS, k = t % HS;
         double acc = 0.0;
-        for (int r = 0; r < nk; ++r) acc = Num<double>::fma(X[r * N + j], H[r * HS + k], acc);
+        for (int r = 0; r < nk; ++r) acc = Num<double>::fma(X[thcl::sw(r, j, N)], H[thcl::sw(r, k, HS)], acc);
         double* m = mu + p.d.mwoff[1] + (long long)j * p.d.ldm[1] + k0 + k;
         *m = Num<double>::fma(scale, acc, *m);
       }
       for (int j = threadIdx.x; j < N; j += blockDim.x) {
         double acc = 0.0;
-        for (int r = 0; r < Rv; ++r) acc = Num<double>::add(acc, X[(off + r) * N + j]);
+        for (int r = 0; r < Rv; ++r) acc = Num<double>::add(acc, X[thcl::sw(off + r, j, N)]);
         double* m = mu + p.d.mboff[1] + j;
         *m = Num<double>::fma(scale, acc, *m);
       }
       for (int k = threadIdx.x; k < HS; k += blockDim.x) {
         double acc = 0.0;
-        for (int r = 0; r < nk; ++r) acc = Num<double>::add(acc, Tt[r * HS + k]);
+        for (int r = 0; r < nk; ++r) acc = Num<double>::add(acc, Tt[thcl::sw(r, k, HS)]);
         double* m = mu + p.d.mboff[0] + k0 + k;
         *m = Num<double>::fma(scale, acc, *m);
       }
@@ -416,7 +380,7 @@ struct ClusterNet {
       for (int t = threadIdx.x; t < HS * N; t += blockDim.x) {
         const int k = t / N, i = t % N;
         double acc = 0.0;
-        for (int r = 0; r < nk; ++r) acc = Num<double>::fma(Tt[r * HS + k], X[r * N + i], acc);
+        for (int r = 0; r < nk; ++r) acc = Num<double>::fma(Tt[thcl::sw(r, k, HS)], X[thcl::sw(r, i, N)], acc);
         double* m = mu + p.d.mwoff[0] + (long long)(k0 + k) * p.d.ldm[0] + i;
         *m = Num<double>::fma(scale, acc, *m);
       }

@@ -90,8 +90,8 @@ def test_backward_euler_and_plain_mlp_field():
     for k in ("u_final", "du0", "dtheta"):
         assert oc.rel_error(np_(getattr(cl, k)), np_(getattr(base, k))) <= TOL64, k
     rng = np.random.default_rng(3)
-    spec = MlpSpec((32, 128, 32), "tanh", False, "f64")
-    model = MlpModel(spec, 0.3 * rng.standard_normal(32 * 128 + 128 + 128 * 32 + 32))
+    spec = MlpSpec((32, 256, 32), "tanh", False, "f64")
+    model = MlpModel(spec, 0.3 * rng.standard_normal(32 * 256 + 256 + 256 * 32 + 32))
     mf = MlpField(model)
     u0 = rng.standard_normal((19, 32))
     from paper_2206_01298_b200.losses import terminal_loss
