@@ -195,13 +195,13 @@ struct ClusterNet {
     }
     __syncthreads();
   }
-  // partial output row r (cluster row index < nk), column j -> the owner's receive buffer
-  OB_DEV void scatter(int r, int j, double v) {
-    if (r >= nk) return;
+  // cluster row r (< nk) -> the remote address of its slot in the owner's receive buffer
+  // (column 0); partial outputs are stored at + 8 j
+  OB_DEV uint32_t scatter_row(int r) const {
     const int big = e * (q + 1);   // rows held by the CTAs with q + 1 rows
     const int c = r < big ? r / (q + 1) : e + (r - big) / max(q, 1);
     const int loc = r < big ? r % (q + 1) : (r - big) % max(q, 1);
-    thcl::st_remote(thcl::remote(recv + ((int)rank * g.R + loc) * g.N + j, (uint32_t)c), v);
+    return thcl::remote(recv + ((int)rank * g.R + loc) * g.N, (uint32_t)c);
   }
 
   // ---- slice products on the fp64 tensor cores (mma.sync m8n8k4).  With FMAs on the vector
@@ -238,10 +238,11 @@ struct ClusterNet {
       for (int m = 0; m < MTG; ++m) {
         const int r = 8 * (mg * MTG + m) + lr;
         if (r < RC) {
+          auto ro = out(r);   // per-row output (the scatter resolves the row's owner once)
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            out(r, 16 * np + 8 * t + 2 * lc, c[m][t][0]);
-            out(r, 16 * np + 8 * t + 2 * lc + 1, c[m][t][1]);
+            ro(16 * np + 8 * t + 2 * lc, c[m][t][0]);
+            ro(16 * np + 8 * t + 2 * lc + 1, c[m][t][1]);
           }
         }
       }
@@ -275,10 +276,11 @@ struct ClusterNet {
       for (int m = 0; m < MTG; ++m) {
         const int r = 8 * (mg * MTG + m) + lr;
         if (r < RC) {
+          auto ro = out(r);   // per-row output (the scatter resolves the row's owner once)
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            out(r, 16 * np + 8 * t + 2 * lc, c[m][t][0]);
-            out(r, 16 * np + 8 * t + 2 * lc + 1, c[m][t][1]);
+            ro(16 * np + 8 * t + 2 * lc, c[m][t][0]);
+            ro(16 * np + 8 * t + 2 * lc + 1, c[m][t][1]);
           }
         }
       }
@@ -286,17 +288,55 @@ struct ClusterNet {
   }
   // A: Z[r][k] = sum_i In[r][i] W1s[k][i]
   template <class Epi>
-  OB_DEV void prod_a(const double* In, Epi epi) { mma_nt<1>(In, nk, w1, g.HS, g.N, epi); }
+  OB_DEV void prod_a(const double* In, Epi epi) {
+    mma_nt<1>(In, nk, w1, g.HS, g.N, [&](int r) { return [=](int k, double v) { epi(r, k, v); }; });
+  }
   // B: O[r][j] = sum_k Tin[r][k] W2s[j][k]  (partial over this slice) -> scatter
   OB_DEV void prod_b(const double* Tin) {
-    mma_nt<3>(Tin, nk, w2, g.N, g.HS, [&](int r, int j, double v) { scatter(r, j, v); });
+    mma_nt<3>(Tin, nk, w2, g.N, g.HS, [&](int r) {
+      const uint32_t base = scatter_row(r);
+      return [=](int j, double v) { thcl::st_remote(base + 8u * (uint32_t)j, v); };
+    });
   }
   // C: G[r][k] = sum_j V[r][j] W2s[j][k]
   template <class Epi>
-  OB_DEV void prod_c(const double* V, Epi epi) { mma_tn<1>(V, nk, w2, g.HS, g.N, epi); }
+  OB_DEV void prod_c(const double* V, Epi epi) {
+    mma_tn<1>(V, nk, w2, g.HS, g.N, [&](int r) { return [=](int k, double v) { epi(r, k, v); }; });
+  }
   // D: O[r][i] = sum_k Tin[r][k] W1s[k][i]  (partial over this slice) -> scatter
   OB_DEV void prod_d(const double* Tin) {
-    mma_tn<3>(Tin, nk, w1, g.N, g.HS, [&](int r, int i, double v) { scatter(r, i, v); });
+    mma_tn<3>(Tin, nk, w1, g.N, g.HS, [&](int r) {
+      const uint32_t base = scatter_row(r);
+      return [=](int i, double v) { thcl::st_remote(base + 8u * (uint32_t)i, v); };
+    });
+  }
+  // parameter cotangents of a slice on the MMA as well: M[a][b] += scale sum_{r < nk} P[r][a] Q[r][b]
+  // (P: [rows][pa], Q: [rows][qb], swizzled; rows past nk masked), added to mu at
+  // dst[a * ldm + b].  One 8 x 16 output tile per task.
+  OB_DEV void outer_acc(const double* P, int pa, const double* Q, int qb, double scale, double* dst, long long ldm) {
+    const int lane = lane_id(), lr = lane >> 2, lc = lane & 3;
+    const int npairs = qb / 16, mtiles = pa / 8;
+    for (int task = warp_id(); task < mtiles * npairs; task += n_warps()) {
+      const int np = task % npairs, mt = task / npairs;
+      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      const int a0 = 8 * mt + lr, n0 = 16 * np + lr, n1 = n0 + 8;
+      for (int rs = 0; rs < nk; rs += 4) {
+        const int r = rs + lc;   // A fragment: A[a][r] = P[r][a]; B fragment: B[r][n] = Q[r][n]
+        const bool ok = r < nk;
+        const double a = ok ? P[thcl::sw(r, a0, pa)] : 0.0;
+        const double b0 = ok ? Q[thcl::sw(r, n0, qb)] : 0.0;
+        const double b1 = ok ? Q[thcl::sw(r, n1, qb)] : 0.0;
+        thcl::dmma(c[0][0], c[0][1], a, b0);
+        thcl::dmma(c[1][0], c[1][1], a, b1);
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          double* m = dst + (long long)a0 * ldm + 16 * np + 8 * t + 2 * lc + u;
+          *m = Num<double>::fma(scale, c[t][u], *m);
+        }
+    }
   }
 
   // hidden activations of the rows in `src` (cached for the tangent / cotangent passes);
@@ -352,13 +392,7 @@ struct ClusterNet {
     __syncthreads();
     if (mu) {   // dW2 slice, db2 (own rows), db1 slice
       const int k0 = (int)rank * HS;
-      for (int t = threadIdx.x; t < N * HS; t += blockDim.x) {
-        const int j = t / HS, k = t % HS;
-        double acc = 0.0;
-        for (int r = 0; r < nk; ++r) acc = Num<double>::fma(X[thcl::sw(r, j, N)], H[thcl::sw(r, k, HS)], acc);
-        double* m = mu + p.d.mwoff[1] + (long long)j * p.d.ldm[1] + k0 + k;
-        *m = Num<double>::fma(scale, acc, *m);
-      }
+      outer_acc(X, N, H, HS, scale, mu + p.d.mwoff[1] + k0, p.d.ldm[1]);   // dW2[j][k0 + k] += v^T a
       for (int j = threadIdx.x; j < N; j += blockDim.x) {
         double acc = 0.0;
         for (int r = 0; r < Rv; ++r) acc = Num<double>::add(acc, X[thcl::sw(off + r, j, N)]);
@@ -377,13 +411,7 @@ struct ClusterNet {
     if (mu) {   // dW1 slice needs the layer input of every row
       gather(xin, ldx, Rv);
       const int k0 = (int)rank * HS;
-      for (int t = threadIdx.x; t < HS * N; t += blockDim.x) {
-        const int k = t / N, i = t % N;
-        double acc = 0.0;
-        for (int r = 0; r < nk; ++r) acc = Num<double>::fma(Tt[thcl::sw(r, k, HS)], X[thcl::sw(r, i, N)], acc);
-        double* m = mu + p.d.mwoff[0] + (long long)(k0 + k) * p.d.ldm[0] + i;
-        *m = Num<double>::fma(scale, acc, *m);
-      }
+      outer_acc(Tt, HS, X, N, scale, mu + p.d.mwoff[0] + (long long)k0 * p.d.ldm[0], p.d.ldm[0]);   // dW1[k0 + k][i]
       __syncthreads();
       thcl::cluster_sync();   // X is rewritten by the next gather of any CTA
     }
