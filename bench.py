@@ -325,7 +325,9 @@ def roofline(ci, scheme, dev, nloc, phases, K, policy_key):
     peak, peak_src = fp_peak(ci.dtype)
     achieved = dfl / (dms / 1e3) / 1e12
     pipe, bound, tc_extra = f"{ci.dtype} FMA (SIMT)", "compute", {}
-    if dev.get("tensor_cores"):
+    if dev.get("tensor_cores") == 2:   # fp64 cluster MLP: same 64 FMA/clk/SM on the DMMA pipe as on the vector pipe
+        pipe = "f64 mma.sync m8n8k4 (weights resident across a cluster of 8 CTAs) + f64 FMA"
+    if dev.get("tensor_cores") == 1:
         # tcgen05 kind::f16 tile: each fp32 product is 3 bf16 MMAs (hi*hi + hi*lo + lo*hi),
         # so the fp32-equivalent ceiling is the measured dense bf16 peak / 3; the executed
         # tensor-pipe FLOPs (split passes and the sample-column padding included) are
@@ -336,7 +338,7 @@ def roofline(ci, scheme, dev, nloc, phases, K, policy_key):
         if ci.kind == "conv":   # fp16 two-term split (same 3 passes at the same rate), one tap per TMEM partial
             peak_src = f"{bf16_src} / 3 (3-pass fp16 split)"
             pipe = "tcgen05 kind::f16 (fp16 3-pass split, per-tap TMEM partials summed in fp32 registers)"
-    if dev.get("tensor_cores") and ci.kind == "mlp":
+    if dev.get("tensor_cores") == 1 and ci.kind == "mlp":
         D0, H = ci.widths[-1], ci.widths[1]
         nmb, t = H // 128, dev["tiles"]
         ncol = 32   # MMA N per tile (samples, padded)

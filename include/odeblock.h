@@ -196,7 +196,8 @@ typedef struct {
   int64_t device_vjp_evals;      /* VJP pairs the device executed (zero cotangents skipped) */
   int64_t tile_rows;             /* samples per CTA tile                                 */
   int64_t tiles;                 /* CTAs per persistent launch                           */
-  int64_t tensor_cores;          /* 1: the MLP contractions ran on tcgen05 (3-pass bf16 split) */
+  int64_t tensor_cores;          /* 1: the contractions ran on a tcgen05 tile (split fp32 products);
+                                    2: fp64 cluster MLP (weights resident across 8 CTAs, mma.sync f64) */
   double ms_pack, ms_forward, ms_reverse, ms_reduce;  /* CUDA-event device times of this call */
 } ob_counters;
 

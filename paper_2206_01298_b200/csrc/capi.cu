@@ -1059,7 +1059,7 @@ int plan_problem(const ob_problem& p, Plan& P, bool allow_tc = false) {
   if (P.adaptive) c = ob_counters{};   // per-sample grids: filled after the run
   c.tile_rows = P.R;
   c.tiles = P.tiles;
-  c.tensor_cores = (P.tc || P.tc_cnf || P.tc_conv) ? 1 : 0;
+  c.tensor_cores = (P.tc || P.tc_cnf || P.tc_conv) ? 1 : (P.theta_cluster || P.rk_cluster) ? 2 : 0;
   c.kernel_launches = 4;
   // workspace
   const long long B = p.batch, N = P.d.N;

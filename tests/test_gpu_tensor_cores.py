@@ -179,7 +179,7 @@ def test_mse_target_loss_on_tensor_cores():
     res64 = grad(MlpField(MlpModel(MlpSpec(widths, "tanh", time_input=False), theta)),
                  tableau_catalog("rk4"), terminal_loss("mse", 1.0, target), u0, 0.0, 1.0,
                  FixedController(10), CheckpointPolicy.parse("store_all"))
-    assert res.device["tensor_cores"] == 1 and res64.device["tensor_cores"] == 0
+    assert res.device["tensor_cores"] == 1 and res64.device["tensor_cores"] != 1   # (fp64: SIMT or cluster MLP)
     assert abs(res.loss - res64.loss) <= 1e-4 * abs(res64.loss)
     assert oc.rel_error(np_(res.dtheta), np_(res64.dtheta)) <= TOL32
     assert oc.rel_error(np_(res.du0), np_(res64.du0)) <= TOL32
