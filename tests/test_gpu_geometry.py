@@ -108,7 +108,8 @@ def test_c5_full_batch_matches_reference(golden):
     ci = make_config("C5")
     res = run_config(ci, "store_all")
     # cluster-resident weights: 15 clusters of 8 CTAs hold 17-18 rows each (up to 3 per CTA)
-    assert res.device["tile_rows"] == 3 and res.device["tiles"] == 120
+    # (120 x 3 with 15 resident clusters, the B200s of this pool; 128 x 2 where 16 fit)
+    assert (res.device["tiles"], res.device["tile_rows"]) in ((120, 3), (128, 2))
     e = errs(res, {"u_final": g["u_final"], "du0": g["du0"], "dtheta": g["dtheta"], "loss": g["loss"]})
     assert max(e.values()) <= TOL64, e
     gn = golden("c5_rows_numpy.npz")

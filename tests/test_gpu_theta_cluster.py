@@ -38,7 +38,7 @@ def np_(x):
     return x.detach().cpu().numpy().astype(np.float64) if isinstance(x, torch.Tensor) else np.asarray(x)
 
 
-@pytest.mark.parametrize("n,tiles,rows", [(16, 8, 2), (37, 24, 2), (250, 120, 3)])
+@pytest.mark.parametrize("n,tiles,rows", [(16, 8, 2), (37, 24, 2), (250, (120, 128), (3, 2))])
 def test_cluster_kernels_match_single_cta_kernels(n, tiles, rows):
     """16 rows = one full cluster; 37 = three clusters of 13 / 12 / 12 rows (CTAs with 2 and 1
     rows); 250 = the one-wave geometry of the C5 bench (15 resident clusters, 16-17 rows
@@ -47,8 +47,10 @@ def test_cluster_kernels_match_single_cta_kernels(n, tiles, rows):
     fld = field_from_config(ci)
     cl = run_config(ci, "store_all", field=fld)
     base = run_config(ci, "store_all", field=fld, tensor_cores=False)
-    assert cl.device["tiles"] == tiles and cl.device["tile_rows"] == rows
-    assert base.device["tiles"] * base.device["tile_rows"] >= n and base.device["tiles"] != tiles
+    # (250 rows: 15 resident clusters of 8 on this pool's B200s -> 120 CTAs x 3 rows; 16 -> 128 x 2)
+    geo = (cl.device["tiles"], cl.device["tile_rows"])
+    assert geo in (list(zip(tiles, rows)) if isinstance(tiles, tuple) else [(tiles, rows)])
+    assert base.device["tiles"] * base.device["tile_rows"] >= n and base.device["tiles"] != geo[0]
     for k in ("u_final", "du0", "dtheta"):
         assert oc.rel_error(np_(getattr(cl, k)), np_(getattr(base, k))) <= TOL64, k
     assert abs(cl.loss - base.loss) <= TOL64 * abs(base.loss)
@@ -129,7 +131,7 @@ def test_full_batch_repeated_runs_identical():
     ci = make_config("C5")
     fld = field_from_config(ci)
     first = run_config(ci, "store_all", field=fld)
-    assert first.device["tiles"] == 120 and first.device["tile_rows"] == 3
+    assert (first.device["tiles"], first.device["tile_rows"]) in ((120, 3), (128, 2))
     again = run_config(ci, "store_all", field=fld)
     assert again.loss == first.loss
     for k in ("u_final", "du0", "dtheta"):
@@ -146,8 +148,10 @@ def test_explicit_rk_on_cluster_matches_single_cta_kernels(scheme, policy):
     fld = field_from_config(ci)
     cl = run_config(ci, policy, field=fld)
     base = run_config(ci, policy, field=fld, tensor_cores=False)
-    assert cl.device["tiles"] == 104 and cl.device["tile_rows"] == 5     # 13 clusters x 8 CTAs x 5 rows
-    assert base.device["tile_rows"] == 4 and base.device["tiles"] == 128
+    # 13 clusters x 8 CTAs x 5 rows with 15 resident clusters (16 resident: 128 CTAs x 4 rows)
+    assert (cl.device["tiles"], cl.device["tile_rows"]) in ((104, 5), (128, 4))
+    assert base.device["tile_rows"] == 4 and base.device["tiles"] == 128 and base.device["tensor_cores"] == 0
+    assert cl.device["tensor_cores"] == 2
     for k in ("u_final", "du0", "dtheta"):
         assert oc.rel_error(np_(getattr(cl, k)), np_(getattr(base, k))) <= 1e-12, k
     assert abs(cl.loss - base.loss) <= 1e-12 * abs(base.loss)
