@@ -23,6 +23,11 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
+# batches of the configs that would take long at full size (C3: tcgen05 conv tile, one image
+# per CTA; C5: cluster theta kernels, two clusters per shard)
+_BATCH = {"C3": 12, "C4": 96, "C5": 64}
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -44,7 +49,7 @@ def _worker(rank, world, port, name, out_q):
         from paper_2206_01298_b200.workloads import (field_from_config, initial_state, loss_for,
                                                      solver_from_config)
 
-        ci = make_config(name, batch=96 if name == "C4" else None)
+        ci = make_config(name, batch=_BATCH.get(name))
         lo, hi = shard_bounds(ci.batch, world, rank)
         fld = field_from_config(ci, rows=slice(lo, hi))
         args = (tableau_catalog(ci.scheme), loss_for(ci, slice(lo, hi)))
@@ -61,7 +66,7 @@ def _worker(rank, world, port, name, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C4"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
 def test_two_rank_grad_sharded_through_engine(name):
     import torch.multiprocessing as mp
     world = 2
@@ -83,7 +88,7 @@ def test_two_rank_grad_sharded_through_engine(name):
     from paper_2206_01298_b200.workloads import (field_from_config, initial_state, loss_for, run_config,
                                                  solver_from_config)
 
-    ci = make_config(name, batch=96 if name == "C4" else None)
+    ci = make_config(name, batch=_BATCH.get(name))
     # the same shards in one process, summed in rank order in fp64
     parts, losses, du0 = [], [], []
     for r in range(world):
