@@ -76,7 +76,7 @@ cudaError_t launch_cnf_tc_field(const RkParams<float>& p, int tiles, int cl, siz
                                 double t, const float* u, const float* w, float* out, cudaStream_t st);
 
 // cluster-resident-weights theta kernels (theta_cl_f64.cu)
-void theta_cluster_geom(int N, int H, int R, int RC, int* region_doubles, int* cluster);
+void theta_cluster_geom(int N, int H, int R, int RC, bool second_x, int* region_doubles, int* cluster);
 int theta_cluster_max_active(size_t smem);
 cudaError_t launch_theta_cluster(const RkParams<double>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
 // explicit-RK kernels on the cluster MLP (rk_cl_f64.cu)
@@ -653,7 +653,7 @@ bool plan_theta_cluster(Plan& P, const ob_field_desc& f, long long B) {
     Q.LR = 1;
     make_dims(f, 1, Q.d);
     int region = 0, cl = 0;
-    theta_cluster_geom(Q.d.N, f.widths[1], R, RC, &region, &cl);
+    theta_cluster_geom(Q.d.N, f.widths[1], R, RC, false, &region, &cl);
     const long long m = Q.gmres_m;
     Q.krylov_stride = (long long)R * ((m + 1) * Q.d.ldn + (m + 1) * m + 2 * m + (m + 1) + m);
     SmemLayout& s = Q.sm;
@@ -722,7 +722,7 @@ bool plan_rk_cluster(Plan& P, const ob_field_desc& f, long long B) {
     Q.LR = 1;
     make_dims(f, 1, Q.d);
     int region = 0, cl = 0;
-    theta_cluster_geom(Q.d.N, f.widths[1], R, 8 * R, &region, &cl);
+    theta_cluster_geom(Q.d.N, f.widths[1], R, 8 * R, true, &region, &cl);
     SmemLayout& s = Q.sm;
     s = SmemLayout{};
     int o = 0;

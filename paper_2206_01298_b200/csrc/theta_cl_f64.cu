@@ -4,8 +4,8 @@
 
 namespace ob {
 
-void theta_cluster_geom(int N, int H, int R, int RC, int* region_doubles, int* cluster) {
-  *region_doubles = thcl_geom(N, H, R, RC).total;
+void theta_cluster_geom(int N, int H, int R, int RC, bool second_x, int* region_doubles, int* cluster) {
+  *region_doubles = thcl_geom(N, H, R, RC, second_x).total;
   *cluster = thcl::kCL;
 }
 

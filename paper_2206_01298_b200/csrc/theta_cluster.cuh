@@ -69,8 +69,9 @@ struct ThclGeom {
   int ld1, ld2;             // leading dims of the W1 slice [HS][ld1] and the W2 slice [N][ld2]
   // offsets in doubles from the start of the cluster region
   int w1, w2, b1, b2, x, hs, ts, recv, flags, total;
+  int x2;   // second row buffer (the VJP's cotangent rows beside the linearisation rows), or -1
 };
-__host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC) {
+__host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC, bool second_x = false) {
   ThclGeom g{};
   g.N = N; g.H = H; g.HS = H / thcl::kCL; g.R = R; g.RC = (RC + 1) & ~1;
   g.ld1 = N;                // rows are XOR-swizzled in 32-byte chunks (thcl::sw), not padded
@@ -86,6 +87,7 @@ __host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC) {
   g.ts = take(g.RC * g.HS);
   g.recv = take(thcl::kCL * R * N);
   g.flags = take(2 * thcl::kCL);   // int pairs inside doubles: 2 x kCL ints fit
+  g.x2 = second_x ? take(g.RC * N) : -1;
   g.total = o;
   return g;
 }
@@ -94,7 +96,7 @@ __host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC) {
 struct ClusterNet {
   const RkParams<double>& p;
   ThclGeom g;
-  double *w1, *w2, *b1, *b2, *X, *Hs, *Ts, *recv;
+  double *w1, *w2, *b1, *b2, *X, *Hs, *Ts, *recv, *X2;
   int* flags;
   uint32_t rank, vpar;
   // rows of the batch are dealt evenly to the clusters, and a cluster's rows evenly
@@ -104,9 +106,11 @@ struct ClusterNet {
   int off;        // its first row within the cluster
 
   OB_DEV ClusterNet(const RkParams<double>& p_, double* region, bool fixed_rows = false)
-      : p(p_), g(thcl_geom(p_.d.N, p_.d.w[1], p_.R, fixed_rows ? thcl::kCL * p_.R : (int)p_.tile_aux)), vpar(0) {
+      : p(p_), g(thcl_geom(p_.d.N, p_.d.w[1], p_.R, fixed_rows ? thcl::kCL * p_.R : (int)p_.tile_aux, fixed_rows)),
+        vpar(0) {
     w1 = region + g.w1; w2 = region + g.w2; b1 = region + g.b1; b2 = region + g.b2;
     X = region + g.x; Hs = region + g.hs; Ts = region + g.ts; recv = region + g.recv;
+    X2 = g.x2 >= 0 ? region + g.x2 : nullptr;
     flags = reinterpret_cast<int*>(region + g.flags);
     rank = thcl::cta_rank();
     if (fixed_rows) {   // the generic RK kernels' mapping: tile t holds rows [t R, t R + R)
@@ -162,8 +166,9 @@ struct ClusterNet {
 
   // ---- step 1: this CTA's rows (src [Rv][ld]) -> every CTA's X at the cluster row index.
   // any_io (nullable): a cluster-wide "any" vote carried on the same barrier.
-  OB_DEV void gather(const double* src, int ld, int, int* any_io = nullptr) {
+  OB_DEV void gather(const double* src, int ld, int, int* any_io = nullptr, double* Xd = nullptr) {
     const int N = g.N;
+    if (!Xd) Xd = X;
     int* f = flags + thcl::kCL * vpar;
     if (any_io) {
       const int loc = __syncthreads_or(*any_io);
@@ -171,7 +176,7 @@ struct ClusterNet {
     }
     for (int i = threadIdx.x; i < Rv * N * thcl::kCL; i += blockDim.x) {
       const int c = i / (Rv * N), el = i % (Rv * N), r = el / N, j = el % N;
-      thcl::st_remote(thcl::remote(X + thcl::sw(off + r, j, N), c), src[r * ld + j]);
+      thcl::st_remote(thcl::remote(Xd + thcl::sw(off + r, j, N), c), src[r * ld + j]);
     }
     thcl::cluster_sync();
     if (any_io) {
@@ -383,19 +388,24 @@ struct ClusterNet {
     const int N = g.N, HS = g.HS, act = p.d.act;
     const double* H = Hs;
     double* Tt = Ts;
-    gather(v, ld, Rv, any_io);   // X = V (all rows of the cluster)
+    // With a second row buffer the cotangent rows go beside the linearisation rows X (still
+    // there from forward()), so dW1 needs no second all-gather and every use of X precedes
+    // the reduce barrier: two cluster barriers per VJP instead of four.
+    const bool keep_x = mu && X2 != nullptr;
+    double* V = keep_x ? X2 : X;
+    gather(v, ld, Rv, any_io, V);   // all cotangent rows of the cluster
     if (any_io && !*any_io) return;
-    prod_c(X, [&](int r, int k, double gk) {
+    prod_c(V, [&](int r, int k, double gk) {
       const double a = H[thcl::sw(r, k, HS)];
       Tt[thcl::sw(r, k, HS)] = Num<double>::mul(gk, act_prime_from(a, a, act));
     });
     __syncthreads();
+    const int k0 = (int)rank * HS;
     if (mu) {   // dW2 slice, db2 (own rows), db1 slice
-      const int k0 = (int)rank * HS;
-      outer_acc(X, N, H, HS, scale, mu + p.d.mwoff[1] + k0, p.d.ldm[1]);   // dW2[j][k0 + k] += v^T a
+      outer_acc(V, N, H, HS, scale, mu + p.d.mwoff[1] + k0, p.d.ldm[1]);   // dW2[j][k0 + k] += v^T a
       for (int j = threadIdx.x; j < N; j += blockDim.x) {
         double acc = 0.0;
-        for (int r = 0; r < Rv; ++r) acc = Num<double>::add(acc, X[thcl::sw(off + r, j, N)]);
+        for (int r = 0; r < Rv; ++r) acc = Num<double>::add(acc, V[thcl::sw(off + r, j, N)]);
         double* m = mu + p.d.mboff[1] + j;
         *m = Num<double>::fma(scale, acc, *m);
       }
@@ -405,13 +415,14 @@ struct ClusterNet {
         double* m = mu + p.d.mboff[0] + k0 + k;
         *m = Num<double>::fma(scale, acc, *m);
       }
+      if (keep_x)   // dW1[k0 + k][i] += (act' o W2^T v)^T x
+        outer_acc(Tt, HS, X, N, scale, mu + p.d.mwoff[0] + (long long)k0 * p.d.ldm[0], p.d.ldm[0]);
     }
     prod_d(Ts);
-    reduce(jtv, ldo, nullptr);   // (cluster barrier: X may be overwritten below)
-    if (mu) {   // dW1 slice needs the layer input of every row
+    reduce(jtv, ldo, nullptr);   // (cluster barrier: X / X2 may be overwritten below)
+    if (mu && !keep_x) {   // dW1 slice needs the layer input of every row: gather it again
       gather(xin, ldx, Rv);
-      const int k0 = (int)rank * HS;
-      outer_acc(Tt, HS, X, N, scale, mu + p.d.mwoff[0] + (long long)k0 * p.d.ldm[0], p.d.ldm[0]);   // dW1[k0 + k][i]
+      outer_acc(Tt, HS, X, N, scale, mu + p.d.mwoff[0] + (long long)k0 * p.d.ldm[0], p.d.ldm[0]);
       __syncthreads();
       thcl::cluster_sync();   // X is rewritten by the next gather of any CTA
     }
