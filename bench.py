@@ -432,10 +432,11 @@ def measure(name, args, steps, warmup, world, rank, local, flush, policy_arg=Non
     # ---- end-to-end through the public API from pinned host memory (H2D in, results D2H)
     # warm-up: the results come back in pinned staging buffers from torch's caching host
     # allocator, and two generations of them are alive at once (the previous result is
-    # released after the next call returns); four calls populate the cache, otherwise
+    # released after the next call returns); four calls that hold their result populate the cache, otherwise
     # cudaHostAlloc (milliseconds per 16 MB) lands in the timed steps
+    r = None
     for _ in range(4):
-        step(u0_host)
+        r = step(u0_host)   # held like in the timed loop, so both generations get allocated
     e2e_s = []
     for _ in range(steps):
         flush.zero_()

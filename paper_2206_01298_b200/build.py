@@ -19,7 +19,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libodeblock.so")
 # longest translation units first (the pool starts them first)
-SOURCES = ["theta_f64_fwd.cu", "theta_f64_rev.cu", "theta_cl_f64.cu", "rk_cl_f64.cu", "theta_f32_fwd.cu", "theta_f32_rev.cu", "rk_f64.cu",
+SOURCES = ["theta_f64_fwd.cu", "theta_f64_rev.cu", "theta_cl_f64.cu", "rk_cl_f64.cu", "rk_cl2_f64.cu", "theta_f32_fwd.cu", "theta_f32_rev.cu", "rk_f64.cu",
            "adaptive_f32.cu", "rk_f32.cu", "adaptive_f64.cu", "cnf_f32.cu", "cnf_tc.cu", "rk_f32s.cu", "rk_tc.cu",
            "conv_f32.cu", "conv_tc.cu", "capi.cu", "optim.cu",
            "revolve.cpp"]

@@ -79,9 +79,13 @@ cudaError_t launch_cnf_tc_field(const RkParams<float>& p, int tiles, int cl, siz
 void theta_cluster_geom(int N, int H, int R, int RC, bool second_x, int* region_doubles, int* cluster);
 int theta_cluster_max_active(size_t smem);
 cudaError_t launch_theta_cluster(const RkParams<double>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
-// explicit-RK kernels on the cluster MLP (rk_cl_f64.cu)
-int rk_cluster_max_active(size_t smem);
-cudaError_t launch_rk_cluster(const RkParams<double>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
+// explicit-RK kernels on the cluster MLP, clusters of 8 and of 2 CTAs (rk_cl_f64.cu, rk_cl2_f64.cu)
+void rk_cluster8_geom(int N, int H, int R, int* region_doubles);
+int rk_cluster8_max_active(size_t smem);
+cudaError_t launch_rk_cluster8(const RkParams<double>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
+void rk_cluster2_geom(int N, int H, int R, int* region_doubles);
+int rk_cluster2_max_active(size_t smem);
+cudaError_t launch_rk_cluster2(const RkParams<double>& p, int tiles, size_t smem, cudaStream_t st, bool forward);
 // tcgen05 conv tile (conv_tc.cu)
 void tc_conv_sizes(unsigned* packed_bytes, unsigned* smem_bytes);
 cudaError_t launch_pack_tc_conv(const Dims& d, const float* theta, void* img, cudaStream_t st);
@@ -231,7 +235,7 @@ struct Plan {
   bool tc_cnf = false;            // tcgen05 CNF tile (cnf_tc.cu)
   bool tc_conv = false;           // tcgen05 conv tile (conv_tc.cu)
   bool theta_cluster = false;     // theta kernels with the weights resident across a cluster
-  bool rk_cluster = false;        // explicit-RK kernels on the cluster MLP (fp64 two-layer MLP fields)
+  int rk_cluster = 0;             // explicit-RK kernels on the cluster MLP (fp64 two-layer MLP fields): CTAs per cluster
   int cluster_rows = 0;           // ... rows per cluster the shared-memory layout is sized for
   long long cnf_log_rec = 0;      // tcgen05 CNF tile: bytes of one VJP record of the dW log
   int cnf_cluster = 1;            // tcgen05 CNF tile: CTAs per cluster sharing the weight stream
@@ -716,47 +720,57 @@ bool rk_cluster_eligible(const ob_problem& p, const Plan& P) {
   return true;
 }
 
+// Cluster size: two CTAs when half of both weight matrices fits one CTA's shared memory and its
+// parameter-cotangent tiles fit the warps' registers (8 warps x 8 tiles of 8 x 16 per matrix:
+// N H / 2 <= 8192) -- an eighth of the exchange traffic and no row-tile padding; else eight.
 bool plan_rk_cluster(Plan& P, const ob_field_desc& f, long long B) {
-  auto layout = [&](Plan& Q, int R) {
-    Q.R = Q.Rt = R;
-    Q.LR = 1;
-    make_dims(f, 1, Q.d);
-    int region = 0, cl = 0;
-    theta_cluster_geom(Q.d.N, f.widths[1], R, 8 * R, true, &region, &cl);
-    SmemLayout& s = Q.sm;
-    s = SmemLayout{};
-    int o = 0;
-    auto take = [&](long long n) { int r = o; o += (int)((n + 1) & ~1LL); return r; };
-    s.tA = s.tB = s.scr = s.kry = s.ring = s.hscr = s.wts = -1;
-    s.ring_elems = s.hscr_elems = s.scr_elems = 0;
-    for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
-    for (int i = 0; i < 8; ++i) s.vec[i] = -1;
-    const long long v = (long long)Q.Rt * Q.d.ldn;
-    s.x0 = take((long long)Q.Rt * Q.d.lda[0]);
-    s.u = take(v);
-    s.lam = take(v);
-    s.lamn = take(v);
-    s.w = take(v);
-    s.jtv = take(v);
-    s.ks = take(2LL * Q.s_stages * v);
-    s.aux = take(region);   // the cluster region (weight slices, exchange buffers)
-    s.total = o;
-    Q.smem_bytes = (size_t)o * 8;
-    return Q.smem_bytes + 1024 <= smem_cap(Q);
+  auto attempt = [&](int CL) {
+    auto geom = CL == 2 ? rk_cluster2_geom : rk_cluster8_geom;
+    auto max_act = CL == 2 ? rk_cluster2_max_active : rk_cluster8_max_active;
+    auto layout = [&](Plan& Q, int R) {
+      Q.R = Q.Rt = R;
+      Q.LR = 1;
+      make_dims(f, 1, Q.d);
+      int region = 0;
+      geom(Q.d.N, f.widths[1], R, &region);
+      SmemLayout& s = Q.sm;
+      s = SmemLayout{};
+      int o = 0;
+      auto take = [&](long long n) { int r = o; o += (int)((n + 1) & ~1LL); return r; };
+      s.tA = s.tB = s.scr = s.kry = s.ring = s.hscr = s.wts = -1;
+      s.ring_elems = s.hscr_elems = s.scr_elems = 0;
+      for (int l = 0; l < OB_MAX_LAYERS; ++l) s.hid[l] = s.pre[l] = -1;
+      for (int i = 0; i < 8; ++i) s.vec[i] = -1;
+      const long long v = (long long)Q.Rt * Q.d.ldn;
+      s.x0 = take((long long)Q.Rt * Q.d.lda[0]);
+      s.u = take(v);
+      s.lam = take(v);
+      s.lamn = take(v);
+      s.w = take(v);
+      s.jtv = take(v);
+      s.ks = take(2LL * Q.s_stages * v);
+      s.aux = take(region);   // the cluster region (weight slices, exchange buffers)
+      s.total = o;
+      Q.smem_bytes = (size_t)o * 8;
+      return Q.smem_bytes + 1024 <= smem_cap(Q);
+    };
+    Plan Q = P;
+    if (!layout(Q, 2)) return false;
+    const int max_active = max_act(Q.smem_bytes);
+    if (max_active < 1) return false;
+    // rows per CTA so that the batch is one wave of resident clusters (<= 6: the tiles' row groups)
+    int R = (int)((B + (long long)CL * max_active - 1) / ((long long)CL * max_active));
+    R = std::max(2, std::min(R, 6));
+    Plan Q2 = P;
+    if (!layout(Q2, R) || max_act(Q2.smem_bytes) < 1) return false;
+    Q2.tiles = (int)(((B + R - 1) / R + CL - 1) / CL * CL);
+    Q2.rk_cluster = CL;
+    P = Q2;
+    return true;
   };
-  Plan Q = P;
-  if (!layout(Q, 2)) return false;
-  const int max_active = rk_cluster_max_active(Q.smem_bytes);
-  if (max_active < 1) return false;
-  // rows per CTA so that the batch is one wave of resident clusters (<= 6: the tiles' row groups)
-  int R = (int)((B + 8LL * max_active - 1) / (8LL * max_active));
-  R = std::max(2, std::min(R, 6));
-  Plan Q2 = P;
-  if (!layout(Q2, R) || rk_cluster_max_active(Q2.smem_bytes) < 1) return false;
-  Q2.tiles = (int)(((B + R - 1) / R + 7) / 8 * 8);
-  Q2.rk_cluster = true;
-  P = Q2;
-  return true;
+  const long long N = f.widths[2], H = f.widths[1];
+  if (!getenv("OB_RK_CLUSTER8") && H % 32 == 0 && N * H / 2 <= 8192 && attempt(2)) return true;
+  return attempt(8);
 }
 
 // Tensor-core conv tile: the C3 block on an explicit fixed-step scheme, one image per CTA.
@@ -1293,7 +1307,8 @@ int run_grad(const ob_problem& p, const ob_buffers& b, Plan& P, cudaStream_t st,
     }
     if (P.rk_cluster) {
       if constexpr (sizeof(T) == 8)
-        return launch_rk_cluster(reinterpret_cast<const RkParams<double>&>(rp), P.tiles, P.smem_bytes, st, fwd);
+        return (P.rk_cluster == 2 ? launch_rk_cluster2 : launch_rk_cluster8)(
+            reinterpret_cast<const RkParams<double>&>(rp), P.tiles, P.smem_bytes, st, fwd);
       return cudaErrorNotSupported;
     }
     if (P.theta) return launch_theta<T>(rp, P.LR, P.tiles, P.smem_bytes, st, fwd);

@@ -24,6 +24,10 @@ OB_DEV void set_status(int* status, int code, int info) {
 // Adapters whose CTAs cooperate across a thread-block cluster (multicast weight
 // streams) must not leave the sweep early: a CTA that hits an error records it and
 // keeps stepping with its cluster (its results are discarded by the host).
+// threads per CTA of the kernels instantiated with adapter F (default kThreads)
+template <class F, class = void> struct BlockThreads { static constexpr int value = kThreads; };
+template <class F>
+struct BlockThreads<F, std::void_t<decltype(F::kBlockThreads)>> { static constexpr int value = F::kBlockThreads; };
 template <class F, class = void> struct NoEarlyExit { static constexpr bool value = false; };
 template <class F>
 struct NoEarlyExit<F, std::void_t<decltype(F::kNoEarlyExit)>> { static constexpr bool value = F::kNoEarlyExit; };
@@ -504,7 +508,7 @@ OB_DEV void loss_seed(const RkParams<T>& p, T* lam, int row0, int Rv) {
 
 // --------------------------------------------------------------- forward
 template <typename T, class F>
-__global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_constant__ RkParams<T> p) {
+__global__ void __launch_bounds__(BlockThreads<F>::value, 1) rk_forward_kernel(const __grid_constant__ RkParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   zero_smem(sm, p.sm.wts >= 0 ? p.sm.wts : p.sm.total);
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1) rk_forward_kernel(const __grid_co
 
 // --------------------------------------------------------------- reverse
 template <typename T, class F>
-__global__ void __launch_bounds__(kThreads, 1) rk_reverse_kernel(const __grid_constant__ RkParams<T> p) {
+__global__ void __launch_bounds__(BlockThreads<F>::value, 1) rk_reverse_kernel(const __grid_constant__ RkParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   if (*(volatile int*)p.status != 0) return;  // forward failed

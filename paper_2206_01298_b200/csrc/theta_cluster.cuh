@@ -25,10 +25,26 @@
 
 #include "theta_impl.cuh"
 
+// CTAs per cluster: 8 (the portable maximum) unless the including translation unit asks for
+// another size.  Everything below lives in an inline namespace named after the size, so the
+// builds of different sizes are distinct entities at link time.
+#ifndef OB_THCL_CL
+#define OB_THCL_CL 8
+#endif
+#define OB_THCL_NS2(n) thcl_cl##n
+#define OB_THCL_NS(n) OB_THCL_NS2(n)
+
 namespace ob {
+inline namespace OB_THCL_NS(OB_THCL_CL) {
 
 namespace thcl {
-constexpr int kCL = 8;   // CTAs per cluster (the portable maximum)
+constexpr int kCL = OB_THCL_CL;
+// parameter cotangents of the explicit-RK adapter accumulate in registers over the whole sweep
+// (clusters of two: a CTA's slice is half of every weight matrix, far too much to
+// read-modify-write through L2 per VJP); kMuSlots output tiles per warp and matrix
+constexpr bool kRegMu = kCL == 2;
+constexpr int kMuSlots = 8;
+constexpr int kRkThreads = kCL == 2 ? 256 : kThreads;
 
 OB_DEV uint32_t cta_rank() {
   uint32_t r;
@@ -73,7 +89,10 @@ struct ThclGeom {
 };
 __host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC, bool second_x = false) {
   ThclGeom g{};
-  g.N = N; g.H = H; g.HS = H / thcl::kCL; g.R = R; g.RC = (RC + 1) & ~1;
+  g.N = N; g.H = H; g.HS = H / thcl::kCL; g.R = R;
+  // the MMA row tiles read whole groups of 8 rows: the fixed-rows geometry (whose last buffer is
+  // a row buffer) allocates them; the theta geometry's row buffers are followed by others
+  g.RC = second_x ? (RC + 7) & ~7 : (RC + 1) & ~1;
   g.ld1 = N;                // rows are XOR-swizzled in 32-byte chunks (thcl::sw), not padded
   g.ld2 = g.HS;
   int o = 0;
@@ -104,6 +123,7 @@ struct ClusterNet {
   int nk, q, e;
   int row0, Rv;   // this CTA's global rows [row0, row0 + Rv)
   int off;        // its first row within the cluster
+  double mu2[thcl::kMuSlots][2][2], mu1[thcl::kMuSlots][2][2];   // kRegMu: dW2 / dW1 slice tiles of this warp
 
   OB_DEV ClusterNet(const RkParams<double>& p_, double* region, bool fixed_rows = false)
       : p(p_), g(thcl_geom(p_.d.N, p_.d.w[1], p_.R, fixed_rows ? thcl::kCL * p_.R : (int)p_.tile_aux, fixed_rows)),
@@ -146,6 +166,12 @@ struct ClusterNet {
     for (int i = threadIdx.x; i < HS; i += blockDim.x) b1[i] = p.W.bias[0][k0 + i];
     for (int i = threadIdx.x; i < N; i += blockDim.x) b2[i] = p.W.bias[1][i];
     for (int i = threadIdx.x; i < 2 * thcl::kCL; i += blockDim.x) flags[i] = 0;
+    if constexpr (thcl::kRegMu) {
+#pragma unroll
+      for (int s = 0; s < thcl::kMuSlots; ++s)
+        mu2[s][0][0] = mu2[s][0][1] = mu2[s][1][0] = mu2[s][1][1] = mu1[s][0][0] = mu1[s][0][1] = mu1[s][1][0] =
+            mu1[s][1][1] = 0.0;
+    }
     __syncthreads();
     thcl::cluster_sync();   // every CTA's buffers exist before anyone writes into them
   }
@@ -298,10 +324,16 @@ struct ClusterNet {
   }
   // B: O[r][j] = sum_k Tin[r][k] W2s[j][k]  (partial over this slice) -> scatter
   OB_DEV void prod_b(const double* Tin) {
-    mma_nt<3>(Tin, nk, w2, g.N, g.HS, [&](int r) {
+    auto out = [&](int r) {
       const uint32_t base = scatter_row(r);
       return [=](int j, double v) { thcl::st_remote(base + 8u * (uint32_t)j, v); };
-    });
+    };
+    if constexpr (thcl::kCL == 2) {   // at most 12 rows per cluster: one or two row tiles
+      if (nk <= 8) mma_nt<1>(Tin, nk, w2, g.N, g.HS, out);
+      else mma_nt<2>(Tin, nk, w2, g.N, g.HS, out);
+    } else {
+      mma_nt<3>(Tin, nk, w2, g.N, g.HS, out);
+    }
   }
   // C: G[r][k] = sum_j V[r][j] W2s[j][k]
   template <class Epi>
@@ -310,10 +342,16 @@ struct ClusterNet {
   }
   // D: O[r][i] = sum_k Tin[r][k] W1s[k][i]  (partial over this slice) -> scatter
   OB_DEV void prod_d(const double* Tin) {
-    mma_tn<3>(Tin, nk, w1, g.N, g.HS, [&](int r) {
+    auto out = [&](int r) {
       const uint32_t base = scatter_row(r);
       return [=](int i, double v) { thcl::st_remote(base + 8u * (uint32_t)i, v); };
-    });
+    };
+    if constexpr (thcl::kCL == 2) {
+      if (nk <= 8) mma_tn<1>(Tin, nk, w1, g.N, g.HS, out);
+      else mma_tn<2>(Tin, nk, w1, g.N, g.HS, out);
+    } else {
+      mma_tn<3>(Tin, nk, w1, g.N, g.HS, out);
+    }
   }
   // parameter cotangents of a slice on the MMA as well: M[a][b] += scale sum_{r < nk} P[r][a] Q[r][b]
   // (P: [rows][pa], Q: [rows][qb], swizzled; rows past nk masked), added to mu at
@@ -344,20 +382,78 @@ struct ClusterNet {
     }
   }
 
+  // the same product into this warp's register tiles (kRegMu): acc[s] is output tile
+  // warp + s * n_warps; the scale goes on the P fragment
+  OB_DEV void outer_reg(const double* P, int pa, const double* Q, int qb, double scale,
+                        double (&acc)[thcl::kMuSlots][2][2]) {
+    const int lane = lane_id(), lr = lane >> 2, lc = lane & 3;
+    const int npairs = qb / 16, ntasks = (pa / 8) * npairs;
+#pragma unroll
+    for (int s = 0; s < thcl::kMuSlots; ++s) {
+      const int task = warp_id() + s * n_warps();
+      if (task < ntasks) {
+        const int np = task % npairs, mt = task / npairs;
+        const int a0 = 8 * mt + lr, n0 = 16 * np + lr, n1 = n0 + 8;
+        for (int rs = 0; rs < nk; rs += 4) {
+          const int r = rs + lc;
+          const bool ok = r < nk;
+          const double a = ok ? Num<double>::mul(scale, P[thcl::sw(r, a0, pa)]) : 0.0;
+          const double b0 = ok ? Q[thcl::sw(r, n0, qb)] : 0.0;
+          const double b1 = ok ? Q[thcl::sw(r, n1, qb)] : 0.0;
+          thcl::dmma(acc[s][0][0], acc[s][0][1], a, b0);
+          thcl::dmma(acc[s][1][0], acc[s][1][1], a, b1);
+        }
+      }
+    }
+  }
+  OB_DEV void flush_reg(int pa, int qb, const double (&acc)[thcl::kMuSlots][2][2], double* dst, long long ldm) {
+    const int lane = lane_id(), lr = lane >> 2, lc = lane & 3;
+    const int npairs = qb / 16, ntasks = (pa / 8) * npairs;
+#pragma unroll
+    for (int s = 0; s < thcl::kMuSlots; ++s) {
+      const int task = warp_id() + s * n_warps();
+      if (task < ntasks) {
+        const int np = task % npairs, mt = task / npairs;
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            double* m = dst + (long long)(8 * mt + lr) * ldm + 16 * np + 8 * t + 2 * lc + u;
+            *m = Num<double>::add(*m, acc[s][t][u]);
+          }
+      }
+    }
+  }
+  // end of the sweep: the register tiles join the CTA's mu slot
+  OB_DEV void finish_mu(double* mu) {
+    if constexpr (thcl::kRegMu) {
+      const int k0 = (int)rank * g.HS;
+      flush_reg(g.N, g.HS, mu2, mu + p.d.mwoff[1] + k0, p.d.ldm[1]);
+      flush_reg(g.HS, g.N, mu1, mu + p.d.mwoff[0] + (long long)k0 * p.d.ldm[0], p.d.ldm[0]);
+    }
+  }
+
   // hidden activations of the rows in `src` (cached for the tangent / cotangent passes);
   // with out: the MLP value W2 act(W1 x + b1) + b2 for this CTA's rows
   OB_DEV void forward(const double* src, int ld, int Rv, double* out, int ldo) {
+    PhaseTimer pt(p.prof ? p.phase : nullptr);
     gather(src, ld, Rv);
+    pt.mark(10);
     const int HS = g.HS, act = p.d.act;
     double* H = Hs;
     const double* bb = b1;
     prod_a(X, [&](int r, int k, double z) { H[thcl::sw(r, k, HS)] = act_fn(Num<double>::add(z, bb[k]), act); });
     __syncthreads();
+    pt.mark(11);
     if (out) {
       prod_b(Hs);
+      __syncthreads();
+      pt.mark(12);
       reduce(out, ldo, b2);
+      pt.mark(13);
     } else {
       thcl::cluster_sync();   // X is rewritten by the next gather of any CTA
+      pt.mark(13);
     }
   }
   // (dMLP/du) v at the cached linearisation (tanh / identity / relu: act' from the value)
@@ -393,16 +489,20 @@ struct ClusterNet {
     // the reduce barrier: two cluster barriers per VJP instead of four.
     const bool keep_x = mu && X2 != nullptr;
     double* V = keep_x ? X2 : X;
+    PhaseTimer pt(p.prof ? p.phase : nullptr);
     gather(v, ld, Rv, any_io, V);   // all cotangent rows of the cluster
     if (any_io && !*any_io) return;
+    pt.mark(14);
     prod_c(V, [&](int r, int k, double gk) {
       const double a = H[thcl::sw(r, k, HS)];
       Tt[thcl::sw(r, k, HS)] = Num<double>::mul(gk, act_prime_from(a, a, act));
     });
     __syncthreads();
+    pt.mark(15);
     const int k0 = (int)rank * HS;
     if (mu) {   // dW2 slice, db2 (own rows), db1 slice
-      outer_acc(V, N, H, HS, scale, mu + p.d.mwoff[1] + k0, p.d.ldm[1]);   // dW2[j][k0 + k] += v^T a
+      if (thcl::kRegMu && keep_x) outer_reg(V, N, H, HS, scale, mu2);
+      else outer_acc(V, N, H, HS, scale, mu + p.d.mwoff[1] + k0, p.d.ldm[1]);   // dW2[j][k0 + k] += v^T a
       for (int j = threadIdx.x; j < N; j += blockDim.x) {
         double acc = 0.0;
         for (int r = 0; r < Rv; ++r) acc = Num<double>::add(acc, V[thcl::sw(off + r, j, N)]);
@@ -415,11 +515,17 @@ struct ClusterNet {
         double* m = mu + p.d.mboff[0] + k0 + k;
         *m = Num<double>::fma(scale, acc, *m);
       }
-      if (keep_x)   // dW1[k0 + k][i] += (act' o W2^T v)^T x
+      if (thcl::kRegMu && keep_x) outer_reg(Tt, HS, X, N, scale, mu1);
+      else if (keep_x)   // dW1[k0 + k][i] += (act' o W2^T v)^T x
         outer_acc(Tt, HS, X, N, scale, mu + p.d.mwoff[0] + (long long)k0 * p.d.ldm[0], p.d.ldm[0]);
     }
+    __syncthreads();
+    pt.mark(6);
     prod_d(Ts);
+    __syncthreads();
+    pt.mark(7);
     reduce(jtv, ldo, nullptr);   // (cluster barrier: X / X2 may be overwritten below)
+    pt.mark(4);
     if (mu && !keep_x) {   // dW1 slice needs the layer input of every row: gather it again
       gather(xin, ldx, Rv);
       outer_acc(Tt, HS, X, N, scale, mu + p.d.mwoff[0] + (long long)k0 * p.d.ldm[0], p.d.ldm[0]);
@@ -438,6 +544,7 @@ struct ClusterMlpAdapter {
   static constexpr int kCombineBatch = 4;
   static constexpr bool kOwnsStep = false;
   static constexpr bool kNoEarlyExit = true;  // the cluster applies its products together
+  static constexpr int kBlockThreads = thcl::kRkThreads;
   const RkParams<double>& p;
   ClusterNet net;
   double* xin;   // field input rows [Rt][lda0]
@@ -449,7 +556,7 @@ struct ClusterMlpAdapter {
   OB_DEV void put_time(double) {}
   OB_DEV void set_scratch(double*, int) {}
   OB_DEV void jvp(const double*, double*) {}
-  OB_DEV void finish(double*) {}
+  OB_DEV void finish(double* mu) { net.finish_mu(mu); }
   OB_DEV void release() { thcl::cluster_sync(); }   // no CTA leaves while a partner may still write into it
   OB_DEV void eval(double* out) { net.forward(xin, p.d.lda[0], net.Rv, out, p.d.ldn); }
   OB_DEV void vjp(const double* w, double* jtv, double* mu, double h, int) {
@@ -739,12 +846,13 @@ __global__ void __launch_bounds__(kThreads, 1) thcl_reverse_kernel(const __grid_
 
 // ------------------------------------------------------------ launchers
 template <typename K>
-static cudaError_t thcl_launch(K kf, int grid, size_t smem, cudaStream_t st, const RkParams<double>& p) {
+static cudaError_t thcl_launch(K kf, int grid, size_t smem, cudaStream_t st, const RkParams<double>& p,
+                               int threads = kThreads) {
   cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -757,4 +865,5 @@ static cudaError_t thcl_launch(K kf, int grid, size_t smem, cudaStream_t st, con
   return cudaLaunchKernelEx(&cfg, kf, p);
 }
 
+}  // inline namespace
 }  // namespace ob
