@@ -86,6 +86,7 @@ struct ThclGeom {
   // offsets in doubles from the start of the cluster region
   int w1, w2, b1, b2, x, hs, ts, recv, flags, total;
   int x2;   // second row buffer (the VJP's cotangent rows beside the linearisation rows), or -1
+  int mb;   // bias-cotangent accumulators of the sweep (db2 [N] | db1 slice [HS]), or -1
 };
 __host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC, bool second_x = false) {
   ThclGeom g{};
@@ -106,6 +107,7 @@ __host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC, bool 
   g.ts = take(g.RC * g.HS);
   g.recv = take(thcl::kCL * R * N);
   g.flags = take(2 * thcl::kCL);   // int pairs inside doubles: 2 x kCL ints fit
+  g.mb = second_x ? take(N + g.HS) : -1;
   g.x2 = second_x ? take(g.RC * N) : -1;
   g.total = o;
   return g;
@@ -115,7 +117,7 @@ __host__ __device__ inline ThclGeom thcl_geom(int N, int H, int R, int RC, bool 
 struct ClusterNet {
   const RkParams<double>& p;
   ThclGeom g;
-  double *w1, *w2, *b1, *b2, *X, *Hs, *Ts, *recv, *X2;
+  double *w1, *w2, *b1, *b2, *X, *Hs, *Ts, *recv, *X2, *mb;
   int* flags;
   uint32_t rank, vpar;
   // rows of the batch are dealt evenly to the clusters, and a cluster's rows evenly
@@ -131,6 +133,7 @@ struct ClusterNet {
     w1 = region + g.w1; w2 = region + g.w2; b1 = region + g.b1; b2 = region + g.b2;
     X = region + g.x; Hs = region + g.hs; Ts = region + g.ts; recv = region + g.recv;
     X2 = g.x2 >= 0 ? region + g.x2 : nullptr;
+    mb = g.mb >= 0 ? region + g.mb : nullptr;
     flags = reinterpret_cast<int*>(region + g.flags);
     rank = thcl::cta_rank();
     if (fixed_rows) {   // the generic RK kernels' mapping: tile t holds rows [t R, t R + R)
@@ -167,6 +170,7 @@ struct ClusterNet {
     for (int i = threadIdx.x; i < N; i += blockDim.x) b2[i] = p.W.bias[1][i];
     for (int i = threadIdx.x; i < 2 * thcl::kCL; i += blockDim.x) flags[i] = 0;
     if constexpr (thcl::kRegMu) {
+      for (int i = threadIdx.x; i < g.N + g.HS; i += blockDim.x) mb[i] = 0.0;
 #pragma unroll
       for (int s = 0; s < thcl::kMuSlots; ++s)
         mu2[s][0][0] = mu2[s][0][1] = mu2[s][1][0] = mu2[s][1][1] = mu1[s][0][0] = mu1[s][0][1] = mu1[s][1][0] =
@@ -388,21 +392,34 @@ struct ClusterNet {
                         double (&acc)[thcl::kMuSlots][2][2]) {
     const int lane = lane_id(), lr = lane >> 2, lc = lane & 3;
     const int npairs = qb / 16, ntasks = (pa / 8) * npairs;
+    int oa[thcl::kMuSlots], o0[thcl::kMuSlots], o1[thcl::kMuSlots];   // operand columns per tile (no branches:
+    bool live[thcl::kMuSlots];                                         // the tiles' loads and MMAs interleave)
 #pragma unroll
     for (int s = 0; s < thcl::kMuSlots; ++s) {
       const int task = warp_id() + s * n_warps();
-      if (task < ntasks) {
-        const int np = task % npairs, mt = task / npairs;
-        const int a0 = 8 * mt + lr, n0 = 16 * np + lr, n1 = n0 + 8;
-        for (int rs = 0; rs < nk; rs += 4) {
-          const int r = rs + lc;
-          const bool ok = r < nk;
-          const double a = ok ? Num<double>::mul(scale, P[thcl::sw(r, a0, pa)]) : 0.0;
-          const double b0 = ok ? Q[thcl::sw(r, n0, qb)] : 0.0;
-          const double b1 = ok ? Q[thcl::sw(r, n1, qb)] : 0.0;
-          thcl::dmma(acc[s][0][0], acc[s][0][1], a, b0);
-          thcl::dmma(acc[s][1][0], acc[s][1][1], a, b1);
-        }
+      live[s] = task < ntasks;
+      const int tt = live[s] ? task : 0;
+      oa[s] = 8 * (tt / npairs) + lr;
+      o0[s] = 16 * (tt % npairs) + lr;
+      o1[s] = o0[s] + 8;
+    }
+    for (int rs = 0; rs < nk; rs += 4) {
+      const bool ok = rs + lc < nk;
+      const int r = ok ? rs + lc : 0;
+      double a[thcl::kMuSlots], b0[thcl::kMuSlots], b1[thcl::kMuSlots];
+#pragma unroll
+      for (int s = 0; s < thcl::kMuSlots; ++s) {
+        // unconditional loads from clamped (valid) addresses: a conditional load compiles to a
+        // branch per operand
+        // (the dead fragments are finite values of row 0 / tile 0 times a zero scale)
+        a[s] = Num<double>::mul((ok && live[s]) ? scale : 0.0, P[thcl::sw(r, oa[s], pa)]);
+        b0[s] = Q[thcl::sw(r, o0[s], qb)];
+        b1[s] = Q[thcl::sw(r, o1[s], qb)];
+      }
+#pragma unroll
+      for (int s = 0; s < thcl::kMuSlots; ++s) {
+        thcl::dmma(acc[s][0][0], acc[s][0][1], a[s], b0[s]);
+        thcl::dmma(acc[s][1][0], acc[s][1][1], a[s], b1[s]);
       }
     }
   }
@@ -430,6 +447,14 @@ struct ClusterNet {
       const int k0 = (int)rank * g.HS;
       flush_reg(g.N, g.HS, mu2, mu + p.d.mwoff[1] + k0, p.d.ldm[1]);
       flush_reg(g.HS, g.N, mu1, mu + p.d.mwoff[0] + (long long)k0 * p.d.ldm[0], p.d.ldm[0]);
+      for (int j = threadIdx.x; j < g.N; j += blockDim.x) {
+        double* m = mu + p.d.mboff[1] + j;
+        *m = Num<double>::add(*m, mb[j]);
+      }
+      for (int k = threadIdx.x; k < g.HS; k += blockDim.x) {
+        double* m = mu + p.d.mboff[0] + k0 + k;
+        *m = Num<double>::add(*m, mb[g.N + k]);
+      }
     }
   }
 
@@ -506,13 +531,13 @@ struct ClusterNet {
       for (int j = threadIdx.x; j < N; j += blockDim.x) {
         double acc = 0.0;
         for (int r = 0; r < Rv; ++r) acc = Num<double>::add(acc, V[thcl::sw(off + r, j, N)]);
-        double* m = mu + p.d.mboff[1] + j;
+        double* m = (thcl::kRegMu && keep_x) ? mb + j : mu + p.d.mboff[1] + j;
         *m = Num<double>::fma(scale, acc, *m);
       }
       for (int k = threadIdx.x; k < HS; k += blockDim.x) {
         double acc = 0.0;
         for (int r = 0; r < nk; ++r) acc = Num<double>::add(acc, Tt[thcl::sw(r, k, HS)]);
-        double* m = mu + p.d.mboff[0] + k0 + k;
+        double* m = (thcl::kRegMu && keep_x) ? mb + N + k : mu + p.d.mboff[0] + k0 + k;
         *m = Num<double>::fma(scale, acc, *m);
       }
       if (thcl::kRegMu && keep_x) outer_reg(Tt, HS, X, N, scale, mu1);
