@@ -460,7 +460,12 @@ struct ClusterNet {
 
   // hidden activations of the rows in `src` (cached for the tangent / cotangent passes);
   // with out: the MLP value W2 act(W1 x + b1) + b2 for this CTA's rows
-  OB_DEV void forward(const double* src, int ld, int Rv, double* out, int ldo) {
+  // (no_sync: the caller's next exchange does not write X -- a VJP that gathers its cotangent
+  // rows into the second row buffer -- so the closing barrier is not needed)
+  OB_DEV void forward(const double* src, int ld, int Rv, double* out, int ldo, bool no_sync = false) {
+    // (profiling slots of tools/profile_step.py --phases: 10 all-gather, 11 hidden product +
+    // activation, 12 output product + scatter, 13 reduce / barrier; in vjp(): 14 all-gather,
+    // 15 W2^T product, 6 parameter cotangents, 7 W1^T product + scatter, 4 reduce)
     PhaseTimer pt(p.prof ? p.phase : nullptr);
     gather(src, ld, Rv);
     pt.mark(10);
@@ -476,7 +481,7 @@ struct ClusterNet {
       pt.mark(12);
       reduce(out, ldo, b2);
       pt.mark(13);
-    } else {
+    } else if (!no_sync) {
       thcl::cluster_sync();   // X is rewritten by the next gather of any CTA
       pt.mark(13);
     }
@@ -585,7 +590,8 @@ struct ClusterMlpAdapter {
   OB_DEV void release() { thcl::cluster_sync(); }   // no CTA leaves while a partner may still write into it
   OB_DEV void eval(double* out) { net.forward(xin, p.d.lda[0], net.Rv, out, p.d.ldn); }
   OB_DEV void vjp(const double* w, double* jtv, double* mu, double h, int) {
-    net.forward(xin, p.d.lda[0], net.Rv, nullptr, 0);   // hidden activations at the stage state
+    // hidden activations at the stage state
+    net.forward(xin, p.d.lda[0], net.Rv, nullptr, 0, mu != nullptr && net.X2 != nullptr);
     net.vjp(w, p.d.ldn, net.Rv, jtv, p.d.ldn, mu, h, xin, p.d.lda[0]);
   }
 };

@@ -163,6 +163,24 @@ def test_explicit_rk_on_cluster_matches_single_cta_kernels(scheme, policy):
         assert oc.rel_error(np_(getattr(cl, k)), ref[k]) <= TOL64, k
 
 
+def test_explicit_rk_cluster_two_row_tiles_per_cluster():
+    """A batch past one wave at 4 rows per CTA: 6 rows per CTA, 12 per cluster of two -- the
+    products run over two MMA row tiles (the second half empty) and the register cotangent
+    tiles take three k-steps."""
+    ci = make_config("C1", batch=800)
+    fld = field_from_config(ci)
+    cl = run_config(ci, "store_all", field=fld)
+    base = run_config(ci, "store_all", field=fld, tensor_cores=False)
+    assert cl.device["tensor_cores"] == 2 and cl.device["tile_rows"] == 6
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(np_(getattr(cl, k)), np_(getattr(base, k))) <= 1e-12, k
+    mlp = oc.Mlp(ci.widths, ci.activation, ci.theta, ci.time_input)
+    ref = oc.grad_terminal(oc.MlpField(mlp), ci.scheme, ci.u0, ci.t0, ci.tF, ci.n_steps, "store_all")
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(np_(getattr(cl, k)), ref[k]) <= TOL64, k
+    assert abs(cl.loss - ref["loss"]) <= TOL64 * abs(ref["loss"])
+
+
 def test_explicit_rk_on_clusters_of_eight():
     """A hidden layer too wide for two CTAs (64-512-64: half of the weights is 256 KB) runs on
     clusters of eight with the parameter cotangents accumulated in the mu slot."""

@@ -27,3 +27,4 @@ for _ in range(n):
     run_config(ci, None, field=fld, u0=u0)
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(15)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(45)
