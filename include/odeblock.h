@@ -197,7 +197,8 @@ typedef struct {
   int64_t tile_rows;             /* samples per CTA tile                                 */
   int64_t tiles;                 /* CTAs per persistent launch                           */
   int64_t tensor_cores;          /* 1: the contractions ran on a tcgen05 tile (split fp32 products);
-                                    2: fp64 cluster MLP (weights resident across 8 CTAs, mma.sync f64) */
+                                    2: fp64 cluster MLP (weights resident across a cluster of 2 or 8 CTAs,
+                                       mma.sync f64) */
   double ms_pack, ms_forward, ms_reverse, ms_reduce;  /* CUDA-event device times of this call */
 } ob_counters;
 
