@@ -388,20 +388,34 @@ struct ClusterNet {
 
   // the same product into this warp's register tiles (kRegMu): acc[s] is output tile
   // warp + s * n_warps; the scale goes on the P fragment
-  OB_DEV void outer_reg(const double* P, int pa, const double* Q, int qb, double scale,
-                        double (&acc)[thcl::kMuSlots][2][2]) {
+  // register tile s of this warp: output tile (row tile mt, column pair np).  When the warps
+  // divide evenly over the column pairs a warp keeps ONE column pair for all its tiles (its B
+  // fragments are then loaded once per k-step for all of them); else tiles are dealt round robin.
+  OB_DEV bool mu_tile(int s, int mtiles, int npairs, int& mt, int& np) const {
+    const int w = warp_id(), nw = n_warps();
+    if (nw % npairs == 0) {
+      np = w % npairs;
+      mt = w / npairs + s * (nw / npairs);
+      return mt < mtiles;
+    }
+    const int task = w + s * nw;
+    np = task % npairs;
+    mt = task / npairs;
+    return task < mtiles * npairs;
+  }
+  template <bool SHARED_B>
+  OB_DEV void outer_reg_impl(const double* P, int pa, const double* Q, int qb, double scale,
+                             double (&acc)[thcl::kMuSlots][2][2]) {
     const int lane = lane_id(), lr = lane >> 2, lc = lane & 3;
-    const int npairs = qb / 16, ntasks = (pa / 8) * npairs;
-    int oa[thcl::kMuSlots], o0[thcl::kMuSlots], o1[thcl::kMuSlots];   // operand columns per tile (no branches:
-    bool live[thcl::kMuSlots];                                         // the tiles' loads and MMAs interleave)
+    const int npairs = qb / 16, mtiles = pa / 8;
+    int oa[thcl::kMuSlots], o0[thcl::kMuSlots];   // operand columns per tile (no branches: the
+    bool live[thcl::kMuSlots];                    // tiles' loads and MMAs interleave)
 #pragma unroll
     for (int s = 0; s < thcl::kMuSlots; ++s) {
-      const int task = warp_id() + s * n_warps();
-      live[s] = task < ntasks;
-      const int tt = live[s] ? task : 0;
-      oa[s] = 8 * (tt / npairs) + lr;
-      o0[s] = 16 * (tt % npairs) + lr;
-      o1[s] = o0[s] + 8;
+      int mt, np;
+      live[s] = mu_tile(s, mtiles, npairs, mt, np);
+      oa[s] = 8 * (live[s] ? mt : 0) + lr;
+      o0[s] = 16 * (live[s] ? np : 0) + lr;
     }
     for (int rs = 0; rs < nk; rs += 4) {
       const bool ok = rs + lc < nk;
@@ -410,11 +424,16 @@ struct ClusterNet {
 #pragma unroll
       for (int s = 0; s < thcl::kMuSlots; ++s) {
         // unconditional loads from clamped (valid) addresses: a conditional load compiles to a
-        // branch per operand
-        // (the dead fragments are finite values of row 0 / tile 0 times a zero scale)
+        // branch per operand (the dead fragments are finite values of row 0 / tile 0 times a
+        // zero scale)
         a[s] = Num<double>::mul((ok && live[s]) ? scale : 0.0, P[thcl::sw(r, oa[s], pa)]);
-        b0[s] = Q[thcl::sw(r, o0[s], qb)];
-        b1[s] = Q[thcl::sw(r, o1[s], qb)];
+        if (!SHARED_B || s == 0) {
+          b0[s] = Q[thcl::sw(r, o0[s], qb)];
+          b1[s] = Q[thcl::sw(r, o0[s] + 8, qb)];
+        } else {
+          b0[s] = b0[0];
+          b1[s] = b1[0];
+        }
       }
 #pragma unroll
       for (int s = 0; s < thcl::kMuSlots; ++s) {
@@ -423,14 +442,18 @@ struct ClusterNet {
       }
     }
   }
+  OB_DEV void outer_reg(const double* P, int pa, const double* Q, int qb, double scale,
+                        double (&acc)[thcl::kMuSlots][2][2]) {
+    if (n_warps() % (qb / 16) == 0) outer_reg_impl<true>(P, pa, Q, qb, scale, acc);
+    else outer_reg_impl<false>(P, pa, Q, qb, scale, acc);
+  }
   OB_DEV void flush_reg(int pa, int qb, const double (&acc)[thcl::kMuSlots][2][2], double* dst, long long ldm) {
     const int lane = lane_id(), lr = lane >> 2, lc = lane & 3;
-    const int npairs = qb / 16, ntasks = (pa / 8) * npairs;
+    const int npairs = qb / 16, mtiles = pa / 8;
 #pragma unroll
     for (int s = 0; s < thcl::kMuSlots; ++s) {
-      const int task = warp_id() + s * n_warps();
-      if (task < ntasks) {
-        const int np = task % npairs, mt = task / npairs;
+      int mt, np;
+      if (mu_tile(s, mtiles, npairs, mt, np)) {
 #pragma unroll
         for (int t = 0; t < 2; ++t)
 #pragma unroll
