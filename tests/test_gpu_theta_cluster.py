@@ -181,6 +181,28 @@ def test_explicit_rk_cluster_two_row_tiles_per_cluster():
     assert abs(cl.loss - ref["loss"]) <= TOL64 * abs(ref["loss"])
 
 
+@pytest.mark.parametrize("activation", ["relu", "identity"])
+def test_explicit_rk_cluster_other_activations_and_uneven_grid(activation):
+    """The other activations the cluster MLP accepts, on an uneven step grid (the step size that
+    scales the register cotangent tiles changes from step to step), against the SIMT tile."""
+    from paper_2206_01298_b200.controls import FixedGridController
+    from paper_2206_01298_b200.engine import grad
+    from paper_2206_01298_b200.policies import CheckpointPolicy
+    from paper_2206_01298_b200.schemes import tableau_catalog
+    from paper_2206_01298_b200.workloads import initial_state, loss_for, solver_from_config
+    ci = dataclasses.replace(make_config("C1").subset(300), activation=activation)
+    fld = field_from_config(ci)
+    ctrl = FixedGridController((0.0, 0.07, 0.2, 0.26, 0.55, 0.8, 1.0))
+    args = (fld, tableau_catalog("bosh3"), loss_for(ci), initial_state(ci), ci.t0, ci.tF, ctrl,
+            CheckpointPolicy.parse("store_all"), solver_from_config(ci))
+    cl = grad(*args)
+    base = grad(*args, tensor_cores=False)
+    assert cl.device["tensor_cores"] == 2 and base.device["tensor_cores"] == 0
+    for k in ("u_final", "du0", "dtheta"):
+        assert oc.rel_error(np_(getattr(cl, k)), np_(getattr(base, k))) <= 1e-12, k
+    assert abs(cl.loss - base.loss) <= 1e-12 * abs(base.loss)
+
+
 def test_explicit_rk_on_clusters_of_eight():
     """A hidden layer too wide for two CTAs (64-512-64: half of the weights is 256 KB) runs on
     clusters of eight with the parameter cotangents accumulated in the mu slot."""
