@@ -18,9 +18,12 @@ void OB_RKCL(rk_cluster, _geom)(int N, int H, int R, int* region_doubles) {
 }
 
 int OB_RKCL(rk_cluster, _max_active)(size_t smem) {
-  static int cached = -1;
-  static size_t cached_smem = 0;
-  if (cached >= 0 && cached_smem == smem) return cached;
+  // (per thread and device: the answer depends on the device, and plans are made per thread)
+  static thread_local int cached = -1, cached_dev = -1;
+  static thread_local size_t cached_smem = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cached >= 0 && cached_smem == smem && cached_dev == dev) return cached;
   auto kf = rk_reverse_kernel<double, ClusterMlpAdapter>;
   if (cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
@@ -44,6 +47,7 @@ int OB_RKCL(rk_cluster, _max_active)(size_t smem) {
   }
   cached = n;
   cached_smem = smem;
+  cached_dev = dev;
   return n;
 }
 

@@ -12,9 +12,12 @@ void theta_cluster_geom(int N, int H, int R, int RC, bool second_x, int* region_
 // clusters of the kernel that can be resident at once with `smem` bytes of dynamic shared
 // memory (GPC granularity: 15 clusters of 8 on a 148-SM B200)
 int theta_cluster_max_active(size_t smem) {
-  static int cached = -1;
-  static size_t cached_smem = 0;
-  if (cached >= 0 && cached_smem == smem) return cached;
+  // (per thread and device: the answer depends on the device, and plans are made per thread)
+  static thread_local int cached = -1, cached_dev = -1;
+  static thread_local size_t cached_smem = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cached >= 0 && cached_smem == smem && cached_dev == dev) return cached;
   if (cudaFuncSetAttribute(thcl_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess) {
     cudaGetLastError();
@@ -38,6 +41,7 @@ int theta_cluster_max_active(size_t smem) {
   }
   cached = n;
   cached_smem = smem;
+  cached_dev = dev;
   return n;
 }
 
