@@ -217,6 +217,17 @@ struct ClusterNet {
       *any_io = r;
     }
   }
+  // two row sets in one exchange (the VJP's linearisation rows -> X and cotangent rows -> X2)
+  OB_DEV void gather_pair(const double* s1, int ld1, const double* s2, int ld2) {
+    const int N = g.N;
+    for (int i = threadIdx.x; i < Rv * N * thcl::kCL; i += blockDim.x) {
+      const int c = i / (Rv * N), el = i % (Rv * N), r = el / N, j = el % N;
+      const int o = thcl::sw(off + r, j, N);
+      thcl::st_remote(thcl::remote(X + o, c), s1[r * ld1 + j]);
+      thcl::st_remote(thcl::remote(X2 + o, c), s2[r * ld2 + j]);
+    }
+    thcl::cluster_sync();
+  }
   // ---- step 3: owner side of the reduce-scatter: out[r][j] = sum over ranks (+ bias)
   OB_DEV void reduce(double* out, int ldo, const double* bias) {
     thcl::cluster_sync();
@@ -485,12 +496,14 @@ struct ClusterNet {
   // with out: the MLP value W2 act(W1 x + b1) + b2 for this CTA's rows
   // (no_sync: the caller's next exchange does not write X -- a VJP that gathers its cotangent
   // rows into the second row buffer -- so the closing barrier is not needed)
-  OB_DEV void forward(const double* src, int ld, int Rv, double* out, int ldo, bool no_sync = false) {
+  // pre_gathered: X already holds the cluster's rows (gather_pair).
+  OB_DEV void forward(const double* src, int ld, int Rv, double* out, int ldo, bool no_sync = false,
+                      bool pre_gathered = false) {
     // (profiling slots of tools/profile_step.py --phases: 10 all-gather, 11 hidden product +
     // activation, 12 output product + scatter, 13 reduce / barrier; in vjp(): 14 all-gather,
     // 15 W2^T product, 6 parameter cotangents, 7 W1^T product + scatter, 4 reduce)
     PhaseTimer pt(p.prof ? p.phase : nullptr);
-    gather(src, ld, Rv);
+    if (!pre_gathered) gather(src, ld, Rv);
     pt.mark(10);
     const int HS = g.HS, act = p.d.act;
     double* H = Hs;
@@ -533,7 +546,7 @@ struct ClusterNet {
   // (dMLP/du)^T v -> jtv; with mu: mu += scale (dMLP/dtheta)^T v over the valid rows.  xin:
   // the rows the linearisation was taken at (for dW1), gathered again when mu is given.
   OB_DEV void vjp(const double* v, int ld, int Rv, double* jtv, int ldo, double* mu, double scale,
-                  const double* xin, int ldx, int* any_io = nullptr) {
+                  const double* xin, int ldx, int* any_io = nullptr, bool pre_gathered = false) {
     const int N = g.N, HS = g.HS, act = p.d.act;
     const double* H = Hs;
     double* Tt = Ts;
@@ -543,7 +556,7 @@ struct ClusterNet {
     const bool keep_x = mu && X2 != nullptr;
     double* V = keep_x ? X2 : X;
     PhaseTimer pt(p.prof ? p.phase : nullptr);
-    gather(v, ld, Rv, any_io, V);   // all cotangent rows of the cluster
+    if (!pre_gathered) gather(v, ld, Rv, any_io, V);   // all cotangent rows of the cluster
     if (any_io && !*any_io) return;
     pt.mark(14);
     prod_c(V, [&](int r, int k, double gk) {
@@ -613,8 +626,16 @@ struct ClusterMlpAdapter {
   OB_DEV void release() { thcl::cluster_sync(); }   // no CTA leaves while a partner may still write into it
   OB_DEV void eval(double* out) { net.forward(xin, p.d.lda[0], net.Rv, out, p.d.ldn); }
   OB_DEV void vjp(const double* w, double* jtv, double* mu, double h, int) {
-    // hidden activations at the stage state
-    net.forward(xin, p.d.lda[0], net.Rv, nullptr, 0, mu != nullptr && net.X2 != nullptr);
+    if (mu != nullptr && net.X2 != nullptr) {
+      // stage-state rows and cotangent rows in ONE exchange (both buffers are free: every read
+      // of the previous VJP precedes its reduce barrier), then the hidden activations at the
+      // stage state and the VJP without further gathers
+      net.gather_pair(xin, p.d.lda[0], w, p.d.ldn);
+      net.forward(xin, p.d.lda[0], net.Rv, nullptr, 0, true, true);
+      net.vjp(w, p.d.ldn, net.Rv, jtv, p.d.ldn, mu, h, xin, p.d.lda[0], nullptr, true);
+      return;
+    }
+    net.forward(xin, p.d.lda[0], net.Rv, nullptr, 0);   // hidden activations at the stage state
     net.vjp(w, p.d.ldn, net.Rv, jtv, p.d.ldn, mu, h, xin, p.d.lda[0]);
   }
 };
