@@ -513,7 +513,7 @@ struct ClusterNet {
     pt.mark(11);
     if (out) {
       prod_b(Hs);
-      __syncthreads();
+      if (p.prof) __syncthreads();
       pt.mark(12);
       reduce(out, ldo, b2);
       pt.mark(13);
@@ -585,10 +585,10 @@ struct ClusterNet {
       else if (keep_x)   // dW1[k0 + k][i] += (act' o W2^T v)^T x
         outer_acc(Tt, HS, X, N, scale, mu + p.d.mwoff[0] + (long long)k0 * p.d.ldm[0], p.d.ldm[0]);
     }
-    __syncthreads();
+    if (p.prof) __syncthreads();   // (phase boundaries only: nothing below depends on the cotangent sums)
     pt.mark(6);
     prod_d(Ts);
-    __syncthreads();
+    if (p.prof) __syncthreads();
     pt.mark(7);
     reduce(jtv, ldo, nullptr);   // (cluster barrier: X / X2 may be overwritten below)
     pt.mark(4);
