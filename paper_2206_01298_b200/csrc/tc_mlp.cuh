@@ -497,6 +497,7 @@ struct TcMlpAdapter {
         if (i > 0) load_u(i - 1);
         continue;
       }
+      PhaseTimer ptr(p.prof ? p.phase : nullptr);
       float ca[OB_MAX_STAGES];
       bool nz[OB_MAX_STAGES];
 #pragma unroll
@@ -517,8 +518,10 @@ struct TcMlpAdapter {
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[e] = Num<float>::add(v[e], Num<float>::mul(ca[j], k[e]));
       }
+      ptr.mark(12);   // cotangent combination from the TMEM slots
       // V = h w (padded samples zero), db2 partial, U_i into X0
       drain();   // the previous stage's dW1 reads X0 and dZ
+      ptr.mark(13);   // wait for the previous stage's dW1 MMAs
       float ps = 0.f;
       if (mine) {
         float hv[8];
@@ -538,6 +541,7 @@ struct TcMlpAdapter {
       }
       if (i > 0) load_u(i - 1);
       put_time(t + p.c[i] * h);
+      ptr.mark(15);   // operand split + stores, next stage state load issued
       vjp_core(mu, slot_col(i), true);
       live |= 1u << i;
     }
